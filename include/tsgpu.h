@@ -1,0 +1,187 @@
+/*
+ * tsgpu.h — C ABI of the B200-native tsidx hot path (iSAX build + exact
+ * Euclidean 1-NN). One shared library: paper_2009_00786_b200/libtsgpu.so.
+ *
+ * Plain pointers and sizes, no exceptions and no torch types cross this
+ * boundary. Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj/core):
+ *
+ *   tsg_index_build          <- tsidx::build_index(Dataset, IndexConfig)
+ *                               include/tsidx/index.hpp:158, src/index.cpp:258-318
+ *   tsg_search               <- tsidx::exact_search(const Index&, span<const float>,
+ *                               Measure, SearchOptions)  include/tsidx/query.hpp:150-151,
+ *                               src/query.cpp:258-298 (Measure::ed() only)
+ *   tsg_approximate_search   <- tsidx::approximate_search  include/tsidx/query.hpp:133-134
+ *   tsg_config               <- tsidx::IndexConfig          include/tsidx/config.hpp:12-32
+ *   tsg_config_validate      <- IndexConfig::validate       src/config.cpp:22-35
+ *   tsg_build_stats          <- tsidx::BuildStats           include/tsidx/index.hpp:121-132
+ *   tsg_search_stats         <- tsidx::SearchStats          include/tsidx/query.hpp:17-27
+ *   tsg_summarise            <- paa_into + symbols_from_paa + root_key_from_symbols
+ *                               (the summarization hot loop, src/index.cpp:162-167)
+ *
+ * Error contract: every call returns a tsg_status. TSG_INVALID_ARGUMENT is
+ * what the reference throws as std::invalid_argument, TSG_LOGIC as
+ * std::logic_error, TSG_RUNTIME as std::runtime_error. The message of the
+ * last failure on the calling thread is tsg_last_error().
+ *
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * call fails with TSG_CUDA.
+ */
+#ifndef TSGPU_H
+#define TSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tsg_status {
+    TSG_OK = 0,
+    TSG_INVALID_ARGUMENT = 1,
+    TSG_RUNTIME = 2,
+    TSG_LOGIC = 3,
+    TSG_CUDA = 4,
+    TSG_NCCL = 5,
+    TSG_OOM = 6
+} tsg_status;
+
+/* Mirrors tsidx::IndexConfig field for field (include/tsidx/config.hpp:12-32).
+ * The worker / queue fields are accepted, validated and ignored: the device
+ * path has no worker threads or leaf queues (their role is played by the
+ * grid and by LB-ordered candidate refinement). */
+typedef struct tsg_config {
+    uint64_t n;                       /* series length, multiple of w */
+    int32_t w;                        /* PAA segments, 1..32 on the device path */
+    int32_t max_card_bits;            /* 1..8 */
+    uint64_t leaf_capacity;           /* >= 2 */
+    uint64_t chunk_size;              /* >= 1 (ignored) */
+    uint32_t n_index_workers;         /* ignored */
+    uint32_t n_search_workers;        /* ignored */
+    uint32_t n_queues;                /* >= 1 (ignored) */
+    int32_t queue_mode;               /* 0 single, 1 multi (ignored) */
+    uint64_t initial_buffer_part_size;/* >= 1 (ignored) */
+} tsg_config;
+
+/* tsidx::BuildStats (include/tsidx/index.hpp:121-132) plus device timings. */
+typedef struct tsg_build_stats {
+    uint64_t build_ns;        /* device work of the build (CUDA events), excludes H2D */
+    uint64_t series;
+    uint64_t nodes;
+    uint64_t inner_nodes;
+    uint64_t leaves;
+    uint64_t empty_leaves;
+    uint64_t overflow_leaves;
+    uint64_t max_depth;       /* root children are depth 1 */
+    /* device-path extras */
+    uint64_t root_children;   /* distinct root keys */
+    uint64_t h2d_ns;          /* host->device copy of the rows (0 for device input) */
+    double summarise_ms;      /* K1 */
+    double organise_ms;       /* K2 sort + gather */
+    double leaves_ms;         /* K3 leaf partition + boxes */
+} tsg_build_stats;
+
+/* tsidx::SearchStats (include/tsidx/query.hpp:17-27). Device meaning:
+ * lb_node_calcs = leaf-box lower bounds, lb_entry_calcs = word lower bounds,
+ * real_dist_calcs = full Euclidean refinements, bsf_updates = strict BSF
+ * improvements, pruned_subtrees = pruned leaves, queue_insertions =
+ * compacted candidates. */
+typedef struct tsg_search_stats {
+    uint64_t lb_node_calcs;
+    uint64_t lb_entry_calcs;
+    uint64_t real_dist_calcs;
+    uint64_t bsf_updates;
+    uint64_t pruned_subtrees;
+    uint64_t queue_insertions;
+} tsg_search_stats;
+
+/* tsidx::SearchResult: distance, position (global dataset row), stats. */
+typedef struct tsg_result {
+    double distance;
+    uint32_t position;
+    uint32_t reserved;
+    tsg_search_stats stats;
+} tsg_result;
+
+typedef struct tsg_ctx tsg_ctx;
+typedef struct tsg_index tsg_index;
+
+const char* tsg_last_error(void);
+const char* tsg_version(void);
+
+/* Defaults of IndexConfig (w=16, 8 bits, leaf 2000, chunk 20000, 24 queues, mq, part 5). */
+void tsg_config_default(tsg_config* cfg);
+tsg_status tsg_config_validate(const tsg_config* cfg);
+
+/* Lifecycle. n_gpus devices (devices may be NULL for 0..n_gpus-1). An index
+ * built on a context shards its rows across the context's devices in
+ * contiguous ranges; search combines the per-device answers. */
+tsg_status tsg_open(int n_gpus, const int* devices, tsg_ctx** out);
+tsg_status tsg_close(tsg_ctx* ctx);
+
+/* Build from HOST rows (count x length float32, row-major). The library
+ * copies the rows into HBM; the caller keeps ownership of its buffer.
+ * position_offset is added to every returned position (a shard's first
+ * global row when one process builds one shard of a larger dataset). */
+tsg_status tsg_index_build(tsg_ctx* ctx, const float* host_rows, uint64_t count,
+                           uint64_t length, const tsg_config* cfg, uint64_t position_offset,
+                           tsg_index** out, tsg_build_stats* stats);
+
+/* Build from rows already resident in device memory on the context's first
+ * device. The index borrows them: they must stay valid until tsg_index_free.
+ * Single-device contexts only. */
+tsg_status tsg_index_build_device(tsg_ctx* ctx, const float* dev_rows, uint64_t count,
+                                  uint64_t length, const tsg_config* cfg,
+                                  uint64_t position_offset, tsg_index** out,
+                                  tsg_build_stats* stats);
+
+tsg_status tsg_index_free(tsg_index* index);
+
+tsg_status tsg_index_info(const tsg_index* index, uint64_t* count, uint64_t* length,
+                          tsg_config* cfg, tsg_build_stats* stats);
+
+/* Exact 1-NN of nq HOST queries (nq x length float32). out[nq] on the host. */
+tsg_status tsg_search(tsg_index* index, const float* host_queries, uint32_t nq,
+                      tsg_result* out);
+
+/* Same for queries already in device memory (first device of the index).
+ * out is a HOST array. */
+tsg_status tsg_search_device(tsg_index* index, const float* dev_queries, uint32_t nq,
+                             tsg_result* out);
+
+/* Approximate answer: the best series inside the query's closest leaf. */
+tsg_status tsg_approximate_search(tsg_index* index, const float* host_query, tsg_result* out);
+
+/* ---- kernel-level entry points (parity tests, benchmarks) ---------------- */
+
+/* K1 alone over device rows: words[count][word_stride] (left-aligned
+ * symbols, segment order, zero padded) and root keys[count]. word_stride is
+ * 16 for w <= 16, else 32. stream may be NULL (legacy default stream). */
+tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length, int w,
+                         int bits, uint8_t* dev_words, uint32_t* dev_root_keys, void* stream);
+
+/* Word stride used by the device layout for a given w. */
+int tsg_word_stride(int w);
+
+/* Copy the index's flat SoA back to the host (single-device index):
+ * words[count][word_stride] in index order, positions[count] (global),
+ * leaf_offsets[leaves+1]. Any pointer may be NULL. */
+tsg_status tsg_index_export(const tsg_index* index, uint8_t* words, uint32_t* positions,
+                            uint32_t* leaf_offsets, uint8_t* leaf_lo, uint8_t* leaf_hi);
+
+/* Device data generator: rows [begin, begin+count) of the reference's
+ * generate_random_walk(., length, seed) (src/dataset.cpp:22-68), optionally
+ * z-normalised the CLI way (degenerate -> zeros, tools/main.cpp:128-139),
+ * written to dev_rows. Input-setup utility, not part of the timed path. */
+tsg_status tsg_generate_random_walk(float* dev_rows, uint64_t begin, uint64_t count,
+                                    uint64_t length, uint64_t seed, int znorm, void* stream);
+
+/* Number of kernel launches this process issued through the library. */
+uint64_t tsg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSGPU_H */

@@ -1,0 +1,531 @@
+// C ABI (include/tsgpu.h) over the device kernels.
+//
+// build:  tsidx::build_index (src/index.cpp:258-318)   -> tsg_index_build
+// search: tsidx::exact_search (src/query.cpp:258-298)  -> tsg_search
+// Validation messages follow IndexConfig::validate (src/config.cpp:22-35),
+// build_index (src/index.cpp:259-266) and QueryState (src/query.cpp:84-87).
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/tsgpu.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tsg {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_error;
+
+struct LogicError : std::logic_error {
+    using std::logic_error::logic_error;
+};
+
+template <typename F>
+tsg_status guarded(F&& f) {
+    try {
+        f();
+        return TSG_OK;
+    } catch (const InvalidArgument& e) {
+        g_error = e.what();
+        return TSG_INVALID_ARGUMENT;
+    } catch (const std::invalid_argument& e) {
+        g_error = e.what();
+        return TSG_INVALID_ARGUMENT;
+    } catch (const OutOfMemory& e) {
+        g_error = e.what();
+        return TSG_OOM;
+    } catch (const CudaError& e) {
+        g_error = e.what();
+        return TSG_CUDA;
+    } catch (const std::logic_error& e) {
+        g_error = e.what();
+        return TSG_LOGIC;
+    } catch (const std::bad_alloc& e) {
+        g_error = "host allocation failed";
+        return TSG_OOM;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return TSG_RUNTIME;
+    } catch (...) {
+        g_error = "unknown error";
+        return TSG_RUNTIME;
+    }
+}
+
+void fail(const std::string& m) { throw InvalidArgument(m); }
+
+void validate_config(const tsg_config& c) {
+    // IndexConfig::validate (src/config.cpp:22-35), same messages.
+    if (c.w < 1) fail("IndexConfig: w must be at least 1");
+    if (c.w > 64) fail("IndexConfig: w must be at most 64 (root keys are 64-bit)");
+    if (c.max_card_bits < 1 || c.max_card_bits > 8) fail("IndexConfig: max_card_bits must be in [1, 8]");
+    if (c.n < static_cast<uint64_t>(c.w)) fail("IndexConfig: n must be at least w");
+    if (c.n % static_cast<uint64_t>(c.w) != 0)
+        fail("IndexConfig: n (" + std::to_string(c.n) + ") must be a multiple of w (" + std::to_string(c.w) + ")");
+    if (c.leaf_capacity < 2) fail("IndexConfig: leaf_capacity must be at least 2");
+    if (c.chunk_size < 1) fail("IndexConfig: chunk_size must be at least 1");
+    if (c.n_queues < 1) fail("IndexConfig: n_queues must be at least 1");
+    if (c.initial_buffer_part_size < 1) fail("IndexConfig: initial_buffer_part_size must be at least 1");
+    // Device-path limits (documented in DESIGN.md).
+    if (c.w > kMaxW) fail("IndexConfig: w must be at most 32 on the device path");
+    if (c.n > 8192) fail("IndexConfig: n must be at most 8192 on the device path");
+}
+
+int device_count() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw CudaError(std::string("no CUDA device available (the device path has no CPU fallback): ") +
+                        cudaGetErrorString(e));
+    return n;
+}
+
+void check_device(int dev) {
+    cudaDeviceProp p{};
+    TSG_CUDA(cudaGetDeviceProperties(&p, dev));
+    if (p.major < 10)
+        throw CudaError("device " + std::to_string(dev) + " is sm_" + std::to_string(p.major * 10 + p.minor) +
+                        "; this library is built for sm_100a");
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int d) {
+        TSG_CUDA(cudaGetDevice(&prev));
+        TSG_CUDA(cudaSetDevice(d));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+}  // namespace tsg
+
+using namespace tsg;
+
+struct tsg_ctx {
+    std::vector<int> devices;
+};
+
+struct tsg_index {
+    tsg_ctx* ctx = nullptr;
+    tsg_config cfg{};
+    uint64_t count = 0, length = 0, position_offset = 0;
+    std::vector<DevIndex> shards;
+    std::vector<uint64_t> shard_first;  // first local row of each shard (relative to position_offset)
+    tsg_build_stats stats{};
+    std::mutex mu;
+};
+
+namespace {
+
+void free_shard(DevIndex& s) {
+    DeviceGuard g(s.device);
+    if (s.own_rows) cudaFree(s.rows);
+    cudaFree(s.thr);
+    cudaFree(s.words);
+    cudaFree(s.pos);
+    cudaFree(s.leaf_off);
+    cudaFree(s.leaf_lo);
+    cudaFree(s.leaf_hi);
+    cudaFree(s.work);
+    cudaFree(s.lut);
+    cudaFree(s.leaf_lb);
+    cudaFree(s.cand_pos);
+    cudaFree(s.cand_lb);
+    cudaFree(s.cand_sq);
+    cudaFree(s.results);
+    cudaFree(s.queries);
+    if (s.stream) cudaStreamDestroy(s.stream);
+    s = DevIndex{};
+}
+
+double* upload_thresholds(int bits) {
+    double h[kThrPad];
+    host_breakpoints(bits, h);
+    double* d = nullptr;
+    TSG_CUDA(cudaMalloc(&d, sizeof(h)));
+    TSG_CUDA(cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice));
+    return d;
+}
+
+// Builds one shard on its device. rows: host (copied) or device (borrowed).
+void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, const tsg_config& cfg,
+                 uint64_t pos_offset, uint64_t* h2d_ns, double ms[3]) {
+    DeviceGuard g(s.device);
+    check_device(s.device);
+    TSG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    TSG_CUDA(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, s.device));
+    s.N = N;
+    s.n = static_cast<int>(cfg.n);
+    s.w = cfg.w;
+    s.bits = cfg.max_card_bits;
+    s.ws = word_stride(cfg.w);
+    s.leaf_cap = cfg.leaf_capacity;
+    s.pos_offset = pos_offset;
+    if (host_rows) {
+        const auto t0 = std::chrono::steady_clock::now();
+        TSG_CUDA(cudaMalloc(&s.rows, N * cfg.n * sizeof(float)));
+        s.own_rows = true;
+        TSG_CUDA(cudaMemcpyAsync(s.rows, rows, N * cfg.n * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+        TSG_CUDA(cudaStreamSynchronize(s.stream));
+        *h2d_ns = static_cast<uint64_t>(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    } else {
+        s.rows = const_cast<float*>(rows);
+        s.own_rows = false;
+        *h2d_ns = 0;
+    }
+    s.thr = upload_thresholds(s.bits);
+    build_layout(s, &ms[0], &ms[1], &ms[2]);
+    // search workspace
+    TSG_CUDA(cudaMalloc(&s.work, sizeof(QueryWork)));
+    TSG_CUDA(cudaMalloc(&s.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&s.leaf_lb, std::max<uint64_t>(s.L, 1) * sizeof(float)));
+    s.cand_cap = N;
+    TSG_CUDA(cudaMalloc(&s.cand_pos, N * sizeof(uint32_t)));
+    TSG_CUDA(cudaMalloc(&s.cand_lb, N * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&s.cand_sq, N * sizeof(double)));
+}
+
+void ensure_results(DevIndex& s, uint32_t nq) {
+    if (s.results_cap >= nq) return;
+    cudaFree(s.results);
+    s.results = nullptr;
+    TSG_CUDA(cudaMalloc(&s.results, static_cast<size_t>(nq) * sizeof(DevResult)));
+    s.results_cap = nq;
+}
+
+void ensure_queries(DevIndex& s, uint32_t nq) {
+    if (s.queries_cap >= nq) return;
+    cudaFree(s.queries);
+    s.queries = nullptr;
+    TSG_CUDA(cudaMalloc(&s.queries, static_cast<size_t>(nq) * s.n * sizeof(float)));
+    s.queries_cap = nq;
+}
+
+void to_result(const DevResult& d, tsg_result& r) {
+    r.distance = d.distance;
+    r.position = d.position;
+    r.reserved = 0;
+    r.stats.lb_node_calcs = d.stats[0];
+    r.stats.lb_entry_calcs = d.stats[1];
+    r.stats.real_dist_calcs = d.stats[2];
+    r.stats.bsf_updates = d.stats[3];
+    r.stats.pruned_subtrees = d.stats[4];
+    r.stats.queue_insertions = d.stats[5];
+}
+
+// Lexicographic (distance, position) merge of per-shard answers: the
+// cross-device step of the sharded search.
+void merge_into(tsg_result& acc, const tsg_result& r, bool first) {
+    if (first || r.distance < acc.distance || (r.distance == acc.distance && r.position < acc.position)) {
+        acc.distance = r.distance;
+        acc.position = r.position;
+    }
+    if (first) {
+        acc.stats = r.stats;
+        return;
+    }
+    acc.stats.lb_node_calcs += r.stats.lb_node_calcs;
+    acc.stats.lb_entry_calcs += r.stats.lb_entry_calcs;
+    acc.stats.real_dist_calcs += r.stats.real_dist_calcs;
+    acc.stats.bsf_updates += r.stats.bsf_updates;
+    acc.stats.pruned_subtrees += r.stats.pruned_subtrees;
+    acc.stats.queue_insertions += r.stats.queue_insertions;
+}
+
+void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg_result* out, bool approximate) {
+    if (!ix) fail("search: null index");
+    if (nq == 0) return;
+    if (!queries || !out) fail("search: null buffer");
+    std::lock_guard<std::mutex> lock(ix->mu);
+    if (!host && ix->shards.size() != 1) fail("tsg_search_device: device queries need a single-device index");
+    std::vector<std::vector<DevResult>> per(ix->shards.size(), std::vector<DevResult>(nq));
+    auto work = [&](size_t k) {
+        DevIndex& s = ix->shards[k];
+        DeviceGuard g(s.device);
+        ensure_results(s, nq);
+        const float* dq = queries;
+        if (host) {
+            ensure_queries(s, nq);
+            TSG_CUDA(cudaMemcpyAsync(s.queries, queries, static_cast<size_t>(nq) * s.n * sizeof(float),
+                                     cudaMemcpyHostToDevice, s.stream));
+            dq = s.queries;
+        }
+        search_batch(s, dq, nq, approximate);
+        TSG_CUDA(cudaMemcpyAsync(per[k].data(), s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
+        TSG_CUDA(cudaStreamSynchronize(s.stream));
+    };
+    if (ix->shards.size() == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        std::vector<std::exception_ptr> errs(ix->shards.size());
+        for (size_t k = 0; k < ix->shards.size(); ++k)
+            th.emplace_back([&, k] {
+                try {
+                    work(k);
+                } catch (...) {
+                    errs[k] = std::current_exception();
+                }
+            });
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    }
+    for (uint32_t q = 0; q < nq; ++q)
+        for (size_t k = 0; k < ix->shards.size(); ++k) {
+            tsg_result r{};
+            to_result(per[k][q], r);
+            merge_into(out[q], r, k == 0);
+        }
+}
+
+tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, uint64_t length,
+                    const tsg_config* cfg, uint64_t position_offset, tsg_index** out, tsg_build_stats* stats) {
+    return guarded([&] {
+        if (!ctx || !out) fail("build_index: null argument");
+        *out = nullptr;
+        if (!cfg) fail("build_index: null config");
+        validate_config(*cfg);
+        if (count == 0) fail("build_index: empty dataset");
+        if (length != cfg->n)
+            fail("build_index: dataset length " + std::to_string(length) + " does not match config.n " +
+                 std::to_string(cfg->n));
+        if (count > 0xFFFFFFFFull) fail("build_index: more than 2^32-1 series");
+        if (!rows) fail("build_index: null rows");
+        if (position_offset + count - 1 > 0xFFFFFFFFull) fail("build_index: positions exceed 2^32-1");
+        if (!host && ctx->devices.size() != 1) fail("tsg_index_build_device: device rows need a single-device context");
+
+        auto ix = std::make_unique<tsg_index>();
+        ix->ctx = ctx;
+        ix->cfg = *cfg;
+        ix->count = count;
+        ix->length = length;
+        ix->position_offset = position_offset;
+        const size_t G = std::min<size_t>(ctx->devices.size(), count);
+        ix->shards.resize(G);
+        ix->shard_first.resize(G);
+        std::vector<uint64_t> h2d(G, 0);
+        std::vector<std::array<double, 3>> ms(G);
+        std::vector<std::exception_ptr> errs(G);
+        const auto t0 = std::chrono::steady_clock::now();
+        auto work = [&](size_t k) {
+            try {
+                const uint64_t b = count * k / G, e = count * (k + 1) / G;
+                ix->shard_first[k] = b;
+                ix->shards[k].device = ctx->devices[k];
+                build_shard(ix->shards[k], rows + b * length, host, e - b, *cfg, position_offset + b, &h2d[k],
+                            ms[k].data());
+            } catch (...) {
+                errs[k] = std::current_exception();
+            }
+        };
+        if (G == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (size_t k = 0; k < G; ++k) th.emplace_back(work, k);
+            for (auto& t : th) t.join();
+        }
+        for (auto& e : errs)
+            if (e) {
+                for (auto& s : ix->shards)
+                    if (s.stream || s.rows) free_shard(s);
+                std::rethrow_exception(e);
+            }
+        (void)t0;
+        tsg_build_stats st{};
+        st.series = count;
+        double sum_ms = 0, org_ms = 0, leaf_ms = 0;
+        for (size_t k = 0; k < G; ++k) {
+            const DevIndex& s = ix->shards[k];
+            st.leaves += s.L;
+            st.inner_nodes += s.inner;
+            st.overflow_leaves += s.overflow;
+            st.max_depth = std::max<uint64_t>(st.max_depth, s.max_depth);
+            st.root_children += s.root_children;
+            st.h2d_ns = std::max(st.h2d_ns, h2d[k]);
+            sum_ms = std::max(sum_ms, ms[k][0]);
+            org_ms = std::max(org_ms, ms[k][1]);
+            leaf_ms = std::max(leaf_ms, ms[k][2]);
+        }
+        st.nodes = st.leaves + st.inner_nodes;
+        st.empty_leaves = 0;
+        st.summarise_ms = sum_ms;
+        st.organise_ms = org_ms;
+        st.leaves_ms = leaf_ms;
+        st.build_ns = static_cast<uint64_t>((sum_ms + org_ms + leaf_ms) * 1e6);
+        ix->stats = st;
+        if (stats) *stats = st;
+        *out = ix.release();
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsg_last_error(void) { return g_error.c_str(); }
+
+const char* tsg_version(void) { return "tsgpu 0.1 (sm_100a)"; }
+
+uint64_t tsg_launch_count(void) { return launch_count(); }
+
+int tsg_word_stride(int w) { return word_stride(w); }
+
+void tsg_config_default(tsg_config* c) {
+    if (!c) return;
+    c->n = 256;
+    c->w = 16;
+    c->max_card_bits = 8;
+    c->leaf_capacity = 2000;
+    c->chunk_size = 20000;
+    c->n_index_workers = 0;
+    c->n_search_workers = 0;
+    c->n_queues = 24;
+    c->queue_mode = 1;
+    c->initial_buffer_part_size = 5;
+}
+
+tsg_status tsg_config_validate(const tsg_config* cfg) {
+    return guarded([&] {
+        if (!cfg) fail("IndexConfig: null");
+        validate_config(*cfg);
+    });
+}
+
+tsg_status tsg_open(int n_gpus, const int* devices, tsg_ctx** out) {
+    return guarded([&] {
+        if (!out) fail("tsg_open: null out");
+        *out = nullptr;
+        if (n_gpus < 1) fail("tsg_open: n_gpus must be at least 1");
+        const int have = device_count();
+        auto ctx = std::make_unique<tsg_ctx>();
+        for (int i = 0; i < n_gpus; ++i) {
+            const int d = devices ? devices[i] : i;
+            if (d < 0 || d >= have) fail("tsg_open: device " + std::to_string(d) + " out of range");
+            check_device(d);
+            ctx->devices.push_back(d);
+        }
+        *out = ctx.release();
+    });
+}
+
+tsg_status tsg_close(tsg_ctx* ctx) {
+    delete ctx;
+    return TSG_OK;
+}
+
+tsg_status tsg_index_build(tsg_ctx* ctx, const float* host_rows, uint64_t count, uint64_t length,
+                           const tsg_config* cfg, uint64_t position_offset, tsg_index** out, tsg_build_stats* stats) {
+    return do_build(ctx, host_rows, true, count, length, cfg, position_offset, out, stats);
+}
+
+tsg_status tsg_index_build_device(tsg_ctx* ctx, const float* dev_rows, uint64_t count, uint64_t length,
+                                  const tsg_config* cfg, uint64_t position_offset, tsg_index** out,
+                                  tsg_build_stats* stats) {
+    return do_build(ctx, dev_rows, false, count, length, cfg, position_offset, out, stats);
+}
+
+tsg_status tsg_index_free(tsg_index* ix) {
+    return guarded([&] {
+        if (!ix) return;
+        for (auto& s : ix->shards) free_shard(s);
+        delete ix;
+    });
+}
+
+tsg_status tsg_index_info(const tsg_index* ix, uint64_t* count, uint64_t* length, tsg_config* cfg,
+                          tsg_build_stats* stats) {
+    return guarded([&] {
+        if (!ix) fail("tsg_index_info: null index");
+        if (count) *count = ix->count;
+        if (length) *length = ix->length;
+        if (cfg) *cfg = ix->cfg;
+        if (stats) *stats = ix->stats;
+    });
+}
+
+tsg_status tsg_search(tsg_index* ix, const float* host_queries, uint32_t nq, tsg_result* out) {
+    return guarded([&] { run_search(ix, host_queries, true, nq, out, false); });
+}
+
+tsg_status tsg_search_device(tsg_index* ix, const float* dev_queries, uint32_t nq, tsg_result* out) {
+    return guarded([&] { run_search(ix, dev_queries, false, nq, out, false); });
+}
+
+tsg_status tsg_approximate_search(tsg_index* ix, const float* host_query, tsg_result* out) {
+    return guarded([&] { run_search(ix, host_query, true, 1, out, true); });
+}
+
+tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length, int w, int bits, uint8_t* dev_words,
+                         uint32_t* dev_root_keys, void* stream) {
+    return guarded([&] {
+        if (w < 1 || w > kMaxW) fail("tsg_summarise: w must be in [1, 32]");
+        if (bits < 1 || bits > 8) fail("tsg_summarise: bits must be in [1, 8]");
+        if (length < static_cast<uint64_t>(w) || length % static_cast<uint64_t>(w) != 0)
+            fail("tsg_summarise: length must be a nonzero multiple of w");
+        if (count == 0) return;
+        if (!dev_rows || !dev_words) fail("tsg_summarise: null buffer");
+        device_count();
+        int dev = 0;
+        TSG_CUDA(cudaGetDevice(&dev));
+        check_device(dev);
+        double h[kThrPad];
+        host_breakpoints(bits, h);
+        double* d = nullptr;
+        auto st = static_cast<cudaStream_t>(stream);
+        TSG_CUDA(cudaMallocAsync(&d, sizeof(h), st));
+        TSG_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        summarise(dev_rows, count, static_cast<int>(length), w, bits, d, dev_words, dev_root_keys, nullptr, st);
+        TSG_CUDA(cudaFreeAsync(d, st));
+        TSG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* positions, uint32_t* leaf_offsets,
+                            uint8_t* leaf_lo, uint8_t* leaf_hi) {
+    return guarded([&] {
+        if (!ix) fail("tsg_index_export: null index");
+        if (ix->shards.size() != 1) fail("tsg_index_export: single-device index only");
+        const DevIndex& s = ix->shards[0];
+        DeviceGuard g(s.device);
+        if (words) TSG_CUDA(cudaMemcpy(words, s.words, s.N * s.ws, cudaMemcpyDeviceToHost));
+        if (positions) {
+            TSG_CUDA(cudaMemcpy(positions, s.pos, s.N * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < s.N; ++i) positions[i] += static_cast<uint32_t>(s.pos_offset);
+        }
+        if (leaf_offsets) TSG_CUDA(cudaMemcpy(leaf_offsets, s.leaf_off, (s.L + 1) * 4, cudaMemcpyDeviceToHost));
+        if (leaf_lo) TSG_CUDA(cudaMemcpy(leaf_lo, s.leaf_lo, s.L * s.ws, cudaMemcpyDeviceToHost));
+        if (leaf_hi) TSG_CUDA(cudaMemcpy(leaf_hi, s.leaf_hi, s.L * s.ws, cudaMemcpyDeviceToHost));
+    });
+}
+
+tsg_status tsg_generate_random_walk(float* dev_rows, uint64_t begin, uint64_t count, uint64_t length, uint64_t seed,
+                                    int znorm, void* stream) {
+    return guarded([&] {
+        if (count == 0) return;
+        if (!dev_rows) fail("generate_random_walk: null rows");
+        device_count();
+        generate_random_walk(dev_rows, begin, count, length, seed, znorm, static_cast<cudaStream_t>(stream));
+        TSG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// Shared device/host helpers for the tsgpu library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "tsgpu is built for sm_100a only"
+#endif
+
+namespace tsg {
+
+// Error classes mapped onto tsg_status at the C ABI.
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct OutOfMemory : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    std::string msg = std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                      std::to_string(line) + ")";
+    if (e == cudaErrorMemoryAllocation) throw OutOfMemory(msg);
+    throw CudaError(msg);
+}
+
+#define TSG_CUDA(expr) ::tsg::cuda_check((expr), #expr, __FILE__, __LINE__)
+
+// Counts every kernel this library launches (reported as gpu_launches).
+void note_launch(int n = 1);
+uint64_t launch_count();
+
+#define TSG_LAUNCHED() \
+    do {                                                        \
+        ::tsg::note_launch();                                   \
+        TSG_CUDA(cudaPeekAtLastError());                        \
+    } while (0)
+
+// Word stride in bytes: 16 for w <= 16, 32 for w <= 32.
+__host__ __device__ inline int word_stride(int w) { return w <= 16 ? 16 : 32; }
+
+constexpr int kMaxW = 32;
+constexpr int kThrPad = 256;  // padded threshold table entries per cardinality
+
+// Device threshold table for one cardinality: thr[0..card-2], padded with
+// +inf up to 256 entries. Computed on the host (breakpoints.cpp), bit
+// identical to tsidx::breakpoints_for (src/breakpoints.cpp:65-114).
+void host_breakpoints(int bits, double* out256);
+
+// ---- small PTX helpers ----------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Upper bound over a padded threshold table in shared memory: the number of
+// thresholds <= v, i.e. std::upper_bound (src/sax.cpp:33-37). Written as
+// !(v < t) so a NaN mean lands in the top region exactly as upper_bound puts it.
+__device__ __forceinline__ unsigned symbol_of(const double* thr, int bits, double v) {
+    unsigned s = 0;
+#pragma unroll
+    for (int b = 7; b >= 0; --b) {
+        if (b < bits) {
+            const unsigned step = 1u << b;
+            if (!(v < thr[s + step - 1])) s += step;
+        }
+    }
+    return s;
+}
+
+}  // namespace tsg

@@ -1,0 +1,81 @@
+// Device-side index layout and the host launchers of every kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tsg {
+
+// Flat structure-of-arrays index of one device shard. Replaces the
+// reference's pointer tree (IndexNode / LeafEntries / RootTable,
+// include/tsidx/index.hpp:19-75): words and positions are sorted by the
+// plane-major iSAX key (root key first), leaves are contiguous ranges.
+struct DevIndex {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t N = 0;           // series on this shard
+    int n = 0, w = 0, bits = 0, ws = 16;
+    uint64_t leaf_cap = 0;
+    uint64_t pos_offset = 0;  // global position of local row 0
+    float* rows = nullptr;    // [N][n] original order
+    bool own_rows = false;
+    double* thr = nullptr;    // [256] thresholds for `bits`, +inf padded
+    uint8_t* words = nullptr; // [N][ws] index order
+    uint32_t* pos = nullptr;  // [N] local row of each index entry
+    uint32_t* leaf_off = nullptr;  // [L+1]
+    uint8_t* leaf_lo = nullptr;    // [L][ws] per-segment min symbol
+    uint8_t* leaf_hi = nullptr;    // [L][ws] per-segment max symbol
+    uint64_t L = 0;
+    uint64_t root_children = 0;
+    uint64_t inner = 0, max_depth = 0, overflow = 0;
+    // search workspace
+    struct QueryWork* work = nullptr;
+    float* lut = nullptr;          // [w][256]
+    float* leaf_lb = nullptr;      // [L]
+    uint32_t* cand_pos = nullptr;  // [cap]
+    float* cand_lb = nullptr;      // [cap]
+    double* cand_sq = nullptr;     // [cap]
+    uint64_t cand_cap = 0;
+    struct DevResult* results = nullptr;  // [results_cap]
+    uint32_t results_cap = 0;
+    float* queries = nullptr;      // staging for host queries
+    uint32_t queries_cap = 0;
+    int sms = 148;
+};
+
+// Per-query device scratch (reset by the prep kernel).
+struct QueryWork {
+    unsigned long long bsf_bits;  // best squared distance so far (double bits)
+    unsigned long long seed_key;  // (leaf LB float bits << 32) | leaf
+    unsigned int ncand;
+    unsigned int nseed;
+    unsigned int work_next;
+    unsigned int best_pos;
+    unsigned long long stats[6];  // SearchStats order
+    double qpaa[32];
+    unsigned char qsym[32];
+};
+
+struct DevResult {
+    double distance;
+    uint32_t position;
+    uint32_t reserved;
+    unsigned long long stats[6];
+};
+
+// K1
+void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
+               uint8_t* words, uint32_t* root_keys, uint32_t* sort_keys, cudaStream_t stream);
+
+// K2 + K3: sort, gather, leaves, boxes. Fills the index arrays of `ix`
+// (rows/thr/N/n/w/bits/leaf_cap must be set). Returns device ms per phase.
+void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, double* ms_leaves);
+
+// Query pipeline for nq device queries; writes ix.results[0..nq).
+void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approximate);
+
+// Input generator (not on the timed path).
+void generate_random_walk(float* rows, uint64_t begin, uint64_t count, uint64_t length,
+                          uint64_t seed, int znorm, cudaStream_t stream);
+
+}  // namespace tsg

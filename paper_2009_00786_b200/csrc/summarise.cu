@@ -1,0 +1,304 @@
+// K1 summarise: float32 rows -> iSAX words + root keys + sort keys.
+//
+// Replaces the summarization hot loop of the reference build
+// (src/index.cpp:162-167): paa_into (src/sax.cpp:10-25) + symbols_from_paa
+// (src/sax.cpp:39-47) + root_key_from_symbols (src/sax.cpp:59-63).
+//
+// Bit-exactness: every PAA segment is summed in FP64, sequentially from 0.0
+// in the reference's order, then divided by the segment length (IEEE
+// division); the symbol is the number of FP64 thresholds <= mean.
+//
+// Data movement (B200): a persistent grid, one producer warp per CTA issues
+// 2-D TMA loads (cp.async.bulk.tensor) of R whole series (R*n*4 bytes, 32 KB
+// for n=256) into a STAGES-deep shared-memory ring with the 128-byte
+// swizzle; 8 consumer warps read their segments back conflict-free (the
+// swizzle XOR spreads the 8 lanes of an LDS.128 phase over all 32 banks),
+// then one thread per series writes the 16-byte word and its keys.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace tsg {
+
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kSumThreads = kConsumers + 32;  // + one producer warp
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Swizzle-128B address of byte offset a inside a 1024-aligned tile.
+__device__ __forceinline__ uint32_t swz(uint32_t a) { return a ^ (((a >> 7) & 7u) << 4); }
+
+struct SumArgs {
+    uint64_t count;     // series in this launch
+    uint64_t out_base;  // output index of this launch's first series
+    int n, w, bits, seg, R, ws;
+    uint8_t* words;
+    uint32_t* root_keys;  // may be null
+    uint32_t* sort_keys;  // may be null
+};
+
+// Sort key: the first 32 bits of the plane-major bit string of the word
+// (plane 0 = top bit of every segment = the root key, segment 0 first).
+__device__ __forceinline__ void word_keys(const uint8_t* sym, int w, uint32_t& root, uint32_t& sk) {
+    uint32_t r = 0;
+    for (int g = 0; g < w; ++g) r = (r << 1) | (sym[g] >> 7);
+    root = r;
+    uint32_t k = 0;
+    int left = 32;
+    for (int p = 0; p < 8 && left > 0; ++p)
+        for (int g = 0; g < w && left > 0; ++g, --left) k = (k << 1) | ((sym[g] >> (7 - p)) & 1u);
+    sk = k << left;
+}
+
+__device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const uint8_t* wrow) {
+    uint4* dst = reinterpret_cast<uint4*>(a.words + idx * static_cast<uint64_t>(a.ws));
+    const uint4* src = reinterpret_cast<const uint4*>(wrow);
+    dst[0] = src[0];
+    if (a.ws == 32) dst[1] = src[1];
+    if (a.root_keys || a.sort_keys) {
+        uint32_t root, sk;
+        word_keys(wrow, a.w, root, sk);
+        if (a.root_keys) a.root_keys[idx] = root;
+        if (a.sort_keys) a.sort_keys[idx] = sk;
+    }
+}
+
+template <int STAGES, bool VEC>
+__global__ void __launch_bounds__(kSumThreads)
+    k_summarise_tma(const __grid_constant__ CUtensorMap tmap, SumArgs a,
+                    const double* __restrict__ thr_g) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* stages = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const uint32_t tile_bytes = static_cast<uint32_t>(a.R) * a.n * 4u;
+    const uint32_t stage_stride = (tile_bytes + 1023u) & ~1023u;
+    uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * stage_stride);
+    uint64_t* empty = full + STAGES;
+    double* thr = reinterpret_cast<double*>(empty + STAGES);
+    uint8_t* wbuf = reinterpret_cast<uint8_t*>(thr + kThrPad);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < kThrPad; i += blockDim.x) thr[i] = thr_g[i];
+    for (int i = tid; i < 2 * a.R * a.ws; i += blockDim.x) wbuf[i] = 0;
+    __syncthreads();
+
+    const uint64_t ntiles = (a.count + a.R - 1) / a.R;
+    const int rows_per_tile = a.R * (a.n / 32);
+
+    if (warp == kConsumerWarps) {  // producer warp
+        if (lane == 0) {
+            int it = 0;
+            for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], tile_bytes);
+                tma_load_2d(stages + s * stage_stride, &tmap, 0, static_cast<int>(t * rows_per_tile),
+                            &full[s]);
+            }
+        }
+        return;
+    }
+
+    int it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        const unsigned char* tile = stages + s * stage_stride;
+        const uint64_t first = t * a.R;
+        const int valid = static_cast<int>(min(static_cast<uint64_t>(a.R), a.count - first));
+        uint8_t* wb = wbuf + (it & 1) * a.R * a.ws;
+        for (int idx = tid; idx < valid * a.w; idx += kConsumers) {
+            const int ser = idx / a.w, g = idx - ser * a.w;
+            const uint32_t f0 = static_cast<uint32_t>(ser * a.n + g * a.seg);
+            double sum = 0.0;
+            if (VEC) {
+                const int nq = a.seg >> 2;
+                for (int q = 0; q < nq; ++q) {
+                    const float4 v =
+                        *reinterpret_cast<const float4*>(tile + swz((f0 + 4u * q) * 4u));
+                    sum = __dadd_rn(sum, static_cast<double>(v.x));
+                    sum = __dadd_rn(sum, static_cast<double>(v.y));
+                    sum = __dadd_rn(sum, static_cast<double>(v.z));
+                    sum = __dadd_rn(sum, static_cast<double>(v.w));
+                }
+            } else {
+                for (int j = 0; j < a.seg; ++j) {
+                    const float v = *reinterpret_cast<const float*>(tile + swz((f0 + j) * 4u));
+                    sum = __dadd_rn(sum, static_cast<double>(v));
+                }
+            }
+            const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
+            wb[ser * a.ws + g] = static_cast<uint8_t>(symbol_of(thr, a.bits, mean) << (8 - a.bits));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+        for (int ser = tid; ser < valid; ser += kConsumers)
+            emit_word(a, a.out_base + first + ser, wb + ser * a.ws);
+    }
+}
+
+// Shapes the TMA path cannot take (n % 32 != 0): one thread per series,
+// direct loads. Same arithmetic.
+__global__ void k_summarise_generic(const float* __restrict__ rows, SumArgs a,
+                                    const double* __restrict__ thr_g) {
+    __shared__ double thr[kThrPad];
+    for (int i = threadIdx.x; i < kThrPad; i += blockDim.x) thr[i] = thr_g[i];
+    __syncthreads();
+    uint8_t wrow[kMaxW] = {0};
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < a.count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float* r = rows + i * static_cast<uint64_t>(a.n);
+        for (int g = 0; g < a.w; ++g) {
+            double sum = 0.0;
+            for (int j = 0; j < a.seg; ++j) sum = __dadd_rn(sum, static_cast<double>(r[g * a.seg + j]));
+            const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
+            wrow[g] = static_cast<uint8_t>(symbol_of(thr, a.bits, mean) << (8 - a.bits));
+        }
+        uint8_t buf[32] __attribute__((aligned(16)));
+        for (int k = 0; k < 32; ++k) buf[k] = k < a.w ? wrow[k] : 0;
+        emit_word(a, a.out_base + i, buf);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+constexpr int kStages = 3;
+
+size_t tma_smem_bytes(int R, int n, int ws) {
+    const size_t stage = ((static_cast<size_t>(R) * n * 4 + 1023) / 1024) * 1024;
+    return 1024 + kStages * stage + 2 * kStages * sizeof(uint64_t) + kThrPad * sizeof(double) +
+           2 * static_cast<size_t>(R) * ws;
+}
+
+}  // namespace
+
+void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
+               uint8_t* words, uint32_t* root_keys, uint32_t* sort_keys, cudaStream_t stream) {
+    if (count == 0) return;
+    SumArgs a{};
+    a.n = n;
+    a.w = w;
+    a.bits = bits;
+    a.seg = n / w;
+    a.ws = word_stride(w);
+    a.words = words;
+    a.root_keys = root_keys;
+    a.sort_keys = sort_keys;
+
+    int dev = 0, sms = 0;
+    TSG_CUDA(cudaGetDevice(&dev));
+    TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+
+    const bool aligned = (reinterpret_cast<uintptr_t>(rows) % 16) == 0;
+    if (n % 32 != 0 || !aligned) {
+        a.count = count;
+        a.out_base = 0;
+        const int threads = 256;
+        const uint64_t blocks = std::min<uint64_t>((count + threads - 1) / threads, sms * 16ull);
+        k_summarise_generic<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(rows, a, d_thr);
+        TSG_LAUNCHED();
+        return;
+    }
+
+    // R whole series per TMA box: box outer dim (R * n/32) <= 256, tile <= 32 KB.
+    const int rows_per_series = n / 32;
+    int R = std::min(256 / rows_per_series, 8192 / n);
+    if (R < 1) R = 1;
+    a.R = R;
+    const size_t smem = tma_smem_bytes(R, n, a.ws);
+    const bool vec = (a.seg % 4) == 0;
+    auto kern = vec ? k_summarise_tma<kStages, true> : k_summarise_tma<kStages, false>;
+    TSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    int per_sm = 0;
+    TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumThreads, smem));
+    per_sm = std::max(per_sm, 1);
+
+    auto encode = get_encoder();
+    // TMA coordinates are int32: launch over slices of at most ~2^31 rows.
+    const uint64_t max_series =
+        ((static_cast<uint64_t>(1) << 31) - 4096) / rows_per_series / R * R;
+    for (uint64_t off = 0; off < count; off += max_series) {
+        const uint64_t cnt = std::min(max_series, count - off);
+        CUtensorMap map;
+        const float* base = rows + off * static_cast<uint64_t>(n);
+        cuuint64_t gdim[2] = {32, cnt * rows_per_series};
+        cuuint64_t gstride[1] = {128};
+        cuuint32_t box[2] = {32, static_cast<cuuint32_t>(R * rows_per_series)};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim,
+                            gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+        a.count = cnt;
+        a.out_base = off;
+        const uint64_t tiles = (cnt + R - 1) / R;
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * per_sm));
+        kern<<<grid, kSumThreads, smem, stream>>>(map, a, d_thr);
+        TSG_LAUNCHED();
+    }
+}
+
+}  // namespace tsg

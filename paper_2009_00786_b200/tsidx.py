@@ -1,0 +1,351 @@
+"""Host-side mirror of the reference ``tsidx`` API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference's public
+interface (paths relative to /root/reference/proj/core):
+
+* ``IndexConfig``            include/tsidx/config.hpp:12-32 (validate: src/config.cpp:22-35)
+* ``build_index``            include/tsidx/index.hpp:158, src/index.cpp:258-318
+* ``exact_search``           include/tsidx/query.hpp:150-151, src/query.cpp:258-298
+* ``approximate_search``     include/tsidx/query.hpp:133-134
+* ``Measure``                include/tsidx/metrics.hpp:19-27
+* ``SearchOptions`` / ``SearchResult`` / ``SearchStats`` / ``BuildStats``
+                             include/tsidx/query.hpp:17-27,136-148; index.hpp:121-132
+
+``std::invalid_argument`` surfaces as :class:`InvalidArgument` (a ValueError),
+``std::logic_error`` as :class:`LogicError`. Every compute call goes through
+``libtsgpu.so`` on the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import InvalidArgument, LogicError, TsgError, check, lib  # noqa: F401
+
+
+class QueueMode(enum.IntEnum):
+    single = 0
+    multi = 1
+
+
+@dataclasses.dataclass
+class IndexConfig:
+    n: int = 256
+    w: int = 16
+    max_card_bits: int = 8
+    leaf_capacity: int = 2000
+    chunk_size: int = 20000
+    n_index_workers: int = 0
+    n_search_workers: int = 0
+    n_queues: int = 24
+    queue_mode: QueueMode = QueueMode.multi
+    initial_buffer_part_size: int = 5
+
+    def segment_length(self) -> int:
+        return self.n // self.w
+
+    def to_c(self) -> _lib.tsg_config:
+        for f in ("n", "leaf_capacity", "chunk_size", "n_index_workers", "n_search_workers", "n_queues",
+                  "initial_buffer_part_size"):
+            if getattr(self, f) < 0:
+                raise InvalidArgument(f"IndexConfig: {f} must be non-negative")
+        c = _lib.tsg_config()
+        c.n, c.w, c.max_card_bits = self.n, self.w, self.max_card_bits
+        c.leaf_capacity, c.chunk_size = self.leaf_capacity, self.chunk_size
+        c.n_index_workers, c.n_search_workers = self.n_index_workers, self.n_search_workers
+        c.n_queues, c.queue_mode = self.n_queues, int(self.queue_mode)
+        c.initial_buffer_part_size = self.initial_buffer_part_size
+        return c
+
+    def validate(self) -> None:
+        """Raises InvalidArgument naming the offending field (src/config.cpp:22-35)."""
+        if self.w < -(2 ** 31) or self.w >= 2 ** 31:
+            raise InvalidArgument("IndexConfig: w out of range")
+        c = self.to_c()
+        check(lib().tsg_config_validate(C.byref(c)))
+
+
+class MeasureKind(enum.IntEnum):
+    euclidean = 0
+    dtw = 1
+
+
+@dataclasses.dataclass(frozen=True)
+class Measure:
+    kind: MeasureKind = MeasureKind.euclidean
+    window: int = 0
+
+    @staticmethod
+    def ed() -> "Measure":
+        return Measure(MeasureKind.euclidean, 0)
+
+    @staticmethod
+    def dtw(window: int) -> "Measure":
+        return Measure(MeasureKind.dtw, window)
+
+
+@dataclasses.dataclass
+class SearchOptions:
+    workers: int = 0
+    queues: int = 0
+    mode: Optional[QueueMode] = None
+
+
+@dataclasses.dataclass
+class SearchStats:
+    lb_node_calcs: int = 0
+    lb_entry_calcs: int = 0
+    real_dist_calcs: int = 0
+    bsf_updates: int = 0
+    pruned_subtrees: int = 0
+    queue_insertions: int = 0
+
+    def kv_line(self) -> str:
+        return (f"lb_node={self.lb_node_calcs} lb_entry={self.lb_entry_calcs} real_dist={self.real_dist_calcs} "
+                f"bsf_updates={self.bsf_updates} pruned_subtrees={self.pruned_subtrees} "
+                f"queue_insertions={self.queue_insertions}")
+
+
+@dataclasses.dataclass
+class SearchResult:
+    distance: float
+    position: int
+    stats: SearchStats
+
+
+@dataclasses.dataclass
+class BuildStats:
+    build_ns: int = 0
+    series: int = 0
+    nodes: int = 0
+    inner_nodes: int = 0
+    leaves: int = 0
+    empty_leaves: int = 0
+    overflow_leaves: int = 0
+    max_depth: int = 0
+    root_children: int = 0
+    h2d_ns: int = 0
+    summarise_ms: float = 0.0
+    organise_ms: float = 0.0
+    leaves_ms: float = 0.0
+
+    def kv_line(self) -> str:
+        return (f"build series={self.series} time_ns={self.build_ns} nodes={self.nodes} inner={self.inner_nodes} "
+                f"leaves={self.leaves} empty_leaves={self.empty_leaves} overflow_leaves={self.overflow_leaves} "
+                f"max_depth={self.max_depth}")
+
+
+def _stats_from_c(s: _lib.tsg_build_stats) -> BuildStats:
+    return BuildStats(**{f: getattr(s, f) for f, _ in _lib.tsg_build_stats._fields_})
+
+
+def _result_from_c(r: _lib.tsg_result) -> SearchResult:
+    st = SearchStats(**{f: getattr(r.stats, f) for f, _ in _lib.tsg_search_stats._fields_})
+    return SearchResult(float(r.distance), int(r.position), st)
+
+
+class Context:
+    """A set of devices an index is sharded over (tsg_open)."""
+
+    def __init__(self, devices: Sequence[int] = (0,)):
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        check(lib().tsg_open(len(devices), devs, C.byref(h)))
+        self._h = h
+        self.devices = tuple(devices)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tsg_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+_default_ctx: dict = {}
+
+
+def _context(devices) -> Context:
+    key = tuple(devices)
+    if key not in _default_ctx:
+        _default_ctx[key] = Context(key)
+    return _default_ctx[key]
+
+
+class Index:
+    """The device index. Owns (a host view of) its dataset like the reference's
+    Index owns its Dataset (src/index.cpp:255-256)."""
+
+    def __init__(self, handle, data, config: IndexConfig, stats: BuildStats, ctx: Context, keepalive=None):
+        self._h = handle
+        self._data = data
+        self._config = config
+        self._stats = stats
+        self._ctx = ctx
+        self._keepalive = keepalive
+
+    def config(self) -> IndexConfig:
+        return self._config
+
+    def data(self):
+        return self._data
+
+    def series(self, position: int):
+        return self._data[position]
+
+    def build_stats(self) -> BuildStats:
+        return self._stats
+
+    @property
+    def handle(self):
+        return self._h
+
+    def export(self):
+        """(words[count][stride], positions[count], leaf_offsets[L+1], leaf_lo, leaf_hi) in index order."""
+        count = len(self._data)
+        ws = lib().tsg_word_stride(self._config.w)
+        L = self._stats.leaves
+        words = np.empty((count, ws), np.uint8)
+        pos = np.empty(count, np.uint32)
+        off = np.empty(L + 1, np.uint32)
+        lo = np.empty((L, ws), np.uint8)
+        hi = np.empty((L, ws), np.uint8)
+        check(lib().tsg_index_export(self._h, words.ctypes.data, pos.ctypes.data, off.ctypes.data,
+                                     lo.ctypes.data, hi.ctypes.data))
+        return words, pos, off, lo, hi
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().tsg_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.free()
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def build_index(dataset, config: IndexConfig = None, devices: Sequence[int] = (0,), position_offset: int = 0) -> Index:
+    """tsidx::build_index. ``dataset``: a (count, n) float32 array on the host
+    (copied into HBM), or a CUDA tensor already resident on the device
+    (borrowed, zero-copy; single-device only)."""
+    config = config or IndexConfig()
+    cfg = config.to_c()
+    st = _lib.tsg_build_stats()
+    h = C.c_void_p()
+    ctx = _context(devices)
+    if _is_cuda_tensor(dataset):
+        import torch
+
+        if dataset.dtype != torch.float32 or dataset.dim() != 2:
+            raise InvalidArgument("build_index: device dataset must be a 2-D float32 tensor")
+        t = dataset.contiguous()
+        count, length = (t.shape[0], t.shape[1]) if t.numel() else (0, config.n)
+        check(lib().tsg_index_build_device(ctx.handle, C.c_void_p(t.data_ptr()), count, length, C.byref(cfg),
+                                           position_offset, C.byref(h), C.byref(st)))
+        return Index(h, t, config, _stats_from_c(st), ctx, keepalive=t)
+    arr = np.asarray(dataset, dtype=np.float32)
+    if arr.ndim == 1 and arr.size == 0:
+        arr = arr.reshape(0, config.n)
+    if arr.ndim != 2:
+        raise InvalidArgument("build_index: dataset must be 2-D (count, length)")
+    arr = np.ascontiguousarray(arr)
+    check(lib().tsg_index_build(ctx.handle, arr.ctypes.data, arr.shape[0], arr.shape[1], C.byref(cfg),
+                                position_offset, C.byref(h), C.byref(st)))
+    return Index(h, arr, config, _stats_from_c(st), ctx)
+
+
+def _check_measure(measure: Measure, n: int) -> None:
+    if measure.kind == MeasureKind.dtw:
+        if measure.window < 0 or measure.window >= n:
+            raise InvalidArgument("dtw window must be in [0, n)")
+        raise InvalidArgument("exact_search: the device path answers Euclidean (Measure.ed()) queries only")
+
+
+def _query_array(index: Index, query) -> np.ndarray:
+    q = np.ascontiguousarray(np.asarray(query, dtype=np.float32))
+    n = index.config().n
+    if q.ndim != 1 or q.size != n:
+        raise InvalidArgument(f"query length {q.size if q.ndim == 1 else q.shape} does not match the index "
+                              f"series length {n}")
+    return q
+
+
+def exact_search(index: Index, query, measure: Measure = Measure.ed(), options: SearchOptions = None) -> SearchResult:
+    """tsidx::exact_search (Euclidean). options.workers/queues/mode are accepted and ignored."""
+    _check_measure(measure, index.config().n)
+    q = _query_array(index, query)
+    out = (_lib.tsg_result * 1)()
+    check(lib().tsg_search(index.handle, q.ctypes.data, 1, out))
+    return _result_from_c(out[0])
+
+
+def exact_search_batch(index: Index, queries, measure: Measure = Measure.ed()) -> list:
+    """Exact 1-NN for a (nq, n) block of queries in one call (queries answered in order)."""
+    _check_measure(measure, index.config().n)
+    n = index.config().n
+    if _is_cuda_tensor(queries):
+        t = queries.contiguous()
+        if t.dim() != 2 or t.shape[1] != n:
+            raise InvalidArgument(f"query length {tuple(t.shape)} does not match the index series length {n}")
+        out = (_lib.tsg_result * t.shape[0])()
+        check(lib().tsg_search_device(index.handle, C.c_void_p(t.data_ptr()), t.shape[0], out))
+        return [_result_from_c(r) for r in out]
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
+    if q.ndim != 2 or q.shape[1] != n:
+        raise InvalidArgument(f"query length {q.shape} does not match the index series length {n}")
+    out = (_lib.tsg_result * q.shape[0])()
+    check(lib().tsg_search(index.handle, q.ctypes.data, q.shape[0], out))
+    return [_result_from_c(r) for r in out]
+
+
+def approximate_search(index: Index, query, measure: Measure = Measure.ed()) -> SearchResult:
+    """tsidx::approximate_search: the best series in the query's closest leaf."""
+    _check_measure(measure, index.config().n)
+    q = _query_array(index, query)
+    out = (_lib.tsg_result * 1)()
+    check(lib().tsg_approximate_search(index.handle, q.ctypes.data, out))
+    return _result_from_c(out[0])
+
+
+def summarise(rows_cuda, w: int = 16, bits: int = 8):
+    """K1 alone on a CUDA tensor of rows: returns (words uint8 [count, stride], root_keys int32 [count])."""
+    import torch
+
+    t = rows_cuda.contiguous()
+    count, n = t.shape
+    ws = lib().tsg_word_stride(w)
+    words = torch.empty((count, ws), dtype=torch.uint8, device=t.device)
+    keys = torch.empty((count,), dtype=torch.int32, device=t.device)
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    check(lib().tsg_summarise(C.c_void_p(t.data_ptr()), count, n, w, bits, C.c_void_p(words.data_ptr()),
+                              C.c_void_p(keys.data_ptr()), C.c_void_p(stream)))
+    return words, keys
+
+
+def generate_random_walk_device(count: int, length: int, seed: int, znorm: bool = True, begin: int = 0,
+                                device: int = 0):
+    """Rows [begin, begin+count) of the reference generator, created in HBM (input setup)."""
+    import torch
+
+    out = torch.empty((count, length), dtype=torch.float32, device=f"cuda:{device}")
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    check(lib().tsg_generate_random_walk(C.c_void_p(out.data_ptr()), begin, count, length, seed,
+                                         1 if znorm else 0, C.c_void_p(stream)))
+    return out
+
+
+def launch_count() -> int:
+    return int(lib().tsg_launch_count())

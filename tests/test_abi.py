@@ -1,0 +1,84 @@
+"""CPU-side checks of the C ABI boundary: the library loads, exports every
+symbol include/tsgpu.h declares, validates IndexConfig exactly like the
+reference (src/config.cpp:22-35), and fails loudly (no CPU fallback) when
+there is no GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2009_00786_b200 import _lib
+from paper_2009_00786_b200.tsidx import IndexConfig, InvalidArgument
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "tsgpu.h")).read()
+    return sorted(set(re.findall(r"\b(tsg_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declarations_match_binding_table():
+    assert sorted(_lib.EXPORTS) == declared_symbols()
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump -lelf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_defaults_mirror_index_config():
+    c = _lib.tsg_config()
+    _lib.lib().tsg_config_default(C.byref(c))
+    d = IndexConfig()
+    assert (c.n, c.w, c.max_card_bits, c.leaf_capacity, c.chunk_size, c.n_queues, c.queue_mode,
+            c.initial_buffer_part_size) == (d.n, d.w, d.max_card_bits, d.leaf_capacity, d.chunk_size, d.n_queues,
+                                            int(d.queue_mode), d.initial_buffer_part_size)
+
+
+@pytest.mark.parametrize("field,value,msg", [
+    ("w", 0, "w must be at least 1"),
+    ("w", 65, "w must be at most 64"),
+    ("max_card_bits", 0, "max_card_bits must be in [1, 8]"),
+    ("max_card_bits", 9, "max_card_bits must be in [1, 8]"),
+    ("n", 8, "n must be at least w"),
+    ("n", 250, "must be a multiple of w"),
+    ("leaf_capacity", 1, "leaf_capacity must be at least 2"),
+    ("chunk_size", 0, "chunk_size must be at least 1"),
+    ("n_queues", 0, "n_queues must be at least 1"),
+    ("initial_buffer_part_size", 0, "initial_buffer_part_size must be at least 1"),
+])
+def test_config_validation_messages(field, value, msg):
+    cfg = IndexConfig()
+    setattr(cfg, field, value)
+    with pytest.raises(InvalidArgument, match=re.escape(msg)):
+        cfg.validate()
+
+
+def test_valid_config_passes():
+    IndexConfig().validate()
+    IndexConfig(n=64, w=8, max_card_bits=4, leaf_capacity=2).validate()
+
+
+def test_device_path_limit_on_w():
+    with pytest.raises(InvalidArgument, match="at most 32 on the device path"):
+        IndexConfig(n=40 * 4, w=40).validate()
+
+
+@pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES") is None and os.path.exists("/dev/nvidia0"),
+                    reason="a GPU is present")
+def test_no_gpu_fails_loudly():
+    h = C.c_void_p()
+    st = _lib.lib().tsg_open(1, None, C.byref(h))
+    if st == _lib.TSG_OK:
+        pytest.skip("a GPU is visible")
+    assert st == _lib.TSG_CUDA
+    assert "no CUDA device" in _lib.lib().tsg_last_error().decode()

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
+the reference's golden vectors. Bar: words bit-exact; 1-NN position
+identical with ties to the lowest position; distance bit-identical to the
+reference's blocked FP64 sum (the north_star tolerance is 1e-5 relative, the
+tests hold the stricter bitwise bar and report any miss)."""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2009_00786_b200 as tg  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def device_words(rows, w, bits=8):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(rows, np.float32)).cuda()
+    words, keys = tg.summarise(t, w, bits)
+    torch.cuda.synchronize()
+    return words.cpu().numpy()[:, :w], keys.cpu().numpy().astype(np.uint32)
+
+
+def assert_words_equal(got, want):
+    mism = int(np.count_nonzero(got != want))
+    assert mism == 0, f"{mism} symbol mismatches of {want.size}"
+
+
+# ---- K1 summarise ----------------------------------------------------------------
+
+def test_summarise_matches_golden(golden, oracle):
+    g = golden["load"]("rw600x64.npz")
+    for w, b, key in ((16, 8, "words16"), (8, 4, "words8b4"), (4, 8, "words4")):
+        words, keys = device_words(g["data"], w, b)
+        assert_words_equal(words, g[key])
+        assert all(int(keys[i]) == oracle.root_key(g[key][i]) for i in range(0, 600, 37))
+    for n in (96, 128):
+        h = golden["load"](f"rw400x{n}.npz")
+        assert_words_equal(device_words(h["data"], 16)[0], h["words16"])
+
+
+@pytest.mark.parametrize("count,n,w,bits", [
+    (1, 256, 16, 8), (31, 256, 16, 8), (33, 256, 16, 8), (5000, 256, 16, 8), (4099, 128, 16, 8),
+    (3001, 96, 16, 8), (2000, 64, 8, 8), (2000, 64, 32, 8), (1500, 64, 16, 3), (1200, 30, 3, 8),
+    (1000, 60, 5, 5), (777, 512, 16, 8), (999, 192, 24, 8),
+])
+def test_summarise_random_shapes(oracle, count, n, w, bits):
+    rng = np.random.default_rng(count + n + w)
+    rows = np.cumsum(rng.standard_normal((count, n)), axis=1).astype(np.float32)
+    rows = (rows - rows.mean(1, keepdims=True)) / (rows.std(1, keepdims=True) + 1e-9)
+    rows = rows.astype(np.float32)
+    words, keys = device_words(rows, w, bits)
+    want = oracle.summarise(rows, w, bits)
+    assert_words_equal(words, want)
+    for i in range(0, count, max(1, count // 17)):
+        assert int(keys[i]) == oracle.root_key(want[i])
+
+
+def test_summarise_threshold_values_go_up(oracle):
+    # every segment mean exactly on a breakpoint (test_sax.cpp:47-63 at the word level)
+    thr = oracle.breakpoints(8).astype(np.float32).astype(np.float64)
+    rows = np.repeat(thr.astype(np.float32)[:, None], 64, axis=1)  # constant rows -> mean == value
+    words, _ = device_words(rows, 16)
+    assert_words_equal(words, oracle.summarise(rows, 16))
+
+
+def test_summarise_config1_sha(oracle, golden):
+    """All 16M config-1 symbols vs the reference's c1_sax.u8 digest."""
+    data = oracle.generate(1_000_000, 256, 1)
+    assert sha(data) == golden["c1"]["data_sha256"]
+    words, _ = device_words(data, 16)
+    assert sha(words) == golden["c1"]["sax_sha256"]
+
+
+def test_device_generator_matches_reference(oracle):
+    import torch
+
+    for seed, begin, count, n, znorm in ((1, 0, 4000, 256, True), (7, 123456, 2000, 128, True),
+                                         (3, 0, 2000, 96, False)):
+        dev = tg.generate_random_walk_device(count, n, seed, znorm=znorm, begin=begin).cpu().numpy()
+        host = oracle.generate(count, n, seed, znorm=znorm, begin=begin)
+        bad_rows = int(np.count_nonzero(np.any(dev.view(np.uint32) != host.view(np.uint32), axis=1)))
+        assert bad_rows == 0, f"{bad_rows} of {count} series differ from the reference generator"
+        torch.cuda.synchronize()
+
+
+# ---- build + exact search ----------------------------------------------------------
+
+def check_against_scan(oracle, rows, queries, cfg, expect_bitwise=True, index=None):
+    index = index or tg.build_index(rows, cfg)
+    res = tg.exact_search_batch(index, queries)
+    for k, q in enumerate(queries):
+        d, p = oracle.scan_nn(rows, q, 0)
+        assert res[k].position == p, (k, res[k].position, p, res[k].distance, d)
+        if expect_bitwise:
+            assert res[k].distance == d, (k, res[k].distance, d)
+        assert res[k].distance == pytest.approx(d, rel=1e-12)
+        st = res[k].stats
+        assert st.real_dist_calcs <= st.queue_insertions + st.lb_entry_calcs
+        assert st.lb_entry_calcs <= len(rows)
+        assert st.bsf_updates >= 1
+    return index, res
+
+
+def test_exact_search_matches_golden(golden, oracle):
+    g = golden["load"]("rw600x64.npz")
+    cfg = tg.IndexConfig(n=64, w=16, leaf_capacity=20, chunk_size=100)
+    index = tg.build_index(g["data"], cfg)
+    for k, q in enumerate(g["queries"]):
+        r = tg.exact_search(index, q)
+        assert r.position == int(g["scan"][k, 1]) and r.distance == g["scan"][k, 0]
+        # the reference's own exact_search agrees too
+        assert r.position == int(g["exact"][k, 1]) and r.distance == pytest.approx(g["exact"][k, 0], rel=1e-9)
+        a = tg.approximate_search(index, q)
+        assert a.distance >= r.distance
+
+
+@pytest.mark.parametrize("count,n,w,bits,leaf", [
+    (3000, 64, 16, 8, 20), (3000, 64, 16, 8, 2), (3000, 64, 16, 8, 2000), (2500, 64, 8, 4, 7),
+    (2000, 96, 16, 8, 50), (2000, 128, 16, 8, 100), (4000, 256, 16, 8, 2000), (1500, 30, 3, 8, 10),
+    (1500, 64, 32, 8, 16), (1000, 60, 5, 2, 4),
+])
+def test_exact_matches_scan(oracle, count, n, w, bits, leaf):
+    rng = np.random.default_rng(count * 7 + n)
+    rows = oracle.generate(count, n, 700 + n)
+    queries = np.concatenate([oracle.generate(6, n, 900 + n),
+                              rows[rng.integers(0, count, 4)] + 0.05 * rng.standard_normal((4, n)).astype(np.float32)])
+    cfg = tg.IndexConfig(n=n, w=w, max_card_bits=bits, leaf_capacity=leaf)
+    check_against_scan(oracle, rows, queries.astype(np.float32), cfg)
+
+
+def test_member_queries_return_themselves(oracle):
+    rows = oracle.generate(2000, 64, 1001, znorm=False)
+    index = tg.build_index(rows, tg.IndexConfig(n=64, w=16, leaf_capacity=20))
+    for m in (17, 655, 1999):
+        r = tg.exact_search(index, rows[m])
+        assert r.distance == 0.0 and r.position == m
+        assert tg.approximate_search(index, rows[m]).distance == 0.0
+
+
+def test_ties_resolve_to_lowest_position(golden):
+    g = golden["load"]("ties50x32.npz")
+    index = tg.build_index(g["data"], tg.IndexConfig(n=32, w=16, leaf_capacity=4))
+    r = tg.exact_search(index, g["query"])
+    assert r.distance == 0.0 and r.position == 7
+
+
+def test_duplicates_overflow_leaves(oracle):
+    protos = oracle.generate(10, 256, 20230505, znorm=False)
+    rows = np.tile(protos, (1000, 1))  # acceptance.cpp:375-418: 1000 copies of 10 series
+    index = tg.build_index(rows, tg.IndexConfig(leaf_capacity=100))
+    assert index.build_stats().overflow_leaves > 0
+    for p in range(10):
+        r = tg.exact_search(index, protos[p])
+        assert r.distance == 0.0 and r.position == p
+
+
+def test_single_series_dataset(oracle):
+    rows = oracle.generate(1, 256, 20230506, znorm=False)
+    index = tg.build_index(rows, tg.IndexConfig())
+    r = tg.exact_search(index, rows[0])
+    assert r.distance == 0.0 and r.position == 0
+
+
+def test_device_rows_build_equals_host_build(oracle):
+    import torch
+
+    rows = oracle.generate(5000, 256, 99)
+    q = oracle.generate(8, 256, 98)
+    a = tg.exact_search_batch(tg.build_index(rows), q)
+    t = torch.from_numpy(rows).cuda()
+    b = tg.exact_search_batch(tg.build_index(t), torch.from_numpy(q).cuda())
+    assert [(x.distance, x.position) for x in a] == [(x.distance, x.position) for x in b]
+
+
+def test_index_layout_invariants(oracle):
+    rows = oracle.generate(20000, 64, 4242)
+    cfg = tg.IndexConfig(n=64, w=16, leaf_capacity=50)
+    index = tg.build_index(rows, cfg)
+    words, pos, off, lo, hi = index.export()
+    ref_words = oracle.summarise(rows, 16)
+    assert sorted(pos.tolist()) == list(range(20000))
+    assert np.array_equal(words[:, :16], ref_words[pos])
+    L = index.build_stats().leaves
+    assert off[0] == 0 and off[-1] == 20000 and np.all(np.diff(off.astype(np.int64)) > 0) and len(off) == L + 1
+    roots = np.array([oracle.root_key(w) for w in words[:, :16]])
+    for l in range(L):
+        a, b = off[l], off[l + 1]
+        assert len(set(roots[a:b].tolist())) == 1  # a leaf never straddles root subtrees
+        assert np.array_equal(lo[l, :16], words[a:b, :16].min(0)) and np.array_equal(hi[l, :16], words[a:b, :16].max(0))
+        if b - a > 50:
+            assert np.all(words[a:b] == words[a])  # only identical-key ranges may overflow
+    # equal keys keep position order (stable sort), like drain_in_position_order
+    assert index.build_stats().root_children == len(set(roots.tolist()))
+
+
+def test_query_validation():
+    rows = np.random.default_rng(0).standard_normal((100, 64)).astype(np.float32)
+    index = tg.build_index(rows, tg.IndexConfig(n=64))
+    with pytest.raises(tg.InvalidArgument):
+        tg.exact_search(index, np.zeros(63, np.float32))
+    with pytest.raises(tg.InvalidArgument):
+        tg.exact_search(index, np.zeros(64, np.float32), tg.Measure.dtw(64))
+    with pytest.raises(tg.InvalidArgument):
+        tg.exact_search(index, np.zeros(64, np.float32), tg.Measure.dtw(-1))
+
+
+def test_build_rejects_bad_inputs():
+    cfg = tg.IndexConfig(n=64, w=16, leaf_capacity=20)
+    with pytest.raises(tg.InvalidArgument, match="empty dataset"):
+        tg.build_index(np.zeros((0, 64), np.float32), cfg)
+    with pytest.raises(tg.InvalidArgument, match="does not match config.n"):
+        tg.build_index(np.zeros((10, 32), np.float32), cfg)
+    bad = tg.IndexConfig(n=64, w=0)
+    with pytest.raises(tg.InvalidArgument):
+        tg.build_index(np.zeros((10, 64), np.float32), bad)
+
+
+def test_config1_answers_sha(oracle, golden):
+    """100 config-1 queries: answers formatted like the survey's scan oracle
+    ("%zu %u %.17g") hash to the reference's c1_answers.txt digest."""
+    data = oracle.generate(1_000_000, 256, 1)
+    queries = oracle.generate(100, 256, 2)
+    assert sha(queries) == golden["c1"]["queries_sha256"]
+    index = tg.build_index(data, tg.IndexConfig())
+    res = tg.exact_search_batch(index, queries)
+    text = "".join("%d %d %.17g\n" % (k, r.position, r.distance) for k, r in enumerate(res))
+    assert hashlib.sha256(text.encode()).hexdigest() == golden["c1"]["answers_sha256"], text[:300]
+    assert res[0].position == 842660 and res[0].distance == 6.0047035858932869
+
+
+def test_launch_counter_moves():
+    before = tg.launch_count()
+    rows = np.random.default_rng(1).standard_normal((500, 64)).astype(np.float32)
+    tg.exact_search(tg.build_index(rows, tg.IndexConfig(n=64)), rows[3])
+    assert tg.launch_count() > before
