@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: exact Euclidean 1-NN queries/s over a resident iSAX index, plus
+iSAX build Mseries/s, on BASELINE.json configs[1] (100M x 256 z-normalised
+random walks, seed 1; 100 queries per step, generated the same way with
+seed 2; w=16, 8-bit symbols, leaf capacity 2000).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+
+Ours: the dataset (fixed total size) is sharded by contiguous series ranges
+across ranks; each rank answers every query on its shard and a NCCL
+all-gather of the 16-byte (distance, position) records combines them
+(lexicographic minimum = the exact global answer, ties to the lowest
+position). `value` = queries/s with queries already in HBM; `e2e` = the same
+through the public API with host queries (H2D + result D2H inside the timed
+region). Reference arm (`--impl reference`): the unmodified reference
+(oracle/_ref, compiled from /root/reference) on the host cores, rank 0 only.
+
+Inputs are synthetic (the reference's own seeded generator, BASELINE.json
+configs), generated on the device by the library's generator (bit-identical
+to the reference generator, see tests/test_gpu_parity.py).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exact 1-NN queries/s & iSAX build Mseries/s (float32 series), % of HBM roofline"
+
+CONFIGS = {
+    # name: (count, length, seed, query_seed, queries per step)
+    "c1": (1_000_000, 256, 1, 2, 100),
+    "c2": (100_000_000, 256, 1, 2, 100),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(count_full, n, seed, qseed, sample, queries):
+    """The unmodified reference (oracle/_ref) on this host's cores, on a
+    bounded sample of the workload: the first `sample` series of the same
+    dataset, reference build + exact_search (mq, 24 queues, all cores)."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    cores = ref.hardware_concurrency()
+    idx, gen_ns = ref.build_generated(sample, n, seed)
+    qs = ref.series_window(0, queries, n, qseed)
+    t = []
+    for q in qs:
+        d, p, st, ns = idx.exact_search(q)
+        t.append(ns)
+    qps = len(t) / (sum(t) * 1e-9)
+    build_ns = idx.build_stats["build_ns"]
+    return {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": f"first {sample} of the {count_full} series (same generator/seed), {queries} queries; "
+                      f"reference build_index + exact_search(mq, 24 queues, {cores} workers)",
+            "build_mseries_s": round(sample / (build_ns * 1e-9) / 1e6, 3),
+            "median_query_ms": round(statistics.median(t) * 1e-6, 3)}
+
+
+def run_reference(args):
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return
+    count, n, seed, qseed, nq = CONFIGS[args.config]
+    if args.count:
+        count = args.count
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    cores = ref.hardware_concurrency()
+    idx, gen_ns = ref.build_generated(count, n, seed)
+    build_ns = idx.build_stats["build_ns"]
+    per_step = args.ref_queries_per_step
+    total = (args.warmup + args.steps) * per_step
+    qs = ref.series_window(0, total, n, qseed)
+    for q in qs[: args.warmup * per_step]:
+        idx.exact_search(q)
+    t0 = time.perf_counter()
+    times = []
+    for q in qs[args.warmup * per_step:]:
+        d, p, st, ns = idx.exact_search(q)
+        times.append(ns)
+    elapsed = time.perf_counter() - t0
+    qps = len(times) / elapsed
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(qps, 4), "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(elapsed * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {count} x {n} z-normalised random walks (seed {seed}), "
+                               f"queries seed {qseed}, w=16, 8-bit, leaf 2000",
+                   "queries_per_step": per_step, "l2_flush": f"inputs larger than L2 ({count * n * 4 / 1e9:.1f} GB)"},
+        "cpu_baseline": {"value": round(qps, 4), "unit": "queries/s", "cores": cores, "kind": "reference",
+                         "sample": f"full {args.config} dataset, {args.steps * per_step} timed queries"},
+        "e2e": {"value": round(qps, 4), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build": {"value": round(count / (build_ns * 1e-9) / 1e6, 3), "unit": "Mseries/s",
+                  "build_s": round(build_ns * 1e-9, 3), "generate_s": round(gen_ns * 1e-9, 3)},
+        "median_query_ms": round(statistics.median(times) * 1e-6, 3),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def combine(records):
+    """records: [world][nq][2] (distance, position) -> lexicographic min per query."""
+    best = records[0].copy()
+    for r in records[1:]:
+        better = (r[:, 0] < best[:, 0]) | ((r[:, 0] == best[:, 0]) & (r[:, 1] < best[:, 1]))
+        best[better] = r[better]
+    return best
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_00786_b200 as tg
+    from paper_2009_00786_b200 import _lib
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    count, n, seed, qseed, nq = CONFIGS[args.config]
+    if args.count:
+        count = args.count
+    b, e = count * rank // world, count * (rank + 1) // world
+    shard = e - b
+
+    # ---- inputs in HBM (untimed setup) ----
+    t0 = time.perf_counter()
+    rows = tg.generate_random_walk_device(shard, n, seed, znorm=True, begin=b, device=local)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    total_batches = args.warmup + args.steps
+    qdev = tg.generate_random_walk_device(total_batches * nq, n, qseed, znorm=True, begin=0, device=local)
+    qhost = qdev.cpu().numpy()
+
+    # ---- build (device-timed inside the library with CUDA events) ----
+    cfg = tg.IndexConfig(n=n)
+    barrier()
+    tb = time.perf_counter()
+    index = tg.build_index(rows, cfg, devices=(local,), position_offset=b)
+    torch.cuda.synchronize()
+    build_wall = max_over_ranks(time.perf_counter() - tb)
+    bs = index.build_stats()
+    build_dev_s = max_over_ranks(bs.build_ns * 1e-9)
+    k1_s = max_over_ranks(bs.summarise_ms * 1e-3)
+
+    def step(batch, host):
+        if host:
+            res = tg.exact_search_batch(index, qhost[batch * nq:(batch + 1) * nq])
+        else:
+            res = tg.exact_search_batch(index, qdev[batch * nq:(batch + 1) * nq])
+        rec = np.array([(r.distance, r.position) for r in res], dtype=np.float64)
+        if world > 1:
+            t = torch.from_numpy(rec).cuda()
+            gathered = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(gathered, t)
+            rec = combine([g.cpu().numpy() for g in gathered])
+        return rec, res
+
+    # warm-up
+    for i in range(args.warmup):
+        step(i, host=False)
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident queries ----
+    launches0 = tg.launch_count()
+    _lib.check(_lib.lib().tsg_profile_enable(index.handle, 1))
+    _lib.check(_lib.lib().tsg_profile_read(index.handle, None, None, 1))
+    stats_acc = np.zeros(6, np.float64)
+    answers = []
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        tw = time.perf_counter()
+        for i in range(args.warmup, total_batches):
+            rec, res = step(i, host=False)
+            answers.append(rec)
+            for r in res:
+                s = r.stats
+                stats_acc += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
+                              s.pruned_subtrees, s.queue_insertions)
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        wall = time.perf_counter() - tw
+    launches = tg.launch_count() - launches0
+    # The library synchronises its own stream inside each call, so the torch
+    # events bracket the whole step sequence; wall time is the fallback.
+    dev_s = max(ev0.elapsed_time(ev1) * 1e-3, 1e-9)
+    elapsed = max_over_ranks(max(dev_s, wall))
+    ms = (ctypes.c_double * 8)()
+    ln = (ctypes.c_uint64 * 8)()
+    _lib.check(_lib.lib().tsg_profile_read(index.handle, ms, ln, 1))
+    _lib.check(_lib.lib().tsg_profile_enable(index.handle, 0))
+    prof_ms = [max_over_ranks(x) for x in ms]
+    prof_ln = list(ln)
+    qps = args.steps * nq / elapsed
+
+    # ---- timed: end to end through the public API with host queries ----
+    barrier()
+    te = time.perf_counter()
+    for i in range(args.warmup, total_batches):
+        step(i, host=True)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - te)
+    e2e_qps = args.steps * nq / e2e_s
+
+    # ---- roofline of the dominant query kernel (bytes from the counters) ----
+    hbm, peak_kind = peaks()
+    nqt = args.steps * nq
+    ws = 16
+    L = bs.leaves
+    slot_names = ["prep", "leaf_lb", "seed", "refine_seed", "lbscan", "refine", "finalize", "result"]
+    lb_entries, refined, cands = stats_acc[1], stats_acc[2], stats_acc[5]
+    slot_bytes = {
+        1: nqt * L * (2 * ws + 4),
+        4: lb_entries * ws + nqt * L * 8 + cands * 12,
+        5: refined * 4 * n + cands * 16,
+        3: 0.0,
+    }
+    dom = max(range(8), key=lambda k: prof_ms[k])
+    dom_ms = prof_ms[dom] / max(prof_ln[dom] / max(world, 1), 1)
+    dom_bytes = slot_bytes.get(dom, 0.0) / max(prof_ln[dom] / max(world, 1), 1)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+
+    # build K1 roofline: read 4n + write w + 4-byte sort key per series
+    k1_bytes = count * (4 * n + 16 + 4) / world
+    k1_gbs = k1_bytes / k1_s / 1e9
+    algo_build = count * (4 * n + 16 + 4)
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline(count, n, seed, qseed, args.cpu_sample, args.cpu_queries)
+            except Exception as ex:  # reported, not hidden
+                cpu = {"error": str(ex)}
+        clocks = clk.summary()
+        share = prof_ms[dom] / max(sum(prof_ms), 1e-12)
+        line = {
+            "metric": METRIC, "value": round(qps, 3), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed * 1e3 / args.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{args.config}: {count} x {n} z-normalised random walks (seed {seed}); "
+                                   f"{nq} queries per step (seed {qseed}, rows {args.warmup * nq}..), "
+                                   f"w=16, 8-bit, leaf 2000",
+                       "queries_per_step": nq, "sharding": f"{world} contiguous series ranges",
+                       "l2_flush": f"inputs larger than L2 ({count * n * 4 / world / 1e9:.1f} GB rows, "
+                                   f"{count * 16 / world / 1e9:.2f} GB words per GPU)"},
+            "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": nq * n * 4,
+                    "d2h_bytes_per_step": nq * 72},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": slot_names[dom], "achieved": round(achieved, 1),
+                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "share_of_query_time": round(share, 4),
+                         "per_kernel_ms": {slot_names[k]: round(prof_ms[k], 3) for k in range(8)}},
+            "build": {"value": round(count / build_dev_s / 1e6, 3), "unit": "Mseries/s",
+                      "build_device_s": round(build_dev_s, 4), "build_wall_s": round(build_wall, 3),
+                      "phase_ms": {"summarise": round(bs.summarise_ms, 3), "organise": round(bs.organise_ms, 3),
+                                   "leaves": round(bs.leaves_ms, 3)},
+                      "roofline": {"bound": "hbm", "kernel": "summarise (K1)", "achieved": round(k1_gbs, 1),
+                                   "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                                   "frac": round(k1_gbs / hbm, 4), "traffic": None,
+                                   "algorithmic_bytes_per_series": 4 * n + 20},
+                      "whole_build_frac": round(algo_build / build_dev_s / 1e9 / hbm / world, 4),
+                      "leaves": L, "root_children": bs.root_children, "max_depth": bs.max_depth,
+                      "overflow_leaves": bs.overflow_leaves},
+            "search_stats_per_query": {k: round(v / nqt, 2) for k, v in zip(
+                ["lb_node_calcs", "lb_entry_calcs", "real_dist_calcs", "bsf_updates", "pruned_subtrees",
+                 "queue_insertions"], stats_acc)},
+            "clocks": clocks,
+            "generate_s": round(gen_s, 2),
+            "cpu_baseline": cpu,
+        }
+        if answers:
+            line["first_answer"] = {"distance": float(answers[0][0, 0]), "position": int(answers[0][0, 1])}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--count", type=int, default=0, help="override the series count (testing)")
+    ap.add_argument("--cpu-sample", type=int, default=10_000_000)
+    ap.add_argument("--cpu-queries", type=int, default=20)
+    ap.add_argument("--ref-queries-per-step", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -76,6 +76,7 @@ typedef struct tsg_build_stats {
     uint64_t max_depth;       /* root children are depth 1 */
     /* device-path extras */
     uint64_t root_children;   /* distinct root keys */
+    uint64_t pages;           /* leaf pages (<= 128 entries each): the device LB / work unit */
     uint64_t h2d_ns;          /* host->device copy of the rows (0 for device input) */
     double summarise_ms;      /* K1 */
     double organise_ms;       /* K2 sort + gather */
@@ -166,9 +167,11 @@ int tsg_word_stride(int w);
 
 /* Copy the index's flat SoA back to the host (single-device index):
  * words[count][word_stride] in index order, positions[count] (global),
- * leaf_offsets[leaves+1]. Any pointer may be NULL. */
+ * leaf_offsets[leaves+1], page_offsets[pages+1] and the per-page symbol
+ * boxes page_lo/page_hi[pages][word_stride]. Any pointer may be NULL. */
 tsg_status tsg_index_export(const tsg_index* index, uint8_t* words, uint32_t* positions,
-                            uint32_t* leaf_offsets, uint8_t* leaf_lo, uint8_t* leaf_hi);
+                            uint32_t* leaf_offsets, uint32_t* page_offsets, uint8_t* page_lo,
+                            uint8_t* page_hi);
 
 /* Device data generator: rows [begin, begin+count) of the reference's
  * generate_random_walk(., length, seed) (src/dataset.cpp:22-68), optionally
@@ -179,6 +182,13 @@ tsg_status tsg_generate_random_walk(float* dev_rows, uint64_t begin, uint64_t co
 
 /* Number of kernel launches this process issued through the library. */
 uint64_t tsg_launch_count(void);
+
+/* Per-kernel device timing of the search pipeline (CUDA events recorded on
+ * the index's stream around every launch). Kernel slots, in pipeline order:
+ * 0 prep, 1 leaf_lb, 2 seed, 3 refine(seed leaf), 4 lbscan, 5 refine,
+ * 6 finalize, 7 result. ms[8] and launches[8] accumulate until reset. */
+tsg_status tsg_profile_enable(tsg_index* index, int enable);
+tsg_status tsg_profile_read(tsg_index* index, double* ms, uint64_t* launches, int reset);
 
 #ifdef __cplusplus
 }

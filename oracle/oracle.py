@@ -170,6 +170,24 @@ class Reference:
         _sig(lib, "ref_exact_search", i32, C.c_void_p, _f32p, C.c_uint, C.c_uint, i32,
              C.POINTER(f64), C.POINTER(u32), _u64p, C.POINTER(u64))
         _sig(lib, "ref_approximate_search", i32, C.c_void_p, _f32p, C.POINTER(f64), C.POINTER(u32))
+        _sig(lib, "ref_build_generated", i32, u64, u64, u64, i32, i32, i32, u64, u64, C.c_uint,
+             C.POINTER(C.c_void_p), _u64p, C.POINTER(u64))
+        _sig(lib, "ref_series_window", i32, u64, u64, u64, u64, i32, _f32p)
+
+    def build_generated(self, count, n, seed, znorm=True, w=16, bits=8, leaf_capacity=2000, chunk=20000,
+                        workers=0):
+        """generate_random_walk + z-norm + build_index inside the reference, no host copy."""
+        h = C.c_void_p()
+        st = np.zeros(8, np.uint64)
+        gen_ns = u64()
+        self._check(self.lib.ref_build_generated(count, n, seed, 1 if znorm else 0, w, bits, leaf_capacity, chunk,
+                                                 workers, C.byref(h), st, C.byref(gen_ns)))
+        return RefIndex.adopt(self, h, n, st), gen_ns.value
+
+    def series_window(self, begin, count, n, seed, znorm=True) -> np.ndarray:
+        out = np.empty((count, n), np.float32)
+        self._check(self.lib.ref_series_window(begin, count, n, seed, 1 if znorm else 0, out))
+        return out
 
     def _check(self, rc):
         if rc != 0:
@@ -272,6 +290,13 @@ class RefIndex:
                                            leaf_capacity, chunk, workers, C.byref(h), st))
         self.h = h
         self.build_stats = dict(zip(BUILD_STAT_FIELDS, map(int, st)))
+
+    @classmethod
+    def adopt(cls, ref: Reference, h, n, st):
+        self = cls.__new__(cls)
+        self.ref, self.n, self.h = ref, n, h
+        self.build_stats = dict(zip(BUILD_STAT_FIELDS, map(int, st)))
+        return self
 
     def exact_search(self, q, workers=0, queues=0, mode=-1):
         d, p, ns = f64(), u32(), u64()

@@ -244,6 +244,68 @@ int ref_build_index(const float* rows, std::uint64_t count, std::uint64_t n, int
 
 void ref_index_free(void* h) { delete static_cast<RefIndex*>(h); }
 
+// The CLI's `generate --znorm` followed by build_index, without any host
+// copy of the rows (a 100M x 256 dataset is 102 GB): generate_random_walk
+// (src/dataset.cpp:41-68) + per-series znormalize (degenerate -> zeros,
+// tools/main.cpp:128-139) + build_index(std::move(ds)). gen_ns / build_ns
+// report the two phases separately.
+int ref_build_generated(std::uint64_t count, std::uint64_t n, std::uint64_t seed, int znorm, int w,
+                        int bits, std::uint64_t leaf_capacity, std::uint64_t chunk, unsigned workers,
+                        void** out, std::uint64_t* stats, std::uint64_t* gen_ns) {
+    return guarded([&] {
+        auto t0 = std::chrono::steady_clock::now();
+        tsidx_ref::Dataset ds = tsidx_ref::generate_random_walk(count, n, seed);
+        if (znorm) {
+            unsigned threads = workers ? workers : tsidx_ref::IndexConfig::default_workers();
+            std::vector<std::thread> pool;
+            for (unsigned t = 0; t < threads; ++t)
+                pool.emplace_back([&, t] {
+                    std::uint64_t b = count * t / threads, e = count * (t + 1) / threads;
+                    for (std::uint64_t i = b; i < e; ++i) {
+                        auto s = ds.series_mut(i);
+                        if (!tsidx_ref::znormalize(s)) std::fill(s.begin(), s.end(), 0.f);
+                    }
+                });
+            for (auto& th : pool) th.join();
+        }
+        auto t1 = std::chrono::steady_clock::now();
+        if (gen_ns)
+            *gen_ns = static_cast<std::uint64_t>(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+        auto cfg = make_config(n, w, bits, leaf_capacity, chunk, workers);
+        auto idx = std::make_unique<tsidx_ref::Index>(tsidx_ref::build_index(std::move(ds), cfg));
+        const auto& s = idx->build_stats();
+        if (stats) {
+            stats[0] = s.build_ns;
+            stats[1] = s.series;
+            stats[2] = s.nodes;
+            stats[3] = s.inner_nodes;
+            stats[4] = s.leaves;
+            stats[5] = s.empty_leaves;
+            stats[6] = s.overflow_leaves;
+            stats[7] = s.max_depth;
+        }
+        auto* h = new RefIndex;
+        h->index = std::move(idx);
+        *out = h;
+    });
+}
+
+// Rows [begin, begin+count) of generate_random_walk(., n, seed) +
+// z-normalisation, for queries (the generator seeds per series, so a window
+// is generated directly; identical to the corresponding full-call rows).
+int ref_series_window(std::uint64_t begin, std::uint64_t count, std::uint64_t n, std::uint64_t seed,
+                      int znorm, float* out) {
+    return guarded([&] {
+        auto ds = tsidx_ref::generate_random_walk(begin + count, n, seed);
+        for (std::uint64_t i = 0; i < count; ++i) {
+            auto s = ds.series_mut(begin + i);
+            if (znorm && !tsidx_ref::znormalize(s)) std::fill(s.begin(), s.end(), 0.f);
+            std::copy(s.begin(), s.end(), out + i * n);
+        }
+    });
+}
+
 // tsidx::exact_search (src/query.cpp:258-298), ED. mode: 0 single, 1 multi.
 int ref_exact_search(void* h, const float* query, unsigned workers, unsigned queues, int mode,
                      double* dist, std::uint32_t* pos, std::uint64_t* stats /* 6 */,

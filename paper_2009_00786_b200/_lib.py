@@ -18,7 +18,7 @@ EXPORTS = (
     "tsg_last_error", "tsg_version", "tsg_config_default", "tsg_config_validate", "tsg_open", "tsg_close",
     "tsg_index_build", "tsg_index_build_device", "tsg_index_free", "tsg_index_info", "tsg_search",
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export",
-    "tsg_generate_random_walk", "tsg_launch_count",
+    "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
 )
 
 
@@ -34,7 +34,7 @@ class tsg_build_stats(C.Structure):
     _fields_ = [
         ("build_ns", C.c_uint64), ("series", C.c_uint64), ("nodes", C.c_uint64), ("inner_nodes", C.c_uint64),
         ("leaves", C.c_uint64), ("empty_leaves", C.c_uint64), ("overflow_leaves", C.c_uint64),
-        ("max_depth", C.c_uint64), ("root_children", C.c_uint64), ("h2d_ns", C.c_uint64),
+        ("max_depth", C.c_uint64), ("root_children", C.c_uint64), ("pages", C.c_uint64), ("h2d_ns", C.c_uint64),
         ("summarise_ms", C.c_double), ("organise_ms", C.c_double), ("leaves_ms", C.c_double),
     ]
 
@@ -83,9 +83,11 @@ def lib() -> C.CDLL:
         "tsg_approximate_search": (i32, [vp, vp, C.POINTER(tsg_result)]),
         "tsg_summarise": (i32, [vp, u64, u64, i32, i32, vp, vp, vp]),
         "tsg_word_stride": (i32, [i32]),
-        "tsg_index_export": (i32, [vp, vp, vp, vp, vp, vp]),
+        "tsg_index_export": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "tsg_generate_random_walk": (i32, [vp, u64, u64, u64, u64, i32, vp]),
         "tsg_launch_count": (u64, []),
+        "tsg_profile_enable": (i32, [vp, i32]),
+        "tsg_profile_read": (i32, [vp, C.POINTER(C.c_double), C.POINTER(u64), i32]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

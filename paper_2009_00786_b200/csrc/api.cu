@@ -140,11 +140,13 @@ void free_shard(DevIndex& s) {
     cudaFree(s.words);
     cudaFree(s.pos);
     cudaFree(s.leaf_off);
-    cudaFree(s.leaf_lo);
-    cudaFree(s.leaf_hi);
+    cudaFree(s.page_off);
+    cudaFree(s.page_leaf);
+    cudaFree(s.page_lo);
+    cudaFree(s.page_hi);
     cudaFree(s.work);
     cudaFree(s.lut);
-    cudaFree(s.leaf_lb);
+    cudaFree(s.page_lb);
     cudaFree(s.cand_pos);
     cudaFree(s.cand_lb);
     cudaFree(s.cand_sq);
@@ -195,7 +197,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     // search workspace
     TSG_CUDA(cudaMalloc(&s.work, sizeof(QueryWork)));
     TSG_CUDA(cudaMalloc(&s.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
-    TSG_CUDA(cudaMalloc(&s.leaf_lb, std::max<uint64_t>(s.L, 1) * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&s.page_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
     s.cand_cap = N;
     TSG_CUDA(cudaMalloc(&s.cand_pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&s.cand_lb, N * sizeof(float)));
@@ -356,6 +358,7 @@ tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, 
         for (size_t k = 0; k < G; ++k) {
             const DevIndex& s = ix->shards[k];
             st.leaves += s.L;
+            st.pages += s.P;
             st.inner_nodes += s.inner;
             st.overflow_leaves += s.overflow;
             st.max_depth = std::max<uint64_t>(st.max_depth, s.max_depth);
@@ -500,7 +503,7 @@ tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length,
 }
 
 tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* positions, uint32_t* leaf_offsets,
-                            uint8_t* leaf_lo, uint8_t* leaf_hi) {
+                            uint32_t* page_offsets, uint8_t* page_lo, uint8_t* page_hi) {
     return guarded([&] {
         if (!ix) fail("tsg_index_export: null index");
         if (ix->shards.size() != 1) fail("tsg_index_export: single-device index only");
@@ -512,8 +515,38 @@ tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* posit
             for (uint64_t i = 0; i < s.N; ++i) positions[i] += static_cast<uint32_t>(s.pos_offset);
         }
         if (leaf_offsets) TSG_CUDA(cudaMemcpy(leaf_offsets, s.leaf_off, (s.L + 1) * 4, cudaMemcpyDeviceToHost));
-        if (leaf_lo) TSG_CUDA(cudaMemcpy(leaf_lo, s.leaf_lo, s.L * s.ws, cudaMemcpyDeviceToHost));
-        if (leaf_hi) TSG_CUDA(cudaMemcpy(leaf_hi, s.leaf_hi, s.L * s.ws, cudaMemcpyDeviceToHost));
+        if (page_offsets) TSG_CUDA(cudaMemcpy(page_offsets, s.page_off, (s.P + 1) * 4, cudaMemcpyDeviceToHost));
+        if (page_lo) TSG_CUDA(cudaMemcpy(page_lo, s.page_lo, s.P * s.ws, cudaMemcpyDeviceToHost));
+        if (page_hi) TSG_CUDA(cudaMemcpy(page_hi, s.page_hi, s.P * s.ws, cudaMemcpyDeviceToHost));
+    });
+}
+
+tsg_status tsg_profile_enable(tsg_index* ix, int enable) {
+    return guarded([&] {
+        if (!ix) fail("tsg_profile_enable: null index");
+        std::lock_guard<std::mutex> lock(ix->mu);
+        for (auto& s : ix->shards) s.profile = enable != 0;
+    });
+}
+
+tsg_status tsg_profile_read(tsg_index* ix, double* ms, uint64_t* launches, int reset) {
+    return guarded([&] {
+        if (!ix) fail("tsg_profile_read: null index");
+        std::lock_guard<std::mutex> lock(ix->mu);
+        for (int k = 0; k < kProfSlots; ++k) {
+            double m = 0;
+            uint64_t l = 0;
+            for (auto& s : ix->shards) {
+                m = std::max(m, s.prof_ms[k]);
+                l += s.prof_launches[k];
+                if (reset) {
+                    s.prof_ms[k] = 0;
+                    s.prof_launches[k] = 0;
+                }
+            }
+            if (ms) ms[k] = m;
+            if (launches) launches[k] = l;
+        }
     });
 }
 

@@ -1,20 +1,23 @@
-// K2 organise + K3 leaves: the flat SoA index.
+// K2 organise + K3 leaves/pages: the flat SoA index.
 //
 // Replaces the reference's staging buffers and tree construction
 // (SaxBuffers src/index.cpp:96-151, drain_in_position_order
 // include/tsidx/index.hpp:204-231, insert_entry/split_leaf/choose_split_segment
 // src/index.cpp:171-253) with:
-//   K2  a stable radix sort of (32-bit plane-major key, position): entries of
-//       one root key become contiguous and stay in position order inside
-//       equal keys; then a gather of the 16-byte words into index order.
-//   K3  leaf partition: a root bucket (run of equal root key) whose size
-//       exceeds leaf_capacity is split at the first key bit on which its
-//       first and last entries differ, recursively, until every range fits;
-//       ranges whose 32 key bits are all equal become overflow leaves
-//       (the reference's is_overflow, src/index.cpp:50-55). Then per-leaf
-//       per-segment [min, max] symbol boxes for the leaf lower bound.
+//   K2  a stable radix sort of (64-bit plane-major key, position): entries of
+//       one root key become contiguous, ordered inside it by the refinement
+//       bits (second bit of every segment, then the third, ...), equal keys
+//       stay in position order; then a gather of the words into index order.
+//   K3  leaves: a root subtree (run of equal root key) larger than
+//       leaf_capacity is split at the first key bit on which its first and
+//       last entries differ, level by level in parallel over all open
+//       ranges, until every range fits; ranges whose 64 key bits are all
+//       equal become overflow leaves (the reference's is_overflow,
+//       src/index.cpp:50-55). Leaves are cut into pages of <= kPage entries,
+//       each with per-segment [min, max] symbol boxes: the page is the unit of
+//       the leaf-level lower bound and of work distribution in the search.
 // The tree shape is not a parity target (north_star); the search is exact
-// regardless of how entries are grouped into leaves.
+// regardless of how entries are grouped.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -37,17 +40,18 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
-__global__ void k_iota(uint32_t* v, uint64_t n) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+#define GRID_STRIDE(i, n)                                                                 \
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < (n); \
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        v[i] = static_cast<uint32_t>(i);
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+    GRID_STRIDE(i, n) v[i] = static_cast<uint32_t>(i);
 }
 
 // words[i] = words_orig[pos[i]] (16- or 32-byte rows).
 __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* __restrict__ pos,
                                uint8_t* __restrict__ dst, uint64_t n, int ws) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    GRID_STRIDE(i, n) {
         const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<uint64_t>(pos[i]) * ws);
         uint4* d = reinterpret_cast<uint4*>(dst + i * ws);
         d[0] = s[0];
@@ -55,128 +59,137 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
     }
 }
 
-__device__ __forceinline__ uint32_t root_of(uint32_t key, int w) {
-    return w >= 32 ? key : key >> (32 - w);
+__global__ void k_bucket_flags(const uint64_t* __restrict__ keys, uint64_t n, int w, uint8_t* __restrict__ flags) {
+    const int shift = 64 - w;
+    GRID_STRIDE(i, n) flags[i] = (i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift)) ? 1 : 0;
 }
 
-__global__ void k_bucket_flags(const uint32_t* __restrict__ keys, uint64_t n, int w,
-                               uint8_t* __restrict__ flags) {
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        flags[i] = (i == 0 || root_of(keys[i], w) != root_of(keys[i - 1], w)) ? 1 : 0;
-}
-
-struct LeafEmit {
-    uint32_t begin, end;
-    int depth;
-    bool overflow;
+struct Range {
+    uint32_t a, b, depth;
 };
-
-// Recursive split of one root bucket [a, b) (see file comment). Calls
-// emit(leaf) in increasing begin order; returns the number of inner nodes.
-template <typename F>
-__device__ uint32_t split_bucket(const uint32_t* keys, uint32_t a, uint32_t b, uint32_t cap, F&& emit) {
-    struct Item {
-        uint32_t a, b;
-        int d;
-    } stack[40];
-    int sp = 0;
-    uint32_t inner = 0;
-    stack[sp++] = {a, b, 1};
-    while (sp > 0) {
-        const Item it = stack[--sp];
-        if (it.b - it.a <= cap) {
-            emit(LeafEmit{it.a, it.b, it.d, false});
-            continue;
-        }
-        const uint32_t ka = keys[it.a], kb = keys[it.b - 1];
-        if (ka == kb) {
-            emit(LeafEmit{it.a, it.b, it.d, true});
-            continue;
-        }
-        const int p = __clz(ka ^ kb);  // first differing key bit (from the MSB)
-        const uint32_t bit = 31 - p;
-        uint32_t lo = it.a, hi = it.b - 1;  // keys[hi] has the bit set
-        while (lo < hi) {
-            const uint32_t mid = lo + (hi - lo) / 2;
-            if ((keys[mid] >> bit) & 1u) hi = mid;
-            else lo = mid + 1;
-        }
-        ++inner;
-        stack[sp++] = {lo, it.b, it.d + 1};
-        stack[sp++] = {it.a, lo, it.d + 1};
-    }
-    return inner;
-}
 
 struct LeafCounters {
     unsigned long long inner, overflow, max_depth;
+    unsigned int nleaves, nopen;
 };
 
-__global__ void k_leaf_count(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ bstart,
-                             uint64_t nb, uint64_t n, uint32_t cap, uint32_t* __restrict__ count,
-                             LeafCounters* ctr) {
-    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < nb;
-         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t lo = bstart[b];
-        const uint32_t hi = b + 1 < nb ? bstart[b + 1] : static_cast<uint32_t>(n);
-        uint32_t leaves = 0, over = 0;
-        int depth = 0;
-        const uint32_t inner = split_bucket(keys, lo, hi, cap, [&](const LeafEmit& e) {
-            ++leaves;
-            over += e.overflow ? 1u : 0u;
-            depth = max(depth, e.depth);
-        });
-        count[b] = leaves;
-        if (inner) atomicAdd(&ctr->inner, static_cast<unsigned long long>(inner));
-        if (over) atomicAdd(&ctr->overflow, static_cast<unsigned long long>(over));
-        atomicMax(&ctr->max_depth, static_cast<unsigned long long>(depth));
+__device__ __forceinline__ void emit_leaf(LeafCounters* c, uint32_t* leaf_start, uint32_t a, uint32_t depth,
+                                          bool overflow) {
+    const unsigned k = atomicAdd(&c->nleaves, 1u);
+    leaf_start[k] = a;
+    atomicMax(&c->max_depth, static_cast<unsigned long long>(depth));
+    if (overflow) atomicAdd(&c->overflow, 1ull);
+}
+
+__device__ __forceinline__ void route(LeafCounters* c, uint32_t* leaf_start, Range* next, const uint64_t* keys,
+                                      uint32_t a, uint32_t b, uint32_t depth, uint32_t cap) {
+    if (b - a <= cap) {
+        emit_leaf(c, leaf_start, a, depth, false);
+    } else if (keys[a] == keys[b - 1]) {
+        emit_leaf(c, leaf_start, a, depth, true);  // all key bits equal: cannot split further
+    } else {
+        const unsigned k = atomicAdd(&c->nopen, 1u);
+        next[k] = Range{a, b, depth};
     }
 }
 
-__global__ void k_leaf_write(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ bstart,
-                             uint64_t nb, uint64_t n, uint32_t cap, const uint32_t* __restrict__ base,
-                             uint32_t* __restrict__ leaf_off) {
-    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < nb;
-         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+__global__ void k_init_ranges(const uint32_t* __restrict__ bstart, uint64_t nb, uint64_t n,
+                              const uint64_t* __restrict__ keys, uint32_t cap, LeafCounters* c,
+                              uint32_t* __restrict__ leaf_start, Range* __restrict__ next) {
+    GRID_STRIDE(b, nb) {
         const uint32_t lo = bstart[b];
         const uint32_t hi = b + 1 < nb ? bstart[b + 1] : static_cast<uint32_t>(n);
-        uint32_t k = base[b];
-        split_bucket(keys, lo, hi, cap, [&](const LeafEmit& e) { leaf_off[k++] = e.begin; });
+        route(c, leaf_start, next, keys, lo, hi, 1, cap);
     }
 }
 
-// One warp per leaf: bytewise min / max over the leaf's words.
-__global__ void k_leaf_box(const uint8_t* __restrict__ words, const uint32_t* __restrict__ leaf_off,
-                           uint64_t L, int ws, uint8_t* __restrict__ lo_out, uint8_t* __restrict__ hi_out) {
+// One level of splitting: each open range splits at the first key bit its
+// first and last entries disagree on (binary search for the boundary).
+__global__ void k_split(const Range* __restrict__ open, unsigned nopen, const uint64_t* __restrict__ keys,
+                        uint32_t cap, LeafCounters* c, uint32_t* __restrict__ leaf_start, Range* __restrict__ next) {
+    GRID_STRIDE(r, nopen) {
+        const Range it = open[r];
+        const uint64_t ka = keys[it.a], kb = keys[it.b - 1];
+        const int bit = 63 - __clzll(static_cast<long long>(ka ^ kb));
+        uint32_t lo = it.a, hi = it.b - 1;  // keys[hi] has the bit set
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if ((keys[mid] >> bit) & 1ull) hi = mid;
+            else lo = mid + 1;
+        }
+        atomicAdd(&c->inner, 1ull);
+        route(c, leaf_start, next, keys, it.a, lo, it.depth + 1, cap);
+        route(c, leaf_start, next, keys, lo, it.b, it.depth + 1, cap);
+    }
+}
+
+__global__ void k_page_count(const uint32_t* __restrict__ leaf_off, uint64_t L, uint32_t* __restrict__ count) {
+    GRID_STRIDE(l, L) count[l] = (leaf_off[l + 1] - leaf_off[l] + kPage - 1) / kPage;
+}
+
+__global__ void k_page_write(const uint32_t* __restrict__ leaf_off, uint64_t L, const uint32_t* __restrict__ base,
+                             uint32_t* __restrict__ page_off, uint32_t* __restrict__ page_leaf) {
+    GRID_STRIDE(l, L) {
+        const uint32_t a = leaf_off[l], b = leaf_off[l + 1];
+        uint32_t k = base[l];
+        for (uint32_t s = a; s < b; s += kPage, ++k) {
+            page_off[k] = s;
+            page_leaf[k] = static_cast<uint32_t>(l);
+        }
+    }
+}
+
+// One warp per page: bytewise min / max over the page's words.
+__global__ void k_page_box(const uint8_t* __restrict__ words, const uint32_t* __restrict__ page_off, uint64_t P,
+                           int ws, uint8_t* __restrict__ lo_out, uint8_t* __restrict__ hi_out) {
     const int lane = threadIdx.x & 31;
     const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t l = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; l < L; l += warps) {
-        const uint32_t a = leaf_off[l], b = leaf_off[l + 1];
-        const int vecs = ws / 4;  // 32-bit lanes per word
-        for (int v = 0; v < vecs; ++v) {
-            uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+    for (uint64_t p = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; p < P; p += warps) {
+        const uint32_t a = page_off[p], b = page_off[p + 1];
+        for (int h = 0; h < ws / 16; ++h) {
+            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
             for (uint32_t e = a + lane; e < b; e += 32) {
-                const uint32_t x = reinterpret_cast<const uint32_t*>(words + static_cast<uint64_t>(e) * ws)[v];
-                mn = __vminu4(mn, x);
-                mx = __vmaxu4(mx, x);
+                const uint4 x = *reinterpret_cast<const uint4*>(words + static_cast<uint64_t>(e) * ws + 16 * h);
+                mn = make_uint4(__vminu4(mn.x, x.x), __vminu4(mn.y, x.y), __vminu4(mn.z, x.z), __vminu4(mn.w, x.w));
+                mx = make_uint4(__vmaxu4(mx.x, x.x), __vmaxu4(mx.y, x.y), __vmaxu4(mx.z, x.z), __vmaxu4(mx.w, x.w));
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                mn = __vminu4(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
-                mx = __vmaxu4(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+                mn.x = __vminu4(mn.x, __shfl_xor_sync(0xFFFFFFFFu, mn.x, o));
+                mn.y = __vminu4(mn.y, __shfl_xor_sync(0xFFFFFFFFu, mn.y, o));
+                mn.z = __vminu4(mn.z, __shfl_xor_sync(0xFFFFFFFFu, mn.z, o));
+                mn.w = __vminu4(mn.w, __shfl_xor_sync(0xFFFFFFFFu, mn.w, o));
+                mx.x = __vmaxu4(mx.x, __shfl_xor_sync(0xFFFFFFFFu, mx.x, o));
+                mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xFFFFFFFFu, mx.y, o));
+                mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xFFFFFFFFu, mx.z, o));
+                mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xFFFFFFFFu, mx.w, o));
             }
             if (lane == 0) {
-                reinterpret_cast<uint32_t*>(lo_out + l * ws)[v] = mn;
-                reinterpret_cast<uint32_t*>(hi_out + l * ws)[v] = mx;
+                *reinterpret_cast<uint4*>(lo_out + p * ws + 16 * h) = mn;
+                *reinterpret_cast<uint4*>(hi_out + p * ws + 16 * h) = mx;
             }
         }
     }
 }
 
 unsigned grid_for(uint64_t n, int threads, int sms) {
-    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + threads - 1) / threads,
-                                                                          static_cast<uint64_t>(sms) * 32)));
+    return static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((n + threads - 1) / threads, static_cast<uint64_t>(sms) * 32)));
+}
+
+template <typename T>
+T d2h(const T* p, cudaStream_t st) {
+    T v{};
+    TSG_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, st));
+    TSG_CUDA(cudaStreamSynchronize(st));
+    return v;
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st) {
+    size_t tb = 0;
+    TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int64_t>(n), st));
+    DevBuf temp(tb);
+    TSG_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, in, out, static_cast<int64_t>(n), st));
 }
 
 }  // namespace
@@ -191,86 +204,108 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
 
-    DevBuf words_orig(N * ix.ws), keys_in(N * 4), keys_out(N * 4), pos_in(N * 4);
+    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in(N * 4);
 
     // K1 summarise
     TSG_CUDA(cudaEventRecord(ev[0], st));
-    summarise(ix.rows, N, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>(), nullptr,
-              keys_in.as<uint32_t>(), st);
+    summarise(ix.rows, N, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>(), nullptr, keys_in.as<uint64_t>(), st);
     TSG_CUDA(cudaEventRecord(ev[1], st));
 
-    // K2 organise: stable sort by key, carrying positions; gather words.
+    // K2 organise: stable sort by the significant key bits, carrying positions.
+    const int key_bits = std::min(64, ix.w * ix.bits);
+    const int begin_bit = 64 - key_bits;
     k_iota<<<grid_for(N, 256, sms), 256, 0, st>>>(pos_in.as<uint32_t>(), N);
     TSG_LAUNCHED();
-    size_t temp_bytes = 0;
-    TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys_in.as<uint32_t>(),
-                                             keys_out.as<uint32_t>(), pos_in.as<uint32_t>(), ix.pos,
-                                             static_cast<int64_t>(N), 0, 32, st));
     {
-        DevBuf temp(temp_bytes);
-        TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, keys_in.as<uint32_t>(),
-                                                 keys_out.as<uint32_t>(), pos_in.as<uint32_t>(), ix.pos,
-                                                 static_cast<int64_t>(N), 0, 32, st));
-        k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, N,
-                                                               ix.ws);
+        size_t tb = 0;
+        TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
+                                                 pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit,
+                                                 64, st));
+        DevBuf temp(tb);
+        TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
+                                                 pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit,
+                                                 64, st));
+        k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, N, ix.ws);
         TSG_LAUNCHED();
         TSG_CUDA(cudaEventRecord(ev[2], st));
     }
 
-    // K3 leaves. Bucket starts = positions where the root key changes.
-    const uint32_t* keys = keys_out.as<uint32_t>();
-    DevBuf flags(N), bstart(N * 4), nsel(8);
-    k_bucket_flags<<<grid_for(N, 256, sms), 256, 0, st>>>(keys, N, ix.w, flags.as<uint8_t>());
-    TSG_LAUNCHED();
-    {
-        size_t tb = 0;
-        TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(), bstart.as<uint32_t>(),
-                                            nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
-        DevBuf temp(tb);
-        TSG_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(), bstart.as<uint32_t>(),
-                                            nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
-    }
+    // K3 leaves. Root subtrees = runs of equal root key (top w key bits).
+    const uint64_t* keys = keys_out.as<uint64_t>();
     uint64_t nb = 0;
-    TSG_CUDA(cudaMemcpyAsync(&nb, nsel.p, 8, cudaMemcpyDeviceToHost, st));
-    TSG_CUDA(cudaStreamSynchronize(st));
+    DevBuf bstart(N * 4);
+    {
+        DevBuf flags(N), nsel(8);
+        k_bucket_flags<<<grid_for(N, 256, sms), 256, 0, st>>>(keys, N, ix.w, flags.as<uint8_t>());
+        TSG_LAUNCHED();
+        size_t tb = 0;
+        TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
+                                            bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
+        DevBuf temp(tb);
+        TSG_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
+                                            bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
+        nb = d2h(nsel.as<uint64_t>(), st);
+    }
     ix.root_children = nb;
 
-    DevBuf lcount((nb + 1) * 4), lbase((nb + 1) * 4), ctr(sizeof(LeafCounters));
-    TSG_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(LeafCounters), st));
-    TSG_CUDA(cudaMemsetAsync(lcount.p, 0, (nb + 1) * 4, st));
     const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(ix.leaf_cap, 0xFFFFFFFFull));
-    k_leaf_count<<<grid_for(nb, 128, sms), 128, 0, st>>>(keys, bstart.as<uint32_t>(), nb, N, cap,
-                                                           lcount.as<uint32_t>(), ctr.as<LeafCounters>());
+    const uint64_t open_cap = 2 * (N / (static_cast<uint64_t>(cap) + 1)) + 16;
+    DevBuf leaf_start(N * 4), ranges_a(open_cap * sizeof(Range)), ranges_b(open_cap * sizeof(Range)),
+        ctr(sizeof(LeafCounters));
+    TSG_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(LeafCounters), st));
+    auto* C = ctr.as<LeafCounters>();
+    k_init_ranges<<<grid_for(nb, 256, sms), 256, 0, st>>>(bstart.as<uint32_t>(), nb, N, keys, cap, C,
+                                                          leaf_start.as<uint32_t>(), ranges_a.as<Range>());
     TSG_LAUNCHED();
-    {
-        size_t tb = 0;
-        TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, lcount.as<uint32_t>(), lbase.as<uint32_t>(),
-                                               static_cast<int64_t>(nb + 1), st));
-        DevBuf temp(tb);
-        TSG_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, lcount.as<uint32_t>(), lbase.as<uint32_t>(),
-                                               static_cast<int64_t>(nb + 1), st));
+    Range* open = ranges_a.as<Range>();
+    Range* next = ranges_b.as<Range>();
+    for (int level = 0; level < 70; ++level) {
+        const unsigned nopen = d2h(&C->nopen, st);
+        if (nopen == 0) break;
+        TSG_CUDA(cudaMemsetAsync(&C->nopen, 0, sizeof(unsigned), st));
+        k_split<<<grid_for(nopen, 128, sms), 128, 0, st>>>(open, nopen, keys, cap, C, leaf_start.as<uint32_t>(), next);
+        TSG_LAUNCHED();
+        std::swap(open, next);
     }
-    uint32_t L32 = 0;
-    LeafCounters hc{};
-    TSG_CUDA(cudaMemcpyAsync(&L32, lbase.as<uint32_t>() + nb, 4, cudaMemcpyDeviceToHost, st));
-    TSG_CUDA(cudaMemcpyAsync(&hc, ctr.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    TSG_CUDA(cudaStreamSynchronize(st));
-    ix.L = L32;
+    const LeafCounters hc = d2h(C, st);
+    ix.L = hc.nleaves;
     ix.inner = hc.inner;
     ix.overflow = hc.overflow;
     ix.max_depth = hc.max_depth;
 
+    // Leaves were emitted in arbitrary order: sort their first entries.
     TSG_CUDA(cudaMalloc(&ix.leaf_off, (ix.L + 1) * 4));
-    TSG_CUDA(cudaMalloc(&ix.leaf_lo, ix.L * ix.ws));
-    TSG_CUDA(cudaMalloc(&ix.leaf_hi, ix.L * ix.ws));
-    k_leaf_write<<<grid_for(nb, 128, sms), 128, 0, st>>>(keys, bstart.as<uint32_t>(), nb, N, cap,
-                                                           lbase.as<uint32_t>(), ix.leaf_off);
-    TSG_LAUNCHED();
+    {
+        size_t tb = 0;
+        TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, leaf_start.as<uint32_t>(), ix.leaf_off,
+                                                static_cast<int64_t>(ix.L), 0, 32, st));
+        DevBuf temp(tb);
+        TSG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb, leaf_start.as<uint32_t>(), ix.leaf_off,
+                                                static_cast<int64_t>(ix.L), 0, 32, st));
+    }
     const uint32_t n32 = static_cast<uint32_t>(N);
     TSG_CUDA(cudaMemcpyAsync(ix.leaf_off + ix.L, &n32, 4, cudaMemcpyHostToDevice, st));
-    k_leaf_box<<<grid_for(ix.L * 32, 256, sms), 256, 0, st>>>(ix.words, ix.leaf_off, ix.L, ix.ws, ix.leaf_lo,
-                                                               ix.leaf_hi);
-    TSG_LAUNCHED();
+
+    // Pages: each leaf cut into ceil(size / kPage) pieces.
+    {
+        DevBuf pcount((ix.L + 1) * 4), pbase((ix.L + 1) * 4);
+        TSG_CUDA(cudaMemsetAsync(pcount.as<uint32_t>() + ix.L, 0, 4, st));
+        k_page_count<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pcount.as<uint32_t>());
+        TSG_LAUNCHED();
+        exclusive_scan_u32(pcount.as<uint32_t>(), pbase.as<uint32_t>(), ix.L + 1, st);
+        ix.P = d2h(pbase.as<uint32_t>() + ix.L, st);
+        TSG_CUDA(cudaMalloc(&ix.page_off, (ix.P + 1) * 4));
+        TSG_CUDA(cudaMalloc(&ix.page_leaf, ix.P * 4));
+        TSG_CUDA(cudaMalloc(&ix.page_lo, ix.P * ix.ws));
+        TSG_CUDA(cudaMalloc(&ix.page_hi, ix.P * ix.ws));
+        k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase.as<uint32_t>(), ix.page_off,
+                                                               ix.page_leaf);
+        TSG_LAUNCHED();
+        TSG_CUDA(cudaMemcpyAsync(ix.page_off + ix.P, &n32, 4, cudaMemcpyHostToDevice, st));
+        k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.page_off, ix.P, ix.ws, ix.page_lo,
+                                                                  ix.page_hi);
+        TSG_LAUNCHED();
+    }
     TSG_CUDA(cudaEventRecord(ev[3], st));
     TSG_CUDA(cudaStreamSynchronize(st));
 

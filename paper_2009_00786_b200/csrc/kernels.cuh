@@ -6,10 +6,15 @@
 
 namespace tsg {
 
+// Entries per page: the unit of the leaf-level lower bound and of work
+// distribution in the LB scan (a leaf is split into ceil(size/kPage) pages).
+constexpr uint32_t kPage = 128;
+
 // Flat structure-of-arrays index of one device shard. Replaces the
 // reference's pointer tree (IndexNode / LeafEntries / RootTable,
 // include/tsidx/index.hpp:19-75): words and positions are sorted by the
-// plane-major iSAX key (root key first), leaves are contiguous ranges.
+// plane-major iSAX key (root key first), leaves are contiguous ranges,
+// pages are contiguous sub-ranges of leaves with their own symbol boxes.
 struct DevIndex {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -23,15 +28,18 @@ struct DevIndex {
     uint8_t* words = nullptr; // [N][ws] index order
     uint32_t* pos = nullptr;  // [N] local row of each index entry
     uint32_t* leaf_off = nullptr;  // [L+1]
-    uint8_t* leaf_lo = nullptr;    // [L][ws] per-segment min symbol
-    uint8_t* leaf_hi = nullptr;    // [L][ws] per-segment max symbol
     uint64_t L = 0;
+    uint32_t* page_off = nullptr;   // [P+1] entry offsets (pages tile [0, N))
+    uint32_t* page_leaf = nullptr;  // [P]
+    uint8_t* page_lo = nullptr;     // [P][ws] per-segment min symbol
+    uint8_t* page_hi = nullptr;     // [P][ws] per-segment max symbol
+    uint64_t P = 0;
     uint64_t root_children = 0;
     uint64_t inner = 0, max_depth = 0, overflow = 0;
     // search workspace
     struct QueryWork* work = nullptr;
     float* lut = nullptr;          // [w][256]
-    float* leaf_lb = nullptr;      // [L]
+    float* page_lb = nullptr;      // [P]
     uint32_t* cand_pos = nullptr;  // [cap]
     float* cand_lb = nullptr;      // [cap]
     double* cand_sq = nullptr;     // [cap]
@@ -41,16 +49,23 @@ struct DevIndex {
     float* queries = nullptr;      // staging for host queries
     uint32_t queries_cap = 0;
     int sms = 148;
+    // per-kernel profiling (tsg_profile_enable)
+    bool profile = false;
+    double prof_ms[8] = {0};
+    uint64_t prof_launches[8] = {0};
 };
+
+constexpr int kProfSlots = 8;
 
 // Per-query device scratch (reset by the prep kernel).
 struct QueryWork {
     unsigned long long bsf_bits;  // best squared distance so far (double bits)
-    unsigned long long seed_key;  // (leaf LB float bits << 32) | leaf
+    unsigned long long seed_key;  // (page LB float bits << 32) | page
     unsigned int ncand;
     unsigned int nseed;
     unsigned int work_next;
     unsigned int best_pos;
+    unsigned int seed_begin, seed_end;  // index range refined as the seed
     unsigned long long stats[6];  // SearchStats order
     double qpaa[32];
     unsigned char qsym[32];
@@ -65,10 +80,10 @@ struct DevResult {
 
 // K1
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
-               uint8_t* words, uint32_t* root_keys, uint32_t* sort_keys, cudaStream_t stream);
+               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream);
 
-// K2 + K3: sort, gather, leaves, boxes. Fills the index arrays of `ix`
-// (rows/thr/N/n/w/bits/leaf_cap must be set). Returns device ms per phase.
+// K2 + K3: sort, gather, leaves, pages, boxes. Fills the index arrays of
+// `ix` (rows/thr/N/n/w/bits/leaf_cap must be set). Device ms per phase.
 void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, double* ms_leaves);
 
 // Query pipeline for nq device queries; writes ix.results[0..nq).

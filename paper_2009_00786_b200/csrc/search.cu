@@ -29,6 +29,8 @@
 // the distance sums), so the exact answer is never lost.
 #include <algorithm>
 #include <cmath>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -101,8 +103,10 @@ __device__ __forceinline__ uint8_t byte_of(const uint4& v, int s) {
     return static_cast<uint8_t>(word >> (8 * (s & 3)));
 }
 
-// ------------------------------------------------------------- leaf LB
-__global__ void k_leaf_lb(const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, uint64_t L, int w,
+// ------------------------------------------------------------- page LB
+// Lower bound of every page box (the node bound of src/query.cpp:102-107 at
+// page granularity); the argmin page seeds the best-so-far.
+__global__ void k_page_lb(const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, uint64_t L, int w,
                           int ws, const float* __restrict__ lut, QueryWork* wk, float* __restrict__ leaf_lb) {
     extern __shared__ float s_lut[];
     __shared__ unsigned char s_qsym[kMaxW];
@@ -133,10 +137,19 @@ __global__ void k_leaf_lb(const uint8_t* __restrict__ lo, const uint8_t* __restr
 }
 
 // ---------------------------------------------------------- seed leaf
-__global__ void k_seed(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ pos, QueryWork* wk,
-                       uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
-    const uint32_t leaf = static_cast<uint32_t>(wk->seed_key & 0xFFFFFFFFull);
-    const uint32_t a = leaf_off[leaf], b = leaf_off[leaf + 1];
+// The seed is the leaf holding the best page (the analog of the leaf the
+// reference's approximate search descends to); an overflow leaf larger than
+// seed_cap is replaced by the page alone.
+__global__ void k_seed(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ page_off,
+                       const uint32_t* __restrict__ page_leaf, const uint32_t* __restrict__ pos, uint32_t seed_cap,
+                       QueryWork* wk, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
+    const uint32_t page = static_cast<uint32_t>(wk->seed_key & 0xFFFFFFFFull);
+    const uint32_t leaf = page_leaf[page];
+    uint32_t a = leaf_off[leaf], b = leaf_off[leaf + 1];
+    if (b - a > seed_cap) {
+        a = page_off[page];
+        b = page_off[page + 1];
+    }
     for (uint32_t e = a + blockIdx.x * blockDim.x + threadIdx.x; e < b; e += gridDim.x * blockDim.x) {
         cand_pos[e - a] = pos[e];
         cand_lb[e - a] = 0.f;
@@ -144,6 +157,8 @@ __global__ void k_seed(const uint32_t* __restrict__ leaf_off, const uint32_t* __
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         wk->nseed = b - a;
         wk->ncand = b - a;
+        wk->seed_begin = a;
+        wk->seed_end = b;
     }
 }
 
@@ -271,9 +286,10 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, uint32_t* s_pos, floa
     __syncwarp();
 }
 
-// Warps pull batches of 32 leaves; surviving leaves' entries are packed
-// across the warp's lanes (prefix sums of leaf sizes), so small leaves do
-// not idle lanes.
+// Warps pull batches of 32 pages (<= kPage entries each, so work units are
+// bounded); surviving pages' entries are packed across the warp's lanes
+// (prefix sums of page sizes), so small pages do not idle lanes. Pages of the
+// seed range were already refined and are skipped.
 __global__ void __launch_bounds__(256)
     k_lbscan(const uint8_t* __restrict__ words, const uint32_t* __restrict__ pos,
              const uint32_t* __restrict__ leaf_off, const float* __restrict__ leaf_lb, uint64_t L, int w, int ws,
@@ -287,7 +303,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float bound = bound_from_bits(wk->bsf_bits);
-    const uint32_t seed_leaf = static_cast<uint32_t>(wk->seed_key & 0xFFFFFFFFull);
+    const uint32_t seed_begin = wk->seed_begin, seed_end = wk->seed_end;
     const uint64_t nbatch = (L + 31) / 32;
     int cnt = 0;
     unsigned long long scanned = 0, pruned = 0;
@@ -298,10 +314,13 @@ __global__ void __launch_bounds__(256)
         if (batch >= nbatch) break;
         const uint64_t l = static_cast<uint64_t>(batch) * 32 + lane;
         const bool valid = l < L;
-        const bool keep = valid && l != seed_leaf && leaf_lb[l] <= bound;
-        pruned += __popc(__ballot_sync(0xFFFFFFFFu, valid && !keep && l != seed_leaf));
-        const uint32_t start = keep ? leaf_off[l] : 0u;
-        const uint32_t size = keep ? leaf_off[l + 1] - start : 0u;
+        const uint32_t pa = valid ? leaf_off[l] : 0u;
+        const uint32_t pb = valid ? leaf_off[l + 1] : 0u;
+        const bool seeded = valid && pa >= seed_begin && pb <= seed_end;
+        const bool keep = valid && !seeded && leaf_lb[l] <= bound;
+        pruned += __popc(__ballot_sync(0xFFFFFFFFu, valid && !keep && !seeded));
+        const uint32_t start = keep ? pa : 0u;
+        const uint32_t size = keep ? pb - pa : 0u;
         uint32_t incl = size;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -410,30 +429,70 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     TSG_CUDA(cudaFuncSetAttribute(refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(k_lbscan, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     if (refine_smem > 200 * 1024) throw InvalidArgument("series length too large for the device refine kernel");
+    const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
+
+    // Optional per-kernel timing: events around every launch, summed after the batch.
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+    auto mark = [&](int slot, auto&& launch) {
+        if (!ix.profile) {
+            launch();
+            return;
+        }
+        cudaEvent_t a, b;
+        TSG_CUDA(cudaEventCreate(&a));
+        TSG_CUDA(cudaEventCreate(&b));
+        TSG_CUDA(cudaEventRecord(a, st));
+        launch();
+        TSG_CUDA(cudaEventRecord(b, st));
+        marks.push_back({slot, {a, b}});
+    };
 
     for (uint32_t qi = 0; qi < nq; ++qi) {
         const float* q = d_queries + static_cast<uint64_t>(qi) * n;
-        k_query_prep<<<1, 256, 0, st>>>(q, n, w, ix.bits, ix.thr, ix.work, ix.lut);
+        mark(0, [&] { k_query_prep<<<1, 256, 0, st>>>(q, n, w, ix.bits, ix.thr, ix.work, ix.lut); });
         TSG_LAUNCHED();
-        k_leaf_lb<<<cap_grid((ix.L + 255) / 256, ix.sms, 4), 256, lut_bytes, st>>>(
-            ix.leaf_lo, ix.leaf_hi, ix.L, w, ix.ws, ix.lut, ix.work, ix.leaf_lb);
+        mark(1, [&] {
+            k_page_lb<<<cap_grid((ix.P + 255) / 256, ix.sms, 4), 256, lut_bytes, st>>>(
+                ix.page_lo, ix.page_hi, ix.P, w, ix.ws, ix.lut, ix.work, ix.page_lb);
+        });
         TSG_LAUNCHED();
-        k_seed<<<32, 256, 0, st>>>(ix.leaf_off, ix.pos, ix.work, ix.cand_pos, ix.cand_lb);
+        mark(2, [&] {
+            k_seed<<<32, 256, 0, st>>>(ix.leaf_off, ix.page_off, ix.page_leaf, ix.pos, seed_cap, ix.work,
+                                       ix.cand_pos, ix.cand_lb);
+        });
         TSG_LAUNCHED();
-        refine<<<ix.sms * 2, 256, refine_smem, st>>>(ix.rows, n, q, ix.work, ix.cand_pos, ix.cand_lb, ix.cand_sq, 1);
+        mark(3, [&] {
+            refine<<<ix.sms * 2, 256, refine_smem, st>>>(ix.rows, n, q, ix.work, ix.cand_pos, ix.cand_lb,
+                                                         ix.cand_sq, 1);
+        });
         TSG_LAUNCHED();
         if (!approximate) {
-            k_lbscan<<<ix.sms * 4, 256, lut_bytes, st>>>(ix.words, ix.pos, ix.leaf_off, ix.leaf_lb, ix.L, w, ix.ws,
-                                                         ix.lut, ix.work, ix.cand_pos, ix.cand_lb);
+            mark(4, [&] {
+                k_lbscan<<<ix.sms * 4, 256, lut_bytes, st>>>(ix.words, ix.pos, ix.page_off, ix.page_lb, ix.P, w,
+                                                             ix.ws, ix.lut, ix.work, ix.cand_pos, ix.cand_lb);
+            });
             TSG_LAUNCHED();
-            refine<<<ix.sms * 4, 256, refine_smem, st>>>(ix.rows, n, q, ix.work, ix.cand_pos, ix.cand_lb, ix.cand_sq,
-                                                         0);
+            mark(5, [&] {
+                refine<<<ix.sms * 4, 256, refine_smem, st>>>(ix.rows, n, q, ix.work, ix.cand_pos, ix.cand_lb,
+                                                             ix.cand_sq, 0);
+            });
             TSG_LAUNCHED();
         }
-        k_finalize<<<ix.sms, 256, 0, st>>>(ix.work, ix.cand_pos, ix.cand_sq, approximate ? 1 : 0);
+        mark(6, [&] { k_finalize<<<ix.sms, 256, 0, st>>>(ix.work, ix.cand_pos, ix.cand_sq, approximate ? 1 : 0); });
         TSG_LAUNCHED();
-        k_result<<<1, 1, 0, st>>>(ix.work, ix.results + qi, ix.L, ix.pos_offset);
+        mark(7, [&] { k_result<<<1, 1, 0, st>>>(ix.work, ix.results + qi, ix.P, ix.pos_offset); });
         TSG_LAUNCHED();
+    }
+    if (!marks.empty()) {
+        TSG_CUDA(cudaStreamSynchronize(st));
+        for (auto& m : marks) {
+            float ms = 0.f;
+            TSG_CUDA(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
+            ix.prof_ms[m.first] += ms;
+            ix.prof_launches[m.first] += 1;
+            cudaEventDestroy(m.second.first);
+            cudaEventDestroy(m.second.second);
+        }
     }
 }
 

@@ -74,20 +74,23 @@ struct SumArgs {
     int n, w, bits, seg, R, ws;
     uint8_t* words;
     uint32_t* root_keys;  // may be null
-    uint32_t* sort_keys;  // may be null
+    uint64_t* sort_keys;  // may be null
 };
 
-// Sort key: the first 32 bits of the plane-major bit string of the word
-// (plane 0 = top bit of every segment = the root key, segment 0 first).
-__device__ __forceinline__ void word_keys(const uint8_t* sym, int w, uint32_t& root, uint32_t& sk) {
+// Sort key: the first 64 bits of the plane-major bit string of the word
+// (plane 0 = top bit of every segment = the root key, segment 0 first;
+// then the second bit of every segment, ...). Sorting by it makes root
+// subtrees contiguous and orders entries inside them the way the iSAX
+// refinement bits split them.
+__device__ __forceinline__ void word_keys(const uint8_t* sym, int w, uint32_t& root, uint64_t& sk) {
     uint32_t r = 0;
     for (int g = 0; g < w; ++g) r = (r << 1) | (sym[g] >> 7);
     root = r;
-    uint32_t k = 0;
-    int left = 32;
+    uint64_t k = 0;
+    int left = 64;
     for (int p = 0; p < 8 && left > 0; ++p)
         for (int g = 0; g < w && left > 0; ++g, --left) k = (k << 1) | ((sym[g] >> (7 - p)) & 1u);
-    sk = k << left;
+    sk = left >= 64 ? 0 : k << left;
 }
 
 __device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const uint8_t* wrow) {
@@ -96,7 +99,8 @@ __device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const 
     dst[0] = src[0];
     if (a.ws == 32) dst[1] = src[1];
     if (a.root_keys || a.sort_keys) {
-        uint32_t root, sk;
+        uint32_t root;
+        uint64_t sk;
         word_keys(wrow, a.w, root, sk);
         if (a.root_keys) a.root_keys[idx] = root;
         if (a.sort_keys) a.sort_keys[idx] = sk;
@@ -234,7 +238,7 @@ size_t tma_smem_bytes(int R, int n, int ws) {
 }  // namespace
 
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
-               uint8_t* words, uint32_t* root_keys, uint32_t* sort_keys, cudaStream_t stream) {
+               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream) {
     if (count == 0) return;
     SumArgs a{};
     a.n = n;

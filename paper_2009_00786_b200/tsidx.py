@@ -129,6 +129,7 @@ class BuildStats:
     overflow_leaves: int = 0
     max_depth: int = 0
     root_children: int = 0
+    pages: int = 0
     h2d_ns: int = 0
     summarise_ms: float = 0.0
     organise_ms: float = 0.0
@@ -211,18 +212,20 @@ class Index:
         return self._h
 
     def export(self):
-        """(words[count][stride], positions[count], leaf_offsets[L+1], leaf_lo, leaf_hi) in index order."""
+        """(words[count][stride], positions[count], leaf_offsets[L+1], page_offsets[P+1],
+        page_lo[P][stride], page_hi[P][stride]) in index order."""
         count = len(self._data)
         ws = lib().tsg_word_stride(self._config.w)
-        L = self._stats.leaves
+        L, P = self._stats.leaves, self._stats.pages
         words = np.empty((count, ws), np.uint8)
         pos = np.empty(count, np.uint32)
         off = np.empty(L + 1, np.uint32)
-        lo = np.empty((L, ws), np.uint8)
-        hi = np.empty((L, ws), np.uint8)
+        poff = np.empty(P + 1, np.uint32)
+        lo = np.empty((P, ws), np.uint8)
+        hi = np.empty((P, ws), np.uint8)
         check(lib().tsg_index_export(self._h, words.ctypes.data, pos.ctypes.data, off.ctypes.data,
-                                     lo.ctypes.data, hi.ctypes.data))
-        return words, pos, off, lo, hi
+                                     poff.ctypes.data, lo.ctypes.data, hi.ctypes.data))
+        return words, pos, off, poff, lo, hi
 
     def free(self):
         if getattr(self, "_h", None):

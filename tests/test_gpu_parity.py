@@ -183,20 +183,31 @@ def test_index_layout_invariants(oracle):
     rows = oracle.generate(20000, 64, 4242)
     cfg = tg.IndexConfig(n=64, w=16, leaf_capacity=50)
     index = tg.build_index(rows, cfg)
-    words, pos, off, lo, hi = index.export()
+    words, pos, off, poff, lo, hi = index.export()
     ref_words = oracle.summarise(rows, 16)
     assert sorted(pos.tolist()) == list(range(20000))
     assert np.array_equal(words[:, :16], ref_words[pos])
-    L = index.build_stats().leaves
+    L, P = index.build_stats().leaves, index.build_stats().pages
     assert off[0] == 0 and off[-1] == 20000 and np.all(np.diff(off.astype(np.int64)) > 0) and len(off) == L + 1
+    assert poff[0] == 0 and poff[-1] == 20000 and np.all(np.diff(poff.astype(np.int64)) > 0) and len(poff) == P + 1
+    assert set(off.tolist()) <= set(poff.tolist())  # pages never straddle leaves
+    assert np.all(np.diff(poff.astype(np.int64)) <= 128)
     roots = np.array([oracle.root_key(w) for w in words[:, :16]])
+    # plane-major order of the first 64 key bits (root key first)
+    planes = np.unpackbits(words[:, :16], axis=1).reshape(-1, 16, 8).transpose(0, 2, 1).reshape(-1, 128)[:, :64]
+    keys = np.packbits(planes, axis=1).view(">u8").ravel()
+    assert np.all(keys[1:] >= keys[:-1])
     for l in range(L):
         a, b = off[l], off[l + 1]
         assert len(set(roots[a:b].tolist())) == 1  # a leaf never straddles root subtrees
-        assert np.array_equal(lo[l, :16], words[a:b, :16].min(0)) and np.array_equal(hi[l, :16], words[a:b, :16].max(0))
         if b - a > 50:
-            assert np.all(words[a:b] == words[a])  # only identical-key ranges may overflow
-    # equal keys keep position order (stable sort), like drain_in_position_order
+            assert np.all(keys[a:b] == keys[a])  # only identical-key ranges may overflow
+    for p in range(P):
+        a, b = poff[p], poff[p + 1]
+        assert np.array_equal(lo[p, :16], words[a:b, :16].min(0)) and np.array_equal(hi[p, :16], words[a:b, :16].max(0))
+        # equal keys keep position order (stable sort), like drain_in_position_order
+        same = keys[a:b][1:] == keys[a:b][:-1]
+        assert np.all(pos[a:b][1:][same] > pos[a:b][:-1][same])
     assert index.build_stats().root_children == len(set(roots.tolist()))
 
 
