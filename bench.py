@@ -173,21 +173,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def combine(records):
-    """records: [world][nq][2] (distance, position) -> lexicographic min per query."""
-    best = records[0].copy()
-    for r in records[1:]:
-        better = (r[:, 0] < best[:, 0]) | ((r[:, 0] == best[:, 0]) & (r[:, 1] < best[:, 1]))
-        best[better] = r[better]
-    return best
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2009_00786_b200 as tg
     from paper_2009_00786_b200 import _lib
+    from paper_2009_00786_b200.shard import allgather_merge, shard_range
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
@@ -208,7 +200,7 @@ def run_ours(args):
     count, n, seed, qseed, nq = CONFIGS[args.config]
     if args.count:
         count = args.count
-    b, e = count * rank // world, count * (rank + 1) // world
+    b, e = shard_range(count, rank, world)
     shard = e - b
 
     # ---- inputs in HBM (untimed setup) ----
@@ -237,86 +229,82 @@ def run_ours(args):
         else:
             res = tg.exact_search_batch(index, qdev[batch * nq:(batch + 1) * nq])
         rec = np.array([(r.distance, r.position) for r in res], dtype=np.float64)
-        if world > 1:
-            t = torch.from_numpy(rec).cuda()
-            gathered = [torch.empty_like(t) for _ in range(world)]
-            dist.all_gather(gathered, t)
-            rec = combine([g.cpu().numpy() for g in gathered])
+        if world > 1:  # the cross-GPU exchange: all-gather of (distance, position) over NCCL
+            rec = allgather_merge(rec, device=f"cuda:{local}")
         return rec, res
+
+    def timed(host, stats=None, answers=None):
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(args.warmup, total_batches):
+            rec, res = step(i, host=host)
+            if answers is not None:
+                answers.append(rec)
+            if stats is not None:
+                for r in res:
+                    s = r.stats
+                    stats += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
+                              s.pruned_subtrees, s.queue_insertions)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(time.perf_counter() - t0)
 
     # warm-up
     for i in range(args.warmup):
         step(i, host=False)
     torch.cuda.synchronize()
 
-    # ---- timed: device-resident queries ----
+    # ---- timed: device-resident queries (the `value`) ----
+    # Each call is synchronous (results come back to the host per batch), so
+    # the wall clock between the synchronize/barrier pairs is the device time
+    # of the K batches plus the per-batch result D2H.
     launches0 = tg.launch_count()
-    _lib.check(_lib.lib().tsg_profile_enable(index.handle, 1))
-    _lib.check(_lib.lib().tsg_profile_read(index.handle, None, None, 1))
     stats_acc = np.zeros(6, np.float64)
     answers = []
     with Clocks(local) as clk:
-        barrier()
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        tw = time.perf_counter()
-        for i in range(args.warmup, total_batches):
-            rec, res = step(i, host=False)
-            answers.append(rec)
-            for r in res:
-                s = r.stats
-                stats_acc += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
-                              s.pruned_subtrees, s.queue_insertions)
-        ev1.record()
-        torch.cuda.synchronize()
-        barrier()
-        wall = time.perf_counter() - tw
+        elapsed = timed(False, stats_acc, answers)
     launches = tg.launch_count() - launches0
-    # The library synchronises its own stream inside each call, so the torch
-    # events bracket the whole step sequence; wall time is the fallback.
-    dev_s = max(ev0.elapsed_time(ev1) * 1e-3, 1e-9)
-    elapsed = max_over_ranks(max(dev_s, wall))
+    qps = args.steps * nq / elapsed
+
+    # ---- timed: end to end through the public API with host queries ----
+    e2e_s = timed(True)
+    e2e_qps = args.steps * nq / e2e_s
+
+    # ---- per-kernel CUDA-event timing pass (the roofline numbers) ----
+    _lib.check(_lib.lib().tsg_profile_enable(index.handle, 1))
+    _lib.check(_lib.lib().tsg_profile_read(index.handle, None, None, 1))
+    prof_s = timed(False)
     ms = (ctypes.c_double * 8)()
     ln = (ctypes.c_uint64 * 8)()
     _lib.check(_lib.lib().tsg_profile_read(index.handle, ms, ln, 1))
     _lib.check(_lib.lib().tsg_profile_enable(index.handle, 0))
     prof_ms = [max_over_ranks(x) for x in ms]
     prof_ln = list(ln)
-    qps = args.steps * nq / elapsed
 
-    # ---- timed: end to end through the public API with host queries ----
-    barrier()
-    te = time.perf_counter()
-    for i in range(args.warmup, total_batches):
-        step(i, host=True)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - te)
-    e2e_qps = args.steps * nq / e2e_s
-
-    # ---- roofline of the dominant query kernel (bytes from the counters) ----
+    # ---- roofline of the dominant query kernel (algorithmic bytes from the counters) ----
     hbm, peak_kind = peaks()
     nqt = args.steps * nq
     ws = 16
-    L = bs.leaves
-    slot_names = ["prep", "leaf_lb", "seed", "refine_seed", "lbscan", "refine", "finalize", "result"]
+    P = bs.pages
+    slot_names = ["-", "bound", "seed", "filter", "lbscan", "refine", "finalize", "-"]
     lb_entries, refined, cands = stats_acc[1], stats_acc[2], stats_acc[5]
     slot_bytes = {
-        1: nqt * L * (2 * ws + 4),
-        4: lb_entries * ws + nqt * L * 8 + cands * 12,
-        5: refined * 4 * n + cands * 16,
-        3: 0.0,
+        1: nqt * P * (2 * ws + 4),                        # page boxes in, page bounds out
+        3: nqt * P * 12,                                  # page bounds + offsets
+        4: lb_entries * ws + cands * 12,                  # words of surviving pages, candidate records
+        5: refined * 4 * n + cands * 16,                  # candidate rows (full length) + records
     }
     dom = max(range(8), key=lambda k: prof_ms[k])
-    dom_ms = prof_ms[dom] / max(prof_ln[dom] / max(world, 1), 1)
-    dom_bytes = slot_bytes.get(dom, 0.0) / max(prof_ln[dom] / max(world, 1), 1)
+    per_launch = max(prof_ln[dom] / max(world, 1), 1)
+    dom_ms = prof_ms[dom] / per_launch
+    dom_bytes = slot_bytes.get(dom, 0.0) / per_launch
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
 
-    # build K1 roofline: read 4n + write w + 4-byte sort key per series
-    k1_bytes = count * (4 * n + 16 + 4) / world
+    # build K1 roofline: read 4n, write the 16-byte word + 8-byte sort key per series
+    k1_bytes = count * (4 * n + 16 + 8) / world
     k1_gbs = k1_bytes / k1_s / 1e9
-    algo_build = count * (4 * n + 16 + 4)
+    algo_build = count * (4 * n + 16 + 4)  # N(4n + w + 4)
 
     line = None
     if rank == 0:
@@ -346,7 +334,8 @@ def run_ours(args):
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": None,
                          "share_of_query_time": round(share, 4),
-                         "per_kernel_ms": {slot_names[k]: round(prof_ms[k], 3) for k in range(8)}},
+                         "per_kernel_ms": {slot_names[k]: round(prof_ms[k], 3) for k in range(8) if slot_names[k] != "-"},
+                         "profiled_pass_s": round(prof_s, 4)},
             "build": {"value": round(count / build_dev_s / 1e6, 3), "unit": "Mseries/s",
                       "build_device_s": round(build_dev_s, 4), "build_wall_s": round(build_wall, 3),
                       "phase_ms": {"summarise": round(bs.summarise_ms, 3), "organise": round(bs.organise_ms, 3),
@@ -354,9 +343,9 @@ def run_ours(args):
                       "roofline": {"bound": "hbm", "kernel": "summarise (K1)", "achieved": round(k1_gbs, 1),
                                    "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                                    "frac": round(k1_gbs / hbm, 4), "traffic": None,
-                                   "algorithmic_bytes_per_series": 4 * n + 20},
+                                   "algorithmic_bytes_per_series": 4 * n + 24},
                       "whole_build_frac": round(algo_build / build_dev_s / 1e9 / hbm / world, 4),
-                      "leaves": L, "root_children": bs.root_children, "max_depth": bs.max_depth,
+                      "leaves": bs.leaves, "pages": P, "root_children": bs.root_children, "max_depth": bs.max_depth,
                       "overflow_leaves": bs.overflow_leaves},
             "search_stats_per_query": {k: round(v / nqt, 2) for k, v in zip(
                 ["lb_node_calcs", "lb_entry_calcs", "real_dist_calcs", "bsf_updates", "pruned_subtrees",

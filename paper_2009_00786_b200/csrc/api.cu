@@ -147,6 +147,7 @@ void free_shard(DevIndex& s) {
     cudaFree(s.work);
     cudaFree(s.lut);
     cudaFree(s.page_lb);
+    cudaFree(s.surv);
     cudaFree(s.cand_pos);
     cudaFree(s.cand_lb);
     cudaFree(s.cand_sq);
@@ -198,6 +199,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     TSG_CUDA(cudaMalloc(&s.work, sizeof(QueryWork)));
     TSG_CUDA(cudaMalloc(&s.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
     TSG_CUDA(cudaMalloc(&s.page_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&s.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
     s.cand_cap = N;
     TSG_CUDA(cudaMalloc(&s.cand_pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&s.cand_lb, N * sizeof(float)));

@@ -40,6 +40,7 @@ struct DevIndex {
     struct QueryWork* work = nullptr;
     float* lut = nullptr;          // [w][256]
     float* page_lb = nullptr;      // [P]
+    uint32_t* surv = nullptr;      // [P] surviving pages of the current query
     uint32_t* cand_pos = nullptr;  // [cap]
     float* cand_lb = nullptr;      // [cap]
     double* cand_sq = nullptr;     // [cap]
@@ -66,6 +67,8 @@ struct QueryWork {
     unsigned int work_next;
     unsigned int best_pos;
     unsigned int seed_begin, seed_end;  // index range refined as the seed
+    unsigned int nsurv;                 // surviving pages
+    unsigned int done_blocks;           // finalize's last-block counter
     unsigned long long stats[6];  // SearchStats order
     double qpaa[32];
     unsigned char qsym[32];

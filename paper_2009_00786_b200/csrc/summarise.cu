@@ -150,7 +150,72 @@ __global__ void __launch_bounds__(kSumThreads)
         return;
     }
 
+    // Segment mean: sum / seg. For a power-of-two seg, multiplying by the exact
+    // reciprocal is the same IEEE result as the division (pure exponent
+    // shift, identical rounding), and far cheaper than DDIV's sequence.
+    const bool pow2 = (a.seg & (a.seg - 1)) == 0;
+    const double inv_seg = 1.0 / static_cast<double>(a.seg);
+    auto segment_symbol = [&](const unsigned char* tile, int ser, int g) -> unsigned {
+        const uint32_t f0 = static_cast<uint32_t>(ser * a.n + g * a.seg);
+        double sum = 0.0;
+        if (VEC) {
+            const int nq = a.seg >> 2;
+            for (int q = 0; q < nq; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(tile + swz((f0 + 4u * q) * 4u));
+                sum = __dadd_rn(sum, static_cast<double>(v.x));
+                sum = __dadd_rn(sum, static_cast<double>(v.y));
+                sum = __dadd_rn(sum, static_cast<double>(v.z));
+                sum = __dadd_rn(sum, static_cast<double>(v.w));
+            }
+        } else {
+            for (int j = 0; j < a.seg; ++j) {
+                const float v = *reinterpret_cast<const float*>(tile + swz((f0 + j) * 4u));
+                sum = __dadd_rn(sum, static_cast<double>(v));
+            }
+        }
+        const double mean = pow2 ? __dmul_rn(sum, inv_seg) : __ddiv_rn(sum, static_cast<double>(a.seg));
+        return symbol_of(thr, a.bits, mean) << (8 - a.bits);
+    };
+
     int it = 0;
+    if (a.w == 16) {
+        // w = 16: a warp owns two whole series per step (lane = 16*half +
+        // segment). Keys come from four warp ballots (planes 0..3, segment 0
+        // = MSB), the word from three shuffles; no block barrier at all.
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            const unsigned char* tile = stages + s * stage_stride;
+            const uint64_t first = t * a.R;
+            const int valid = static_cast<int>(min(static_cast<uint64_t>(a.R), a.count - first));
+            const int half = lane >> 4, g = lane & 15;
+            for (int pair = warp; 2 * pair < valid; pair += kConsumerWarps) {
+                const int ser = 2 * pair + half;
+                const bool ok = ser < valid;
+                const unsigned sym = ok ? segment_symbol(tile, ser, g) : 0u;
+                uint64_t key = 0;
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const unsigned b = __ballot_sync(0xFFFFFFFFu, (sym >> (7 - p)) & 1u);
+                    key = (key << 16) | (__brev((b >> (16 * half)) & 0xFFFFu) >> 16);
+                }
+                const unsigned b1 = __shfl_down_sync(0xFFFFFFFFu, sym, 1);
+                const unsigned b2 = __shfl_down_sync(0xFFFFFFFFu, sym, 2);
+                const unsigned b3 = __shfl_down_sync(0xFFFFFFFFu, sym, 3);
+                const uint64_t idx = a.out_base + first + ser;
+                if (ok && (g & 3) == 0)
+                    reinterpret_cast<uint32_t*>(a.words + idx * 16)[g >> 2] = sym | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                if (ok && g == 0) {
+                    if (a.sort_keys) a.sort_keys[idx] = key;
+                    if (a.root_keys) a.root_keys[idx] = static_cast<uint32_t>(key >> 48);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        return;
+    }
+
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
@@ -160,26 +225,7 @@ __global__ void __launch_bounds__(kSumThreads)
         uint8_t* wb = wbuf + (it & 1) * a.R * a.ws;
         for (int idx = tid; idx < valid * a.w; idx += kConsumers) {
             const int ser = idx / a.w, g = idx - ser * a.w;
-            const uint32_t f0 = static_cast<uint32_t>(ser * a.n + g * a.seg);
-            double sum = 0.0;
-            if (VEC) {
-                const int nq = a.seg >> 2;
-                for (int q = 0; q < nq; ++q) {
-                    const float4 v =
-                        *reinterpret_cast<const float4*>(tile + swz((f0 + 4u * q) * 4u));
-                    sum = __dadd_rn(sum, static_cast<double>(v.x));
-                    sum = __dadd_rn(sum, static_cast<double>(v.y));
-                    sum = __dadd_rn(sum, static_cast<double>(v.z));
-                    sum = __dadd_rn(sum, static_cast<double>(v.w));
-                }
-            } else {
-                for (int j = 0; j < a.seg; ++j) {
-                    const float v = *reinterpret_cast<const float*>(tile + swz((f0 + j) * 4u));
-                    sum = __dadd_rn(sum, static_cast<double>(v));
-                }
-            }
-            const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
-            wb[ser * a.ws + g] = static_cast<uint8_t>(symbol_of(thr, a.bits, mean) << (8 - a.bits));
+            wb[ser * a.ws + g] = static_cast<uint8_t>(segment_symbol(tile, ser, g));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
