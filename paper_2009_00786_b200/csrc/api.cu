@@ -142,15 +142,20 @@ void free_shard(DevIndex& s) {
     cudaFree(s.leaf_off);
     cudaFree(s.page_off);
     cudaFree(s.page_leaf);
+    cudaFree(s.page_key);
     cudaFree(s.page_lo);
     cudaFree(s.page_hi);
-    cudaFree(s.work);
-    cudaFree(s.lut);
-    cudaFree(s.page_lb);
-    cudaFree(s.surv);
-    cudaFree(s.cand_pos);
-    cudaFree(s.cand_lb);
-    cudaFree(s.cand_sq);
+    cudaFree(s.page_dir);
+    for (int k = 0; k < DevIndex::kLanes; ++k) {
+        DevIndex::Lane& l = s.lanes[k];
+        cudaFree(l.work);
+        cudaFree(l.surv);
+        cudaFree(l.cand_pos);
+        cudaFree(l.cand_lb);
+        cudaFree(l.cand_sq);
+        if (l.done) cudaEventDestroy(l.done);
+        if (k > 0 && l.stream) cudaStreamDestroy(l.stream);
+    }
     cudaFree(s.results);
     cudaFree(s.queries);
     if (s.stream) cudaStreamDestroy(s.stream);
@@ -194,16 +199,25 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         *h2d_ns = 0;
     }
     s.thr = upload_thresholds(s.bits);
+    if (const char* e = std::getenv("TSG_REFINE_SPLIT")) s.refine_split = static_cast<float>(std::atof(e));
     build_layout(s, &ms[0], &ms[1], &ms[2]);
-    // search workspace
-    TSG_CUDA(cudaMalloc(&s.work, sizeof(QueryWork)));
-    TSG_CUDA(cudaMalloc(&s.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
-    TSG_CUDA(cudaMalloc(&s.page_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
-    TSG_CUDA(cudaMalloc(&s.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
+    // search workspace: query lanes (stream + private scratch each)
+    s.nlanes = 4;
+    if (const char* e = std::getenv("TSG_QUERY_LANES"))
+        s.nlanes = std::max(1, std::min(DevIndex::kLanes, std::atoi(e)));
     s.cand_cap = N;
-    TSG_CUDA(cudaMalloc(&s.cand_pos, N * sizeof(uint32_t)));
-    TSG_CUDA(cudaMalloc(&s.cand_lb, N * sizeof(float)));
-    TSG_CUDA(cudaMalloc(&s.cand_sq, N * sizeof(double)));
+    for (int k = 0; k < s.nlanes; ++k) {
+        DevIndex::Lane& l = s.lanes[k];
+        if (k == 0) l.stream = s.stream;
+        else TSG_CUDA(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+        TSG_CUDA(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
+        TSG_CUDA(cudaMalloc(&l.work, sizeof(QueryWork)));
+        TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
+        TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
+        TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));
+        TSG_CUDA(cudaMalloc(&l.cand_lb, N * sizeof(float)));
+        TSG_CUDA(cudaMalloc(&l.cand_sq, N * sizeof(double)));
+    }
 }
 
 void ensure_results(DevIndex& s, uint32_t nq) {

@@ -139,6 +139,11 @@ __global__ void k_page_write(const uint32_t* __restrict__ leaf_off, uint64_t L, 
     }
 }
 
+__global__ void k_page_key(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ page_off, uint64_t P,
+                           uint64_t* __restrict__ page_key) {
+    GRID_STRIDE(p, P) page_key[p] = keys[page_off[p]];
+}
+
 // One warp per page: bytewise min / max over the page's words.
 __global__ void k_page_box(const uint8_t* __restrict__ words, const uint32_t* __restrict__ page_off, uint64_t P,
                            int ws, uint8_t* __restrict__ lo_out, uint8_t* __restrict__ hi_out) {
@@ -185,13 +190,6 @@ T d2h(const T* p, cudaStream_t st) {
     return v;
 }
 
-void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st) {
-    size_t tb = 0;
-    TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int64_t>(n), st));
-    DevBuf temp(tb);
-    TSG_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb, in, out, static_cast<int64_t>(n), st));
-}
-
 }  // namespace
 
 void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf) {
@@ -201,10 +199,30 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     cudaEvent_t ev[4];
     for (auto& e : ev) TSG_CUDA(cudaEventCreate(&e));
 
+    // Every temporary is reserved up front and released after the last
+    // event, so no cudaMalloc/cudaFree (which synchronise and map/unmap GBs)
+    // falls inside the timed build.
+    const int key_bits = std::min(64, ix.w * ix.bits);
+    const int begin_bit = 64 - key_bits;
+    const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(ix.leaf_cap, 0xFFFFFFFFull));
+    const uint64_t open_cap = 2 * (N / (static_cast<uint64_t>(cap) + 1)) + 16;
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
-
-    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in(N * 4);
+    TSG_CUDA(cudaMalloc(&ix.leaf_off, (N + 1) * 4));
+    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in(N * 4), flags(N), bstart(N * 4), nsel(8),
+        leaf_start(N * 4), ranges_a(open_cap * sizeof(Range)), ranges_b(open_cap * sizeof(Range)),
+        ctr(sizeof(LeafCounters));
+    size_t tb_sort = 0, tb_sel = 0, tb_lsort = 0, tb_scan = 0;
+    TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
+                                             pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
+    TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb_sel, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
+                                        bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
+    TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_lsort, leaf_start.as<uint32_t>(), ix.leaf_off,
+                                            static_cast<int64_t>(N), 0, 32, st));
+    TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, bstart.as<uint32_t>(), pos_in.as<uint32_t>(),
+                                           static_cast<int64_t>(N + 1), st));
+    DevBuf temp(std::max({tb_sort, tb_sel, tb_lsort, tb_scan}));
+    TSG_CUDA(cudaStreamSynchronize(st));
 
     // K1 summarise
     TSG_CUDA(cudaEventRecord(ev[0], st));
@@ -212,46 +230,23 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaEventRecord(ev[1], st));
 
     // K2 organise: stable sort by the significant key bits, carrying positions.
-    const int key_bits = std::min(64, ix.w * ix.bits);
-    const int begin_bit = 64 - key_bits;
     k_iota<<<grid_for(N, 256, sms), 256, 0, st>>>(pos_in.as<uint32_t>(), N);
     TSG_LAUNCHED();
-    {
-        size_t tb = 0;
-        TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
-                                                 pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit,
-                                                 64, st));
-        DevBuf temp(tb);
-        TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
-                                                 pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit,
-                                                 64, st));
-        k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, N, ix.ws);
-        TSG_LAUNCHED();
-        TSG_CUDA(cudaEventRecord(ev[2], st));
-    }
+    TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
+                                             pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
+    k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, N, ix.ws);
+    TSG_LAUNCHED();
+    TSG_CUDA(cudaEventRecord(ev[2], st));
 
     // K3 leaves. Root subtrees = runs of equal root key (top w key bits).
     const uint64_t* keys = keys_out.as<uint64_t>();
-    uint64_t nb = 0;
-    DevBuf bstart(N * 4);
-    {
-        DevBuf flags(N), nsel(8);
-        k_bucket_flags<<<grid_for(N, 256, sms), 256, 0, st>>>(keys, N, ix.w, flags.as<uint8_t>());
-        TSG_LAUNCHED();
-        size_t tb = 0;
-        TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
-                                            bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
-        DevBuf temp(tb);
-        TSG_CUDA(cub::DeviceSelect::Flagged(temp.p, tb, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
-                                            bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
-        nb = d2h(nsel.as<uint64_t>(), st);
-    }
+    k_bucket_flags<<<grid_for(N, 256, sms), 256, 0, st>>>(keys, N, ix.w, flags.as<uint8_t>());
+    TSG_LAUNCHED();
+    TSG_CUDA(cub::DeviceSelect::Flagged(temp.p, tb_sel, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
+                                        bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
+    const uint64_t nb = d2h(nsel.as<uint64_t>(), st);
     ix.root_children = nb;
 
-    const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(ix.leaf_cap, 0xFFFFFFFFull));
-    const uint64_t open_cap = 2 * (N / (static_cast<uint64_t>(cap) + 1)) + 16;
-    DevBuf leaf_start(N * 4), ranges_a(open_cap * sizeof(Range)), ranges_b(open_cap * sizeof(Range)),
-        ctr(sizeof(LeafCounters));
     TSG_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(LeafCounters), st));
     auto* C = ctr.as<LeafCounters>();
     k_init_ranges<<<grid_for(nb, 256, sms), 256, 0, st>>>(bstart.as<uint32_t>(), nb, N, keys, cap, C,
@@ -274,38 +269,36 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     ix.max_depth = hc.max_depth;
 
     // Leaves were emitted in arbitrary order: sort their first entries.
-    TSG_CUDA(cudaMalloc(&ix.leaf_off, (ix.L + 1) * 4));
-    {
-        size_t tb = 0;
-        TSG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, leaf_start.as<uint32_t>(), ix.leaf_off,
-                                                static_cast<int64_t>(ix.L), 0, 32, st));
-        DevBuf temp(tb);
-        TSG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb, leaf_start.as<uint32_t>(), ix.leaf_off,
-                                                static_cast<int64_t>(ix.L), 0, 32, st));
-    }
+    TSG_CUDA(cub::DeviceRadixSort::SortKeys(temp.p, tb_lsort, leaf_start.as<uint32_t>(), ix.leaf_off,
+                                            static_cast<int64_t>(ix.L), 0, 32, st));
     const uint32_t n32 = static_cast<uint32_t>(N);
     TSG_CUDA(cudaMemcpyAsync(ix.leaf_off + ix.L, &n32, 4, cudaMemcpyHostToDevice, st));
 
-    // Pages: each leaf cut into ceil(size / kPage) pieces.
-    {
-        DevBuf pcount((ix.L + 1) * 4), pbase((ix.L + 1) * 4);
-        TSG_CUDA(cudaMemsetAsync(pcount.as<uint32_t>() + ix.L, 0, 4, st));
-        k_page_count<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pcount.as<uint32_t>());
-        TSG_LAUNCHED();
-        exclusive_scan_u32(pcount.as<uint32_t>(), pbase.as<uint32_t>(), ix.L + 1, st);
-        ix.P = d2h(pbase.as<uint32_t>() + ix.L, st);
-        TSG_CUDA(cudaMalloc(&ix.page_off, (ix.P + 1) * 4));
-        TSG_CUDA(cudaMalloc(&ix.page_leaf, ix.P * 4));
-        TSG_CUDA(cudaMalloc(&ix.page_lo, ix.P * ix.ws));
-        TSG_CUDA(cudaMalloc(&ix.page_hi, ix.P * ix.ws));
-        k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase.as<uint32_t>(), ix.page_off,
-                                                               ix.page_leaf);
-        TSG_LAUNCHED();
-        TSG_CUDA(cudaMemcpyAsync(ix.page_off + ix.P, &n32, 4, cudaMemcpyHostToDevice, st));
-        k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.page_off, ix.P, ix.ws, ix.page_lo,
-                                                                  ix.page_hi);
-        TSG_LAUNCHED();
-    }
+    // Pages: each leaf cut into ceil(size / kPage) pieces (counts and bases
+    // reuse the bucket-start and iota buffers).
+    uint32_t* pcount = bstart.as<uint32_t>();
+    uint32_t* pbase = pos_in.as<uint32_t>();
+    TSG_CUDA(cudaMemsetAsync(pcount + ix.L, 0, 4, st));
+    k_page_count<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pcount);
+    TSG_LAUNCHED();
+    TSG_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb_scan, pcount, pbase, static_cast<int64_t>(ix.L + 1), st));
+    ix.P = d2h(pbase + ix.L, st);
+    const uint64_t ndir = (ix.P + 255) / 256;
+    TSG_CUDA(cudaMalloc(&ix.page_off, (ix.P + 1) * 4));
+    TSG_CUDA(cudaMalloc(&ix.page_leaf, ix.P * 4));
+    TSG_CUDA(cudaMalloc(&ix.page_lo, ix.P * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.page_hi, ix.P * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.page_key, ix.P * 8));
+    TSG_CUDA(cudaMalloc(&ix.page_dir, ndir * 8));
+    k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase, ix.page_off, ix.page_leaf);
+    TSG_LAUNCHED();
+    TSG_CUDA(cudaMemcpyAsync(ix.page_off + ix.P, &n32, 4, cudaMemcpyHostToDevice, st));
+    k_page_key<<<grid_for(ix.P, 256, sms), 256, 0, st>>>(keys, ix.page_off, ix.P, ix.page_key);
+    TSG_LAUNCHED();
+    TSG_CUDA(cudaMemcpy2DAsync(ix.page_dir, 8, ix.page_key, 256 * 8, 8, ndir, cudaMemcpyDeviceToDevice, st));
+    k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.page_off, ix.P, ix.ws, ix.page_lo,
+                                                              ix.page_hi);
+    TSG_LAUNCHED();
     TSG_CUDA(cudaEventRecord(ev[3], st));
     TSG_CUDA(cudaStreamSynchronize(st));
 

@@ -31,25 +31,34 @@ struct DevIndex {
     uint64_t L = 0;
     uint32_t* page_off = nullptr;   // [P+1] entry offsets (pages tile [0, N))
     uint32_t* page_leaf = nullptr;  // [P]
+    uint64_t* page_key = nullptr;   // [P] sort key of each page's first entry
     uint8_t* page_lo = nullptr;     // [P][ws] per-segment min symbol
     uint8_t* page_hi = nullptr;     // [P][ws] per-segment max symbol
     uint64_t P = 0;
     uint64_t root_children = 0;
     uint64_t inner = 0, max_depth = 0, overflow = 0;
-    // search workspace
-    struct QueryWork* work = nullptr;
-    float* lut = nullptr;          // [w][256]
-    float* page_lb = nullptr;      // [P]
-    uint32_t* surv = nullptr;      // [P] surviving pages of the current query
-    uint32_t* cand_pos = nullptr;  // [cap]
-    float* cand_lb = nullptr;      // [cap]
-    double* cand_sq = nullptr;     // [cap]
+    uint64_t* page_dir = nullptr;   // [(P + 255) / 256] page_key of every 256th page
+    // search workspace: kLanes query lanes, each a stream with private
+    // scratch, so consecutive queries of a batch run concurrently.
+    struct Lane {
+        cudaStream_t stream = nullptr;  // lane 0 uses the index stream
+        cudaEvent_t done = nullptr;
+        struct QueryWork* work = nullptr;
+        uint32_t* surv = nullptr;      // [P] surviving pages of the lane's query
+        uint32_t* cand_pos = nullptr;  // [cap]
+        float* cand_lb = nullptr;      // [cap]
+        double* cand_sq = nullptr;     // [cap]
+    };
+    static constexpr int kLanes = 8;
+    Lane lanes[kLanes];
+    int nlanes = 1;                // lanes in use (TSG_QUERY_LANES, default kLanes)
     uint64_t cand_cap = 0;
     struct DevResult* results = nullptr;  // [results_cap]
     uint32_t results_cap = 0;
     float* queries = nullptr;      // staging for host queries
     uint32_t queries_cap = 0;
     int sms = 148;
+    float refine_split = 0.5f;     // wave-0 fraction of the scan bound (TSG_REFINE_SPLIT)
     // per-kernel profiling (tsg_profile_enable)
     bool profile = false;
     double prof_ms[8] = {0};
@@ -68,7 +77,9 @@ struct QueryWork {
     unsigned int best_pos;
     unsigned int seed_begin, seed_end;  // index range refined as the seed
     unsigned int nsurv;                 // surviving pages
+    unsigned int nhigh;                 // wave-1 candidates, stored at the top of the candidate arrays
     unsigned int done_blocks;           // finalize's last-block counter
+    float scan_bound;                   // BSF bound the page/word filters used
     unsigned long long stats[6];  // SearchStats order
     double qpaa[32];
     unsigned char qsym[32];

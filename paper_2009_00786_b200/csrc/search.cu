@@ -1,38 +1,37 @@
 // Exact Euclidean 1-NN over the flat SoA index (one device shard).
 //
 // Replaces exact_search (src/query.cpp:258-298) and its pieces. Per query,
-// five kernels on the index's stream:
-//   bound     QueryState (src/query.cpp:81-100) + node_lower_bound
-//             (src/query.cpp:102-107): every block computes the query PAA in
-//             FP64 reference order, the query symbols and a [w][256] table of
-//             per-segment squared region gaps (mindist_bands,
-//             src/metrics.cpp:47-70) rounded DOWN to float, so every float
-//             bound here is <= the exact FP64 bound (sound pruning); then the
-//             bound of every page box, and the argmin page.
-//   seed      approximate_search_state (src/query.cpp:226-238): the leaf of
-//             the argmin page is refined exhaustively and seeds the BSF.
-//   filter    traverse_root_subtree's pruning (src/query.cpp:154-171) at page
-//             granularity: pages whose box bound exceeds the BSF are dropped;
-//             survivors are compacted (block-aggregated).
+// six kernels on the index's stream:
+//   seed      approximate_search_state (src/query.cpp:226-238): the leaf the
+//             query's own iSAX word descends to (binary search of its
+//             plane-major key over the page keys) is refined exhaustively
+//             and seeds the best-so-far (BSF).
+//   bound     node_lower_bound over every page box (src/query.cpp:102-107)
+//             + the pruning test (src/query.cpp:159): pages whose bound is
+//             within the BSF survive (block-aggregated compaction).
 //   lbscan    the entry-level filter of calculate_real_distance_leaf
 //             (src/query.cpp:129-134): words of surviving pages are bounded
-//             with 16 table lookups and compacted with warp ballot + prefix
-//             popcount into the candidate list.
-//   refine    euclidean (src/metrics.cpp:17-40, 95-104): one thread per
-//             candidate row, 256-bit loads of 8-float blocks, FP64 block sums
-//             without FMA added left to right exactly like squared_l2, early
-//             abandonment when the running sum exceeds the live best-so-far
-//             (strict, so ties survive); the BSF is an atomicMin on the double
+//             with one table lookup per segment and compacted with warp
+//             ballot + prefix popcount into two LB-ordered candidate waves.
+//   refine x2 euclidean (src/metrics.cpp:17-40, 95-104), wave 0 (bounds up
+//             to `split` x the scan bound) then wave 1, the GPU analog of
+//             MESSI's LB-ordered priority queues (src/query.cpp:173-184): an
+//             8-lane group per candidate row, 256-bit loads of 8-float
+//             blocks, FP64 block sums without FMA, added left to right
+//             exactly like squared_l2; the BSF is an atomicMin on the double
 //             bit pattern (non-negative doubles order as unsigned integers),
-//             the SharedBsf analog (src/query.cpp:35-42). A candidate whose
+//             the SharedBsf analog (src/query.cpp:35-42); a candidate whose
 //             bound exceeds the live BSF is skipped (`LB >= cutoff -> skip`).
 //   finalize  result = min over refined candidates of (sqrt(sum), position):
 //             ties resolve to the lowest position exactly as scan_nn does
 //             (src/scan.cpp:54-59); the last block writes the result and
 //             resets the scratch for the next query.
-// Pruning keeps ties: a candidate is dropped only when its bound (or partial
-// sum) is strictly above the best-so-far widened by 1e-9 relative (covering
-// FP64 rounding of the distance sums), so the exact answer is never lost.
+// Every kernel computes the query PAA in FP64 reference order, the query
+// symbols and, where needed, a [w][256] table of per-segment squared region
+// gaps (mindist_bands, src/metrics.cpp:47-70) scaled by n/w and rounded DOWN
+// to float, so every float bound here is <= the exact FP64 bound. Pruning
+// keeps ties: an entry is dropped only when its bound is strictly above the
+// BSF widened by 1e-9 relative (covering FP64 rounding of the sums).
 #include <algorithm>
 #include <cmath>
 #include <utility>
@@ -48,6 +47,7 @@ namespace {
 constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
 constexpr double kSlack = 1.0 + 1e-9;
 constexpr int kThreads = 256;
+constexpr int kRowLanes = 8;  // lanes per candidate row in the refine kernels
 
 enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
 
@@ -59,10 +59,11 @@ __device__ __forceinline__ float bound_from_bits(unsigned long long bits) {
     return __double2float_ru(bsf_of(bits) * kSlack);
 }
 
-__device__ __forceinline__ uint8_t byte_of(const uint4& v, int s) {
-    const uint32_t word = s < 4 ? v.x : s < 8 ? v.y : s < 12 ? v.z : v.w;
-    return static_cast<uint8_t>(word >> (8 * (s & 3)));
+__device__ __forceinline__ uint32_t word32(const uint4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
+
+__device__ __forceinline__ uint32_t byte_of(const uint4& v, int s) { return (word32(v, s >> 2) >> (8 * (s & 3))) & 255u; }
 
 struct QueryShared {
     double thr[kThrPad];
@@ -70,8 +71,8 @@ struct QueryShared {
     unsigned char qsym[kMaxW];
 };
 
-// Block-local query preparation: PAA (FP64, reference order), symbols, and
-// the [w][256] squared-gap table (scaled by n/w, rounded down).
+// Block-local query preparation: PAA (FP64, reference order) and symbols;
+// with lut != nullptr also the [w][256] squared-gap table.
 __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
                               QueryShared& qs, float* s_lut) {
     for (int i = threadIdx.x; i < kThrPad; i += blockDim.x) qs.thr[i] = thr_g[i];
@@ -86,6 +87,7 @@ __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bit
         qs.qsym[g] = static_cast<unsigned char>(symbol_of(qs.thr, bits, mean) << (8 - bits));
     }
     __syncthreads();
+    if (!s_lut) return;
     const unsigned card = 1u << bits;
     const double scale = static_cast<double>(n) / static_cast<double>(w);
     for (int idx = threadIdx.x; idx < w * 256; idx += blockDim.x) {
@@ -102,11 +104,26 @@ __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bit
     __syncthreads();
 }
 
+// Bound of one word: sum over segments of the table entry of its symbol.
+// W16: compile-time w = 16 (fully unrolled); otherwise runtime w.
+template <bool W16>
+__device__ __forceinline__ float word_bound(const float* s_lut, const uint4* v, int w) {
+    float lb = 0.f;
+    if (W16) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) lb = __fadd_rd(lb, s_lut[s * 256 + byte_of(v[0], s)]);
+    } else {
+        for (int s = 0; s < w; ++s) lb = __fadd_rd(lb, s_lut[s * 256 + byte_of(v[s >> 4], s & 15)]);
+    }
+    return lb;
+}
+
 __device__ __forceinline__ void reset_work(QueryWork* wk) {
     wk->bsf_bits = kInfBits;
     wk->seed_key = ~0ull;
     wk->ncand = 0;
     wk->nseed = 0;
+    wk->nhigh = 0;
     wk->work_next = 0;
     wk->best_pos = 0xFFFFFFFFu;
     wk->nsurv = 0;
@@ -116,37 +133,6 @@ __device__ __forceinline__ void reset_work(QueryWork* wk) {
 __global__ void k_reset(QueryWork* wk) {
     reset_work(wk);
     wk->done_blocks = 0;
-}
-
-// ------------------------------------------------------------ bound
-__global__ void __launch_bounds__(kThreads)
-    k_bound(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
-            const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, uint64_t P, int ws, QueryWork* wk,
-            float* __restrict__ page_lb) {
-    extern __shared__ float s_lut[];
-    __shared__ QueryShared qs;
-    prepare_query(q, n, w, bits, thr_g, qs, s_lut);
-    unsigned long long best = ~0ull;
-    for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < P;
-         p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        float lb = 0.f;
-        for (int h = 0; h < ws / 16; ++h) {
-            const uint4 a = ld_stream_u4(lo + p * ws + 16 * h);
-            const uint4 b = ld_stream_u4(hi + p * ws + 16 * h);
-            const int smax = min(16, w - 16 * h);
-            for (int s = 0; s < smax; ++s) {
-                const int g = 16 * h + s;
-                const uint8_t ql = qs.qsym[g], bl = byte_of(a, s), bh = byte_of(b, s);
-                const float gv = ql < bl ? s_lut[g * 256 + bl] : (ql > bh ? s_lut[g * 256 + bh] : 0.f);
-                lb = __fadd_rd(lb, gv);
-            }
-        }
-        page_lb[p] = lb;
-        best = min(best, (static_cast<unsigned long long>(__float_as_uint(lb)) << 32) | p);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
-    if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(&wk->seed_key, best);
 }
 
 // ---------------------------------------------------- row refinement
@@ -174,58 +160,60 @@ __device__ __forceinline__ double block_sq(const float* x, const float* q, int c
     return blk;
 }
 
-constexpr int kGroup = 4;  // blocks of 8 floats in flight per thread
-
-// Squared Euclidean distance of one row to the query in squared_l2's exact
-// order; returns +inf as soon as the running sum exceeds the live bound
-// (re-read from `bsf` every kGroup blocks). VEC: n % 8 == 0, 32-byte aligned.
+// Squared distance of a row computed by an 8-lane group: lane j owns blocks
+// j, j+8, j+16, j+24 of each 32-block round (the 8 lanes read 256 contiguous
+// bytes per load); the group leader then adds the block sums left to right,
+// squared_l2's order. Rows longer than 256 take several rounds; after each
+// round the running sum is checked against the live BSF (strict), the
+// reference's abandonment (metrics.cpp:28). All 32 lanes must call this.
+// Returns the sum on the group leader (lane % 8 == 0), +inf if abandoned.
 template <bool VEC>
-__device__ __forceinline__ double row_sq(const float* __restrict__ row, const float* __restrict__ s_q, int n,
-                                         const unsigned long long* bsf) {
+__device__ __forceinline__ double group_row_sq(const float* __restrict__ row, bool live, const float* __restrict__ s_q,
+                                               int n, const unsigned long long* bsf) {
+    const int lane = threadIdx.x & 31, j = lane & (kRowLanes - 1), base = lane & ~(kRowLanes - 1);
     const int nb = (n + 7) >> 3;
     double sum = 0.0;
-    for (int b0 = 0; b0 < nb; b0 += kGroup) {
+    bool dead = !live;
+    for (int r0 = 0; r0 < nb; r0 += 32) {
+        double blk[4];
         if (VEC) {
-            F8 x[kGroup];
+            F8 x[4];
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j)
-                if (b0 + j < nb) x[j] = ld256(row + 8 * (b0 + j));
+            for (int t = 0; t < 4; ++t) {
+                const int b = r0 + j + kRowLanes * t;
+                if (!dead && b < nb) x[t] = ld256(row + 8 * b);
+            }
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j)
-                if (b0 + j < nb) sum = __dadd_rn(sum, block_sq(x[j].v, s_q + 8 * (b0 + j), 8));
+            for (int t = 0; t < 4; ++t) {
+                const int b = r0 + j + kRowLanes * t;
+                blk[t] = (!dead && b < nb) ? block_sq(x[t].v, s_q + 8 * b, 8) : 0.0;
+            }
         } else {
 #pragma unroll
-            for (int j = 0; j < kGroup; ++j) {
-                const int b = b0 + j;
-                if (b >= nb) break;
-                const int cnt = min(8, n - 8 * b);
-                float x[8];
+            for (int t = 0; t < 4; ++t) {
+                const int b = r0 + j + kRowLanes * t;
+                blk[t] = 0.0;
+                if (!dead && b < nb) {
+                    const int cnt = min(8, n - 8 * b);
+                    float x[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) x[k] = k < cnt ? row[8 * b + k] : 0.f;
-                sum = __dadd_rn(sum, block_sq(x, s_q + 8 * b, cnt));
+                    for (int k = 0; k < 8; ++k) x[k] = k < cnt ? row[8 * b + k] : 0.f;
+                    blk[t] = block_sq(x, s_q + 8 * b, cnt);
+                }
             }
         }
-        if (bsf && sum > bsf_of(ld_volatile_u64(bsf)) * kSlack) return INFINITY;
+        // Left-to-right over the round's blocks: block r0 + 8t + i lives in
+        // lane base+i, slot t.
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < kRowLanes; ++i) {
+                const double v = __shfl_sync(0xFFFFFFFFu, blk[t], base + i);
+                if (r0 + kRowLanes * t + i < nb) sum = __dadd_rn(sum, v);
+            }
+        if (r0 + 32 < nb && bsf && !dead && sum > bsf_of(ld_volatile_u64(bsf)) * kSlack) dead = true;
     }
-    return sum;
-}
-
-__device__ __forceinline__ void seed_range(const uint32_t* leaf_off, const uint32_t* page_off,
-                                           const uint32_t* page_leaf, uint32_t seed_cap, unsigned long long key,
-                                           uint32_t& a, uint32_t& b) {
-    const uint32_t page = static_cast<uint32_t>(key & 0xFFFFFFFFull);
-    const uint32_t leaf = page_leaf[page];
-    a = leaf_off[leaf];
-    b = leaf_off[leaf + 1];
-    if (b - a > seed_cap) {
-        a = page_off[page];
-        b = page_off[page + 1];
-    }
-}
-
-__device__ __forceinline__ void load_query(float* s_q, const float* q, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s_q[i] = q[i];
-    __syncthreads();
+    return dead ? INFINITY : sum;
 }
 
 // Publishes a finished sum: candidate record, BSF atomicMin only when it can
@@ -238,58 +226,137 @@ __device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, u
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
 }
 
-// -------------------------------------------------------------- seed
-// The leaf holding the best page (the leaf the reference's approximate
-// search descends to); an overflow leaf larger than seed_cap is replaced by
-// that page alone. Every entry is refined against the running seed BSF.
-template <bool VEC>
-__global__ void __launch_bounds__(128)
-    k_seed(const float* __restrict__ rows, int n, const float* __restrict__ query,
-           const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ page_off,
-           const uint32_t* __restrict__ page_leaf, const uint32_t* __restrict__ pos, uint32_t seed_cap,
-           QueryWork* wk, uint32_t* __restrict__ cand_pos, double* __restrict__ cand_sq) {
-    extern __shared__ float s_q[];
-    load_query(s_q, query, n);
-    uint32_t a, b;
-    seed_range(leaf_off, page_off, page_leaf, seed_cap, wk->seed_key, a, b);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        wk->nseed = b - a;
-        wk->ncand = b - a;
-        wk->seed_begin = a;
-        wk->seed_end = b;
-        wk->stats[kRealDist] += b - a;
-    }
-    unsigned long long updates = 0;
-    for (uint32_t e = a + blockIdx.x * blockDim.x + threadIdx.x; e < b; e += gridDim.x * blockDim.x) {
-        const uint32_t p = pos[e];
-        cand_pos[e - a] = p;
-        const double s = row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
-        updates += publish(wk, s, e - a, cand_sq);
-    }
-    for (int o = 16; o > 0; o >>= 1) updates += __shfl_xor_sync(0xFFFFFFFFu, updates, o);
-    if ((threadIdx.x & 31) == 0 && updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+__device__ __forceinline__ void load_query(float* s_q, const float* q, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_q[i] = q[i];
+    __syncthreads();
 }
 
-// ------------------------------------------------------------ filter
-// Pages with bound <= BSF (and outside the seed range) survive; one atomic
-// per block reserves their slots in the survivor list.
+// The page the query's own key falls into: the largest p with
+// page_key[p] <= key (0 if none), i.e. where the query's iSAX word would be
+// stored. Two parallel rounds instead of a serial binary search: the block
+// counts the directory entries (every 256th page key) <= key, then counts
+// the keys <= key inside that 256-page window. blockDim.x must be 256.
+__device__ __forceinline__ uint32_t locate_page(const uint64_t* __restrict__ page_key,
+                                                const uint64_t* __restrict__ page_dir, uint64_t P, uint64_t key) {
+    __shared__ unsigned s_part[kThreads / 32];
+    const uint64_t nd = (P + 255) / 256;
+    unsigned c = 0;
+    for (uint64_t i = threadIdx.x; i < nd; i += blockDim.x) c += page_dir[i] <= key ? 1u : 0u;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    unsigned dirs = 0;
+    for (int i = 0; i < kThreads / 32; ++i) dirs += s_part[i];
+    const uint64_t w0 = dirs == 0 ? 0 : static_cast<uint64_t>(dirs - 1) * 256;
+    const uint64_t p = w0 + threadIdx.x;
+    const int cnt = __syncthreads_count(p < P && page_key[p] <= key);
+    return static_cast<uint32_t>(cnt == 0 ? 0 : w0 + cnt - 1);
+}
+
+// Plane-major 64-bit key of the query word (same layout as the index keys).
+__device__ __forceinline__ uint64_t query_key(const unsigned char* qsym, int w) {
+    uint64_t k = 0;
+    int left = 64;
+    for (int p = 0; p < 8 && left > 0; ++p)
+        for (int g = 0; g < w && left > 0; ++g, --left) k = (k << 1) | ((qsym[g] >> (7 - p)) & 1u);
+    return left >= 64 ? 0 : k << left;
+}
+
+// -------------------------------------------------------------- seed
+// The leaf the query's own iSAX word descends to; an overflow leaf larger
+// than seed_cap is replaced by that page alone. Every entry is refined.
+template <bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    k_filter(const float* __restrict__ page_lb, const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk,
-             uint32_t* __restrict__ surv) {
+    k_seed(const float* __restrict__ rows, int n, int w, int bits, const double* __restrict__ thr_g,
+           const float* __restrict__ query, const uint32_t* __restrict__ leaf_off,
+           const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ page_leaf,
+           const uint64_t* __restrict__ page_key, const uint64_t* __restrict__ page_dir, uint64_t P,
+           const uint32_t* __restrict__ pos, uint32_t seed_cap, QueryWork* wk, uint32_t* __restrict__ cand_pos,
+           double* __restrict__ cand_sq) {
+    extern __shared__ float s_q[];
+    __shared__ QueryShared qs;
+    __shared__ uint32_t s_range[2];
+    load_query(s_q, query, n);
+    prepare_query(s_q, n, w, bits, thr_g, qs, nullptr);
+    const uint32_t page = locate_page(page_key, page_dir, P, query_key(qs.qsym, w));
+    if (threadIdx.x == 0) {
+        const uint32_t leaf = page_leaf[page];
+        uint32_t a = leaf_off[leaf], b = leaf_off[leaf + 1];
+        if (b - a > seed_cap) {
+            a = page_off[page];
+            b = page_off[page + 1];
+        }
+        s_range[0] = a;
+        s_range[1] = b;
+        if (blockIdx.x == 0) {
+            wk->seed_key = page;
+            wk->nseed = b - a;
+            wk->ncand = b - a;
+            wk->seed_begin = a;
+            wk->seed_end = b;
+            wk->stats[kRealDist] += b - a;
+        }
+    }
+    __syncthreads();
+    const uint32_t a = s_range[0], b = s_range[1];
+    const int lane = threadIdx.x & 31;
+    const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
+    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
+    unsigned long long updates = 0;
+    // Uniform trip count per warp: every lane iterates while any group of the warp has work.
+    const uint64_t warp_group0 = group - ((lane & 31) / kRowLanes);
+    for (uint64_t k = 0; a + warp_group0 + k * ngroups < b; ++k) {
+        const uint64_t e = a + group + k * ngroups;
+        const bool live = e < b;
+        const uint32_t p = live ? pos[e] : 0u;
+        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, live, s_q, n, &wk->bsf_bits);
+        if (live && (lane & (kRowLanes - 1)) == 0) {
+            cand_pos[e - a] = p;
+            updates += publish(wk, s, e - a, cand_sq);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) updates += __shfl_xor_sync(0xFFFFFFFFu, updates, o);
+    if (lane == 0 && updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+}
+
+// ------------------------------------------------------- bound + filter
+// Box bound per page: per segment the table entry of the query symbol
+// clamped into the box [lo, hi] (0 when the query symbol is inside).
+template <int WS, bool W16>
+__global__ void __launch_bounds__(kThreads)
+    k_bound(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
+            const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, const uint32_t* __restrict__ page_off,
+            uint64_t P, QueryWork* wk, uint32_t* __restrict__ surv) {
+    extern __shared__ float s_lut[];
+    __shared__ QueryShared qs;
     __shared__ uint32_t s_cnt[kThreads / 32];
     __shared__ uint32_t s_base;
+    prepare_query(q, n, w, bits, thr_g, qs, s_lut);
+    uint4 q4[WS / 16];
+#pragma unroll
+    for (int h = 0; h < WS / 16; ++h) q4[h] = *reinterpret_cast<const uint4*>(qs.qsym + 16 * h);
     const float bound = bound_from_bits(wk->bsf_bits);
     const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
     unsigned long long pruned = 0;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < P;
          base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t p = base + threadIdx.x;
         bool keep = false;
         if (p < P) {
-            const uint32_t a = page_off[p], b = page_off[p + 1];
-            const bool seeded = a >= sa && b <= sb;
-            keep = !seeded && page_lb[p] <= bound;
+            uint4 c[WS / 16];
+#pragma unroll
+            for (int h = 0; h < WS / 16; ++h) {
+                const uint4 a = ld_stream_u4(lo + p * WS + 16 * h);
+                const uint4 b = ld_stream_u4(hi + p * WS + 16 * h);
+                c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, a.x), b.x), __vminu4(__vmaxu4(q4[h].y, a.y), b.y),
+                                  __vminu4(__vmaxu4(q4[h].z, a.z), b.z), __vminu4(__vmaxu4(q4[h].w, a.w), b.w));
+            }
+            const float lb = word_bound<W16>(s_lut, c, w);
+            const uint32_t ea = page_off[p], eb = page_off[p + 1];
+            const bool seeded = ea >= sa && eb <= sb;
+            keep = !seeded && lb <= bound;
             pruned += (!keep && !seeded) ? 1 : 0;
         }
         const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
@@ -298,9 +365,9 @@ __global__ void __launch_bounds__(kThreads)
         if (threadIdx.x == 0) {
             uint32_t tot = 0;
             for (int i = 0; i < kThreads / 32; ++i) {
-                const uint32_t c = s_cnt[i];
+                const uint32_t cnt = s_cnt[i];
                 s_cnt[i] = tot;
-                tot += c;
+                tot += cnt;
             }
             s_base = tot ? atomicAdd(&wk->nsurv, tot) : 0u;
         }
@@ -315,14 +382,34 @@ __global__ void __launch_bounds__(kThreads)
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
 
+// Writes a warp's staged candidates: wave 0 (bound <= cut) grows upward
+// from ncand, wave 1 grows downward from the top of the candidate arrays.
 __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
-                                            uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&wk->ncand, static_cast<unsigned>(cnt));
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    for (int i = lane; i < cnt; i += 32) {
-        cand_pos[base + i] = s_pos[i];
-        cand_lb[base + i] = s_lb[i];
+                                            float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
+                                            float* __restrict__ cand_lb) {
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+        const int i = i0 + lane;
+        const bool valid = i < cnt;
+        const float lb = valid ? s_lb[i] : 0.f;
+        const bool low = valid && lb <= cut;
+        const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
+        uint32_t bl = 0, bh = 0;
+        if (lane == 0) {
+            if (ml) bl = atomicAdd(&wk->ncand, static_cast<unsigned>(__popc(ml)));
+            if (mh) bh = atomicAdd(&wk->nhigh, static_cast<unsigned>(__popc(mh)));
+        }
+        bl = __shfl_sync(0xFFFFFFFFu, bl, 0);
+        bh = __shfl_sync(0xFFFFFFFFu, bh, 0);
+        const unsigned below = (1u << lane) - 1u;
+        if (low) {
+            const uint64_t at = bl + __popc(ml & below);
+            cand_pos[at] = s_pos[i];
+            cand_lb[at] = lb;
+        } else if (valid) {
+            const uint64_t at = cap - 1 - (bh + __popc(mh & below));
+            cand_pos[at] = s_pos[i];
+            cand_lb[at] = lb;
+        }
     }
     __syncwarp();
 }
@@ -330,12 +417,12 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
 // Surviving pages round-robin over warps (each page <= kPage entries, so
 // work units are bounded); a lane bounds entries lane, lane+32, ... of the
 // page with all of its loads in flight at once.
-template <int WS>
+template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_lbscan(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
              const uint8_t* __restrict__ words, const uint32_t* __restrict__ pos,
-             const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ surv, QueryWork* wk,
-             uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
+             const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ surv, QueryWork* wk, float split,
+             uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
     extern __shared__ float s_lut[];
     __shared__ QueryShared qs;
     __shared__ uint32_t s_pos[kThreads / 32][kStageCap];
@@ -345,6 +432,7 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int K = kPage / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float bound = bound_from_bits(wk->bsf_bits);
+    const float cut = wk->scan_bound * split;
     const uint32_t nsurv = wk->nsurv;
     const uint64_t gwarp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -365,14 +453,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const uint32_t e = a + lane + 32 * k;
-            float lb = 0.f;
-#pragma unroll
-            for (int h = 0; h < H; ++h) {
-                const int smax = min(16, w - 16 * h);
-#pragma unroll
-                for (int s = 0; s < 16; ++s)
-                    if (s < smax) lb = __fadd_rd(lb, s_lut[(16 * h + s) * 256 + byte_of(wv[k][h], s)]);
-            }
+            const float lb = word_bound<W16>(s_lut, wv[k], w);
             const bool pass = e < b && lb <= bound;
             const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
             if (m) {
@@ -384,44 +465,54 @@ __global__ void __launch_bounds__(kThreads)
                 cnt += __popc(m);
                 __syncwarp();
                 if (cnt > kStageCap - 32) {
-                    flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cand_pos, cand_lb);
+                    flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
                     cnt = 0;
                 }
             }
         }
     }
-    if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cand_pos, cand_lb);
+    if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
     if (lane == 0 && scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
 }
 
 // ------------------------------------------------------------ refine
+// One wave: wave 0 = [nseed, ncand), wave 1 = [cap - nhigh, cap).
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads)
     k_refine(const float* __restrict__ rows, int n, const float* __restrict__ query, QueryWork* wk,
              const uint32_t* __restrict__ cand_pos, const float* __restrict__ cand_lb,
-             double* __restrict__ cand_sq) {
+             double* __restrict__ cand_sq, int wave, uint64_t cap) {
     extern __shared__ float s_q[];
     load_query(s_q, query, n);
-    const uint32_t begin = wk->nseed, end = wk->ncand;
+    const uint64_t begin = wave == 0 ? wk->nseed : cap - wk->nhigh;
+    const uint64_t end = wave == 0 ? wk->ncand : cap;
+    const int lane = threadIdx.x & 31;
+    const bool leader = (lane & (kRowLanes - 1)) == 0;
+    const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
+    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
+    const uint64_t warp_group0 = group - lane / kRowLanes;
     unsigned long long refined = 0, updates = 0;
-    for (uint64_t c = begin + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < end;
-         c += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const float lb = cand_lb[c];
-        const uint32_t p = cand_pos[c];
-        if (lb > bound_from_bits(ld_volatile_u64(&wk->bsf_bits))) {
-            cand_sq[c] = INFINITY;
-            continue;
+    for (uint64_t k = 0; begin + warp_group0 + k * ngroups < end; ++k) {
+        const uint64_t c = begin + group + k * ngroups;
+        bool live = c < end;
+        uint32_t p = 0;
+        if (live) {
+            p = cand_pos[c];
+            live = cand_lb[c] <= bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            if (!live && leader) cand_sq[c] = INFINITY;
         }
-        refined += 1;
-        const double s = row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
-        updates += publish(wk, s, c, cand_sq);
+        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, live, s_q, n, &wk->bsf_bits);
+        if (live && leader) {
+            refined += 1;
+            updates += publish(wk, s, c, cand_sq);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         refined += __shfl_xor_sync(0xFFFFFFFFu, refined, o);
         updates += __shfl_xor_sync(0xFFFFFFFFu, updates, o);
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         if (refined) atomicAdd(&wk->stats[kRealDist], refined);
         if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
     }
@@ -432,13 +523,16 @@ __global__ void __launch_bounds__(kThreads)
 // distance; the last block to finish writes the result and resets `wk`.
 __global__ void __launch_bounds__(kThreads)
     k_finalize(QueryWork* wk, const uint32_t* __restrict__ cand_pos, const double* __restrict__ cand_sq, int seed_only,
-               DevResult* out, uint64_t P, uint64_t pos_offset) {
+               uint64_t cap, DevResult* out, uint64_t P, uint64_t pos_offset) {
     const double best = bsf_of(wk->bsf_bits);
     const double dist = sqrt(best);
     const double lim = best * kSlack;
-    const uint32_t end = seed_only ? wk->nseed : wk->ncand;
+    const uint64_t lo_end = seed_only ? wk->nseed : wk->ncand;
+    const uint64_t hi_n = seed_only ? 0 : wk->nhigh;
     uint32_t mine = 0xFFFFFFFFu;
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < end; c += gridDim.x * blockDim.x) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < lo_end + hi_n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t c = i < lo_end ? i : cap - 1 - (i - lo_end);
         const double s = cand_sq[c];
         if (s <= lim && sqrt(s) == dist) mine = min(mine, cand_pos[c]);
     }
@@ -461,7 +555,7 @@ __global__ void __launch_bounds__(kThreads)
     out->stats[kRealDist] = wk->stats[kRealDist];
     out->stats[kBsfUpd] = wk->stats[kBsfUpd];
     out->stats[kPruned] = wk->stats[kPruned];
-    out->stats[kQueueIns] = wk->ncand - wk->nseed;
+    out->stats[kQueueIns] = wk->ncand - wk->nseed + wk->nhigh;
     reset_work(wk);  // for the next query on this stream
     __threadfence();
     wk->done_blocks = 0;
@@ -469,6 +563,13 @@ __global__ void __launch_bounds__(kThreads)
 
 unsigned cap_grid(uint64_t want, int sms, int per_sm) {
     return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms) * per_sm)));
+}
+
+template <typename K>
+int blocks_per_sm(K kernel, size_t smem) {
+    int b = 0;
+    TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, smem));
+    return std::max(b, 1);
 }
 
 }  // namespace
@@ -479,22 +580,30 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     const size_t lut_bytes = static_cast<size_t>(w) * 256 * sizeof(float);
     const size_t q_bytes = static_cast<size_t>(n) * sizeof(float);
     const bool vec = (n % 8) == 0 && (reinterpret_cast<uintptr_t>(ix.rows) % 32) == 0;
+    const bool w16 = w == 16;
     auto refine = vec ? k_refine<true> : k_refine<false>;
     auto seed = vec ? k_seed<true> : k_seed<false>;
-    auto lbscan = ix.ws == 16 ? k_lbscan<16> : k_lbscan<32>;
+    auto lbscan = ix.ws == 16 ? (w16 ? k_lbscan<16, true> : k_lbscan<16, false>) : k_lbscan<32, false>;
+    auto bound = ix.ws == 16 ? (w16 ? k_bound<16, true> : k_bound<16, false>) : k_bound<32, false>;
     // Per-device function attributes (cheap; set on every call so each device is covered).
     TSG_CUDA(cudaFuncSetAttribute(refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(lbscan, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    TSG_CUDA(cudaFuncSetAttribute(k_bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    TSG_CUDA(cudaFuncSetAttribute(bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
-    const unsigned bound_grid = cap_grid((ix.P + kThreads - 1) / kThreads, ix.sms, 4);
-    const unsigned filter_grid = cap_grid((ix.P + kThreads - 1) / kThreads, ix.sms, 8);
-    const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) + 127) / 128, ix.sms, 2);
+    const unsigned bound_grid =
+        cap_grid((ix.P + kThreads - 1) / kThreads, ix.sms, blocks_per_sm(bound, lut_bytes));
+    const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
+                                        ix.sms, blocks_per_sm(seed, q_bytes));
+    const unsigned scan_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(lbscan, lut_bytes));
+    const unsigned refine_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(refine, q_bytes));
+    const uint64_t cap = ix.cand_cap;
+    // Profiling runs one lane so per-kernel times are not overlapped.
+    const int nl = ix.profile ? 1 : std::max(1, std::min<int>(ix.nlanes, static_cast<int>(nq)));
 
     // Optional per-kernel timing: events around every launch, summed after the batch.
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
-    auto mark = [&](int slot, auto&& launch) {
+    auto mark = [&](cudaStream_t ls, int slot, auto&& launch) {
         if (!ix.profile) {
             launch();
             return;
@@ -502,46 +611,60 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
         cudaEvent_t a, b;
         TSG_CUDA(cudaEventCreate(&a));
         TSG_CUDA(cudaEventCreate(&b));
-        TSG_CUDA(cudaEventRecord(a, st));
+        TSG_CUDA(cudaEventRecord(a, ls));
         launch();
-        TSG_CUDA(cudaEventRecord(b, st));
+        TSG_CUDA(cudaEventRecord(b, ls));
         marks.push_back({slot, {a, b}});
     };
 
-    k_reset<<<1, 1, 0, st>>>(ix.work);
-    TSG_LAUNCHED();
-    for (uint32_t qi = 0; qi < nq; ++qi) {
-        const float* q = d_queries + static_cast<uint64_t>(qi) * n;
-        mark(1, [&] {
-            k_bound<<<bound_grid, kThreads, lut_bytes, st>>>(q, n, w, ix.bits, ix.thr, ix.page_lo, ix.page_hi, ix.P,
-                                                             ix.ws, ix.work, ix.page_lb);
-        });
+    // Fork: every lane starts after the work already queued on the index stream.
+    TSG_CUDA(cudaEventRecord(ix.lanes[0].done, st));
+    for (int k = 0; k < nl; ++k) {
+        DevIndex::Lane& L = ix.lanes[k];
+        if (k > 0) TSG_CUDA(cudaStreamWaitEvent(L.stream, ix.lanes[0].done, 0));
+        k_reset<<<1, 1, 0, L.stream>>>(L.work);
         TSG_LAUNCHED();
-        mark(2, [&] {
-            seed<<<seed_grid, 128, q_bytes, st>>>(ix.rows, n, q, ix.leaf_off, ix.page_off, ix.page_leaf, ix.pos,
-                                                  seed_cap, ix.work, ix.cand_pos, ix.cand_sq);
+    }
+    for (uint32_t qi = 0; qi < nq; ++qi) {
+        const DevIndex::Lane& L = ix.lanes[qi % nl];
+        cudaStream_t ls = L.stream;
+        const float* q = d_queries + static_cast<uint64_t>(qi) * n;
+        mark(ls, 2, [&] {
+            seed<<<seed_grid, kThreads, q_bytes, ls>>>(ix.rows, n, w, ix.bits, ix.thr, q, ix.leaf_off, ix.page_off,
+                                                       ix.page_leaf, ix.page_key, ix.page_dir, ix.P, ix.pos, seed_cap,
+                                                       L.work, L.cand_pos, L.cand_sq);
         });
         TSG_LAUNCHED();
         if (!approximate) {
-            mark(3, [&] { k_filter<<<filter_grid, kThreads, 0, st>>>(ix.page_lb, ix.page_off, ix.P, ix.work, ix.surv); });
-            TSG_LAUNCHED();
-            mark(4, [&] {
-                lbscan<<<ix.sms * 4, kThreads, lut_bytes, st>>>(q, n, w, ix.bits, ix.thr, ix.words, ix.pos,
-                                                                ix.page_off, ix.surv, ix.work, ix.cand_pos,
-                                                                ix.cand_lb);
+            mark(ls, 1, [&] {
+                bound<<<bound_grid, kThreads, lut_bytes, ls>>>(q, n, w, ix.bits, ix.thr, ix.page_lo, ix.page_hi,
+                                                               ix.page_off, ix.P, L.work, L.surv);
             });
             TSG_LAUNCHED();
-            mark(5, [&] {
-                refine<<<ix.sms * 8, kThreads, q_bytes, st>>>(ix.rows, n, q, ix.work, ix.cand_pos, ix.cand_lb,
-                                                              ix.cand_sq);
+            mark(ls, 4, [&] {
+                lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(q, n, w, ix.bits, ix.thr, ix.words, ix.pos,
+                                                               ix.page_off, L.surv, L.work, ix.refine_split, cap,
+                                                               L.cand_pos, L.cand_lb);
             });
             TSG_LAUNCHED();
+            for (int wave = 0; wave < 2; ++wave) {
+                mark(ls, wave == 0 ? 3 : 5, [&] {
+                    refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, L.work, L.cand_pos, L.cand_lb,
+                                                                   L.cand_sq, wave, cap);
+                });
+                TSG_LAUNCHED();
+            }
         }
-        mark(6, [&] {
-            k_finalize<<<ix.sms, kThreads, 0, st>>>(ix.work, ix.cand_pos, ix.cand_sq, approximate ? 1 : 0,
+        mark(ls, 6, [&] {
+            k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
                                                     ix.results + qi, ix.P, ix.pos_offset);
         });
         TSG_LAUNCHED();
+    }
+    // Join: the index stream waits for every lane.
+    for (int k = 1; k < nl; ++k) {
+        TSG_CUDA(cudaEventRecord(ix.lanes[k].done, ix.lanes[k].stream));
+        TSG_CUDA(cudaStreamWaitEvent(st, ix.lanes[k].done, 0));
     }
     if (!marks.empty()) {
         TSG_CUDA(cudaStreamSynchronize(st));
