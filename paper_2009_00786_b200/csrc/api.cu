@@ -149,6 +149,7 @@ void free_shard(DevIndex& s) {
     for (int k = 0; k < DevIndex::kLanes; ++k) {
         DevIndex::Lane& l = s.lanes[k];
         cudaFree(l.work);
+        cudaFree(l.lut);
         cudaFree(l.surv);
         cudaFree(l.cand_pos);
         cudaFree(l.cand_lb);
@@ -212,6 +213,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         else TSG_CUDA(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
         TSG_CUDA(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
         TSG_CUDA(cudaMalloc(&l.work, sizeof(QueryWork)));
+        TSG_CUDA(cudaMalloc(&l.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
         TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
         TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
         TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));

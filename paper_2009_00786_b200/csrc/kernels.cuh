@@ -44,6 +44,7 @@ struct DevIndex {
         cudaStream_t stream = nullptr;  // lane 0 uses the index stream
         cudaEvent_t done = nullptr;
         struct QueryWork* work = nullptr;
+        float* lut = nullptr;          // [w][256] squared-gap table of the lane's query
         uint32_t* surv = nullptr;      // [P] surviving pages of the lane's query
         uint32_t* cand_pos = nullptr;  // [cap]
         float* cand_lb = nullptr;      // [cap]

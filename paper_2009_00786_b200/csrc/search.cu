@@ -71,6 +71,24 @@ struct QueryShared {
     unsigned char qsym[kMaxW];
 };
 
+// The [w][256] table: per segment s and symbol byte v, the squared gap
+// between the query's PAA mean and v's region, times n/w, rounded down.
+__device__ __forceinline__ void fill_lut(const QueryShared& qs, int n, int w, int bits, float* out) {
+    const unsigned card = 1u << bits;
+    const double scale = static_cast<double>(n) / static_cast<double>(w);
+    for (int idx = threadIdx.x; idx < w * 256; idx += blockDim.x) {
+        const int s = idx >> 8, v = idx & 255;
+        const unsigned prefix = static_cast<unsigned>(v) >> (8 - bits);
+        const double lo = prefix == 0 ? -INFINITY : qs.thr[prefix - 1];
+        const double hi = prefix == card - 1 ? INFINITY : qs.thr[prefix];
+        const double x = qs.qpaa[s];
+        double gap = 0.0;
+        if (x < lo) gap = lo - x;
+        else if (x > hi) gap = x - hi;
+        out[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
+    }
+}
+
 // Block-local query preparation: PAA (FP64, reference order) and symbols;
 // with lut != nullptr also the [w][256] squared-gap table.
 __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
@@ -88,19 +106,18 @@ __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bit
     }
     __syncthreads();
     if (!s_lut) return;
-    const unsigned card = 1u << bits;
-    const double scale = static_cast<double>(n) / static_cast<double>(w);
-    for (int idx = threadIdx.x; idx < w * 256; idx += blockDim.x) {
-        const int s = idx >> 8, v = idx & 255;
-        const unsigned prefix = static_cast<unsigned>(v) >> (8 - bits);
-        const double lo = prefix == 0 ? -INFINITY : qs.thr[prefix - 1];
-        const double hi = prefix == card - 1 ? INFINITY : qs.thr[prefix];
-        const double x = qs.qpaa[s];
-        double gap = 0.0;
-        if (x < lo) gap = lo - x;
-        else if (x > hi) gap = x - hi;
-        s_lut[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
-    }
+    fill_lut(qs, n, w, bits, s_lut);
+    __syncthreads();
+}
+
+// Loads the table and the query symbols the seed kernel prepared for this
+// query (one 16 KB L2 read per block instead of recomputing 4K FP64 gaps).
+__device__ __forceinline__ void load_prepared(const float* __restrict__ lut_g, const QueryWork* wk, int w,
+                                              float* s_lut, unsigned char* qsym) {
+    const float4* src = reinterpret_cast<const float4*>(lut_g);
+    float4* dst = reinterpret_cast<float4*>(s_lut);
+    for (int i = threadIdx.x; i < w * 64; i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < kMaxW; i += blockDim.x) qsym[i] = i < w ? wk->qsym[i] : 0;
     __syncthreads();
 }
 
@@ -272,12 +289,16 @@ __global__ void __launch_bounds__(kThreads)
            const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ page_leaf,
            const uint64_t* __restrict__ page_key, const uint64_t* __restrict__ page_dir, uint64_t P,
            const uint32_t* __restrict__ pos, uint32_t seed_cap, QueryWork* wk, uint32_t* __restrict__ cand_pos,
-           double* __restrict__ cand_sq) {
+           double* __restrict__ cand_sq, float* __restrict__ lut_out) {
     extern __shared__ float s_q[];
     __shared__ QueryShared qs;
     __shared__ uint32_t s_range[2];
     load_query(s_q, query, n);
     prepare_query(s_q, n, w, bits, thr_g, qs, nullptr);
+    if (blockIdx.x == gridDim.x - 1) {  // one block publishes the query's table and symbols
+        fill_lut(qs, n, w, bits, lut_out);
+        if (threadIdx.x < w) wk->qsym[threadIdx.x] = qs.qsym[threadIdx.x];
+    }
     const uint32_t page = locate_page(page_key, page_dir, P, query_key(qs.qsym, w));
     if (threadIdx.x == 0) {
         const uint32_t leaf = page_leaf[page];
@@ -321,46 +342,72 @@ __global__ void __launch_bounds__(kThreads)
 
 // ------------------------------------------------------- bound + filter
 // Box bound per page: per segment the table entry of the query symbol
-// clamped into the box [lo, hi] (0 when the query symbol is inside).
+// clamped into the box [lo, hi] (0 when the query symbol is inside). Pages
+// whose bound is within the BSF (and outside the seed range) survive. A
+// persistent grid; each thread bounds kPP pages per round (all loads issued
+// first) and one atomic per block and round reserves survivor slots.
+constexpr int kPP = 4;
+
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
-    k_bound(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
-            const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, const uint32_t* __restrict__ page_off,
-            uint64_t P, QueryWork* wk, uint32_t* __restrict__ surv) {
+    k_bound(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
+            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, uint32_t* __restrict__ surv) {
     extern __shared__ float s_lut[];
-    __shared__ QueryShared qs;
+    __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_cnt[kThreads / 32];
     __shared__ uint32_t s_base;
-    prepare_query(q, n, w, bits, thr_g, qs, s_lut);
+    load_prepared(lut_g, wk, w, s_lut, qsym);
     uint4 q4[WS / 16];
 #pragma unroll
-    for (int h = 0; h < WS / 16; ++h) q4[h] = *reinterpret_cast<const uint4*>(qs.qsym + 16 * h);
+    for (int h = 0; h < WS / 16; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
     const float bound = bound_from_bits(wk->bsf_bits);
     const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
     unsigned long long pruned = 0;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < P;
-         base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t p = base + threadIdx.x;
-        bool keep = false;
-        if (p < P) {
-            uint4 c[WS / 16];
+    constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kPP;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < P;
+         base += static_cast<uint64_t>(gridDim.x) * kRound) {
+        uint4 blo[kPP][WS / 16], bhi[kPP][WS / 16];
+        uint32_t ea[kPP], eb[kPP];
+#pragma unroll
+        for (int k = 0; k < kPP; ++k) {
+            const uint64_t p = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            const bool in = p < P;
 #pragma unroll
             for (int h = 0; h < WS / 16; ++h) {
-                const uint4 a = ld_stream_u4(lo + p * WS + 16 * h);
-                const uint4 b = ld_stream_u4(hi + p * WS + 16 * h);
-                c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, a.x), b.x), __vminu4(__vmaxu4(q4[h].y, a.y), b.y),
-                                  __vminu4(__vmaxu4(q4[h].z, a.z), b.z), __vminu4(__vmaxu4(q4[h].w, a.w), b.w));
+                blo[k][h] = in ? ld_stream_u4(lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bhi[k][h] = in ? ld_stream_u4(hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
             }
+            ea[k] = in ? page_off[p] : 0u;
+            eb[k] = in ? page_off[p + 1] : 0u;
+        }
+        unsigned keepmask = 0;
+#pragma unroll
+        for (int k = 0; k < kPP; ++k) {
+            const uint64_t p = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            if (p >= P) continue;
+            uint4 c[WS / 16];
+#pragma unroll
+            for (int h = 0; h < WS / 16; ++h)
+                c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, blo[k][h].x), bhi[k][h].x),
+                                  __vminu4(__vmaxu4(q4[h].y, blo[k][h].y), bhi[k][h].y),
+                                  __vminu4(__vmaxu4(q4[h].z, blo[k][h].z), bhi[k][h].z),
+                                  __vminu4(__vmaxu4(q4[h].w, blo[k][h].w), bhi[k][h].w));
             const float lb = word_bound<W16>(s_lut, c, w);
-            const uint32_t ea = page_off[p], eb = page_off[p + 1];
-            const bool seeded = ea >= sa && eb <= sb;
-            keep = !seeded && lb <= bound;
+            const bool seeded = ea[k] >= sa && eb[k] <= sb;
+            const bool keep = !seeded && lb <= bound;
+            keepmask |= keep ? (1u << k) : 0u;
             pruned += (!keep && !seeded) ? 1 : 0;
         }
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
-        if (lane == 0) s_cnt[warp] = __popc(m);
+        const int mine = __popc(keepmask);
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_cnt[warp] = incl;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint32_t tot = 0;
@@ -372,7 +419,10 @@ __global__ void __launch_bounds__(kThreads)
             s_base = tot ? atomicAdd(&wk->nsurv, tot) : 0u;
         }
         __syncthreads();
-        if (keep) surv[s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = static_cast<uint32_t>(p);
+        uint32_t at = s_base + s_cnt[warp] + (incl - mine);
+#pragma unroll
+        for (int k = 0; k < kPP; ++k)
+            if (keepmask & (1u << k)) surv[at++] = static_cast<uint32_t>(base + threadIdx.x + kThreads * k);
         __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
@@ -419,15 +469,15 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
 // page with all of its loads in flight at once.
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
-    k_lbscan(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
-             const uint8_t* __restrict__ words, const uint32_t* __restrict__ pos,
+    k_lbscan(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ words,
+             const uint32_t* __restrict__ pos,
              const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ surv, QueryWork* wk, float split,
              uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
     extern __shared__ float s_lut[];
-    __shared__ QueryShared qs;
+    __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_pos[kThreads / 32][kStageCap];
     __shared__ float s_lb[kThreads / 32][kStageCap];
-    prepare_query(q, n, w, bits, thr_g, qs, s_lut);
+    load_prepared(lut_g, wk, w, s_lut, qsym);
     constexpr int H = WS / 16;
     constexpr int K = kPage / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -591,8 +641,8 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     TSG_CUDA(cudaFuncSetAttribute(lbscan, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
-    const unsigned bound_grid =
-        cap_grid((ix.P + kThreads - 1) / kThreads, ix.sms, blocks_per_sm(bound, lut_bytes));
+    const unsigned bound_grid = cap_grid((ix.P + kThreads * kPP - 1) / (kThreads * kPP), ix.sms,
+                                         std::min(2, blocks_per_sm(bound, lut_bytes)));
     const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
                                         ix.sms, blocks_per_sm(seed, q_bytes));
     const unsigned scan_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(lbscan, lut_bytes));
@@ -632,19 +682,18 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
         mark(ls, 2, [&] {
             seed<<<seed_grid, kThreads, q_bytes, ls>>>(ix.rows, n, w, ix.bits, ix.thr, q, ix.leaf_off, ix.page_off,
                                                        ix.page_leaf, ix.page_key, ix.page_dir, ix.P, ix.pos, seed_cap,
-                                                       L.work, L.cand_pos, L.cand_sq);
+                                                       L.work, L.cand_pos, L.cand_sq, L.lut);
         });
         TSG_LAUNCHED();
         if (!approximate) {
             mark(ls, 1, [&] {
-                bound<<<bound_grid, kThreads, lut_bytes, ls>>>(q, n, w, ix.bits, ix.thr, ix.page_lo, ix.page_hi,
-                                                               ix.page_off, ix.P, L.work, L.surv);
+                bound<<<bound_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.page_lo, ix.page_hi, ix.page_off, ix.P,
+                                                               L.work, L.surv);
             });
             TSG_LAUNCHED();
             mark(ls, 4, [&] {
-                lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(q, n, w, ix.bits, ix.thr, ix.words, ix.pos,
-                                                               ix.page_off, L.surv, L.work, ix.refine_split, cap,
-                                                               L.cand_pos, L.cand_lb);
+                lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, ix.page_off, L.surv,
+                                                               L.work, ix.refine_split, cap, L.cand_pos, L.cand_lb);
             });
             TSG_LAUNCHED();
             for (int wave = 0; wave < 2; ++wave) {
