@@ -209,7 +209,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&ix.leaf_off, (N + 1) * 4));
-    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in(N * 4), flags(N), bstart(N * 4), nsel(8),
+    // pos_in / bstart are reused for the L+1 page counts / bases (L <= N).
+    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in((N + 1) * 4), flags(N), bstart((N + 1) * 4),
+        nsel(8),
         leaf_start(N * 4), ranges_a(open_cap * sizeof(Range)), ranges_b(open_cap * sizeof(Range)),
         ctr(sizeof(LeafCounters));
     size_t tb_sort = 0, tb_sel = 0, tb_lsort = 0, tb_scan = 0;
