@@ -20,7 +20,10 @@ LIB = os.path.join(PKG, "libtsgpu.so")
 BUILD = os.path.join(PKG, "_build")
 
 CU_SOURCES = ["summarise.cu", "build.cu", "search.cu", "generate.cu", "api.cu"]
-CPP_SOURCES = ["breakpoints.cpp"]
+# host C++: (file, extra flags). breakpoints.cpp must match the reference's
+# x86-64 arithmetic (no -march, no FMA); tsidx_api.cpp is the C++20 drop-in API.
+CPP_SOURCES = [("breakpoints.cpp", ["-std=c++17"]),
+               ("tsidx_api.cpp", ["-std=c++20", "-I/usr/local/cuda/include"])]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,7 +32,7 @@ NVCC_FLAGS = [
     "-I" + os.path.join(ROOT, "include"),
 ]
 # Host C++ that must be bit-identical to the reference's x86-64 build: no -march, no FMA.
-CXX_FLAGS = ["-std=c++17", "-O3", "-fPIC", "-ffp-contract=off"]
+CXX_FLAGS = ["-O3", "-fPIC", "-ffp-contract=off"]
 
 
 def _run(cmd):
@@ -57,11 +60,11 @@ def build_library(force: bool = False, verbose_ptxas: bool = False) -> str:
             _run([NVCC, *NVCC_FLAGS, *extra, "-c", s, "-o", o])
         objs.append(o)
     cxx = os.environ.get("CXX", "g++")
-    for src in CPP_SOURCES:
+    for src, extra in CPP_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
-        if force or _stale(o, [s]):
-            _run([cxx, *CXX_FLAGS, "-c", s, "-o", o])
+        if force or _stale(o, [s, *headers, os.path.join(ROOT, "include", "tsidx", "tsidx.hpp")]):
+            _run([cxx, *CXX_FLAGS, *extra, "-c", s, "-o", o])
         objs.append(o)
     if force or _stale(LIB, objs):
         _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs,
