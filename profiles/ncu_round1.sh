@@ -1,9 +1,17 @@
 #!/bin/bash
-# ncu captures for round 1 (run under gpurun from the repo root).
-# Plain run first (must exit 0), then one full-set capture per hot kernel.
+# Round-1 ncu evidence (run under gpurun from the repo root, one GPU).
+#  1. plain run of the bench command (must exit 0 first),
+#  2. launch list: every kernel launch with its device time (cold-cache,
+#     serialised: compare SHARES, not absolutes),
+#  3. one --set full capture per hot kernel (K1 summarise, bound, lbscan, refine).
 set -e
-CMD="python bench.py --count 20000000 --steps 1 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/ncu_plain.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_summarise -c 1 -o gpurun_out/prof_k1 $CMD > gpurun_out/ncu_k1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_lbscan -s 200 -c 2 -o gpurun_out/prof_lbscan $CMD > gpurun_out/ncu_lbscan.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_refine -s 400 -c 2 -o gpurun_out/prof_refine $CMD > gpurun_out/ncu_refine.log 2>&1
+TSG_QUERY_LANES=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_summarise -c 1 \
+    -o gpurun_out/prof_k_summarise $CMD > gpurun_out/ncu_k1.log 2>&1
+for k in k_bound k_lbscan k_refine; do
+  TSG_QUERY_LANES=1 ncu --set full --clock-control none --import-source on -k regex:$k -s 40 -c 2 \
+      -o gpurun_out/prof_$k $CMD > gpurun_out/ncu_$k.log 2>&1
+done
