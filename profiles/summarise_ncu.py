@@ -72,7 +72,7 @@ def read_launches(path):
     for r in rows[1:]:
         if r[mi] != "gpu__time_duration.sum":
             continue
-        name = r[ki].replace("void ", "").replace("(anonymous namespace)::", "").replace("unnamed>::", "")
+        name = r[ki].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
         name = name.split("(")[0].split("<")[0].strip()
         v = float(r[vi].replace(",", "")) * UNIT_SCALE.get(r[ui], 1.0)
         per[name]["launches"] += 1
