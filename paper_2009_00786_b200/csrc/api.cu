@@ -140,12 +140,11 @@ void free_shard(DevIndex& s) {
     cudaFree(s.words);
     cudaFree(s.pos);
     cudaFree(s.leaf_off);
-    cudaFree(s.page_off);
-    cudaFree(s.page_leaf);
-    cudaFree(s.page_key);
-    cudaFree(s.page_lo);
-    cudaFree(s.page_hi);
-    cudaFree(s.page_dir);
+    // page arrays come from the stream-ordered pool (build.cu)
+    for (void* p : {static_cast<void*>(s.page_off), static_cast<void*>(s.page_leaf), static_cast<void*>(s.page_key),
+                    static_cast<void*>(s.page_lo), static_cast<void*>(s.page_hi), static_cast<void*>(s.page_dir)})
+        if (p) cudaFreeAsync(p, s.stream);
+    if (s.stream) cudaStreamSynchronize(s.stream);
     for (int k = 0; k < DevIndex::kLanes; ++k) {
         DevIndex::Lane& l = s.lanes[k];
         cudaFree(l.work);
@@ -163,12 +162,20 @@ void free_shard(DevIndex& s) {
     s = DevIndex{};
 }
 
+// Host image of the device threshold block: 256 doubles + the fast-symbol bins.
+std::vector<unsigned char> threshold_block(int bits) {
+    std::vector<unsigned char> blk(kThrBytes);
+    double* thr = reinterpret_cast<double*>(blk.data());
+    host_breakpoints(bits, thr);
+    host_symbol_bins(thr, bits, kBinRange, kBins, blk.data() + kThrPad * sizeof(double));
+    return blk;
+}
+
 double* upload_thresholds(int bits) {
-    double h[kThrPad];
-    host_breakpoints(bits, h);
+    const auto h = threshold_block(bits);
     double* d = nullptr;
-    TSG_CUDA(cudaMalloc(&d, sizeof(h)));
-    TSG_CUDA(cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice));
+    TSG_CUDA(cudaMalloc(&d, h.size()));
+    TSG_CUDA(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
     return d;
 }
 
@@ -508,12 +515,11 @@ tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length,
         int dev = 0;
         TSG_CUDA(cudaGetDevice(&dev));
         check_device(dev);
-        double h[kThrPad];
-        host_breakpoints(bits, h);
+        const auto h = threshold_block(bits);
         double* d = nullptr;
         auto st = static_cast<cudaStream_t>(stream);
-        TSG_CUDA(cudaMallocAsync(&d, sizeof(h), st));
-        TSG_CUDA(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, st));
+        TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), h.size(), st));
+        TSG_CUDA(cudaMemcpyAsync(d, h.data(), h.size(), cudaMemcpyHostToDevice, st));
         summarise(dev_rows, count, static_cast<int>(length), w, bits, d, dev_words, dev_root_keys, nullptr, st);
         TSG_CUDA(cudaFreeAsync(d, st));
         TSG_CUDA(cudaStreamSynchronize(st));

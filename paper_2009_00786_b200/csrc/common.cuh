@@ -54,6 +54,14 @@ constexpr int kThrPad = 256;  // padded threshold table entries per cardinality
 // identical to tsidx::breakpoints_for (src/breakpoints.cpp:65-114).
 void host_breakpoints(int bits, double* out256);
 
+// Fast-symbol bins (see host_symbol_bins): kBins bins over [-kBinRange, kBinRange).
+constexpr int kBins = 4096;
+constexpr double kBinRange = 6.0;
+void host_symbol_bins(const double* thr256, int bits, double range, int nbins, unsigned char* bins);
+
+// Layout of the device threshold block: 256 doubles then kBins bytes.
+constexpr size_t kThrBytes = kThrPad * sizeof(double) + kBins;
+
 // ---- small PTX helpers ----------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -94,6 +102,21 @@ __device__ __forceinline__ unsigned symbol_of(const double* thr, int bits, doubl
             if (!(v < thr[s + step - 1])) s += step;
         }
     }
+    return s;
+}
+
+// The same number of thresholds <= v via the bin table: start from the bin's
+// count and walk to the exact upper_bound (0-1 steps when bins are narrower
+// than the threshold spacing). Out-of-range values and NaN take the plain
+// binary search.
+__device__ __forceinline__ unsigned symbol_fast(const double* thr, const unsigned char* bins, int bits, double v) {
+    if (!(v >= -kBinRange && v < kBinRange)) return symbol_of(thr, bits, v);
+    int b = __double2int_rz(__dmul_rn(__dadd_rn(v, kBinRange), kBins / (2.0 * kBinRange)));
+    b = min(max(b, 0), kBins - 1);
+    unsigned s = bins[b];
+    const unsigned top = (1u << bits) - 1u;
+    while (s > 0 && v < thr[s - 1]) --s;
+    while (s < top && !(v < thr[s])) ++s;
     return s;
 }
 

@@ -182,35 +182,36 @@ __device__ __forceinline__ double block_sq(const float* x, const float* q, int c
 // bytes per load); the group leader then adds the block sums left to right,
 // squared_l2's order. Rows longer than 256 take several rounds; after each
 // round the running sum is checked against the live BSF (strict), the
-// reference's abandonment (metrics.cpp:28). All 32 lanes must call this.
-// Returns the sum on the group leader (lane % 8 == 0), +inf if abandoned.
+// reference's abandonment (metrics.cpp:28). Group-local: only the group's 8
+// lanes take part (shuffles use the group mask), so groups of a warp work on
+// different candidates independently. Every lane of the group returns the
+// sum, +inf if abandoned.
 template <bool VEC>
-__device__ __forceinline__ double group_row_sq(const float* __restrict__ row, bool live, const float* __restrict__ s_q,
-                                               int n, const unsigned long long* bsf) {
+__device__ __forceinline__ double group_row_sq(const float* __restrict__ row, const float* __restrict__ s_q, int n,
+                                               const unsigned long long* bsf) {
     const int lane = threadIdx.x & 31, j = lane & (kRowLanes - 1), base = lane & ~(kRowLanes - 1);
+    const unsigned gmask = 0xFFu << base;
     const int nb = (n + 7) >> 3;
     double sum = 0.0;
-    bool dead = !live;
     for (int r0 = 0; r0 < nb; r0 += 32) {
-        double blk[4];
+        double blk[4] = {0.0, 0.0, 0.0, 0.0};
         if (VEC) {
             F8 x[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int b = r0 + j + kRowLanes * t;
-                if (!dead && b < nb) x[t] = ld256(row + 8 * b);
+                if (b < nb) x[t] = ld256(row + 8 * b);
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int b = r0 + j + kRowLanes * t;
-                blk[t] = (!dead && b < nb) ? block_sq(x[t].v, s_q + 8 * b, 8) : 0.0;
+                if (b < nb) blk[t] = block_sq(x[t].v, s_q + 8 * b, 8);
             }
         } else {
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int b = r0 + j + kRowLanes * t;
-                blk[t] = 0.0;
-                if (!dead && b < nb) {
+                if (b < nb) {
                     const int cnt = min(8, n - 8 * b);
                     float x[8];
 #pragma unroll
@@ -225,21 +226,26 @@ __device__ __forceinline__ double group_row_sq(const float* __restrict__ row, bo
         for (int t = 0; t < 4; ++t)
 #pragma unroll
             for (int i = 0; i < kRowLanes; ++i) {
-                const double v = __shfl_sync(0xFFFFFFFFu, blk[t], base + i);
+                const double v = __shfl_sync(gmask, blk[t], base + i);
                 if (r0 + kRowLanes * t + i < nb) sum = __dadd_rn(sum, v);
             }
-        if (r0 + 32 < nb && bsf && !dead && sum > bsf_of(ld_volatile_u64(bsf)) * kSlack) dead = true;
+        if (r0 + 32 < nb && bsf && sum > bsf_of(ld_volatile_u64(bsf)) * kSlack) return INFINITY;
     }
-    return dead ? INFINITY : sum;
+    return sum;
 }
 
 // Publishes a finished sum: candidate record, BSF atomicMin only when it can
-// improve, strict-improvement count.
-__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq) {
+// improve, strict-improvement count. *seen receives the BSF observed (an
+// upper bound of the current BSF, for the caller's cached pruning bound).
+__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq,
+                                                      unsigned long long* seen = nullptr) {
     cand_sq[c] = s;
+    const unsigned long long cur = ld_volatile_u64(&wk->bsf_bits);
+    if (seen) *seen = cur;
     if (!(s < INFINITY)) return 0;
     const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(s));
-    if (sb >= ld_volatile_u64(&wk->bsf_bits)) return 0;
+    if (sb >= cur) return 0;
+    if (seen) *seen = sb;
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
 }
 
@@ -324,20 +330,15 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
     unsigned long long updates = 0;
-    // Uniform trip count per warp: every lane iterates while any group of the warp has work.
-    const uint64_t warp_group0 = group - ((lane & 31) / kRowLanes);
-    for (uint64_t k = 0; a + warp_group0 + k * ngroups < b; ++k) {
-        const uint64_t e = a + group + k * ngroups;
-        const bool live = e < b;
-        const uint32_t p = live ? pos[e] : 0u;
-        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, live, s_q, n, &wk->bsf_bits);
-        if (live && (lane & (kRowLanes - 1)) == 0) {
+    for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
+        const uint32_t p = pos[e];
+        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
+        if ((lane & (kRowLanes - 1)) == 0) {
             cand_pos[e - a] = p;
             updates += publish(wk, s, e - a, cand_sq);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) updates += __shfl_xor_sync(0xFFFFFFFFu, updates, o);
-    if (lane == 0 && updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+    if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
 }
 
 // ------------------------------------------------------- bound + filter
@@ -488,18 +489,31 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
     int cnt = 0;
     unsigned long long scanned = 0;
-    for (uint64_t i = gwarp; i < nsurv; i += nwarps) {
+    // Software pipeline: the next page's words are in flight while this one is bounded.
+    uint32_t na = 0, nb = 0;
+    uint4 nwv[K][H];
+    auto fetch = [&](uint64_t i) {
         const uint32_t page = surv[i];
-        const uint32_t a = page_off[page], b = page_off[page + 1];
-        scanned += b - a;
-        uint4 wv[K][H];
+        na = page_off[page];
+        nb = page_off[page + 1];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            const uint32_t e = a + lane + 32 * k;
+            const uint32_t e = na + lane + 32 * k;
 #pragma unroll
             for (int h = 0; h < H; ++h)
-                wv[k][h] = e < b ? ld_stream_u4(words + static_cast<uint64_t>(e) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                nwv[k][h] = e < nb ? ld_stream_u4(words + static_cast<uint64_t>(e) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
         }
+    };
+    if (gwarp < nsurv) fetch(gwarp);
+    for (uint64_t i = gwarp; i < nsurv; i += nwarps) {
+        const uint32_t a = na, b = nb;
+        uint4 wv[K][H];
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int h = 0; h < H; ++h) wv[k][h] = nwv[k][h];
+        if (i + nwarps < nsurv) fetch(i + nwarps);
+        scanned += b - a;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const uint32_t e = a + lane + 32 * k;
@@ -538,31 +552,39 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t end = wave == 0 ? wk->ncand : cap;
     const int lane = threadIdx.x & 31;
     const bool leader = (lane & (kRowLanes - 1)) == 0;
+    unsigned long long refined = 0, updates = 0;
+    // Each 8-lane group walks its own candidates (group-stride), the next
+    // candidate's record prefetched while the current row is refined; a
+    // candidate whose bound exceeds the live BSF costs one check.
     const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
-    const uint64_t warp_group0 = group - lane / kRowLanes;
-    unsigned long long refined = 0, updates = 0;
-    for (uint64_t k = 0; begin + warp_group0 + k * ngroups < end; ++k) {
-        const uint64_t c = begin + group + k * ngroups;
-        bool live = c < end;
-        uint32_t p = 0;
-        if (live) {
-            p = cand_pos[c];
-            live = cand_lb[c] <= bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
-            if (!live && leader) cand_sq[c] = INFINITY;
+    const unsigned gmask = 0xFFu << (lane & ~(kRowLanes - 1));
+    uint64_t c = begin + group;
+    float nlb = c < end ? cand_lb[c] : 0.f;
+    uint32_t np = c < end ? cand_pos[c] : 0u;
+    // Cached pruning bound: refreshed from the BSF each publish observes, so a
+    // skipped candidate costs no memory access (a stale bound only refines more).
+    float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+    for (; c < end; c += ngroups) {
+        const float lb = nlb;
+        const uint32_t p = np;
+        if (c + ngroups < end) {
+            nlb = cand_lb[c + ngroups];
+            np = cand_pos[c + ngroups];
         }
-        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, live, s_q, n, &wk->bsf_bits);
-        if (live && leader) {
+        if (lb > bnd) {
+            if (leader) cand_sq[c] = INFINITY;
+            continue;
+        }
+        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
+        unsigned long long seen = 0;
+        if (leader) {
             refined += 1;
-            updates += publish(wk, s, c, cand_sq);
+            updates += publish(wk, s, c, cand_sq, &seen);
         }
+        bnd = bound_from_bits(__shfl_sync(gmask, seen, lane & ~(kRowLanes - 1)));
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        refined += __shfl_xor_sync(0xFFFFFFFFu, refined, o);
-        updates += __shfl_xor_sync(0xFFFFFFFFu, updates, o);
-    }
-    if (lane == 0) {
+    if (leader) {
         if (refined) atomicAdd(&wk->stats[kRealDist], refined);
         if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
     }
@@ -642,7 +664,7 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     TSG_CUDA(cudaFuncSetAttribute(bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
     const unsigned bound_grid = cap_grid((ix.P + kThreads * kPP - 1) / (kThreads * kPP), ix.sms,
-                                         std::min(2, blocks_per_sm(bound, lut_bytes)));
+                                         std::min(6, blocks_per_sm(bound, lut_bytes)));
     const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
                                         ix.sms, blocks_per_sm(seed, q_bytes));
     const unsigned scan_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(lbscan, lut_bytes));

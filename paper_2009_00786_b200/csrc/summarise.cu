@@ -119,7 +119,8 @@ __global__ void __launch_bounds__(kSumThreads)
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * stage_stride);
     uint64_t* empty = full + STAGES;
     double* thr = reinterpret_cast<double*>(empty + STAGES);
-    uint8_t* wbuf = reinterpret_cast<uint8_t*>(thr + kThrPad);
+    unsigned char* bins = reinterpret_cast<unsigned char*>(thr + kThrPad);
+    uint8_t* wbuf = bins + kBins;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -130,6 +131,10 @@ __global__ void __launch_bounds__(kSumThreads)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < kThrPad; i += blockDim.x) thr[i] = thr_g[i];
+    {
+        const unsigned char* bins_g = reinterpret_cast<const unsigned char*>(thr_g + kThrPad);
+        for (int i = tid; i < kBins; i += blockDim.x) bins[i] = bins_g[i];
+    }
     for (int i = tid; i < 2 * a.R * a.ws; i += blockDim.x) wbuf[i] = 0;
     __syncthreads();
 
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kSumThreads)
             }
         }
         const double mean = pow2 ? __dmul_rn(sum, inv_seg) : __ddiv_rn(sum, static_cast<double>(a.seg));
-        return symbol_of(thr, a.bits, mean) << (8 - a.bits);
+        return symbol_fast(thr, bins, a.bits, mean) << (8 - a.bits);
     };
 
     int it = 0;
@@ -240,7 +245,10 @@ __global__ void __launch_bounds__(kSumThreads)
 __global__ void k_summarise_generic(const float* __restrict__ rows, SumArgs a,
                                     const double* __restrict__ thr_g) {
     __shared__ double thr[kThrPad];
+    __shared__ unsigned char bins[kBins];
     for (int i = threadIdx.x; i < kThrPad; i += blockDim.x) thr[i] = thr_g[i];
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
+        bins[i] = reinterpret_cast<const unsigned char*>(thr_g + kThrPad)[i];
     __syncthreads();
     uint8_t wrow[kMaxW] = {0};
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < a.count;
@@ -250,7 +258,7 @@ __global__ void k_summarise_generic(const float* __restrict__ rows, SumArgs a,
             double sum = 0.0;
             for (int j = 0; j < a.seg; ++j) sum = __dadd_rn(sum, static_cast<double>(r[g * a.seg + j]));
             const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
-            wrow[g] = static_cast<uint8_t>(symbol_of(thr, a.bits, mean) << (8 - a.bits));
+            wrow[g] = static_cast<uint8_t>(symbol_fast(thr, bins, a.bits, mean) << (8 - a.bits));
         }
         uint8_t buf[32] __attribute__((aligned(16)));
         for (int k = 0; k < 32; ++k) buf[k] = k < a.w ? wrow[k] : 0;
@@ -277,8 +285,7 @@ constexpr int kStages = 3;
 
 size_t tma_smem_bytes(int R, int n, int ws) {
     const size_t stage = ((static_cast<size_t>(R) * n * 4 + 1023) / 1024) * 1024;
-    return 1024 + kStages * stage + 2 * kStages * sizeof(uint64_t) + kThrPad * sizeof(double) +
-           2 * static_cast<size_t>(R) * ws;
+    return 1024 + kStages * stage + 2 * kStages * sizeof(uint64_t) + kThrBytes + 2 * static_cast<size_t>(R) * ws;
 }
 
 }  // namespace
