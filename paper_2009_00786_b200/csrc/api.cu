@@ -150,6 +150,7 @@ void free_shard(DevIndex& s) {
         cudaFree(l.work);
         cudaFree(l.lut);
         cudaFree(l.surv);
+        cudaFree(l.surv_lb);
         cudaFree(l.cand_pos);
         cudaFree(l.cand_lb);
         cudaFree(l.cand_sq);
@@ -223,6 +224,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         TSG_CUDA(cudaMalloc(&l.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
         TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
         TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
+        TSG_CUDA(cudaMalloc(&l.surv_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
         TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));
         TSG_CUDA(cudaMalloc(&l.cand_lb, N * sizeof(float)));
         TSG_CUDA(cudaMalloc(&l.cand_sq, N * sizeof(double)));

@@ -45,7 +45,8 @@ struct DevIndex {
         cudaEvent_t done = nullptr;
         struct QueryWork* work = nullptr;
         float* lut = nullptr;          // [w][256] squared-gap table of the lane's query
-        uint32_t* surv = nullptr;      // [P] surviving pages of the lane's query
+        uint32_t* surv = nullptr;      // [P] surviving pages: wave 0 from the front, wave 1 from the back
+        float* surv_lb = nullptr;      // [P] their box bounds
         uint32_t* cand_pos = nullptr;  // [cap]
         float* cand_lb = nullptr;      // [cap]
         double* cand_sq = nullptr;     // [cap]
@@ -59,7 +60,7 @@ struct DevIndex {
     float* queries = nullptr;      // staging for host queries
     uint32_t queries_cap = 0;
     int sms = 148;
-    float refine_split = 0.5f;     // wave-0 fraction of the scan bound (TSG_REFINE_SPLIT)
+    float refine_split = 0.5f;     // wave-0 page-bound fraction of the seed bound (TSG_REFINE_SPLIT)
     // per-kernel profiling (tsg_profile_enable)
     bool profile = false;
     double prof_ms[8] = {0};
@@ -77,7 +78,8 @@ struct QueryWork {
     unsigned int work_next;
     unsigned int best_pos;
     unsigned int seed_begin, seed_end;  // index range refined as the seed
-    unsigned int nsurv;                 // surviving pages
+    unsigned int nsurv;                 // surviving pages, wave 0 (bound <= split x seed bound)
+    unsigned int nsurv_hi;              // surviving pages, wave 1 (stored from the back of surv)
     unsigned int nhigh;                 // wave-1 candidates, stored at the top of the candidate arrays
     unsigned int done_blocks;           // finalize's last-block counter
     float scan_bound;                   // BSF bound the page/word filters used

@@ -144,6 +144,7 @@ __device__ __forceinline__ void reset_work(QueryWork* wk) {
     wk->work_next = 0;
     wk->best_pos = 0xFFFFFFFFu;
     wk->nsurv = 0;
+    wk->nsurv_hi = 0;
     for (int i = 0; i < 6; ++i) wk->stats[i] = 0;
 }
 
@@ -352,11 +353,12 @@ constexpr int kPP = 4;
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_bound(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
-            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, uint32_t* __restrict__ surv) {
+            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, float split, uint32_t* __restrict__ surv,
+            float* __restrict__ surv_lb) {
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_cnt[kThreads / 32];
-    __shared__ uint32_t s_base;
+    __shared__ uint32_t s_base, s_base_hi;
     load_prepared(lut_g, wk, w, s_lut, qsym);
     uint4 q4[WS / 16];
 #pragma unroll
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
+    const float cut = bound * split;  // wave 0: the most promising pages
     unsigned long long pruned = 0;
     constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kPP;
     for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < P;
@@ -383,10 +386,12 @@ __global__ void __launch_bounds__(kThreads)
             ea[k] = in ? page_off[p] : 0u;
             eb[k] = in ? page_off[p + 1] : 0u;
         }
-        unsigned keepmask = 0;
+        unsigned lowmask = 0, highmask = 0;
+        float lbs[kPP];
 #pragma unroll
         for (int k = 0; k < kPP; ++k) {
             const uint64_t p = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            lbs[k] = 0.f;
             if (p >= P) continue;
             uint4 c[WS / 16];
 #pragma unroll
@@ -396,12 +401,15 @@ __global__ void __launch_bounds__(kThreads)
                                   __vminu4(__vmaxu4(q4[h].z, blo[k][h].z), bhi[k][h].z),
                                   __vminu4(__vmaxu4(q4[h].w, blo[k][h].w), bhi[k][h].w));
             const float lb = word_bound<W16>(s_lut, c, w);
+            lbs[k] = lb;
             const bool seeded = ea[k] >= sa && eb[k] <= sb;
             const bool keep = !seeded && lb <= bound;
-            keepmask |= keep ? (1u << k) : 0u;
+            lowmask |= (keep && lb <= cut) ? (1u << k) : 0u;
+            highmask |= (keep && lb > cut) ? (1u << k) : 0u;
             pruned += (!keep && !seeded) ? 1 : 0;
         }
-        const int mine = __popc(keepmask);
+        // wave-0 count in the low 16 bits, wave-1 count in the high 16 bits
+        const int mine = __popc(lowmask) | (__popc(highmask) << 16);
         int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -417,13 +425,25 @@ __global__ void __launch_bounds__(kThreads)
                 s_cnt[i] = tot;
                 tot += cnt;
             }
-            s_base = tot ? atomicAdd(&wk->nsurv, tot) : 0u;
+            s_base = (tot & 0xFFFFu) ? atomicAdd(&wk->nsurv, tot & 0xFFFFu) : 0u;
+            s_base_hi = (tot >> 16) ? atomicAdd(&wk->nsurv_hi, tot >> 16) : 0u;
         }
         __syncthreads();
-        uint32_t at = s_base + s_cnt[warp] + (incl - mine);
+        const uint32_t before = s_cnt[warp] + (incl - mine);
+        uint32_t at = s_base + (before & 0xFFFFu);
+        uint32_t at_hi = s_base_hi + (before >> 16);
 #pragma unroll
-        for (int k = 0; k < kPP; ++k)
-            if (keepmask & (1u << k)) surv[at++] = static_cast<uint32_t>(base + threadIdx.x + kThreads * k);
+        for (int k = 0; k < kPP; ++k) {
+            const uint32_t p = static_cast<uint32_t>(base + threadIdx.x + kThreads * k);
+            if (lowmask & (1u << k)) {
+                surv_lb[at] = lbs[k];
+                surv[at++] = p;
+            } else if (highmask & (1u << k)) {
+                const uint64_t slot = P - 1 - at_hi++;
+                surv_lb[slot] = lbs[k];
+                surv[slot] = p;
+            }
+        }
         __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
@@ -433,8 +453,9 @@ __global__ void __launch_bounds__(kThreads)
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
 
-// Writes a warp's staged candidates: wave 0 (bound <= cut) grows upward
-// from ncand, wave 1 grows downward from the top of the candidate arrays.
+// Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
+// upward from ncand, wave B downward from the top of the candidate arrays
+// (nhigh). cut = +inf sends everything to A, cut < 0 everything to B.
 __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
                                             float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
@@ -465,15 +486,19 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
     __syncwarp();
 }
 
-// Surviving pages round-robin over warps (each page <= kPage entries, so
-// work units are bounded); a lane bounds entries lane, lane+32, ... of the
-// page with all of its loads in flight at once.
+// One page wave: wave 0 scans the pages whose box bound is within `split`
+// of the seed bound (surv[0, nsurv)), wave 1 the rest (surv[P - nsurv_hi, P)),
+// re-filtered against the BSF that wave 0's refinement tightened — MESSI's
+// LB-ordered leaf processing (src/query.cpp:173-184) at page granularity.
+// Surviving pages go round-robin over warps (each <= kPage entries, so work
+// units are bounded); a lane bounds entries lane, lane+32, ... of a page, the
+// next page's words in flight while the current one is bounded.
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_lbscan(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ words,
-             const uint32_t* __restrict__ pos,
-             const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ surv, QueryWork* wk, float split,
-             uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
+             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ page_off,
+             const uint32_t* __restrict__ surv, const float* __restrict__ surv_lb, uint64_t P, QueryWork* wk,
+             int wave, float split, uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_pos[kThreads / 32][kStageCap];
@@ -483,19 +508,26 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int K = kPage / 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float bound = bound_from_bits(wk->bsf_bits);
-    const float cut = wk->scan_bound * split;
-    const uint32_t nsurv = wk->nsurv;
+    // Page wave 0 splits its candidates into refinement waves A and B by their
+    // own bound; page wave 1 (scanned after wave A is refined) feeds wave B.
+    const float cut = wave == 0 ? wk->scan_bound * split : -1.f;
+    const uint32_t nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
     const uint64_t gwarp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
     int cnt = 0;
-    unsigned long long scanned = 0;
-    // Software pipeline: the next page's words are in flight while this one is bounded.
+    unsigned long long scanned = 0, pruned = 0;
     uint32_t na = 0, nb = 0;
     uint4 nwv[K][H];
     auto fetch = [&](uint64_t i) {
-        const uint32_t page = surv[i];
-        na = page_off[page];
-        nb = page_off[page + 1];
+        const uint64_t slot = wave == 0 ? i : P - 1 - i;
+        na = nb = 0;
+        if (wave == 0 || surv_lb[slot] <= bound) {
+            const uint32_t page = surv[slot];
+            na = page_off[page];
+            nb = page_off[page + 1];
+        } else {
+            pruned += lane == 0 ? 1 : 0;
+        }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const uint32_t e = na + lane + 32 * k;
@@ -513,6 +545,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
             for (int h = 0; h < H; ++h) wv[k][h] = nwv[k][h];
         if (i + nwarps < nsurv) fetch(i + nwarps);
+        if (a == b) continue;
         scanned += b - a;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -537,6 +570,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
     if (lane == 0 && scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
+    if (lane == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
 }
 
 // ------------------------------------------------------------ refine
@@ -710,15 +744,16 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
         if (!approximate) {
             mark(ls, 1, [&] {
                 bound<<<bound_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.page_lo, ix.page_hi, ix.page_off, ix.P,
-                                                               L.work, L.surv);
-            });
-            TSG_LAUNCHED();
-            mark(ls, 4, [&] {
-                lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, ix.page_off, L.surv,
-                                                               L.work, ix.refine_split, cap, L.cand_pos, L.cand_lb);
+                                                               L.work, ix.refine_split, L.surv, L.surv_lb);
             });
             TSG_LAUNCHED();
             for (int wave = 0; wave < 2; ++wave) {
+                mark(ls, 4, [&] {
+                    lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, ix.page_off, L.surv,
+                                                                   L.surv_lb, ix.P, L.work, wave, ix.refine_split, cap,
+                                                                   L.cand_pos, L.cand_lb);
+                });
+                TSG_LAUNCHED();
                 mark(ls, wave == 0 ? 3 : 5, [&] {
                     refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, L.work, L.cand_pos, L.cand_lb,
                                                                    L.cand_sq, wave, cap);
