@@ -180,6 +180,17 @@ tsg_status tsg_index_export(const tsg_index* index, uint8_t* words, uint32_t* po
 tsg_status tsg_generate_random_walk(float* dev_rows, uint64_t begin, uint64_t count,
                                     uint64_t length, uint64_t seed, int znorm, void* stream);
 
+/* Device generators for the BASELINE workloads (input setup, not timed):
+ * kind 0 = random walk (as tsg_generate_random_walk), 3 = config 3 (AR(1) +
+ * sinusoid), 4 = config 4 (1024-component Gaussian mixture), 5 = config 5
+ * queries: rows [begin, begin+count) of query stream `seed`, each a
+ * z-normalised random-walk row of (data_seed, data_count) chosen by the
+ * stream plus N(0, noise^2), re-z-normalised. Definitions and their CPU
+ * restatement: oracle/tsidx_oracle.cpp. */
+tsg_status tsg_generate_series(int kind, float* dev_rows, uint64_t begin, uint64_t count, uint64_t length,
+                               uint64_t seed, int znorm, double noise, uint64_t data_count,
+                               uint64_t data_seed, void* stream);
+
 /* Number of kernel launches this process issued through the library. */
 uint64_t tsg_launch_count(void);
 

@@ -60,6 +60,8 @@ class Oracle:
         _sig(lib, "orc_random_walk_series", None, u64, u64, u64, _f32p)
         _sig(lib, "orc_znormalize", i32, _f32p, u64)
         _sig(lib, "orc_generate_rows", None, u64, u64, u64, u64, i32, C.c_uint, _f32p)
+        _sig(lib, "orc_generate_kind", None, i32, u64, u64, u64, u64, C.c_uint, _f32p)
+        _sig(lib, "orc_c5_query", None, u64, u64, f64, u64, u64, u64, _f32p, C.POINTER(u64))
         _sig(lib, "orc_paa", None, _f32p, u64, i32, _f64p)
         _sig(lib, "orc_summarise", None, _f32p, u64, u64, i32, i32, C.c_uint, _u8p)
         _sig(lib, "orc_root_key", u64, _u8p, i32)
@@ -79,6 +81,28 @@ class Oracle:
         out = np.empty((count, length), np.float32)
         self.lib.orc_generate_rows(seed, begin, begin + count, length, 1 if znorm else 0, threads, out)
         return out
+
+    def generate_c3(self, count, length, seed, begin=0, threads=0) -> np.ndarray:
+        """BASELINE config 3: AR(1) + random-phase sinusoid, z-normalised."""
+        out = np.empty((count, length), np.float32)
+        self.lib.orc_generate_kind(3, seed, begin, count, length, threads, out)
+        return out
+
+    def generate_c4(self, count, length, seed, begin=0, threads=0) -> np.ndarray:
+        """BASELINE config 4: 1024-component Gaussian mixture, z-normalised."""
+        out = np.empty((count, length), np.float32)
+        self.lib.orc_generate_kind(4, seed, begin, count, length, threads, out)
+        return out
+
+    def c5_queries(self, nq, sigma, query_seed, data_seed, count, length, begin=0):
+        """BASELINE config 5: dataset rows (regenerated) + N(0, sigma^2), re-z-normalised."""
+        out = np.empty((nq, length), np.float32)
+        rows = np.empty(nq, np.uint64)
+        for j in range(nq):
+            r = u64()
+            self.lib.orc_c5_query(query_seed, begin + j, sigma, data_seed, count, length, out[j], C.byref(r))
+            rows[j] = r.value
+        return out, rows
 
     def znormalize(self, s: np.ndarray) -> bool:
         return bool(self.lib.orc_znormalize(s, s.size))

@@ -19,6 +19,7 @@ EXPORTS = (
     "tsg_index_build", "tsg_index_build_device", "tsg_index_free", "tsg_index_info", "tsg_search",
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
+    "tsg_generate_series",
 )
 
 
@@ -86,6 +87,7 @@ def lib() -> C.CDLL:
         "tsg_index_export": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "tsg_generate_random_walk": (i32, [vp, u64, u64, u64, u64, i32, vp]),
         "tsg_launch_count": (u64, []),
+        "tsg_generate_series": (i32, [i32, vp, u64, u64, u64, u64, i32, C.c_double, u64, u64, vp]),
         "tsg_profile_enable": (i32, [vp, i32]),
         "tsg_profile_read": (i32, [vp, C.POINTER(C.c_double), C.POINTER(u64), i32]),
     }

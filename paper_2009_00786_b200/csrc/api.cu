@@ -547,6 +547,21 @@ tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* posit
     });
 }
 
+tsg_status tsg_generate_series(int kind, float* dev_rows, uint64_t begin, uint64_t count, uint64_t length,
+                               uint64_t seed, int znorm, double noise, uint64_t data_count, uint64_t data_seed,
+                               void* stream) {
+    return guarded([&] {
+        if (count == 0) return;
+        if (!dev_rows) fail("generate: null rows");
+        if (kind != kGenRandomWalk && kind != kGenC3 && kind != kGenC4 && kind != kGenC5)
+            fail("generate: kind must be 0, 3, 4 or 5");
+        device_count();
+        generate_series(kind, dev_rows, begin, count, length, seed, znorm, noise, data_count, data_seed,
+                        static_cast<cudaStream_t>(stream));
+        TSG_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    });
+}
+
 tsg_status tsg_profile_enable(tsg_index* ix, int enable) {
     return guarded([&] {
         if (!ix) fail("tsg_profile_enable: null index");

@@ -1,20 +1,22 @@
-// Device input generator: the reference's seeded random walks on the GPU.
+// Device input generators (setup utilities, not on the timed path).
 //
-// Restates generate_random_walk / fill_walk / mix_seed (src/dataset.cpp:22-68)
-// and the CLI's z-normalisation (src/dataset.cpp:70-85, tools/main.cpp:128-139)
-// so 100M-series workloads can be created in HBM in seconds instead of
-// minutes on the host. Per series: splitmix64(seed, i) seeds an MT19937-64
-// (the std::mt19937_64 parameter set); uniforms are libstdc++'s
-// generate_canonical<double, 53> (one draw / 2^64); normals come from the
-// Marsaglia polar method with one cached deviate, in libstdc++'s order;
-// the walk accumulates in FP64 and stores floats. All arithmetic is IEEE
-// round-to-nearest without FMA, so the only possible difference from the
-// host generator is the last bit of log() (glibc vs CUDA libdevice); the
-// test suite counts mismatching series against the reference.
+// RW:  the reference's generate_random_walk / fill_walk / mix_seed
+//      (src/dataset.cpp:22-68) + the CLI z-normalisation (src/dataset.cpp:70-85,
+//      tools/main.cpp:128-139), bit-identical to the reference (tested).
+// C3/C4/C5: BASELINE.json configs 3-5, which the reference does not define;
+//      specified (with the same per-series seeding) in oracle/tsidx_oracle.cpp
+//      and restated here.
+// Per series: splitmix64(seed, i) seeds an MT19937-64 (the std::mt19937_64
+// parameter set); uniforms are libstdc++'s generate_canonical<double, 53>
+// (one draw / 2^64); normals come from the Marsaglia polar method with one
+// cached deviate, in libstdc++'s order. All arithmetic is IEEE
+// round-to-nearest without FMA; log/sin come from libdevice, so the host
+// generator can differ in the last bit of those (the tests count it).
 //
-// One warp per series: the twist and the polar accept/reject run across
-// lanes; the inherently serial steps (seeding recurrence, the walk, the
-// z-normalisation sums) run on lane 0 in the reference order.
+// One warp per series: the MT twist and the polar accept/reject run across
+// lanes over a cursor into the tempered output stream; the serial steps
+// (seeding recurrence, the walk / AR recursion, the z-normalisation sums) run
+// on lane 0 in the reference order.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -25,6 +27,8 @@ namespace {
 constexpr int kMtN = 312, kMtM = 156;
 constexpr int kGenWarps = 4;
 constexpr int kMaxLen = 512;
+constexpr int kOutCap = 384;  // tempered outputs kept ahead of the cursor (>= 64 + 312)
+constexpr double kTwoPi = 6.283185307179586;
 
 __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t i) {
     uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
@@ -52,144 +56,298 @@ __device__ __forceinline__ double canonical(uint64_t x) {
     return r;
 }
 
-// In-place MT twist over the 312-word state, in the sequential order's
-// dependency structure: [0,156) reads old words, [156,311) reads the new
-// [0,155), and 311 reads the new word 0.
-__device__ void mt_twist(uint64_t* x, int lane) {
-    uint64_t v[5];
+// Warp-cooperative MT19937-64 stream: state + tempered outputs [cur, avail).
+struct MtStream {
+    uint64_t* x;    // [312] state
+    uint64_t* out;  // [kOutCap] tempered outputs
+    int cur, avail;
+
+    __device__ void seed(uint64_t s, int lane) {
+        if (lane == 0) {
+            uint64_t v = s;
+            x[0] = v;
+            for (int k = 1; k < kMtN; ++k) {
+                v = 6364136223846793005ull * (v ^ (v >> 62)) + static_cast<uint64_t>(k);
+                x[k] = v;
+            }
+        }
+        cur = avail = 0;
+        __syncwarp();
+    }
+
+    // In-place twist in the sequential order's dependency structure:
+    // [0,156) reads old words, [156,311) reads the new [0,155), 311 reads the new word 0.
+    __device__ void twist(int lane) {
+        uint64_t v[5];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        const int i = lane + 32 * r;
-        if (i < kMtM) v[r] = twist_one(x[i], x[i + 1], x[i + kMtM]);
+        for (int r = 0; r < 5; ++r) {
+            const int i = lane + 32 * r;
+            if (i < kMtM) v[r] = twist_one(x[i], x[i + 1], x[i + kMtM]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int i = lane + 32 * r;
+            if (i < kMtM) x[i] = v[r];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int i = kMtM + lane + 32 * r;
+            if (i < kMtN - 1) v[r] = twist_one(x[i], x[i + 1], x[i - kMtM]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const int i = kMtM + lane + 32 * r;
+            if (i < kMtN - 1) x[i] = v[r];
+        }
+        __syncwarp();
+        if (lane == 0) x[kMtN - 1] = twist_one(x[kMtN - 1], x[0], x[kMtM - 1]);
+        __syncwarp();
+    }
+
+    // At least k outputs available from the cursor (k <= 64).
+    __device__ void ensure(int k, int lane) {
+        if (avail - cur >= k) return;
+        const int keep = avail - cur;
+        uint64_t t0 = lane < keep ? out[cur + lane] : 0, t1 = lane + 32 < keep ? out[cur + lane + 32] : 0;
+        __syncwarp();
+        if (lane < keep) out[lane] = t0;
+        if (lane + 32 < keep) out[lane + 32] = t1;
+        __syncwarp();
+        twist(lane);
+        for (int i = lane; i < kMtN; i += 32) out[keep + i] = temper(x[i]);
+        cur = 0;
+        avail = keep + kMtN;
+        __syncwarp();
+    }
+
+    __device__ double uniform(int lane) {
+        ensure(1, lane);
+        return canonical(out[cur++]);
+    }
+
+    // Appends `need` N(0,1) deviates (polar method, libstdc++ order: y*mult
+    // then the cached x*mult) to dst[have..]. Pairs are consumed 32 at a time,
+    // so draws past the last needed pair are burnt: callers draw no uniform
+    // after their normals.
+    __device__ void normals(double* dst, int need, int lane) {
+        int have = 0;
+        while (have < need) {
+            ensure(64, lane);
+            const double u1 = canonical(out[cur + 2 * lane]);
+            const double u2 = canonical(out[cur + 2 * lane + 1]);
+            const double xx = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
+            const double yy = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
+            const double r2 = __dadd_rn(__dmul_rn(xx, xx), __dmul_rn(yy, yy));
+            const bool acc = !(r2 > 1.0 || r2 == 0.0);
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, acc);
+            if (acc) {
+                const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
+                const int slot = have + 2 * __popc(m & ((1u << lane) - 1u));
+                if (slot < need) dst[slot] = __dmul_rn(yy, mult);
+                if (slot + 1 < need) dst[slot + 1] = __dmul_rn(xx, mult);
+            }
+            have += 2 * __popc(m);
+            cur += 64;
+            __syncwarp();
+        }
+    }
+};
+
+// z-normalisation of out[0, n) in the reference's order (lane 0 sums).
+__device__ void znorm_row(float* out, int n, int lane, double* s_ms) {
+    if (lane == 0) {
+        double sum = 0.0;
+        for (int j = 0; j < n; ++j) sum = __dadd_rn(sum, static_cast<double>(out[j]));
+        const double mean = __ddiv_rn(sum, static_cast<double>(n));
+        double sq = 0.0;
+        for (int j = 0; j < n; ++j) {
+            const double d = __dsub_rn(static_cast<double>(out[j]), mean);
+            sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+        s_ms[0] = mean;
+        s_ms[1] = __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n)));
     }
     __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        const int i = lane + 32 * r;
-        if (i < kMtM) x[i] = v[r];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        const int i = kMtM + lane + 32 * r;
-        if (i < kMtN - 1) v[r] = twist_one(x[i], x[i + 1], x[i - kMtM]);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 5; ++r) {
-        const int i = kMtM + lane + 32 * r;
-        if (i < kMtN - 1) x[i] = v[r];
-    }
-    __syncwarp();
-    if (lane == 0) x[kMtN - 1] = twist_one(x[kMtN - 1], x[0], x[kMtM - 1]);
+    const double mean = s_ms[0], sd = s_ms[1];
+    for (int j = lane; j < n; j += 32)
+        out[j] = sd <= 1e-12 ? 0.f : __double2float_rn(__ddiv_rn(__dsub_rn(static_cast<double>(out[j]), mean), sd));
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kGenWarps * 32)
-    k_generate(float* __restrict__ rows, uint64_t begin, uint64_t count, int n, uint64_t seed, int znorm) {
+struct GenArgs {
+    int kind;               // GenKind
+    uint64_t seed, begin, count;
+    int n, znorm;
+    const uint64_t* index;  // optional per-output series index (RW base rows)
+    const double* sigma;    // c4 component sigmas [1024]
+    const double* centres;  // c4 component centres [1024][n]
+    double noise;           // c5 sigma
+    float* rows;            // output [count][n] (c5: holds the base rows, updated in place)
+    double* comp_out;       // c4 components: sigma [1024] then centres [1024][n]
+    uint64_t* row_out;      // c5 rows: chosen dataset rows
+    uint64_t data_count;    // c5 rows: dataset size
+};
+
+__global__ void __launch_bounds__(kGenWarps * 32) k_generate(GenArgs a) {
     __shared__ uint64_t s_mt[kGenWarps][kMtN];
-    __shared__ double s_norm[kGenWarps][kMaxLen + 2];
-    __shared__ float s_out[kGenWarps][kMaxLen];
+    __shared__ uint64_t s_out[kGenWarps][kOutCap];
+    __shared__ double s_norm[kGenWarps][kMaxLen];
+    __shared__ float s_row[kGenWarps][kMaxLen];
+    __shared__ double s_ms[kGenWarps][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* mt = s_mt[warp];
+    MtStream g{s_mt[warp], s_out[warp], 0, 0};
     double* nrm = s_norm[warp];
-    float* out = s_out[warp];
+    float* out = s_row[warp];
+    const int n = a.n;
     const uint64_t gw = blockIdx.x * static_cast<uint64_t>(kGenWarps) + warp;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kGenWarps;
-    for (uint64_t s = gw; s < count; s += nw) {
-        const uint64_t idx = begin + s;
-        if (lane == 0) {
-            uint64_t x = mix_seed(seed, idx);
-            mt[0] = x;
-            for (int k = 1; k < kMtN; ++k) {
-                x = 6364136223846793005ull * (x ^ (x >> 62)) + static_cast<uint64_t>(k);
-                mt[k] = x;
-            }
-        }
-        __syncwarp();
-        int have = 0;  // normals produced
-        while (have < n) {
-            mt_twist(mt, lane);
-            // 156 pairs per twist, 32 at a time, in order.
-            for (int p0 = 0; p0 < kMtN / 2 && have < n; p0 += 32) {
-                const int p = p0 + lane;
-                bool acc = false;
-                double gx = 0.0, gy = 0.0;
-                if (p < kMtN / 2) {
-                    const double u1 = canonical(temper(mt[2 * p]));
-                    const double u2 = canonical(temper(mt[2 * p + 1]));
-                    const double x = __dsub_rn(__dmul_rn(2.0, u1), 1.0);
-                    const double y = __dsub_rn(__dmul_rn(2.0, u2), 1.0);
-                    const double r2 = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
-                    acc = !(r2 > 1.0 || r2 == 0.0);
-                    if (acc) {
-                        const double mult = __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, log(r2)), r2));
-                        gy = __dmul_rn(y, mult);  // returned first
-                        gx = __dmul_rn(x, mult);  // cached, returned second
-                    }
-                }
-                const unsigned m = __ballot_sync(0xFFFFFFFFu, acc);
-                if (acc) {
-                    const int slot = have + 2 * __popc(m & ((1u << lane) - 1u));
-                    if (slot < kMaxLen + 2) {
-                        nrm[slot] = gy;
-                        nrm[slot + 1] = gx;
-                    }
-                }
-                have += 2 * __popc(m);
-            }
+    for (uint64_t s = gw; s < a.count; s += nw) {
+        const uint64_t idx = a.index ? a.index[s] : a.begin + s;
+        if (a.kind == kGenC4Comp) {
+            g.seed(mix_seed(a.seed ^ 0x5DEECE66Dull, idx), lane);
+            const double sigma = 0.1 + 0.4 * g.uniform(lane);
+            g.normals(nrm, n, lane);
+            if (lane == 0) a.comp_out[idx] = sigma;
+            for (int j = lane; j < n; j += 32) a.comp_out[1024 + idx * n + j] = nrm[j];
             __syncwarp();
+            continue;
         }
-        __syncwarp();
-        if (lane == 0) {
-            double v = 0.0;
-            for (int j = 0; j < n; ++j) {
-                v = __dadd_rn(v, nrm[j]);
-                out[j] = __double2float_rn(v);
-            }
+        if (a.kind == kGenC5Rows) {
+            g.seed(mix_seed(a.seed, idx), lane);
+            uint64_t r = static_cast<uint64_t>(__dmul_rn(g.uniform(lane), static_cast<double>(a.data_count)));
+            if (r >= a.data_count) r = a.data_count - 1;
+            if (lane == 0) a.row_out[s] = r;
+            continue;
         }
-        __syncwarp();
-        if (znorm) {
-            __shared__ double s_ms[kGenWarps][2];
+        g.seed(mix_seed(a.seed, idx), lane);
+        float* dst = a.rows + s * static_cast<uint64_t>(n);
+        if (a.kind == kGenRandomWalk) {
+            g.normals(nrm, n, lane);
             if (lane == 0) {
-                double sum = 0.0;
-                for (int j = 0; j < n; ++j) sum = __dadd_rn(sum, static_cast<double>(out[j]));
-                const double mean = __ddiv_rn(sum, static_cast<double>(n));
-                double sq = 0.0;
+                double v = 0.0;
                 for (int j = 0; j < n; ++j) {
-                    const double d = __dsub_rn(static_cast<double>(out[j]), mean);
-                    sq = __dadd_rn(sq, __dmul_rn(d, d));
+                    v = __dadd_rn(v, nrm[j]);
+                    out[j] = __double2float_rn(v);
                 }
-                s_ms[warp][0] = mean;
-                s_ms[warp][1] = __dsqrt_rn(__ddiv_rn(sq, static_cast<double>(n)));
             }
-            __syncwarp();
-            const double mean = s_ms[warp][0], sd = s_ms[warp][1];
+        } else if (a.kind == kGenC3) {
+            const double period = __dadd_rn(8.0, __dmul_rn(56.0, g.uniform(lane)));
+            const double amp = __dmul_rn(2.0, g.uniform(lane));
+            const double phase = __dmul_rn(kTwoPi, g.uniform(lane));
+            g.normals(nrm, n, lane);
+            if (lane == 0) {
+                double ar = 0.0;
+                for (int t = 0; t < n; ++t) {
+                    ar = t == 0 ? nrm[0] : __dadd_rn(__dmul_rn(0.95, ar), nrm[t]);
+                    const double ang = __dadd_rn(__ddiv_rn(__dmul_rn(kTwoPi, static_cast<double>(t)), period), phase);
+                    out[t] = __double2float_rn(__dadd_rn(ar, __dmul_rn(amp, sin(ang))));
+                }
+            }
+        } else if (a.kind == kGenC4) {
+            int k = static_cast<int>(__dmul_rn(g.uniform(lane), 1024.0));
+            if (k >= 1024) k = 1023;
+            g.normals(nrm, n, lane);
+            const double sig = a.sigma[k];
             for (int j = lane; j < n; j += 32)
-                out[j] = sd <= 1e-12 ? 0.f
-                                     : __double2float_rn(__ddiv_rn(__dsub_rn(static_cast<double>(out[j]), mean), sd));
-            __syncwarp();
+                out[j] = __double2float_rn(__dadd_rn(a.centres[static_cast<uint64_t>(k) * n + j], __dmul_rn(sig, nrm[j])));
+        } else {  // kGenC5Noise: base row already in dst, first draw chose it
+            (void)g.uniform(lane);
+            g.normals(nrm, n, lane);
+            for (int j = lane; j < n; j += 32)
+                out[j] = __double2float_rn(__dadd_rn(static_cast<double>(dst[j]), __dmul_rn(a.noise, nrm[j])));
         }
-        float* dst = rows + s * static_cast<uint64_t>(n);
+        __syncwarp();
+        if (a.znorm) znorm_row(out, n, lane, s_ms[warp]);
         for (int j = lane; j < n; j += 32) dst[j] = out[j];
         __syncwarp();
     }
+}
+
+unsigned gen_grid(uint64_t count) {
+    int dev = 0, sms = 0;
+    TSG_CUDA(cudaGetDevice(&dev));
+    TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((count + kGenWarps - 1) / kGenWarps,
+                                                                          static_cast<uint64_t>(sms) * 16)));
+}
+
+void check_len(uint64_t length) {
+    if (length == 0 || length > static_cast<uint64_t>(kMaxLen))
+        throw InvalidArgument("generate: device generators support 1 <= length <= 512");
 }
 
 }  // namespace
 
 void generate_random_walk(float* rows, uint64_t begin, uint64_t count, uint64_t length, uint64_t seed, int znorm,
                           cudaStream_t stream) {
-    if (length == 0 || length > static_cast<uint64_t>(kMaxLen))
-        throw InvalidArgument("generate_random_walk: device generator supports 1 <= length <= 512");
+    generate_series(kGenRandomWalk, rows, begin, count, length, seed, znorm, 0.0, 0, 0, stream);
+}
+
+void generate_series(int kind, float* rows, uint64_t begin, uint64_t count, uint64_t length, uint64_t seed, int znorm,
+                     double noise, uint64_t data_count, uint64_t data_seed, cudaStream_t stream) {
+    check_len(length);
     if (count == 0) return;
-    int dev = 0, sms = 0;
-    TSG_CUDA(cudaGetDevice(&dev));
-    TSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const uint64_t blocks = std::min<uint64_t>((count + kGenWarps - 1) / kGenWarps, static_cast<uint64_t>(sms) * 16);
-    k_generate<<<static_cast<unsigned>(blocks), kGenWarps * 32, 0, stream>>>(rows, begin, count,
-                                                                            static_cast<int>(length), seed, znorm);
-    TSG_LAUNCHED();
+    GenArgs a{};
+    a.seed = seed;
+    a.begin = begin;
+    a.count = count;
+    a.n = static_cast<int>(length);
+    a.znorm = znorm;
+    a.rows = rows;
+    if (kind == kGenRandomWalk || kind == kGenC3) {
+        a.kind = kind;
+        k_generate<<<gen_grid(count), kGenWarps * 32, 0, stream>>>(a);
+        TSG_LAUNCHED();
+        return;
+    }
+    if (kind == kGenC4) {
+        double* comp = nullptr;
+        TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&comp), (1024 + 1024 * length) * sizeof(double), stream));
+        GenArgs c = a;
+        c.kind = kGenC4Comp;
+        c.begin = 0;
+        c.count = 1024;
+        c.comp_out = comp;
+        k_generate<<<gen_grid(1024), kGenWarps * 32, 0, stream>>>(c);
+        TSG_LAUNCHED();
+        a.kind = kGenC4;
+        a.sigma = comp;
+        a.centres = comp + 1024;
+        k_generate<<<gen_grid(count), kGenWarps * 32, 0, stream>>>(a);
+        TSG_LAUNCHED();
+        TSG_CUDA(cudaFreeAsync(comp, stream));
+        return;
+    }
+    if (kind == kGenC5) {
+        // queries [begin, begin+count) of stream `seed`: choose rows, regenerate
+        // them (z-normalised random walks of data seed 1's generator), add noise.
+        if (data_count == 0) throw InvalidArgument("generate: c5 queries need the dataset size");
+        uint64_t* chosen = nullptr;
+        TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&chosen), count * sizeof(uint64_t), stream));
+        GenArgs r = a;
+        r.kind = kGenC5Rows;
+        r.row_out = chosen;
+        r.data_count = data_count;
+        k_generate<<<gen_grid(count), kGenWarps * 32, 0, stream>>>(r);
+        TSG_LAUNCHED();
+        GenArgs b = a;
+        b.kind = kGenRandomWalk;
+        b.seed = data_seed;
+        b.index = chosen;
+        b.znorm = 1;
+        k_generate<<<gen_grid(count), kGenWarps * 32, 0, stream>>>(b);
+        TSG_LAUNCHED();
+        a.kind = kGenC5Noise;
+        a.noise = noise;
+        k_generate<<<gen_grid(count), kGenWarps * 32, 0, stream>>>(a);
+        TSG_LAUNCHED();
+        TSG_CUDA(cudaFreeAsync(chosen, stream));
+        return;
+    }
+    throw InvalidArgument("generate: unknown kind");
 }
 
 }  // namespace tsg

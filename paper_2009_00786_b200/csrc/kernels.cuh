@@ -106,8 +106,19 @@ void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, doubl
 // Query pipeline for nq device queries; writes ix.results[0..nq).
 void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approximate);
 
-// Input generator (not on the timed path).
+// Input generators (not on the timed path), see generate.cu.
+enum GenKind {
+    kGenRandomWalk = 0,  // the reference's random walks (BASELINE configs 1-2)
+    kGenC3 = 3,          // AR(1) + sinusoid (config 3)
+    kGenC4 = 4,          // Gaussian mixture (config 4)
+    kGenC5 = 5,          // noisy dataset rows (config 5 queries)
+    kGenC4Comp = 100,    // internal: mixture components
+    kGenC5Rows = 101,    // internal: rows chosen by c5 queries
+    kGenC5Noise = 102,   // internal: c5 noise on regenerated rows
+};
 void generate_random_walk(float* rows, uint64_t begin, uint64_t count, uint64_t length,
                           uint64_t seed, int znorm, cudaStream_t stream);
+void generate_series(int kind, float* rows, uint64_t begin, uint64_t count, uint64_t length, uint64_t seed,
+                     int znorm, double noise, uint64_t data_count, uint64_t data_seed, cudaStream_t stream);
 
 }  // namespace tsg

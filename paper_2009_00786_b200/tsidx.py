@@ -350,5 +350,19 @@ def generate_random_walk_device(count: int, length: int, seed: int, znorm: bool 
     return out
 
 
+def generate_device(kind: str, count: int, length: int, seed: int, begin: int = 0, device: int = 0,
+                    noise: float = 0.0, data_count: int = 0, data_seed: int = 1, znorm: bool = True):
+    """BASELINE workloads generated in HBM: kind 'rw' (configs 1-2), 'c3', 'c4', or 'c5'
+    (noisy queries over a `data_count`-series random-walk dataset of `data_seed`)."""
+    import torch
+
+    kinds = {"rw": 0, "c3": 3, "c4": 4, "c5": 5}
+    out = torch.empty((count, length), dtype=torch.float32, device=f"cuda:{device}")
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    check(lib().tsg_generate_series(kinds[kind], C.c_void_p(out.data_ptr()), begin, count, length, seed,
+                                    1 if znorm else 0, float(noise), data_count, data_seed, C.c_void_p(stream)))
+    return out
+
+
 def launch_count() -> int:
     return int(lib().tsg_launch_count())

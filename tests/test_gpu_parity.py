@@ -251,3 +251,42 @@ def test_launch_counter_moves():
     rows = np.random.default_rng(1).standard_normal((500, 64)).astype(np.float32)
     tg.exact_search(tg.build_index(rows, tg.IndexConfig(n=64)), rows[3])
     assert tg.launch_count() > before
+
+
+# ---- BASELINE configs 3-5: generators and exact search on their distributions ------
+
+def _row_mismatch(a, b):
+    return int(np.count_nonzero(np.any(a.view(np.uint32) != b.view(np.uint32), axis=1)))
+
+
+def test_device_generators_c3_c4_c5_match_oracle(oracle):
+    import torch
+
+    c4d = tg.generate_device("c4", 3000, 96, 41, begin=5000).cpu().numpy()
+    assert _row_mismatch(c4d, oracle.generate_c4(3000, 96, 41, begin=5000)) == 0
+    c5d = tg.generate_device("c5", 200, 256, 77, noise=0.1, data_count=100_000_000, data_seed=1).cpu().numpy()
+    c5h, _ = oracle.c5_queries(200, 0.1, 77, 1, 100_000_000, 256)
+    assert _row_mismatch(c5d, c5h) == 0
+    # c3 evaluates sin(): libdevice vs glibc may differ in the last bit of a few values
+    c3d = tg.generate_device("c3", 3000, 128, 31, begin=123).cpu().numpy()
+    c3h = oracle.generate_c3(3000, 128, 31, begin=123)
+    assert float(np.abs(c3d - c3h).max()) < 1e-4
+    assert _row_mismatch(c3d, c3h) <= 30, _row_mismatch(c3d, c3h)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("kind,n,leaf", [("c3", 128, 2000), ("c3", 128, 50), ("c4", 96, 2000), ("c4", 96, 64)])
+def test_exact_matches_scan_c3_c4(oracle, kind, n, leaf):
+    gen = oracle.generate_c3 if kind == "c3" else oracle.generate_c4
+    rows = gen(20000, n, 900)
+    queries = gen(12, n, 900, begin=10_000_000)  # same process, unseen series
+    check_against_scan(oracle, rows, queries, tg.IndexConfig(n=n, leaf_capacity=leaf))
+
+
+@pytest.mark.parametrize("sigma", [0.01, 0.1, 0.5, 1.0])
+def test_exact_matches_scan_c5_noisy_queries(oracle, sigma):
+    rows = oracle.generate(30000, 256, 1)  # the first 30000 rows of configs 1/2
+    queries, src = oracle.c5_queries(10, sigma, 5, 1, 30000, 256)
+    _, res = check_against_scan(oracle, rows, queries, tg.IndexConfig())
+    if sigma <= 0.01:  # near-duplicates find their source row
+        assert sum(int(r.position) == int(s) for r, s in zip(res, src)) >= 8
