@@ -39,9 +39,14 @@ sys.path.insert(0, ROOT)
 METRIC = "exact 1-NN queries/s & iSAX build Mseries/s (float32 series), % of HBM roofline"
 
 CONFIGS = {
-    # name: (count, length, seed, query_seed, queries per step)
-    "c1": (1_000_000, 256, 1, 2, 100),
-    "c2": (100_000_000, 256, 1, 2, 100),
+    # BASELINE.json configs. data: (kind, count, length, seed); queries: (kind, seed, begin) where
+    # begin=None means "the next series of the same process" (index count, count+1, ...).
+    # c4's count is per GPU (1B over 8 GPUs = 125M each); c5 = c2's data with noisy queries.
+    "c1": {"data": ("rw", 1_000_000, 256, 1), "queries": ("rw", 2, 0), "nq": 100},
+    "c2": {"data": ("rw", 100_000_000, 256, 1), "queries": ("rw", 2, 0), "nq": 100},
+    "c3": {"data": ("c3", 200_000_000, 128, 3), "queries": ("c3", 3, None), "nq": 100},
+    "c4": {"data": ("c4", 125_000_000, 96, 4), "queries": ("c4", 4, None), "nq": 100, "per_gpu": True},
+    "c5": {"data": ("rw", 100_000_000, 256, 1), "queries": ("c5", 5, 0), "nq": 100},
 }
 
 
@@ -107,16 +112,55 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_baseline(count_full, n, seed, qseed, sample, queries):
+def workload_text(name, count, n, sigma=None):
+    spec = CONFIGS[name]
+    dkind, _, _, seed = spec["data"]
+    qkind, qseed, _ = spec["queries"]
+    what = {"rw": "z-normalised random walks", "c3": "AR(1)+sinusoid series, z-normalised",
+            "c4": "1024-component Gaussian-mixture vectors, z-normalised"}[dkind]
+    q = {"rw": f"random walks (seed {qseed})", "c3": "unseen series of the same process",
+         "c4": "unseen vectors of the same mixture",
+         "c5": f"dataset rows + N(0, {sigma}^2) noise, re-z-normalised (seed {qseed})"}[qkind]
+    return f"{name}: {count} x {n} {what} (seed {seed}); queries: {q}; w=16, 8-bit, leaf 2000"
+
+
+def ref_inputs(name, count, n, nq_total, sigma, sample_cap):
+    """Reference-side index + queries for a config (RW data is built inside the
+    reference without a host copy; c3/c4 data and c5 queries come from the
+    oracle's generators, the only other code allowed here). Returns
+    (index, queries, dataset_count, generate_ns)."""
+    from oracle.oracle import Oracle, Reference
+
+    spec = CONFIGS[name]
+    dkind, _, _, seed = spec["data"]
+    qkind, qseed, qbegin = spec["queries"]
+    ref, orc = Reference(), Oracle()
+    if dkind == "rw":
+        idx, gen_ns = ref.build_generated(count, n, seed)
+    else:
+        count = min(count, sample_cap)
+        t0 = time.perf_counter()
+        rows = (orc.generate_c3 if dkind == "c3" else orc.generate_c4)(count, n, seed)
+        gen_ns = int((time.perf_counter() - t0) * 1e9)
+        idx = ref.build_index(rows)
+        del rows
+    if qkind == "rw":
+        qs = ref.series_window(qbegin, nq_total, n, qseed)
+    elif qkind == "c5":
+        qs, _ = orc.c5_queries(nq_total, sigma, qseed, seed, count, n)
+    else:
+        qs = (orc.generate_c3 if qkind == "c3" else orc.generate_c4)(nq_total, n, qseed, begin=count)
+    return idx, qs, count, gen_ns
+
+
+def cpu_baseline(name, count_full, n, sigma, sample, queries):
     """The unmodified reference (oracle/_ref) on this host's cores, on a
-    bounded sample of the workload: the first `sample` series of the same
-    dataset, reference build + exact_search (mq, 24 queues, all cores)."""
+    bounded sample of the workload (the first `sample` series of the same
+    dataset): reference build_index + exact_search (mq, 24 queues, all cores)."""
     from oracle.oracle import Reference
 
-    ref = Reference()
-    cores = ref.hardware_concurrency()
-    idx, gen_ns = ref.build_generated(sample, n, seed)
-    qs = ref.series_window(0, queries, n, qseed)
+    cores = Reference().hardware_concurrency()
+    idx, qs, used, _ = ref_inputs(name, min(sample, count_full), n, queries, sigma, sample)
     t = []
     for q in qs:
         d, p, st, ns = idx.exact_search(q)
@@ -124,9 +168,9 @@ def cpu_baseline(count_full, n, seed, qseed, sample, queries):
     qps = len(t) / (sum(t) * 1e-9)
     build_ns = idx.build_stats["build_ns"]
     return {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "reference",
-            "sample": f"first {sample} of the {count_full} series (same generator/seed), {queries} queries; "
+            "sample": f"first {used} of the {count_full} series (same generator/seed), {queries} queries; "
                       f"reference build_index + exact_search(mq, 24 queues, {cores} workers)",
-            "build_mseries_s": round(sample / (build_ns * 1e-9) / 1e6, 3),
+            "build_mseries_s": round(used / (build_ns * 1e-9) / 1e6, 3),
             "median_query_ms": round(statistics.median(t) * 1e-6, 3)}
 
 
@@ -134,18 +178,19 @@ def run_reference(args):
     world, rank, local = dist_setup()
     if rank != 0:
         return
-    count, n, seed, qseed, nq = CONFIGS[args.config]
-    if args.count:
-        count = args.count
     from oracle.oracle import Reference
 
-    ref = Reference()
-    cores = ref.hardware_concurrency()
-    idx, gen_ns = ref.build_generated(count, n, seed)
-    build_ns = idx.build_stats["build_ns"]
+    spec = CONFIGS[args.config]
+    _, count, n, _ = spec["data"]
+    if spec.get("per_gpu"):
+        count *= max(args.gpus, 1)
+    if args.count:
+        count = args.count
+    cores = Reference().hardware_concurrency()
     per_step = args.ref_queries_per_step
     total = (args.warmup + args.steps) * per_step
-    qs = ref.series_window(0, total, n, qseed)
+    idx, qs, used, gen_ns = ref_inputs(args.config, count, n, total, args.sigma, args.ref_sample)
+    build_ns = idx.build_stats["build_ns"]
     for q in qs[: args.warmup * per_step]:
         idx.exact_search(q)
     t0 = time.perf_counter()
@@ -160,13 +205,12 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(elapsed * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {count} x {n} z-normalised random walks (seed {seed}), "
-                               f"queries seed {qseed}, w=16, 8-bit, leaf 2000",
-                   "queries_per_step": per_step, "l2_flush": f"inputs larger than L2 ({count * n * 4 / 1e9:.1f} GB)"},
+        "config": {"workload": workload_text(args.config, used, n, args.sigma),
+                   "queries_per_step": per_step, "l2_flush": f"inputs larger than L2 ({used * n * 4 / 1e9:.1f} GB)"},
         "cpu_baseline": {"value": round(qps, 4), "unit": "queries/s", "cores": cores, "kind": "reference",
-                         "sample": f"full {args.config} dataset, {args.steps * per_step} timed queries"},
+                         "sample": f"{used} of {count} series, {args.steps * per_step} timed queries"},
         "e2e": {"value": round(qps, 4), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "build": {"value": round(count / (build_ns * 1e-9) / 1e6, 3), "unit": "Mseries/s",
+        "build": {"value": round(used / (build_ns * 1e-9) / 1e6, 3), "unit": "Mseries/s",
                   "build_s": round(build_ns * 1e-9, 3), "generate_s": round(gen_ns * 1e-9, 3)},
         "median_query_ms": round(statistics.median(times) * 1e-6, 3),
     }
@@ -197,19 +241,25 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    count, n, seed, qseed, nq = CONFIGS[args.config]
+    spec = CONFIGS[args.config]
+    dkind, count, n, seed = spec["data"]
+    qkind, qseed, qbegin = spec["queries"]
+    nq = args.batch or spec["nq"]
+    if spec.get("per_gpu"):
+        count *= world
     if args.count:
         count = args.count
     b, e = shard_range(count, rank, world)
     shard = e - b
 
-    # ---- inputs in HBM (untimed setup) ----
+    # ---- inputs in HBM (untimed setup), generated on the device ----
     t0 = time.perf_counter()
-    rows = tg.generate_random_walk_device(shard, n, seed, znorm=True, begin=b, device=local)
+    rows = tg.generate_device(dkind, shard, n, seed, begin=b, device=local)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     total_batches = args.warmup + args.steps
-    qdev = tg.generate_random_walk_device(total_batches * nq, n, qseed, znorm=True, begin=0, device=local)
+    qdev = tg.generate_device(qkind, total_batches * nq, n, qseed, begin=count if qbegin is None else qbegin,
+                              device=local, noise=args.sigma, data_count=count, data_seed=seed)
     qhost = qdev.cpu().numpy()
 
     # ---- build (device-timed inside the library with CUDA events) ----
@@ -311,7 +361,7 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cpu = cpu_baseline(count, n, seed, qseed, args.cpu_sample, args.cpu_queries)
+                cpu = cpu_baseline(args.config, count, n, args.sigma, args.cpu_sample, args.cpu_queries)
             except Exception as ex:  # reported, not hidden
                 cpu = {"error": str(ex)}
         clocks = clk.summary()
@@ -321,10 +371,9 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed * 1e3 / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: {count} x {n} z-normalised random walks (seed {seed}); "
-                                   f"{nq} queries per step (seed {qseed}, rows {args.warmup * nq}..), "
-                                   f"w=16, 8-bit, leaf 2000",
-                       "queries_per_step": nq, "sharding": f"{world} contiguous series ranges",
+            "config": {"workload": workload_text(args.config, count, n, args.sigma),
+                       "queries_per_step": nq, "query_rows": f"{args.warmup * nq}.. of the query stream",
+                       "sharding": f"{world} contiguous series ranges",
                        "l2_flush": f"inputs larger than L2 ({count * n * 4 / world / 1e9:.1f} GB rows, "
                                    f"{count * 16 / world / 1e9:.2f} GB words per GPU)"},
             "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": nq * n * 4,
@@ -351,6 +400,9 @@ def run_ours(args):
             "search_stats_per_query": {k: round(v / nqt, 2) for k, v in zip(
                 ["lb_node_calcs", "lb_entry_calcs", "real_dist_calcs", "bsf_updates", "pruned_subtrees",
                  "queue_insertions"], stats_acc)},
+            # pruning ratio = 1 - refined rows / dataset rows (BASELINE config 5's difficulty measure)
+            "pruning_ratio": round(1.0 - stats_acc[2] / nqt / count, 6),
+            "query_bytes_gbs": round((lb_entries * ws + refined * 4 * n + nqt * P * (2 * ws + 8)) / elapsed / 1e9, 1),
             "clocks": clocks,
             "generate_s": round(gen_s, 2),
             "cpu_baseline": cpu,
@@ -373,6 +425,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=10_000_000)
     ap.add_argument("--cpu-queries", type=int, default=20)
     ap.add_argument("--ref-queries-per-step", type=int, default=4)
+    ap.add_argument("--ref-sample", type=int, default=20_000_000,
+                    help="cap on host-generated (c3/c4) datasets for the reference arm")
+    ap.add_argument("--batch", type=int, default=0, help="queries per step (default: the config's 100)")
+    ap.add_argument("--sigma", type=float, default=0.1, help="c5 query noise")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
