@@ -211,7 +211,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     if (const char* e = std::getenv("TSG_REFINE_SPLIT")) s.refine_split = static_cast<float>(std::atof(e));
     build_layout(s, &ms[0], &ms[1], &ms[2]);
     // search workspace: query lanes (stream + private scratch each)
-    s.nlanes = 4;
+    s.nlanes = 8;
     if (const char* e = std::getenv("TSG_QUERY_LANES"))
         s.nlanes = std::max(1, std::min(DevIndex::kLanes, std::atoi(e)));
     s.cand_cap = N;
@@ -223,7 +223,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         TSG_CUDA(cudaMalloc(&l.work, sizeof(QueryWork)));
         TSG_CUDA(cudaMalloc(&l.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
         TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
-        TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint32_t)));
+        TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint2)));
         TSG_CUDA(cudaMalloc(&l.surv_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
         TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));
         TSG_CUDA(cudaMalloc(&l.cand_lb, N * sizeof(float)));

@@ -45,13 +45,13 @@ struct DevIndex {
         cudaEvent_t done = nullptr;
         struct QueryWork* work = nullptr;
         float* lut = nullptr;          // [w][256] squared-gap table of the lane's query
-        uint32_t* surv = nullptr;      // [P] surviving pages: wave 0 from the front, wave 1 from the back
+        uint2* surv = nullptr;         // [P] surviving pages' entry ranges: wave 0 from the front, wave 1 from the back
         float* surv_lb = nullptr;      // [P] their box bounds
         uint32_t* cand_pos = nullptr;  // [cap]
         float* cand_lb = nullptr;      // [cap]
         double* cand_sq = nullptr;     // [cap]
     };
-    static constexpr int kLanes = 8;
+    static constexpr int kLanes = 16;
     Lane lanes[kLanes];
     int nlanes = 1;                // lanes in use (TSG_QUERY_LANES, default kLanes)
     uint64_t cand_cap = 0;

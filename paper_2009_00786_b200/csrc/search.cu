@@ -34,6 +34,7 @@
 // BSF widened by 1e-9 relative (covering FP64 rounding of the sums).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t p = pos[e];
         const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
         if ((lane & (kRowLanes - 1)) == 0) {
-            cand_pos[e - a] = p;
+            cand_pos[e - a] = static_cast<uint32_t>(e);  // index-order entry (finalize maps via pos[])
             updates += publish(wk, s, e - a, cand_sq);
         }
     }
@@ -353,7 +354,7 @@ constexpr int kPP = 4;
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_bound(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
-            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, float split, uint32_t* __restrict__ surv,
+            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, float split, uint2* __restrict__ surv,
             float* __restrict__ surv_lb) {
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
@@ -434,14 +435,13 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t at_hi = s_base_hi + (before >> 16);
 #pragma unroll
         for (int k = 0; k < kPP; ++k) {
-            const uint32_t p = static_cast<uint32_t>(base + threadIdx.x + kThreads * k);
             if (lowmask & (1u << k)) {
                 surv_lb[at] = lbs[k];
-                surv[at++] = p;
+                surv[at++] = make_uint2(ea[k], eb[k]);
             } else if (highmask & (1u << k)) {
                 const uint64_t slot = P - 1 - at_hi++;
                 surv_lb[slot] = lbs[k];
-                surv[slot] = p;
+                surv[slot] = make_uint2(ea[k], eb[k]);
             }
         }
         __syncthreads();
@@ -496,8 +496,8 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_lbscan(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ words,
-             const uint32_t* __restrict__ pos, const uint32_t* __restrict__ page_off,
-             const uint32_t* __restrict__ surv, const float* __restrict__ surv_lb, uint64_t P, QueryWork* wk,
+             const uint32_t* __restrict__ pos, const uint2* __restrict__ surv, const float* __restrict__ surv_lb,
+             uint64_t P, QueryWork* wk,
              int wave, float split, uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
@@ -522,9 +522,9 @@ __global__ void __launch_bounds__(kThreads)
         const uint64_t slot = wave == 0 ? i : P - 1 - i;
         na = nb = 0;
         if (wave == 0 || surv_lb[slot] <= bound) {
-            const uint32_t page = surv[slot];
-            na = page_off[page];
-            nb = page_off[page + 1];
+            const uint2 r = surv[slot];
+            na = r.x;
+            nb = r.y;
         } else {
             pruned += lane == 0 ? 1 : 0;
         }
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kThreads)
             if (m) {
                 if (pass) {
                     const int slot = cnt + __popc(m & ((1u << lane) - 1u));
-                    s_pos[warp][slot] = pos[e];
+                    s_pos[warp][slot] = e;  // refine gathers pos[e] off this kernel's path
                     s_lb[warp][slot] = lb;
                 }
                 cnt += __popc(m);
@@ -568,7 +568,46 @@ __global__ void __launch_bounds__(kThreads)
             }
         }
     }
-    if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
+    // Final flush, one atomic pair per block instead of one per warp.
+    __shared__ uint32_t s_wcnt[kThreads / 32], s_wbase[2];
+    int lo_cnt = 0;
+    for (int i = lane; i < cnt; i += 32) lo_cnt += s_lb[warp][i] <= cut ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
+    if (lane == 0) s_wcnt[warp] = static_cast<uint32_t>(lo_cnt) | (static_cast<uint32_t>(cnt - lo_cnt) << 16);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int i = 0; i < kThreads / 32; ++i) {
+            const uint32_t c2 = s_wcnt[i];
+            s_wcnt[i] = tot;
+            tot += c2;
+        }
+        s_wbase[0] = (tot & 0xFFFFu) ? atomicAdd(&wk->ncand, tot & 0xFFFFu) : 0u;
+        s_wbase[1] = (tot >> 16) ? atomicAdd(&wk->nhigh, tot >> 16) : 0u;
+    }
+    __syncthreads();
+    {
+        uint32_t at_lo = s_wbase[0] + (s_wcnt[warp] & 0xFFFFu), at_hi = s_wbase[1] + (s_wcnt[warp] >> 16);
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const bool valid = i < cnt;
+            const float lb = valid ? s_lb[warp][i] : 0.f;
+            const bool low = valid && lb <= cut;
+            const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
+            const unsigned below = (1u << lane) - 1u;
+            if (low) {
+                const uint64_t at = at_lo + __popc(ml & below);
+                cand_pos[at] = s_pos[warp][i];
+                cand_lb[at] = lb;
+            } else if (valid) {
+                const uint64_t at = cap - 1 - (at_hi + __popc(mh & below));
+                cand_pos[at] = s_pos[warp][i];
+                cand_lb[at] = lb;
+            }
+            at_lo += __popc(ml);
+            at_hi += __popc(mh);
+        }
+    }
     if (lane == 0 && scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
     if (lane == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
 }
@@ -577,7 +616,8 @@ __global__ void __launch_bounds__(kThreads)
 // One wave: wave 0 = [nseed, ncand), wave 1 = [cap - nhigh, cap).
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    k_refine(const float* __restrict__ rows, int n, const float* __restrict__ query, QueryWork* wk,
+    k_refine(const float* __restrict__ rows, int n, const float* __restrict__ query, const uint32_t* __restrict__ pos,
+             QueryWork* wk,
              const uint32_t* __restrict__ cand_pos, const float* __restrict__ cand_lb,
              double* __restrict__ cand_sq, int wave, uint64_t cap) {
     extern __shared__ float s_q[];
@@ -592,10 +632,9 @@ __global__ void __launch_bounds__(kThreads)
     // candidate whose bound exceeds the live BSF costs one check.
     const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
-    const unsigned gmask = 0xFFu << (lane & ~(kRowLanes - 1));
     uint64_t c = begin + group;
     float nlb = c < end ? cand_lb[c] : 0.f;
-    uint32_t np = c < end ? cand_pos[c] : 0u;
+    uint32_t np = c < end ? pos[cand_pos[c]] : 0u;  // candidate records hold index-order entries
     // Cached pruning bound: refreshed from the BSF each publish observes, so a
     // skipped candidate costs no memory access (a stale bound only refines more).
     float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
@@ -604,19 +643,20 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t p = np;
         if (c + ngroups < end) {
             nlb = cand_lb[c + ngroups];
-            np = cand_pos[c + ngroups];
+            np = pos[cand_pos[c + ngroups]];
         }
         if (lb > bnd) {
             if (leader) cand_sq[c] = INFINITY;
             continue;
         }
+        // read the BSF for the next candidate's bound while this row is in flight
+        const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
         const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
-        unsigned long long seen = 0;
         if (leader) {
             refined += 1;
-            updates += publish(wk, s, c, cand_sq, &seen);
+            updates += publish(wk, s, c, cand_sq);
         }
-        bnd = bound_from_bits(__shfl_sync(gmask, seen, lane & ~(kRowLanes - 1)));
+        bnd = bound_from_bits(min(seen, static_cast<unsigned long long>(__double_as_longlong(s < INFINITY ? s : INFINITY))));
     }
     if (leader) {
         if (refined) atomicAdd(&wk->stats[kRealDist], refined);
@@ -628,7 +668,8 @@ __global__ void __launch_bounds__(kThreads)
 // Lowest position among the candidates whose sqrt(sum) equals the best
 // distance; the last block to finish writes the result and resets `wk`.
 __global__ void __launch_bounds__(kThreads)
-    k_finalize(QueryWork* wk, const uint32_t* __restrict__ cand_pos, const double* __restrict__ cand_sq, int seed_only,
+    k_finalize(QueryWork* wk, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cand_pos,
+               const double* __restrict__ cand_sq, int seed_only,
                uint64_t cap, DevResult* out, uint64_t P, uint64_t pos_offset) {
     const double best = bsf_of(wk->bsf_bits);
     const double dist = sqrt(best);
@@ -640,7 +681,7 @@ __global__ void __launch_bounds__(kThreads)
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t c = i < lo_end ? i : cap - 1 - (i - lo_end);
         const double s = cand_sq[c];
-        if (s <= lim && sqrt(s) == dist) mine = min(mine, cand_pos[c]);
+        if (s <= lim && sqrt(s) == dist) mine = min(mine, pos[cand_pos[c]]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
@@ -697,12 +738,17 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     TSG_CUDA(cudaFuncSetAttribute(lbscan, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
+    // With several query lanes, each kernel gets a share of the GPU so kernels
+    // of different queries co-reside (TSG_GRID_SHARE: 1/share of the
+    // resident-block capacity; default 2 when lanes run concurrently).
+    const int share_env = std::getenv("TSG_GRID_SHARE") ? std::atoi(std::getenv("TSG_GRID_SHARE")) : 0;
+    const int share = std::max(1, share_env > 0 ? share_env : (ix.nlanes > 1 && !ix.profile ? 2 : 1));
     const unsigned bound_grid = cap_grid((ix.P + kThreads * kPP - 1) / (kThreads * kPP), ix.sms,
-                                         std::min(6, blocks_per_sm(bound, lut_bytes)));
+                                         std::max(1, std::min(6, blocks_per_sm(bound, lut_bytes)) / share));
     const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
                                         ix.sms, blocks_per_sm(seed, q_bytes));
-    const unsigned scan_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(lbscan, lut_bytes));
-    const unsigned refine_grid = static_cast<unsigned>(ix.sms * blocks_per_sm(refine, q_bytes));
+    const unsigned scan_grid = static_cast<unsigned>(std::max(ix.sms, ix.sms * blocks_per_sm(lbscan, lut_bytes) / share));
+    const unsigned refine_grid = static_cast<unsigned>(std::max(ix.sms, ix.sms * blocks_per_sm(refine, q_bytes) / share));
     const uint64_t cap = ix.cand_cap;
     // Profiling runs one lane so per-kernel times are not overlapped.
     const int nl = ix.profile ? 1 : std::max(1, std::min<int>(ix.nlanes, static_cast<int>(nq)));
@@ -749,20 +795,20 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
             TSG_LAUNCHED();
             for (int wave = 0; wave < 2; ++wave) {
                 mark(ls, 4, [&] {
-                    lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, ix.page_off, L.surv,
-                                                                   L.surv_lb, ix.P, L.work, wave, ix.refine_split, cap,
-                                                                   L.cand_pos, L.cand_lb);
+                    lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, L.surv, L.surv_lb,
+                                                                   ix.P, L.work, wave, ix.refine_split, cap, L.cand_pos,
+                                                                   L.cand_lb);
                 });
                 TSG_LAUNCHED();
                 mark(ls, wave == 0 ? 3 : 5, [&] {
-                    refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, L.work, L.cand_pos, L.cand_lb,
+                    refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, ix.pos, L.work, L.cand_pos, L.cand_lb,
                                                                    L.cand_sq, wave, cap);
                 });
                 TSG_LAUNCHED();
             }
         }
         mark(ls, 6, [&] {
-            k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
+            k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, ix.pos, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
                                                     ix.results + qi, ix.P, ix.pos_offset);
         });
         TSG_LAUNCHED();
