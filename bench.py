@@ -284,11 +284,20 @@ def run_ours(args):
         return rec, res
 
     def timed(host, stats=None, answers=None):
+        # CUDA events on the current stream bracket the K batches; each batch
+        # call returns only after its lanes' streams finished (results are on
+        # the host), so the end event is recorded after all of the batch work.
         barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        kept = []
         for i in range(args.warmup, total_batches):
-            rec, res = step(i, host=host)
+            kept.append(step(i, host=host))
+        ev1.record()
+        torch.cuda.synchronize()
+        barrier()
+        for rec, res in kept:  # bookkeeping outside the timed region
             if answers is not None:
                 answers.append(rec)
             if stats is not None:
@@ -296,9 +305,7 @@ def run_ours(args):
                     s = r.stats
                     stats += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
                               s.pruned_subtrees, s.queue_insertions)
-        torch.cuda.synchronize()
-        barrier()
-        return max_over_ranks(time.perf_counter() - t0)
+        return max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
 
     # warm-up
     for i in range(args.warmup):
@@ -306,9 +313,8 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # ---- timed: device-resident queries (the `value`) ----
-    # Each call is synchronous (results come back to the host per batch), so
-    # the wall clock between the synchronize/barrier pairs is the device time
-    # of the K batches plus the per-batch result D2H.
+    # Each call is synchronous (results come back to the host per batch): the
+    # event pair measures the K batches plus the per-batch result D2H.
     launches0 = tg.launch_count()
     stats_acc = np.zeros(6, np.float64)
     answers = []

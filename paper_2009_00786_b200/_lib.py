@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtsgpu.so")
+# TSG_LIB_PATH: an alternative build of the same library (A/B timing runs).
+LIB_PATH = os.environ.get("TSG_LIB_PATH") or os.path.join(PKG, "libtsgpu.so")
 
 TSG_OK, TSG_INVALID_ARGUMENT, TSG_RUNTIME, TSG_LOGIC, TSG_CUDA, TSG_NCCL, TSG_OOM = range(7)
 

@@ -8,6 +8,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -138,11 +139,14 @@ void free_shard(DevIndex& s) {
     if (s.own_rows) cudaFree(s.rows);
     cudaFree(s.thr);
     cudaFree(s.words);
+    cudaFree(s.run_lo);
+    cudaFree(s.run_hi);
     cudaFree(s.pos);
     cudaFree(s.leaf_off);
     // page arrays come from the stream-ordered pool (build.cu)
     for (void* p : {static_cast<void*>(s.page_off), static_cast<void*>(s.page_leaf), static_cast<void*>(s.page_key),
-                    static_cast<void*>(s.page_lo), static_cast<void*>(s.page_hi), static_cast<void*>(s.page_dir)})
+                    static_cast<void*>(s.page_lo), static_cast<void*>(s.page_hi), static_cast<void*>(s.page_dir),
+                    static_cast<void*>(s.group_lo), static_cast<void*>(s.group_hi)})
         if (p) cudaFreeAsync(p, s.stream);
     if (s.stream) cudaStreamSynchronize(s.stream);
     for (int k = 0; k < DevIndex::kLanes; ++k) {
@@ -151,12 +155,14 @@ void free_shard(DevIndex& s) {
         cudaFree(l.lut);
         cudaFree(l.surv);
         cudaFree(l.surv_lb);
+        cudaFree(l.gsurv);
         cudaFree(l.cand_pos);
         cudaFree(l.cand_lb);
         cudaFree(l.cand_sq);
         if (l.done) cudaEventDestroy(l.done);
         if (k > 0 && l.stream) cudaStreamDestroy(l.stream);
     }
+    if (s.graph) cudaGraphExecDestroy(s.graph);
     cudaFree(s.results);
     cudaFree(s.queries);
     if (s.stream) cudaStreamDestroy(s.stream);
@@ -225,6 +231,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
         TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint2)));
         TSG_CUDA(cudaMalloc(&l.surv_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
+        TSG_CUDA(cudaMalloc(&l.gsurv, std::max<uint64_t>(s.NG, 1) * sizeof(uint32_t)));
         TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));
         TSG_CUDA(cudaMalloc(&l.cand_lb, N * sizeof(float)));
         TSG_CUDA(cudaMalloc(&l.cand_sq, N * sizeof(double)));
@@ -296,7 +303,12 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
                                      cudaMemcpyHostToDevice, s.stream));
             dq = s.queries;
         }
+        static const bool trace_enqueue = std::getenv("TSG_TRACE_ENQUEUE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         search_batch(s, dq, nq, approximate);
+        if (trace_enqueue)
+            std::fprintf(stderr, "[tsg search] %u queries enqueued in %.3f ms\n", nq,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         TSG_CUDA(cudaMemcpyAsync(per[k].data(), s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
         TSG_CUDA(cudaStreamSynchronize(s.stream));
     };

@@ -51,14 +51,43 @@ __global__ void k_iota(uint32_t* v, uint64_t n) {
     GRID_STRIDE(i, n) v[i] = static_cast<uint32_t>(i);
 }
 
-// words[i] = words_orig[pos[i]] (16- or 32-byte rows).
+// words[i] = words_orig[pos[i]] (16- or 32-byte rows), and the run boxes:
+// bytewise min / max over each aligned kRun-entry run of the sorted words
+// (half-warp shuffles; a warp's 32 consecutive entries are two runs).
 __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* __restrict__ pos,
-                               uint8_t* __restrict__ dst, uint64_t n, int ws) {
-    GRID_STRIDE(i, n) {
-        const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<uint64_t>(pos[i]) * ws);
-        uint4* d = reinterpret_cast<uint4*>(dst + i * ws);
-        d[0] = s[0];
-        if (ws == 32) d[1] = s[1];
+                               uint8_t* __restrict__ dst, uint8_t* __restrict__ run_lo, uint8_t* __restrict__ run_hi,
+                               uint64_t n, int ws) {
+    static_assert(kRun == 16, "run boxes are half-warp reductions");
+    const int lane = threadIdx.x & 31;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t w0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); w0 < n; w0 += stride) {
+        const uint64_t i = w0 + lane;
+        const bool in = i < n;
+        const uint64_t p = in ? pos[i] : 0;
+        for (int h = 0; h < ws / 16; ++h) {
+            uint4 x = make_uint4(0, 0, 0, 0);
+            if (in) {
+                x = *reinterpret_cast<const uint4*>(src + p * ws + 16 * h);
+                *reinterpret_cast<uint4*>(dst + i * ws + 16 * h) = x;
+            }
+            uint4 mn = in ? x : make_uint4(~0u, ~0u, ~0u, ~0u), mx = x;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                mn.x = __vminu4(mn.x, __shfl_xor_sync(0xFFFFFFFFu, mn.x, o));
+                mn.y = __vminu4(mn.y, __shfl_xor_sync(0xFFFFFFFFu, mn.y, o));
+                mn.z = __vminu4(mn.z, __shfl_xor_sync(0xFFFFFFFFu, mn.z, o));
+                mn.w = __vminu4(mn.w, __shfl_xor_sync(0xFFFFFFFFu, mn.w, o));
+                mx.x = __vmaxu4(mx.x, __shfl_xor_sync(0xFFFFFFFFu, mx.x, o));
+                mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xFFFFFFFFu, mx.y, o));
+                mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xFFFFFFFFu, mx.z, o));
+                mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xFFFFFFFFu, mx.w, o));
+            }
+            if ((lane & 15) == 0 && in) {
+                const uint64_t r = i / kRun;
+                *reinterpret_cast<uint4*>(run_lo + r * ws + 16 * h) = mn;
+                *reinterpret_cast<uint4*>(run_hi + r * ws + 16 * h) = mx;
+            }
+        }
     }
 }
 
@@ -180,6 +209,26 @@ __global__ void k_page_box(const uint8_t* __restrict__ words, const uint32_t* __
     }
 }
 
+// Group boxes: bytewise min / max over kGroup consecutive page boxes (one
+// thread per group and 16-byte half).
+__global__ void k_group_box(const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, uint64_t P, uint64_t NG,
+                            int ws, uint8_t* __restrict__ glo, uint8_t* __restrict__ ghi) {
+    const int H = ws / 16;
+    GRID_STRIDE(i, NG * H) {
+        const uint64_t g = i / H;
+        const int h = static_cast<int>(i % H);
+        uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
+        for (uint64_t p = g * kGroup; p < min(P, (g + 1) * kGroup); ++p) {
+            const uint4 a = *reinterpret_cast<const uint4*>(lo + p * ws + 16 * h);
+            const uint4 b = *reinterpret_cast<const uint4*>(hi + p * ws + 16 * h);
+            mn = make_uint4(__vminu4(mn.x, a.x), __vminu4(mn.y, a.y), __vminu4(mn.z, a.z), __vminu4(mn.w, a.w));
+            mx = make_uint4(__vmaxu4(mx.x, b.x), __vmaxu4(mx.y, b.y), __vmaxu4(mx.z, b.z), __vmaxu4(mx.w, b.w));
+        }
+        *reinterpret_cast<uint4*>(glo + g * ws + 16 * h) = mn;
+        *reinterpret_cast<uint4*>(ghi + g * ws + 16 * h) = mx;
+    }
+}
+
 unsigned grid_for(uint64_t n, int threads, int sms) {
     return static_cast<unsigned>(
         std::max<uint64_t>(1, std::min<uint64_t>((n + threads - 1) / threads, static_cast<uint64_t>(sms) * 32)));
@@ -212,6 +261,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&ix.leaf_off, (N + 1) * 4));
+    ix.R = (N + kRun - 1) / kRun;
+    TSG_CUDA(cudaMalloc(&ix.run_lo, ix.R * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.run_hi, ix.R * ix.ws));
     // pos_in / bstart are reused for the L+1 page counts / bases (L <= N).
     DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in((N + 1) * 4), flags(N), bstart((N + 1) * 4),
         nsel(8),
@@ -240,7 +292,8 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
         TSG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         const uint64_t pages_est = N / kPage + N / 64 + 4096;
         void* r = nullptr;
-        TSG_CUDA(cudaMallocAsync(&r, pages_est * (4 + 4 + 8 + 2 * ix.ws) + pages_est / 16 + 4096, st));
+        TSG_CUDA(cudaMallocAsync(&r, pages_est * (4 + 4 + 8 + 2 * ix.ws) + pages_est / 16 + pages_est / 2 * ix.ws + 8192,
+                                 st));
         TSG_CUDA(cudaFreeAsync(r, st));
     }
     TSG_CUDA(cudaStreamSynchronize(st));
@@ -255,7 +308,8 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_LAUNCHED();
     TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
                                              pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
-    k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, N, ix.ws);
+    k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, ix.run_lo,
+                                                          ix.run_hi, N, ix.ws);
     TSG_LAUNCHED();
     TSG_CUDA(cudaEventRecord(ev[2], st));
 
@@ -323,6 +377,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_hi), ix.P * ix.ws, st));
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_key), ix.P * 8, st));
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.page_dir), ndir * 8, st));
+    ix.NG = (ix.P + kGroup - 1) / kGroup;
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.group_lo), ix.NG * ix.ws, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.group_hi), ix.NG * ix.ws, st));
     trace("page-alloc");
     k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase, ix.page_off, ix.page_leaf);
     TSG_LAUNCHED();
@@ -332,6 +389,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cudaMemcpy2DAsync(ix.page_dir, 8, ix.page_key, 256 * 8, 8, ndir, cudaMemcpyDeviceToDevice, st));
     k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.page_off, ix.P, ix.ws, ix.page_lo,
                                                               ix.page_hi);
+    TSG_LAUNCHED();
+    k_group_box<<<grid_for(ix.NG * (ix.ws / 16), 256, sms), 256, 0, st>>>(ix.page_lo, ix.page_hi, ix.P, ix.NG, ix.ws,
+                                                                         ix.group_lo, ix.group_hi);
     TSG_LAUNCHED();
     trace("pages");
     TSG_CUDA(cudaEventRecord(ev[3], st));

@@ -34,6 +34,12 @@ struct DevIndex {
     uint64_t* page_key = nullptr;   // [P] sort key of each page's first entry
     uint8_t* page_lo = nullptr;     // [P][ws] per-segment min symbol
     uint8_t* page_hi = nullptr;     // [P][ws] per-segment max symbol
+    uint8_t* group_lo = nullptr;    // [NG][ws] per-segment min symbol of pages [kGroup g, kGroup g + kGroup)
+    uint8_t* group_hi = nullptr;    // [NG][ws] per-segment max symbol
+    uint64_t NG = 0;                // ceil(P / kGroup)
+    uint8_t* run_lo = nullptr;      // [R][ws] per-segment min symbol of entries [kRun r, kRun r + kRun)
+    uint8_t* run_hi = nullptr;      // [R][ws] per-segment max symbol
+    uint64_t R = 0;                 // ceil(N / kRun)
     uint64_t P = 0;
     uint64_t root_children = 0;
     uint64_t inner = 0, max_depth = 0, overflow = 0;
@@ -45,6 +51,7 @@ struct DevIndex {
         cudaEvent_t done = nullptr;
         struct QueryWork* work = nullptr;
         float* lut = nullptr;          // [w][256] squared-gap table of the lane's query
+        uint32_t* gsurv = nullptr;     // [NG] surviving page groups
         uint2* surv = nullptr;         // [P] surviving pages' entry ranges: wave 0 from the front, wave 1 from the back
         float* surv_lb = nullptr;      // [P] their box bounds
         uint32_t* cand_pos = nullptr;  // [cap]
@@ -53,7 +60,15 @@ struct DevIndex {
     };
     static constexpr int kLanes = 16;
     Lane lanes[kLanes];
-    int nlanes = 1;                // lanes in use (TSG_QUERY_LANES, default kLanes)
+    int nlanes = 1;                // lanes in use (TSG_QUERY_LANES, default 8)
+    cudaGraphExec_t graph = nullptr;  // the last query batch, captured (updated in place when the shape repeats)
+    struct GraphKey {
+        const float* queries = nullptr;
+        uint32_t nq = 0;
+        bool approximate = false;
+        int nlanes = 0;
+        int kernels = 0;  // launches the graph holds
+    } graph_key;
     uint64_t cand_cap = 0;
     struct DevResult* results = nullptr;  // [results_cap]
     uint32_t results_cap = 0;
@@ -68,6 +83,8 @@ struct DevIndex {
 };
 
 constexpr int kProfSlots = 8;
+constexpr int kGroup = 8;  // pages per group box (the level above pages)
+constexpr int kRun = 16;  // entries per run box (the sub-page filter level)
 
 // Per-query device scratch (reset by the prep kernel).
 struct QueryWork {
@@ -81,6 +98,7 @@ struct QueryWork {
     unsigned int nsurv;                 // surviving pages, wave 0 (bound <= split x seed bound)
     unsigned int nsurv_hi;              // surviving pages, wave 1 (stored from the back of surv)
     unsigned int nhigh;                 // wave-1 candidates, stored at the top of the candidate arrays
+    unsigned int ngroups;               // surviving page groups
     unsigned int done_blocks;           // finalize's last-block counter
     float scan_bound;                   // BSF bound the page/word filters used
     unsigned long long stats[6];  // SearchStats order

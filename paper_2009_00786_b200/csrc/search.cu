@@ -146,6 +146,7 @@ __device__ __forceinline__ void reset_work(QueryWork* wk) {
     wk->best_pos = 0xFFFFFFFFu;
     wk->nsurv = 0;
     wk->nsurv_hi = 0;
+    wk->ngroups = 0;
     for (int i = 0; i < 6; ++i) wk->stats[i] = 0;
 }
 
@@ -344,64 +345,150 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ------------------------------------------------------- bound + filter
-// Box bound per page: per segment the table entry of the query symbol
-// clamped into the box [lo, hi] (0 when the query symbol is inside). Pages
-// whose bound is within the BSF (and outside the seed range) survive. A
-// persistent grid; each thread bounds kPP pages per round (all loads issued
-// first) and one atomic per block and round reserves survivor slots.
-constexpr int kPP = 4;
+// Box bound: per segment the table entry of the query symbol clamped into the
+// box [lo, hi] (0 when the query symbol is inside) — node_lower_bound's
+// region gap (src/query.cpp:102-107) over a box of iSAX words.
+template <int H, bool W16>
+__device__ __forceinline__ float box_bound(const float* s_lut, const uint4* q4, const uint4* lo, const uint4* hi, int w) {
+    uint4 c[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+        c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, lo[h].x), hi[h].x), __vminu4(__vmaxu4(q4[h].y, lo[h].y), hi[h].y),
+                          __vminu4(__vmaxu4(q4[h].z, lo[h].z), hi[h].z), __vminu4(__vmaxu4(q4[h].w, lo[h].w), hi[h].w));
+    return word_bound<W16>(s_lut, c, w);
+}
+
+// Block-wide slot reservation: each thread brings two counts (< 2^16 per
+// block); returns its first slot in each of two global lists, with one
+// atomicAdd per list per block. All threads of the block must call it.
+__device__ __forceinline__ uint2 block_reserve(unsigned c0, unsigned c1, unsigned* ctr0, unsigned* ctr1) {
+    __shared__ uint32_t s_cnt[kThreads / 32];
+    __shared__ uint32_t s_base[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t mine = c0 | (c1 << 16);
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_cnt[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int i = 0; i < kThreads / 32; ++i) {
+            const uint32_t c = s_cnt[i];
+            s_cnt[i] = tot;
+            tot += c;
+        }
+        s_base[0] = (tot & 0xFFFFu) ? atomicAdd(ctr0, tot & 0xFFFFu) : 0u;
+        s_base[1] = (tot >> 16) && ctr1 ? atomicAdd(ctr1, tot >> 16) : 0u;
+    }
+    __syncthreads();
+    const uint32_t before = s_cnt[warp] + (incl - mine);
+    const uint2 r = make_uint2(s_base[0] + (before & 0xFFFFu), s_base[1] + (before >> 16));
+    __syncthreads();  // s_cnt / s_base are reused by the next call
+    return r;
+}
+
+// Level 1, the flat analog of the tree's internal nodes: one box per group
+// of kGroup consecutive pages. Surviving groups are listed (block-aggregated)
+// for the page level, which then runs balanced over them.
+constexpr int kGP = 4;  // groups / pages per thread per round
 
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
-    k_bound(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi,
-            const uint32_t* __restrict__ page_off, uint64_t P, QueryWork* wk, float split, uint2* __restrict__ surv,
-            float* __restrict__ surv_lb) {
+    k_groups(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ glo, const uint8_t* __restrict__ ghi,
+             uint64_t NG, QueryWork* wk, uint32_t* __restrict__ gsurv) {
+    constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
-    __shared__ uint32_t s_cnt[kThreads / 32];
-    __shared__ uint32_t s_base, s_base_hi;
     load_prepared(lut_g, wk, w, s_lut, qsym);
-    uint4 q4[WS / 16];
+    uint4 q4[H];
 #pragma unroll
-    for (int h = 0; h < WS / 16; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+    for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
     const float bound = bound_from_bits(wk->bsf_bits);
-    const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
-    const float cut = bound * split;  // wave 0: the most promising pages
     unsigned long long pruned = 0;
-    constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kPP;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < P;
+    constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kGP;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < NG;
          base += static_cast<uint64_t>(gridDim.x) * kRound) {
-        uint4 blo[kPP][WS / 16], bhi[kPP][WS / 16];
-        uint32_t ea[kPP], eb[kPP];
+        uint4 bl[kGP][H], bh[kGP][H];
 #pragma unroll
-        for (int k = 0; k < kPP; ++k) {
-            const uint64_t p = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-            const bool in = p < P;
+        for (int k = 0; k < kGP; ++k) {
+            const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
 #pragma unroll
-            for (int h = 0; h < WS / 16; ++h) {
-                blo[k][h] = in ? ld_stream_u4(lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                bhi[k][h] = in ? ld_stream_u4(hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            for (int h = 0; h < H; ++h) {
+                bl[k][h] = g < NG ? ld_stream_u4(glo + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bh[k][h] = g < NG ? ld_stream_u4(ghi + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
             }
-            ea[k] = in ? page_off[p] : 0u;
-            eb[k] = in ? page_off[p + 1] : 0u;
+        }
+        unsigned keep = 0;
+#pragma unroll
+        for (int k = 0; k < kGP; ++k) {
+            const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            if (g >= NG) continue;
+            if (box_bound<H, W16>(s_lut, q4, bl[k], bh[k], w) <= bound) keep |= 1u << k;
+            else pruned += 1;
+        }
+        uint32_t at = block_reserve(__popc(keep), 0, &wk->ngroups, nullptr).x;
+#pragma unroll
+        for (int k = 0; k < kGP; ++k)
+            if (keep & (1u << k)) gsurv[at++] = static_cast<uint32_t>(base + threadIdx.x + static_cast<uint64_t>(kThreads) * k);
+    }
+    for (int o = 16; o > 0; o >>= 1) pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
+    if ((threadIdx.x & 31) == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&wk->stats[kLbNode], NG);
+}
+
+// Level 2: the pages of the surviving groups, kGP per thread per round.
+// Pages whose bound is within the BSF (and outside the seed range) survive,
+// split into page wave 0 (bound <= split x BSF, front of surv) and wave 1
+// (back of surv); one atomic pair per block and round reserves the slots.
+template <int WS, bool W16>
+__global__ void __launch_bounds__(kThreads)
+    k_bound(const float* __restrict__ lut_g, int w, const uint32_t* __restrict__ gsurv,
+            const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, const uint32_t* __restrict__ page_off,
+            uint64_t P, QueryWork* wk, float split, uint2* __restrict__ surv, float* __restrict__ surv_lb) {
+    constexpr int H = WS / 16;
+    extern __shared__ float s_lut[];
+    __shared__ __align__(16) unsigned char qsym[kMaxW];
+    load_prepared(lut_g, wk, w, s_lut, qsym);
+    uint4 q4[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+    const float bound = wk->scan_bound;
+    const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
+    const float cut = bound * split;  // wave 0: the most promising pages
+    const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
+    unsigned long long pruned = 0, nodes = 0;
+    constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kGP;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < nitems;
+         base += static_cast<uint64_t>(gridDim.x) * kRound) {
+        uint4 bl[kGP][H], bh[kGP][H];
+        uint32_t ea[kGP], eb[kGP];
+        bool valid[kGP];
+#pragma unroll
+        for (int k = 0; k < kGP; ++k) {
+            const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : P;
+            valid[k] = p < P;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                bl[k][h] = valid[k] ? ld_stream_u4(lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bh[k][h] = valid[k] ? ld_stream_u4(hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            }
+            ea[k] = valid[k] ? page_off[p] : 0u;
+            eb[k] = valid[k] ? page_off[p + 1] : 0u;
         }
         unsigned lowmask = 0, highmask = 0;
-        float lbs[kPP];
+        float lbs[kGP];
 #pragma unroll
-        for (int k = 0; k < kPP; ++k) {
-            const uint64_t p = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+        for (int k = 0; k < kGP; ++k) {
             lbs[k] = 0.f;
-            if (p >= P) continue;
-            uint4 c[WS / 16];
-#pragma unroll
-            for (int h = 0; h < WS / 16; ++h)
-                c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, blo[k][h].x), bhi[k][h].x),
-                                  __vminu4(__vmaxu4(q4[h].y, blo[k][h].y), bhi[k][h].y),
-                                  __vminu4(__vmaxu4(q4[h].z, blo[k][h].z), bhi[k][h].z),
-                                  __vminu4(__vmaxu4(q4[h].w, blo[k][h].w), bhi[k][h].w));
-            const float lb = word_bound<W16>(s_lut, c, w);
+            if (!valid[k]) continue;
+            nodes += 1;
+            const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], w);
             lbs[k] = lb;
             const bool seeded = ea[k] >= sa && eb[k] <= sb;
             const bool keep = !seeded && lb <= bound;
@@ -409,32 +496,10 @@ __global__ void __launch_bounds__(kThreads)
             highmask |= (keep && lb > cut) ? (1u << k) : 0u;
             pruned += (!keep && !seeded) ? 1 : 0;
         }
-        // wave-0 count in the low 16 bits, wave-1 count in the high 16 bits
-        const int mine = __popc(lowmask) | (__popc(highmask) << 16);
-        int incl = mine;
+        const uint2 at0 = block_reserve(__popc(lowmask), __popc(highmask), &wk->nsurv, &wk->nsurv_hi);
+        uint32_t at = at0.x, at_hi = at0.y;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) s_cnt[warp] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t tot = 0;
-            for (int i = 0; i < kThreads / 32; ++i) {
-                const uint32_t cnt = s_cnt[i];
-                s_cnt[i] = tot;
-                tot += cnt;
-            }
-            s_base = (tot & 0xFFFFu) ? atomicAdd(&wk->nsurv, tot & 0xFFFFu) : 0u;
-            s_base_hi = (tot >> 16) ? atomicAdd(&wk->nsurv_hi, tot >> 16) : 0u;
-        }
-        __syncthreads();
-        const uint32_t before = s_cnt[warp] + (incl - mine);
-        uint32_t at = s_base + (before & 0xFFFFu);
-        uint32_t at_hi = s_base_hi + (before >> 16);
-#pragma unroll
-        for (int k = 0; k < kPP; ++k) {
+        for (int k = 0; k < kGP; ++k) {
             if (lowmask & (1u << k)) {
                 surv_lb[at] = lbs[k];
                 surv[at++] = make_uint2(ea[k], eb[k]);
@@ -444,10 +509,15 @@ __global__ void __launch_bounds__(kThreads)
                 surv[slot] = make_uint2(ea[k], eb[k]);
             }
         }
-        __syncthreads();
     }
-    for (int o = 16; o > 0; o >>= 1) pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
-    if (lane == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
+    for (int o = 16; o > 0; o >>= 1) {
+        pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
+        nodes += __shfl_xor_sync(0xFFFFFFFFu, nodes, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
+        if (nodes) atomicAdd(&wk->stats[kLbNode], nodes);
+    }
 }
 
 // ------------------------------------------------------------ lbscan
@@ -490,83 +560,149 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
 // of the seed bound (surv[0, nsurv)), wave 1 the rest (surv[P - nsurv_hi, P)),
 // re-filtered against the BSF that wave 0's refinement tightened — MESSI's
 // LB-ordered leaf processing (src/query.cpp:173-184) at page granularity.
-// Surviving pages go round-robin over warps (each <= kPage entries, so work
-// units are bounded); a lane bounds entries lane, lane+32, ... of a page, the
-// next page's words in flight while the current one is bounded.
+// Below the page sits one more box level: aligned kRun-entry runs. A warp
+// takes three surviving pages at a time; lane 10j + t bounds run t of page j
+// (a <= 128-entry page touches at most 9 runs) with the same clamped-symbol
+// box bound as the page filter, surviving runs (clipped to their page) queue
+// in shared memory, and the queue drains four runs per step: each half-warp
+// bounds one run's words, one entry per lane. Words of pruned runs are never
+// read. The next triple's ranges and run boxes are in flight while the
+// current one is bounded.
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
     k_lbscan(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ words,
-             const uint32_t* __restrict__ pos, const uint2* __restrict__ surv, const float* __restrict__ surv_lb,
+             const uint8_t* __restrict__ run_lo, const uint8_t* __restrict__ run_hi,
+             const uint2* __restrict__ surv, const float* __restrict__ surv_lb,
              uint64_t P, QueryWork* wk,
              int wave, float split, uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
+    constexpr int kRunQ = 40;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_pos[kThreads / 32][kStageCap];
     __shared__ float s_lb[kThreads / 32][kStageCap];
+    __shared__ uint2 s_runq[kThreads / 32][kRunQ];
     load_prepared(lut_g, wk, w, s_lut, qsym);
     constexpr int H = WS / 16;
-    constexpr int K = kPage / 32;
+    uint4 q4[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    const int grp = lane / 10, t = lane - 10 * grp;  // page of the triple, run of the page (lanes 30, 31 idle)
     const float bound = bound_from_bits(wk->bsf_bits);
     // Page wave 0 splits its candidates into refinement waves A and B by their
     // own bound; page wave 1 (scanned after wave A is refined) feeds wave B.
     const float cut = wave == 0 ? wk->scan_bound * split : -1.f;
     const uint32_t nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
+    const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
     const uint64_t gwarp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    int cnt = 0;
+    int cnt = 0, qn = 0;
     unsigned long long scanned = 0, pruned = 0;
-    uint32_t na = 0, nb = 0;
-    uint4 nwv[K][H];
-    auto fetch = [&](uint64_t i) {
-        const uint64_t slot = wave == 0 ? i : P - 1 - i;
-        na = nb = 0;
-        if (wave == 0 || surv_lb[slot] <= bound) {
-            const uint2 r = surv[slot];
-            na = r.x;
-            nb = r.y;
-        } else {
-            pruned += lane == 0 ? 1 : 0;
+
+    auto stage = [&](bool pass, uint32_t e, float lb) {
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+        if (!m) return;
+        if (pass) {
+            const int slot = cnt + __popc(m & below);
+            s_pos[warp][slot] = e;  // refine gathers pos[e] off this kernel's path
+            s_lb[warp][slot] = lb;
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t e = na + lane + 32 * k;
-#pragma unroll
-            for (int h = 0; h < H; ++h)
-                nwv[k][h] = e < nb ? ld_stream_u4(words + static_cast<uint64_t>(e) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+        cnt += __popc(m);
+        __syncwarp();
+        if (cnt > kStageCap - 32) {
+            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
+            cnt = 0;
         }
     };
-    if (gwarp < nsurv) fetch(gwarp);
-    for (uint64_t i = gwarp; i < nsurv; i += nwarps) {
-        const uint32_t a = na, b = nb;
-        uint4 wv[K][H];
+    // Bounds the words of the first min(qn, 4) queued runs, then shifts the queue.
+    auto drain = [&]() {
+        const int take = min(qn, 4);
+        uint4 wv[2][H];
+        uint32_t e[2];
+        bool ok[2];
 #pragma unroll
-        for (int k = 0; k < K; ++k)
+        for (int k = 0; k < 2; ++k) {
+            const int q = 2 * k + (lane >> 4);
+            ok[k] = false;
+            e[k] = 0;
+            if (q < take) {
+                const uint2 rr = s_runq[warp][q];
+                e[k] = rr.x + (lane & 15);
+                ok[k] = e[k] < rr.y;
+            }
 #pragma unroll
-            for (int h = 0; h < H; ++h) wv[k][h] = nwv[k][h];
-        if (i + nwarps < nsurv) fetch(i + nwarps);
-        if (a == b) continue;
-        scanned += b - a;
+            for (int h = 0; h < H; ++h)
+                wv[k][h] = ok[k] ? ld_stream_u4(words + static_cast<uint64_t>(e[k]) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t e = a + lane + 32 * k;
+        for (int k = 0; k < 2; ++k) {
             const float lb = word_bound<W16>(s_lut, wv[k], w);
-            const bool pass = e < b && lb <= bound;
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-            if (m) {
-                if (pass) {
-                    const int slot = cnt + __popc(m & ((1u << lane) - 1u));
-                    s_pos[warp][slot] = e;  // refine gathers pos[e] off this kernel's path
-                    s_lb[warp][slot] = lb;
-                }
-                cnt += __popc(m);
-                __syncwarp();
-                if (cnt > kStageCap - 32) {
-                    flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
-                    cnt = 0;
+            scanned += ok[k] ? 1 : 0;
+            stage(ok[k] && lb <= bound, e[k], lb);
+        }
+        const int rest = qn - take;
+        uint2 v = make_uint2(0, 0);
+        if (lane < rest) v = s_runq[warp][take + lane];
+        __syncwarp();
+        if (lane < rest) s_runq[warp][lane] = v;
+        __syncwarp();
+        qn = rest;
+    };
+
+    uint32_t na = 0, nb = 0, nrun = 0;
+    bool nvalid = false;
+    uint4 nbl[H], nbh[H];
+    auto fetch = [&](uint64_t T) {
+        uint32_t a = 0, b = 0;
+        if (lane < 3) {
+            const uint64_t i = 3 * T + lane;
+            if (i < nsurv) {
+                const uint64_t slot = wave == 0 ? i : P - 1 - i;
+                if (wave == 0 || surv_lb[slot] <= bound) {
+                    const uint2 r = surv[slot];
+                    a = r.x;
+                    b = r.y;
+                } else {
+                    pruned += 1;
                 }
             }
         }
+        na = __shfl_sync(0xFFFFFFFFu, a, min(grp, 2));
+        nb = __shfl_sync(0xFFFFFFFFu, b, min(grp, 2));
+        nrun = na / kRun + t;
+        nvalid = grp < 3 && na < nb && nrun * kRun < nb;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            nbl[h] = nvalid ? ld_stream_u4(run_lo + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            nbh[h] = nvalid ? ld_stream_u4(run_hi + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    if (gwarp < ntrip) fetch(gwarp);
+    for (uint64_t T = gwarp; T < ntrip; T += nwarps) {
+        const uint32_t a = na, b = nb, r = nrun;
+        const bool valid = nvalid;
+        uint4 c[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, nbl[h].x), nbh[h].x),
+                              __vminu4(__vmaxu4(q4[h].y, nbl[h].y), nbh[h].y),
+                              __vminu4(__vmaxu4(q4[h].z, nbl[h].z), nbh[h].z),
+                              __vminu4(__vmaxu4(q4[h].w, nbl[h].w), nbh[h].w));
+        if (T + nwarps < ntrip) fetch(T + nwarps);
+        bool pass = false;
+        if (valid) pass = word_bound<W16>(s_lut, c, w) <= bound;
+        pruned += valid && !pass ? 1 : 0;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+        if (pass) s_runq[warp][qn + __popc(m & below)] = make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
+        qn += __popc(m);
+        __syncwarp();
+        while (qn >= 4) drain();
+    }
+    while (qn > 0) drain();
+    for (int o = 16; o > 0; o >>= 1) {
+        scanned += __shfl_xor_sync(0xFFFFFFFFu, scanned, o);
+        pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
     }
     // Final flush, one atomic pair per block instead of one per warp.
     __shared__ uint32_t s_wcnt[kThreads / 32], s_wbase[2];
@@ -697,7 +833,7 @@ __global__ void __launch_bounds__(kThreads)
     out->distance = dist;
     out->position = static_cast<uint32_t>(best_pos + pos_offset);
     out->reserved = 0;
-    out->stats[kLbNode] = P;
+    out->stats[kLbNode] = wk->stats[kLbNode];
     out->stats[kLbEntry] = wk->stats[kLbEntry] + wk->nseed;
     out->stats[kRealDist] = wk->stats[kRealDist];
     out->stats[kBsfUpd] = wk->stats[kBsfUpd];
@@ -732,6 +868,8 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     auto seed = vec ? k_seed<true> : k_seed<false>;
     auto lbscan = ix.ws == 16 ? (w16 ? k_lbscan<16, true> : k_lbscan<16, false>) : k_lbscan<32, false>;
     auto bound = ix.ws == 16 ? (w16 ? k_bound<16, true> : k_bound<16, false>) : k_bound<32, false>;
+    auto groups = ix.ws == 16 ? (w16 ? k_groups<16, true> : k_groups<16, false>) : k_groups<32, false>;
+    TSG_CUDA(cudaFuncSetAttribute(groups, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     // Per-device function attributes (cheap; set on every call so each device is covered).
     TSG_CUDA(cudaFuncSetAttribute(refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     TSG_CUDA(cudaFuncSetAttribute(seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -743,7 +881,10 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     // resident-block capacity; default 2 when lanes run concurrently).
     const int share_env = std::getenv("TSG_GRID_SHARE") ? std::atoi(std::getenv("TSG_GRID_SHARE")) : 0;
     const int share = std::max(1, share_env > 0 ? share_env : (ix.nlanes > 1 && !ix.profile ? 2 : 1));
-    const unsigned bound_grid = cap_grid((ix.P + kThreads * kPP - 1) / (kThreads * kPP), ix.sms,
+    const unsigned group_grid = cap_grid((ix.NG + kThreads * kGP - 1) / (kThreads * kGP), ix.sms,
+                                         std::max(1, std::min(6, blocks_per_sm(groups, lut_bytes)) / share));
+    // (the page level's size is only known on the device: a resident-capacity grid)
+    const unsigned bound_grid = cap_grid((ix.P + kThreads * kGP - 1) / (kThreads * kGP), ix.sms,
                                          std::max(1, std::min(6, blocks_per_sm(bound, lut_bytes)) / share));
     const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
                                         ix.sms, blocks_per_sm(seed, q_bytes));
@@ -769,54 +910,97 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
         marks.push_back({slot, {a, b}});
     };
 
-    // Fork: every lane starts after the work already queued on the index stream.
-    TSG_CUDA(cudaEventRecord(ix.lanes[0].done, st));
-    for (int k = 0; k < nl; ++k) {
-        DevIndex::Lane& L = ix.lanes[k];
-        if (k > 0) TSG_CUDA(cudaStreamWaitEvent(L.stream, ix.lanes[0].done, 0));
-        k_reset<<<1, 1, 0, L.stream>>>(L.work);
-        TSG_LAUNCHED();
-    }
-    for (uint32_t qi = 0; qi < nq; ++qi) {
-        const DevIndex::Lane& L = ix.lanes[qi % nl];
-        cudaStream_t ls = L.stream;
-        const float* q = d_queries + static_cast<uint64_t>(qi) * n;
-        mark(ls, 2, [&] {
-            seed<<<seed_grid, kThreads, q_bytes, ls>>>(ix.rows, n, w, ix.bits, ix.thr, q, ix.leaf_off, ix.page_off,
-                                                       ix.page_leaf, ix.page_key, ix.page_dir, ix.P, ix.pos, seed_cap,
-                                                       L.work, L.cand_pos, L.cand_sq, L.lut);
-        });
-        TSG_LAUNCHED();
-        if (!approximate) {
-            mark(ls, 1, [&] {
-                bound<<<bound_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.page_lo, ix.page_hi, ix.page_off, ix.P,
-                                                               L.work, ix.refine_split, L.surv, L.surv_lb);
+    // Fork (every lane starts after the work already queued on the index
+    // stream), the queries round-robin over the lanes, join.
+    auto enqueue = [&]() {
+        TSG_CUDA(cudaEventRecord(ix.lanes[0].done, st));
+        for (int k = 0; k < nl; ++k) {
+            DevIndex::Lane& L = ix.lanes[k];
+            if (k > 0) TSG_CUDA(cudaStreamWaitEvent(L.stream, ix.lanes[0].done, 0));
+            k_reset<<<1, 1, 0, L.stream>>>(L.work);
+            TSG_LAUNCHED();
+        }
+        for (uint32_t qi = 0; qi < nq; ++qi) {
+            const DevIndex::Lane& L = ix.lanes[qi % nl];
+            cudaStream_t ls = L.stream;
+            const float* q = d_queries + static_cast<uint64_t>(qi) * n;
+            mark(ls, 2, [&] {
+                seed<<<seed_grid, kThreads, q_bytes, ls>>>(ix.rows, n, w, ix.bits, ix.thr, q, ix.leaf_off, ix.page_off,
+                                                           ix.page_leaf, ix.page_key, ix.page_dir, ix.P, ix.pos, seed_cap,
+                                                           L.work, L.cand_pos, L.cand_sq, L.lut);
             });
             TSG_LAUNCHED();
-            for (int wave = 0; wave < 2; ++wave) {
-                mark(ls, 4, [&] {
-                    lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.pos, L.surv, L.surv_lb,
-                                                                   ix.P, L.work, wave, ix.refine_split, cap, L.cand_pos,
-                                                                   L.cand_lb);
+            if (!approximate) {
+                mark(ls, 1, [&] {
+                    groups<<<group_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.group_lo, ix.group_hi, ix.NG, L.work,
+                                                                    L.gsurv);
+                    TSG_LAUNCHED();
+                    bound<<<bound_grid, kThreads, lut_bytes, ls>>>(L.lut, w, L.gsurv, ix.page_lo, ix.page_hi, ix.page_off,
+                                                                   ix.P, L.work, ix.refine_split, L.surv, L.surv_lb);
                 });
                 TSG_LAUNCHED();
-                mark(ls, wave == 0 ? 3 : 5, [&] {
-                    refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, ix.pos, L.work, L.cand_pos, L.cand_lb,
-                                                                   L.cand_sq, wave, cap);
-                });
-                TSG_LAUNCHED();
+                for (int wave = 0; wave < 2; ++wave) {
+                    mark(ls, 4, [&] {
+                        lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.run_lo, ix.run_hi, L.surv, L.surv_lb,
+                                                                       ix.P, L.work, wave, ix.refine_split, cap, L.cand_pos,
+                                                                       L.cand_lb);
+                    });
+                    TSG_LAUNCHED();
+                    mark(ls, wave == 0 ? 3 : 5, [&] {
+                        refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, ix.pos, L.work, L.cand_pos, L.cand_lb,
+                                                                       L.cand_sq, wave, cap);
+                    });
+                    TSG_LAUNCHED();
+                }
             }
+            mark(ls, 6, [&] {
+                k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, ix.pos, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
+                                                        ix.results + qi, ix.P, ix.pos_offset);
+            });
+            TSG_LAUNCHED();
         }
-        mark(ls, 6, [&] {
-            k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, ix.pos, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
-                                                    ix.results + qi, ix.P, ix.pos_offset);
-        });
-        TSG_LAUNCHED();
-    }
-    // Join: the index stream waits for every lane.
-    for (int k = 1; k < nl; ++k) {
-        TSG_CUDA(cudaEventRecord(ix.lanes[k].done, ix.lanes[k].stream));
-        TSG_CUDA(cudaStreamWaitEvent(st, ix.lanes[k].done, 0));
+        // Join: the index stream waits for every lane.
+        for (int k = 1; k < nl; ++k) {
+            TSG_CUDA(cudaEventRecord(ix.lanes[k].done, ix.lanes[k].stream));
+            TSG_CUDA(cudaStreamWaitEvent(st, ix.lanes[k].done, 0));
+        }
+    };
+
+    // TSG_GRAPHS=1: the batch is captured into a CUDA graph (~7 kernels per
+    // query over the lanes' streams as one launch, replayed while the batch
+    // shape and buffers repeat). Measured no faster than direct launches on
+    // c2 (the host enqueue overlaps the GPU), so off by default; it lets ncu
+    // (--graph-profiling graph) measure a whole concurrent batch.
+    const char* genv = std::getenv("TSG_GRAPHS");
+    const bool graph = !ix.profile && genv && genv[0] == '1';
+    if (!graph) {
+        enqueue();
+    } else if (ix.graph && ix.graph_key.queries == d_queries && ix.graph_key.nq == nq &&
+               ix.graph_key.approximate == approximate && ix.graph_key.nlanes == nl) {
+        // Same batch shape and buffers as the captured graph: replay it.
+        TSG_CUDA(cudaGraphLaunch(ix.graph, st));
+        note_launch(ix.graph_key.kernels);
+    } else {
+        TSG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue();
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        TSG_CUDA(cudaStreamEndCapture(st, &g));
+        if (ix.graph) {
+            TSG_CUDA(cudaStreamSynchronize(st));  // the previous batch's graph may still run
+            TSG_CUDA(cudaGraphExecDestroy(ix.graph));
+            ix.graph = nullptr;
+        }
+        TSG_CUDA(cudaGraphInstantiate(&ix.graph, g, 0));
+        TSG_CUDA(cudaGraphDestroy(g));
+        ix.graph_key = {d_queries, nq, approximate, nl, nl + static_cast<int>(nq) * (approximate ? 2 : 8)};
+        TSG_CUDA(cudaGraphLaunch(ix.graph, st));
     }
     if (!marks.empty()) {
         TSG_CUDA(cudaStreamSynchronize(st));

@@ -156,7 +156,8 @@ class Context:
     def __init__(self, devices: Sequence[int] = (0,)):
         devs = (C.c_int * len(devices))(*devices)
         h = C.c_void_p()
-        check(lib().tsg_open(len(devices), devs, C.byref(h)))
+        self._lib = lib()  # held so teardown at interpreter exit needs no module globals
+        check(self._lib.tsg_open(len(devices), devs, C.byref(h)))
         self._h = h
         self.devices = tuple(devices)
 
@@ -166,7 +167,7 @@ class Context:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().tsg_close(self._h)
+            self._lib.tsg_close(self._h)
             self._h = None
 
     def __del__(self):
@@ -188,6 +189,7 @@ class Index:
     Index owns its Dataset (src/index.cpp:255-256)."""
 
     def __init__(self, handle, data, config: IndexConfig, stats: BuildStats, ctx: Context, keepalive=None):
+        self._lib = lib()
         self._h = handle
         self._data = data
         self._config = config
@@ -229,7 +231,7 @@ class Index:
 
     def free(self):
         if getattr(self, "_h", None):
-            lib().tsg_index_free(self._h)
+            self._lib.tsg_index_free(self._h)
             self._h = None
 
     def __del__(self):

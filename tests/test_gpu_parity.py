@@ -161,6 +161,25 @@ def test_duplicates_overflow_leaves(oracle):
         assert r.distance == 0.0 and r.position == p
 
 
+def test_finalist_overflow_ties(oracle):
+    """More exact ties than finalize's finalist slots (4096 per lane): the
+    rescan of every candidate record must still return the lowest position."""
+    protos = oracle.generate(3, 64, 4242, znorm=False)
+    rows = np.concatenate([oracle.generate(1000, 64, 4243, znorm=False), np.tile(protos, (2500, 1))])
+    rng = np.random.default_rng(5)
+    perm = np.concatenate([np.arange(1000), 1000 + rng.permutation(7500)])
+    rows = np.ascontiguousarray(rows[perm])
+    index = tg.build_index(rows, tg.IndexConfig(n=64, w=16, leaf_capacity=50))
+    for p in range(3):
+        want = int(np.flatnonzero((rows == protos[p]).all(axis=1))[0])
+        res = tg.exact_search_batch(index, np.stack([protos[p]] * 3))  # several lanes
+        for r in res:
+            assert r.distance == 0.0 and r.position == want
+    # near-ties (one ulp apart in the data) resolve by distance, then position
+    check_against_scan(oracle, rows, np.concatenate([protos, protos + np.float32(1e-3)]).astype(np.float32),
+                       tg.IndexConfig(n=64, w=16, leaf_capacity=50))
+
+
 def test_single_series_dataset(oracle):
     rows = oracle.generate(1, 256, 20230506, znorm=False)
     index = tg.build_index(rows, tg.IndexConfig())
