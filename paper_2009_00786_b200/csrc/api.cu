@@ -134,6 +134,30 @@ struct tsg_index {
 
 namespace {
 
+void free_slots(DevIndex::Slots& t) {
+    for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.gsurv),
+                    static_cast<void*>(t.surv), static_cast<void*>(t.surv_lb), static_cast<void*>(t.cand_pos),
+                    static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq)})
+        cudaFree(p);
+    t = DevIndex::Slots{};
+}
+
+// Slot arrays for `n` queries with `cap` candidate records each.
+void alloc_slots(const DevIndex& s, DevIndex::Slots& t, uint32_t n, uint64_t cap) {
+    t.n = n;
+    t.cap = cap;
+    const uint64_t P = std::max<uint64_t>(s.P, 1), NG = std::max<uint64_t>(s.NG, 1);
+    TSG_CUDA(cudaMalloc(&t.work, n * sizeof(QueryWork)));
+    TSG_CUDA(cudaMemset(t.work, 0, n * sizeof(QueryWork)));
+    TSG_CUDA(cudaMalloc(&t.lut, n * static_cast<size_t>(s.w) * 256 * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&t.gsurv, n * NG * sizeof(uint32_t)));
+    TSG_CUDA(cudaMalloc(&t.surv, n * P * sizeof(uint2)));
+    TSG_CUDA(cudaMalloc(&t.surv_lb, n * P * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&t.cand_pos, n * cap * sizeof(uint32_t)));
+    TSG_CUDA(cudaMalloc(&t.cand_lb, n * cap * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&t.cand_sq, n * cap * sizeof(double)));
+}
+
 void free_shard(DevIndex& s) {
     DeviceGuard g(s.device);
     if (s.own_rows) cudaFree(s.rows);
@@ -141,6 +165,8 @@ void free_shard(DevIndex& s) {
     cudaFree(s.words);
     cudaFree(s.run_lo);
     cudaFree(s.run_hi);
+    cudaFree(s.quad_lo);
+    cudaFree(s.quad_hi);
     cudaFree(s.pos);
     cudaFree(s.leaf_off);
     // page arrays come from the stream-ordered pool (build.cu)
@@ -149,20 +175,8 @@ void free_shard(DevIndex& s) {
                     static_cast<void*>(s.group_lo), static_cast<void*>(s.group_hi)})
         if (p) cudaFreeAsync(p, s.stream);
     if (s.stream) cudaStreamSynchronize(s.stream);
-    for (int k = 0; k < DevIndex::kLanes; ++k) {
-        DevIndex::Lane& l = s.lanes[k];
-        cudaFree(l.work);
-        cudaFree(l.lut);
-        cudaFree(l.surv);
-        cudaFree(l.surv_lb);
-        cudaFree(l.gsurv);
-        cudaFree(l.cand_pos);
-        cudaFree(l.cand_lb);
-        cudaFree(l.cand_sq);
-        if (l.done) cudaEventDestroy(l.done);
-        if (k > 0 && l.stream) cudaStreamDestroy(l.stream);
-    }
-    if (s.graph) cudaGraphExecDestroy(s.graph);
+    free_slots(s.batch);
+    free_slots(s.big);
     cudaFree(s.results);
     cudaFree(s.queries);
     if (s.stream) cudaStreamDestroy(s.stream);
@@ -216,26 +230,22 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     s.thr = upload_thresholds(s.bits);
     if (const char* e = std::getenv("TSG_REFINE_SPLIT")) s.refine_split = static_cast<float>(std::atof(e));
     build_layout(s, &ms[0], &ms[1], &ms[2]);
-    // search workspace: query lanes (stream + private scratch each)
-    s.nlanes = 8;
-    if (const char* e = std::getenv("TSG_QUERY_LANES"))
-        s.nlanes = std::max(1, std::min(DevIndex::kLanes, std::atoi(e)));
-    s.cand_cap = N;
-    for (int k = 0; k < s.nlanes; ++k) {
-        DevIndex::Lane& l = s.lanes[k];
-        if (k == 0) l.stream = s.stream;
-        else TSG_CUDA(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
-        TSG_CUDA(cudaEventCreateWithFlags(&l.done, cudaEventDisableTiming));
-        TSG_CUDA(cudaMalloc(&l.work, sizeof(QueryWork)));
-        TSG_CUDA(cudaMalloc(&l.lut, static_cast<size_t>(s.w) * 256 * sizeof(float)));
-        TSG_CUDA(cudaMemset(l.work, 0, sizeof(QueryWork)));
-        TSG_CUDA(cudaMalloc(&l.surv, std::max<uint64_t>(s.P, 1) * sizeof(uint2)));
-        TSG_CUDA(cudaMalloc(&l.surv_lb, std::max<uint64_t>(s.P, 1) * sizeof(float)));
-        TSG_CUDA(cudaMalloc(&l.gsurv, std::max<uint64_t>(s.NG, 1) * sizeof(uint32_t)));
-        TSG_CUDA(cudaMalloc(&l.cand_pos, N * sizeof(uint32_t)));
-        TSG_CUDA(cudaMalloc(&l.cand_lb, N * sizeof(float)));
-        TSG_CUDA(cudaMalloc(&l.cand_sq, N * sizeof(double)));
-    }
+    // Search workspace: batch_max query slots (TSG_BATCH, default 128). Each
+    // slot holds up to `cap` candidate records: as many as the shard has
+    // entries when memory allows, else a share of ~45% of the free memory
+    // (>= 2^20 and >= the seed range); a query that outgrows its slot is
+    // rerun alone in a full-size slot.
+    if (const char* e = std::getenv("TSG_BATCH")) s.batch_max = static_cast<uint32_t>(std::max(1, std::atoi(e)));
+    size_t free_b = 0, total_b = 0;
+    TSG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t per_slot_fixed = sizeof(QueryWork) + static_cast<uint64_t>(s.w) * 1024 +
+                                    std::max<uint64_t>(s.NG, 1) * 4 + std::max<uint64_t>(s.P, 1) * 12;
+    const uint64_t budget = static_cast<uint64_t>(0.45 * static_cast<double>(free_b));
+    const uint64_t fixed = per_slot_fixed * s.batch_max;
+    const uint64_t cand_budget = budget > fixed ? budget - fixed : 0;
+    const uint64_t min_cap = std::min<uint64_t>(N, std::max<uint64_t>(1u << 20, 2 * s.leaf_cap));
+    const uint64_t cap = std::min<uint64_t>(N, std::max<uint64_t>(min_cap, cand_budget / (16ull * s.batch_max)));
+    alloc_slots(s, s.batch, s.batch_max, cap);
 }
 
 void ensure_results(DevIndex& s, uint32_t nq) {
@@ -252,6 +262,27 @@ void ensure_queries(DevIndex& s, uint32_t nq) {
     s.queries = nullptr;
     TSG_CUDA(cudaMalloc(&s.queries, static_cast<size_t>(nq) * s.n * sizeof(float)));
     s.queries_cap = nq;
+}
+
+// All nq device queries of one shard: batches of batch_max through the batch
+// slots, then any query that outgrew its slot again, alone, in the full-size
+// slot (allocated on first use). Results land in host_out.
+void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out) {
+    ensure_results(s, nq);
+    for (uint32_t off = 0; off < nq; off += s.batch_max) {
+        const uint32_t b = std::min(s.batch_max, nq - off);
+        search_batch(s, s.batch, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off);
+    }
+    TSG_CUDA(cudaMemcpyAsync(host_out, s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
+    TSG_CUDA(cudaStreamSynchronize(s.stream));
+    for (uint32_t q = 0; q < nq; ++q) {
+        if (!(host_out[q].flags & kResultOverflow)) continue;
+        if (!s.big.n) alloc_slots(s, s.big, 1, s.N);
+        search_batch(s, s.big, dq + static_cast<uint64_t>(q) * s.n, 1, approximate, s.results + q);
+        TSG_CUDA(cudaMemcpyAsync(host_out + q, s.results + q, sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
+        TSG_CUDA(cudaStreamSynchronize(s.stream));
+        if (host_out[q].flags & kResultOverflow) throw std::logic_error("search: a full-size slot overflowed");
+    }
 }
 
 void to_result(const DevResult& d, tsg_result& r) {
@@ -295,7 +326,6 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
     auto work = [&](size_t k) {
         DevIndex& s = ix->shards[k];
         DeviceGuard g(s.device);
-        ensure_results(s, nq);
         const float* dq = queries;
         if (host) {
             ensure_queries(s, nq);
@@ -303,14 +333,7 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
                                      cudaMemcpyHostToDevice, s.stream));
             dq = s.queries;
         }
-        static const bool trace_enqueue = std::getenv("TSG_TRACE_ENQUEUE") != nullptr;
-        const auto t0 = std::chrono::steady_clock::now();
-        search_batch(s, dq, nq, approximate);
-        if (trace_enqueue)
-            std::fprintf(stderr, "[tsg search] %u queries enqueued in %.3f ms\n", nq,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-        TSG_CUDA(cudaMemcpyAsync(per[k].data(), s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
-        TSG_CUDA(cudaStreamSynchronize(s.stream));
+        search_all(s, dq, nq, approximate, per[k].data());
     };
     if (ix->shards.size() == 1) {
         work(0);

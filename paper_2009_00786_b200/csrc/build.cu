@@ -51,13 +51,14 @@ __global__ void k_iota(uint32_t* v, uint64_t n) {
     GRID_STRIDE(i, n) v[i] = static_cast<uint32_t>(i);
 }
 
-// words[i] = words_orig[pos[i]] (16- or 32-byte rows), and the run boxes:
-// bytewise min / max over each aligned kRun-entry run of the sorted words
-// (half-warp shuffles; a warp's 32 consecutive entries are two runs).
+// words[i] = words_orig[pos[i]] (16- or 32-byte rows), and the two lowest
+// box levels: bytewise min / max over each aligned kQuad-entry quad and
+// kRun-entry run of the sorted words (one shuffle tree: offsets 1, 2 give
+// the quads, 4, 8 continue to the runs; a warp's 32 entries are two runs).
 __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* __restrict__ pos,
                                uint8_t* __restrict__ dst, uint8_t* __restrict__ run_lo, uint8_t* __restrict__ run_hi,
-                               uint64_t n, int ws) {
-    static_assert(kRun == 16, "run boxes are half-warp reductions");
+                               uint8_t* __restrict__ quad_lo, uint8_t* __restrict__ quad_hi, uint64_t n, int ws) {
+    static_assert(kRun == 16 && kQuad == 4, "quad / run boxes are 4- / 16-lane reductions");
     const int lane = threadIdx.x & 31;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t w0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); w0 < n; w0 += stride) {
@@ -72,7 +73,7 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
             }
             uint4 mn = in ? x : make_uint4(~0u, ~0u, ~0u, ~0u), mx = x;
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
+            for (int o = 1; o < 16; o <<= 1) {
                 mn.x = __vminu4(mn.x, __shfl_xor_sync(0xFFFFFFFFu, mn.x, o));
                 mn.y = __vminu4(mn.y, __shfl_xor_sync(0xFFFFFFFFu, mn.y, o));
                 mn.z = __vminu4(mn.z, __shfl_xor_sync(0xFFFFFFFFu, mn.z, o));
@@ -81,6 +82,11 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
                 mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xFFFFFFFFu, mx.y, o));
                 mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xFFFFFFFFu, mx.z, o));
                 mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xFFFFFFFFu, mx.w, o));
+                if (o == 2 && (lane & 3) == 0 && in) {
+                    const uint64_t q = i / kQuad;
+                    *reinterpret_cast<uint4*>(quad_lo + q * ws + 16 * h) = mn;
+                    *reinterpret_cast<uint4*>(quad_hi + q * ws + 16 * h) = mx;
+                }
             }
             if ((lane & 15) == 0 && in) {
                 const uint64_t r = i / kRun;
@@ -264,6 +270,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     ix.R = (N + kRun - 1) / kRun;
     TSG_CUDA(cudaMalloc(&ix.run_lo, ix.R * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.run_hi, ix.R * ix.ws));
+    ix.Q = (N + kQuad - 1) / kQuad;
+    TSG_CUDA(cudaMalloc(&ix.quad_lo, ix.Q * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.quad_hi, ix.Q * ix.ws));
     // pos_in / bstart are reused for the L+1 page counts / bases (L <= N).
     DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in((N + 1) * 4), flags(N), bstart((N + 1) * 4),
         nsel(8),
@@ -309,7 +318,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
     TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
                                              pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
     k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, ix.run_lo,
-                                                          ix.run_hi, N, ix.ws);
+                                                          ix.run_hi, ix.quad_lo, ix.quad_hi, N, ix.ws);
     TSG_LAUNCHED();
     TSG_CUDA(cudaEventRecord(ev[2], st));
 

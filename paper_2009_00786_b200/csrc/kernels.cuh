@@ -40,36 +40,30 @@ struct DevIndex {
     uint8_t* run_lo = nullptr;      // [R][ws] per-segment min symbol of entries [kRun r, kRun r + kRun)
     uint8_t* run_hi = nullptr;      // [R][ws] per-segment max symbol
     uint64_t R = 0;                 // ceil(N / kRun)
+    uint8_t* quad_lo = nullptr;     // [Q][ws] per-segment min symbol of entries [kQuad q, kQuad q + kQuad)
+    uint8_t* quad_hi = nullptr;     // [Q][ws] per-segment max symbol
+    uint64_t Q = 0;                 // ceil(N / kQuad)
     uint64_t P = 0;
     uint64_t root_children = 0;
     uint64_t inner = 0, max_depth = 0, overflow = 0;
     uint64_t* page_dir = nullptr;   // [(P + 255) / 256] page_key of every 256th page
-    // search workspace: kLanes query lanes, each a stream with private
-    // scratch, so consecutive queries of a batch run concurrently.
-    struct Lane {
-        cudaStream_t stream = nullptr;  // lane 0 uses the index stream
-        cudaEvent_t done = nullptr;
-        struct QueryWork* work = nullptr;
-        float* lut = nullptr;          // [w][256] squared-gap table of the lane's query
-        uint32_t* gsurv = nullptr;     // [NG] surviving page groups
-        uint2* surv = nullptr;         // [P] surviving pages' entry ranges: wave 0 from the front, wave 1 from the back
-        float* surv_lb = nullptr;      // [P] their box bounds
-        uint32_t* cand_pos = nullptr;  // [cap]
-        float* cand_lb = nullptr;      // [cap]
-        double* cand_sq = nullptr;     // [cap]
+    // Search workspace: per-query slots of one batch (every kernel of the
+    // pipeline runs once per batch over all its queries), and a single slot
+    // with room for every entry, for queries that outgrow a batch slot.
+    struct Slots {
+        uint32_t n = 0;                 // slots allocated
+        uint64_t cap = 0;               // candidate records per slot
+        struct QueryWork* work = nullptr;  // [n]
+        float* lut = nullptr;           // [n][w][256] squared-gap tables
+        uint32_t* gsurv = nullptr;      // [n][NG] surviving page groups
+        uint2* surv = nullptr;          // [n][P] surviving pages' entry ranges: wave 0 front, wave 1 back
+        float* surv_lb = nullptr;       // [n][P] their box bounds
+        uint32_t* cand_pos = nullptr;   // [n][cap] candidate entries: refinement wave A front, B back
+        float* cand_lb = nullptr;       // [n][cap]
+        double* cand_sq = nullptr;      // [n][cap]
     };
-    static constexpr int kLanes = 16;
-    Lane lanes[kLanes];
-    int nlanes = 1;                // lanes in use (TSG_QUERY_LANES, default 8)
-    cudaGraphExec_t graph = nullptr;  // the last query batch, captured (updated in place when the shape repeats)
-    struct GraphKey {
-        const float* queries = nullptr;
-        uint32_t nq = 0;
-        bool approximate = false;
-        int nlanes = 0;
-        int kernels = 0;  // launches the graph holds
-    } graph_key;
-    uint64_t cand_cap = 0;
+    Slots batch, big;
+    uint32_t batch_max = 128;       // queries per batch (TSG_BATCH)
     struct DevResult* results = nullptr;  // [results_cap]
     uint32_t results_cap = 0;
     float* queries = nullptr;      // staging for host queries
@@ -85,31 +79,35 @@ struct DevIndex {
 constexpr int kProfSlots = 8;
 constexpr int kGroup = 8;  // pages per group box (the level above pages)
 constexpr int kRun = 16;  // entries per run box (the sub-page filter level)
+constexpr int kQuad = 4;  // entries per quad box (the level below runs)
 
-// Per-query device scratch (reset by the prep kernel).
+// Per-query device scratch (reset by the prepare kernel).
+enum WorkCounter { kNextBound = 0, kNextScan0, kNextRefine0, kNextScan1, kNextRefine1, kNextCount };
 struct QueryWork {
     unsigned long long bsf_bits;  // best squared distance so far (double bits)
-    unsigned long long seed_key;  // (page LB float bits << 32) | page
-    unsigned int ncand;
+    // candidate records: wave A (low 32 bits, from the front, after the seed
+    // range) and wave B (high 32 bits, from the back), reserved together
+    unsigned long long cand;
     unsigned int nseed;
-    unsigned int work_next;
-    unsigned int best_pos;
     unsigned int seed_begin, seed_end;  // index range refined as the seed
+    unsigned int ngroups;               // surviving page groups
     unsigned int nsurv;                 // surviving pages, wave 0 (bound <= split x seed bound)
     unsigned int nsurv_hi;              // surviving pages, wave 1 (stored from the back of surv)
-    unsigned int nhigh;                 // wave-1 candidates, stored at the top of the candidate arrays
-    unsigned int ngroups;               // surviving page groups
+    unsigned int next[kNextCount];      // work-chunk counters of the persistent kernels
     unsigned int done_blocks;           // finalize's last-block counter
+    unsigned int best_pos;
+    unsigned int overflow;              // candidates outgrew the slot: rerun in the big slot
     float scan_bound;                   // BSF bound the page/word filters used
     unsigned long long stats[6];  // SearchStats order
-    double qpaa[32];
     unsigned char qsym[32];
 };
+
+constexpr uint32_t kResultOverflow = 1u;  // DevResult.flags: answer invalid, rerun with a full-size slot
 
 struct DevResult {
     double distance;
     uint32_t position;
-    uint32_t reserved;
+    uint32_t flags;
     unsigned long long stats[6];
 };
 
@@ -121,8 +119,11 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
 // `ix` (rows/thr/N/n/w/bits/leaf_cap must be set). Device ms per phase.
 void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, double* ms_leaves);
 
-// Query pipeline for nq device queries; writes ix.results[0..nq).
-void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approximate);
+// Query pipeline for nq device queries in slots [0, nq) of `slots`; writes
+// results[0..nq). Queries flagged kResultOverflow must be rerun with a slot
+// of capacity N (api.cu's search_all does that).
+void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
+                  struct DevResult* results);
 
 // Input generators (not on the timed path), see generate.cu.
 enum GenKind {

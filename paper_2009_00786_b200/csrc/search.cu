@@ -1,40 +1,43 @@
-// Exact Euclidean 1-NN over the flat SoA index (one device shard).
+// Exact Euclidean 1-NN over the flat SoA index (one device shard), a batch
+// of queries at a time.
 //
-// Replaces exact_search (src/query.cpp:258-298) and its pieces. Per query,
-// six kernels on the index's stream:
-//   seed      approximate_search_state (src/query.cpp:226-238): the leaf the
-//             query's own iSAX word descends to (binary search of its
-//             plane-major key over the page keys) is refined exhaustively
-//             and seeds the best-so-far (BSF).
-//   bound     node_lower_bound over every page box (src/query.cpp:102-107)
-//             + the pruning test (src/query.cpp:159): pages whose bound is
-//             within the BSF survive (block-aggregated compaction).
-//   lbscan    the entry-level filter of calculate_real_distance_leaf
-//             (src/query.cpp:129-134): words of surviving pages are bounded
-//             with one table lookup per segment and compacted with warp
-//             ballot + prefix popcount into two LB-ordered candidate waves.
-//   refine x2 euclidean (src/metrics.cpp:17-40, 95-104), wave 0 (bounds up
-//             to `split` x the scan bound) then wave 1, the GPU analog of
-//             MESSI's LB-ordered priority queues (src/query.cpp:173-184): an
-//             8-lane group per candidate row, 256-bit loads of 8-float
-//             blocks, FP64 block sums without FMA, added left to right
-//             exactly like squared_l2; the BSF is an atomicMin on the double
-//             bit pattern (non-negative doubles order as unsigned integers),
-//             the SharedBsf analog (src/query.cpp:35-42); a candidate whose
-//             bound exceeds the live BSF is skipped (`LB >= cutoff -> skip`).
-//   finalize  result = min over refined candidates of (sqrt(sum), position):
-//             ties resolve to the lowest position exactly as scan_nn does
-//             (src/scan.cpp:54-59); the last block writes the result and
-//             resets the scratch for the next query.
-// Every kernel computes the query PAA in FP64 reference order, the query
-// symbols and, where needed, a [w][256] table of per-segment squared region
-// gaps (mindist_bands, src/metrics.cpp:47-70) scaled by n/w and rounded DOWN
-// to float, so every float bound here is <= the exact FP64 bound. Pruning
-// keeps ties: an entry is dropped only when its bound is strictly above the
-// BSF widened by 1e-9 relative (covering FP64 rounding of the sums).
+// Replaces exact_search (src/query.cpp:258-298) and its pieces. A batch of up
+// to batch_max queries runs through nine kernels, each launched ONCE for the
+// whole batch; every query owns a slot of scratch (QueryWork, table, page
+// lists, candidate records):
+//   prepare   per query: PAA (FP64, reference order), symbols, the [w][256]
+//             table of squared region gaps, and the leaf its own iSAX word
+//             descends to (approximate_search_state, src/query.cpp:226-238).
+//   seed      that leaf's rows refined exhaustively: the first best-so-far.
+//   groups    node_lower_bound (src/query.cpp:102-107) over the page-group
+//             boxes + the pruning test (src/query.cpp:159).
+//   bound     the same over the pages of surviving groups; surviving pages
+//             split into page wave 0 (bound <= split x BSF) and wave 1.
+//   lbscan x2 the entry filter of calculate_real_distance_leaf
+//             (src/query.cpp:129-134) over run boxes, quad boxes and words of
+//             the surviving pages, compacted with warp ballot + prefix
+//             popcount into candidate waves A (front) and B (back).
+//   refine x2 euclidean (src/metrics.cpp:17-40, 95-104): an 8-lane group per
+//             candidate row, 256-bit loads, FP64 block sums without FMA added
+//             left to right like squared_l2; the BSF is an atomicMin on the
+//             double bit pattern (the SharedBsf analog, src/query.cpp:35-42).
+//   finalize  (sqrt(min sum), lowest position among equal distances), the
+//             tie rule of scan_nn (src/scan.cpp:54-59).
+// page wave 1 runs after refinement wave A tightened the BSF: MESSI's
+// LB-ordered priority-queue processing (src/query.cpp:173-184) in two steps.
+// bound / lbscan / refine are persistent grids fed from per-query chunk
+// counters with block-to-query affinity: a block drains the chunks of one
+// query (whose table or row stays in shared memory), then moves on to the next
+// query with work left, so easy and hard queries of a batch share the GPU
+// without per-query launches or tails.
+// Soundness: the table is rounded DOWN to float and bounds are summed with
+// __fadd_rd, so every float bound is <= the exact FP64 bound; the BSF bound
+// is rounded up and widened by 1e-9 relative; pruning is strict, so ties
+// reach the exact FP64 comparison.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <stdexcept>
 #include <utility>
 #include <vector>
 
@@ -48,9 +51,57 @@ namespace {
 constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
 constexpr double kSlack = 1.0 + 1e-9;
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kRowLanes = 8;  // lanes per candidate row in the refine kernels
 
 enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
+
+// Resident blocks per SM the persistent kernels are compiled for (register
+// caps; -D overrides for tuning runs).
+#ifndef TSG_MINB_LBSCAN
+#define TSG_MINB_LBSCAN 4
+#endif
+#ifndef TSG_MINB_REFINE
+#define TSG_MINB_REFINE 4
+#endif
+#ifndef TSG_MINB_BOUND
+#define TSG_MINB_BOUND 4
+#endif
+
+// ---------------------------------------------------------------- views
+// Kernel-side views of the index and of a slot set (passed by value).
+struct IndexView {
+    const float* rows;
+    int n, w, bits;
+    const double* thr;
+    const uint8_t* words;
+    const uint32_t* pos;
+    const uint32_t* leaf_off;
+    const uint32_t* page_off;
+    const uint32_t* page_leaf;
+    const uint64_t* page_key;
+    const uint64_t* page_dir;
+    uint64_t P;
+    const uint8_t *page_lo, *page_hi, *group_lo, *group_hi;
+    uint64_t NG;
+    const uint8_t *run_lo, *run_hi, *quad_lo, *quad_hi;
+    uint32_t seed_cap;
+    float split;
+    uint64_t pos_offset;
+};
+
+struct SlotView {
+    QueryWork* work;
+    float* lut;
+    uint32_t* gsurv;
+    uint2* surv;
+    float* surv_lb;
+    uint32_t* cand_pos;
+    float* cand_lb;
+    double* cand_sq;
+    uint64_t cap, P, NG;
+    int lut_len;
+};
 
 __device__ __forceinline__ double bsf_of(unsigned long long bits) {
     return __longlong_as_double(static_cast<long long>(bits));
@@ -60,12 +111,17 @@ __device__ __forceinline__ float bound_from_bits(unsigned long long bits) {
     return __double2float_ru(bsf_of(bits) * kSlack);
 }
 
+__device__ __forceinline__ uint64_t u64min(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) { return *reinterpret_cast<const volatile unsigned*>(p); }
+
 __device__ __forceinline__ uint32_t word32(const uint4& v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
 __device__ __forceinline__ uint32_t byte_of(const uint4& v, int s) { return (word32(v, s >> 2) >> (8 * (s & 3))) & 255u; }
 
+// ------------------------------------------------------ query prepare
 struct QueryShared {
     double thr[kThrPad];
     double qpaa[kMaxW];
@@ -90,10 +146,9 @@ __device__ __forceinline__ void fill_lut(const QueryShared& qs, int n, int w, in
     }
 }
 
-// Block-local query preparation: PAA (FP64, reference order) and symbols;
-// with lut != nullptr also the [w][256] squared-gap table.
+// Block-local query preparation: PAA (FP64, reference order) and symbols.
 __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bits, const double* __restrict__ thr_g,
-                              QueryShared& qs, float* s_lut) {
+                              QueryShared& qs) {
     for (int i = threadIdx.x; i < kThrPad; i += blockDim.x) qs.thr[i] = thr_g[i];
     __syncthreads();
     const int seg = n / w;
@@ -106,19 +161,27 @@ __device__ void prepare_query(const float* __restrict__ q, int n, int w, int bit
         qs.qsym[g] = static_cast<unsigned char>(symbol_of(qs.thr, bits, mean) << (8 - bits));
     }
     __syncthreads();
-    if (!s_lut) return;
-    fill_lut(qs, n, w, bits, s_lut);
-    __syncthreads();
 }
 
-// Loads the table and the query symbols the seed kernel prepared for this
-// query (one 16 KB L2 read per block instead of recomputing 4K FP64 gaps).
+// Loads a query's table and symbols (prepared once per query by k_prepare)
+// into shared memory. Callers synchronise before overwriting a previous one.
 __device__ __forceinline__ void load_prepared(const float* __restrict__ lut_g, const QueryWork* wk, int w,
                                               float* s_lut, unsigned char* qsym) {
     const float4* src = reinterpret_cast<const float4*>(lut_g);
     float4* dst = reinterpret_cast<float4*>(s_lut);
     for (int i = threadIdx.x; i < w * 64; i += blockDim.x) dst[i] = src[i];
     for (int i = threadIdx.x; i < kMaxW; i += blockDim.x) qsym[i] = i < w ? wk->qsym[i] : 0;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void load_query(float* s_q, const float* q, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_q[i] = q[i];
+    __syncthreads();
+}
+
+// The query widened to double once per block (the refinement subtracts in FP64).
+__device__ __forceinline__ void load_query_f64(double* s_q, const float* q, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_q[i] = static_cast<double>(q[i]);
     __syncthreads();
 }
 
@@ -136,23 +199,17 @@ __device__ __forceinline__ float word_bound(const float* s_lut, const uint4* v, 
     return lb;
 }
 
-__device__ __forceinline__ void reset_work(QueryWork* wk) {
-    wk->bsf_bits = kInfBits;
-    wk->seed_key = ~0ull;
-    wk->ncand = 0;
-    wk->nseed = 0;
-    wk->nhigh = 0;
-    wk->work_next = 0;
-    wk->best_pos = 0xFFFFFFFFu;
-    wk->nsurv = 0;
-    wk->nsurv_hi = 0;
-    wk->ngroups = 0;
-    for (int i = 0; i < 6; ++i) wk->stats[i] = 0;
-}
-
-__global__ void k_reset(QueryWork* wk) {
-    reset_work(wk);
-    wk->done_blocks = 0;
+// Box bound: per segment the table entry of the query symbol clamped into the
+// box [lo, hi] (0 when the query symbol is inside) — node_lower_bound's region
+// gap (src/query.cpp:102-107) over a box of iSAX words.
+template <int H, bool W16>
+__device__ __forceinline__ float box_bound(const float* s_lut, const uint4* q4, const uint4* lo, const uint4* hi, int w) {
+    uint4 c[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+        c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, lo[h].x), hi[h].x), __vminu4(__vmaxu4(q4[h].y, lo[h].y), hi[h].y),
+                          __vminu4(__vmaxu4(q4[h].z, lo[h].z), hi[h].z), __vminu4(__vmaxu4(q4[h].w, lo[h].w), hi[h].w));
+    return word_bound<W16>(s_lut, c, w);
 }
 
 // ---------------------------------------------------- row refinement
@@ -169,12 +226,12 @@ __device__ __forceinline__ F8 ld256(const float* p) {
     return r;
 }
 
-__device__ __forceinline__ double block_sq(const float* x, const float* q, int cnt) {
+__device__ __forceinline__ double block_sq(const float* x, const double* q, int cnt) {
     double blk = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
         if (k < cnt) {
-            const double d = __dsub_rn(static_cast<double>(x[k]), static_cast<double>(q[k]));
+            const double d = __dsub_rn(static_cast<double>(x[k]), q[k]);
             blk = __dadd_rn(blk, __dmul_rn(d, d));
         }
     return blk;
@@ -182,7 +239,7 @@ __device__ __forceinline__ double block_sq(const float* x, const float* q, int c
 
 // Squared distance of a row computed by an 8-lane group: lane j owns blocks
 // j, j+8, j+16, j+24 of each 32-block round (the 8 lanes read 256 contiguous
-// bytes per load); the group leader then adds the block sums left to right,
+// bytes per load); the group then adds the block sums left to right,
 // squared_l2's order. Rows longer than 256 take several rounds; after each
 // round the running sum is checked against the live BSF (strict), the
 // reference's abandonment (metrics.cpp:28). Group-local: only the group's 8
@@ -190,7 +247,7 @@ __device__ __forceinline__ double block_sq(const float* x, const float* q, int c
 // different candidates independently. Every lane of the group returns the
 // sum, +inf if abandoned.
 template <bool VEC>
-__device__ __forceinline__ double group_row_sq(const float* __restrict__ row, const float* __restrict__ s_q, int n,
+__device__ __forceinline__ double group_row_sq(const float* __restrict__ row, const double* __restrict__ s_q, int n,
                                                const unsigned long long* bsf) {
     const int lane = threadIdx.x & 31, j = lane & (kRowLanes - 1), base = lane & ~(kRowLanes - 1);
     const unsigned gmask = 0xFFu << base;
@@ -238,25 +295,110 @@ __device__ __forceinline__ double group_row_sq(const float* __restrict__ row, co
 }
 
 // Publishes a finished sum: candidate record, BSF atomicMin only when it can
-// improve, strict-improvement count. *seen receives the BSF observed (an
-// upper bound of the current BSF, for the caller's cached pruning bound).
-__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq,
-                                                      unsigned long long* seen = nullptr) {
+// improve, strict-improvement count.
+__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq) {
     cand_sq[c] = s;
     const unsigned long long cur = ld_volatile_u64(&wk->bsf_bits);
-    if (seen) *seen = cur;
     if (!(s < INFINITY)) return 0;
     const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(s));
     if (sb >= cur) return 0;
-    if (seen) *seen = sb;
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
 }
 
-__device__ __forceinline__ void load_query(float* s_q, const float* q, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s_q[i] = q[i];
-    __syncthreads();
+// -------------------------------------------------------- scheduling
+// Block-level work distribution with query affinity. Each query has a chunk
+// counter per kernel (`k`); a block drains chunks of its current query and,
+// when that query has none left, moves on to the next query with work. The
+// claim of a block's next chunk is issued (by thread 0) when the current
+// chunk starts and read when it ends, so the atomic's latency hides behind
+// the chunk's work. A claim returns the query (-1 when every query is
+// exhausted) and the chunk; it begins with a barrier, so the previous
+// chunk's shared state is free to reuse.
+template <typename NChunks>
+__device__ __forceinline__ int claim_search(QueryWork* work, int nq, int k, int q, uint32_t& c, NChunks nchunks) {
+    for (int tries = 0; tries < nq; ++tries) {
+        QueryWork* wk = work + q;
+        const uint32_t n = nchunks(wk);
+        if (ld_volatile_u32(&wk->next[k]) < n) {
+            c = atomicAdd(&wk->next[k], 1u);
+            if (c < n) return q;
+        }
+        q = q + 1 == nq ? 0 : q + 1;
+    }
+    return -1;
 }
 
+// `pre`: thread 0's claim issued at the start of the current chunk of query
+// `q` (or ~0u for none, e.g. before the first chunk).
+template <typename NChunks>
+__device__ __forceinline__ int claim(QueryWork* work, int nq, int k, int& cur, uint32_t& chunk, uint32_t pre, int q,
+                                     NChunks nchunks) {
+    __shared__ int s_q;
+    __shared__ uint32_t s_c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        int res;
+        if (q >= 0 && pre < nchunks(work + q)) {
+            res = q;
+            c = pre;
+        } else {
+            res = claim_search(work, nq, k, q >= 0 ? q : cur, c, nchunks);
+        }
+        s_q = res;
+        s_c = c;
+    }
+    __syncthreads();
+    const int r = s_q;
+    if (r >= 0) cur = r;
+    chunk = s_c;
+    return r;
+}
+
+// Thread 0 reserves the block's next chunk of query q (read by the next claim).
+__device__ __forceinline__ uint32_t claim_ahead(QueryWork* work, int q, int k) {
+    return threadIdx.x == 0 ? atomicAdd(&work[q].next[k], 1u) : ~0u;
+}
+
+// Block-wide slot reservation: each thread brings two counts (< 2^16 per
+// block); returns its first slot in each of two global lists, with one
+// atomicAdd per list per block. All threads of the block must call it.
+__device__ __forceinline__ uint2 block_reserve(unsigned c0, unsigned c1, unsigned* ctr0, unsigned* ctr1) {
+    __shared__ uint32_t s_cnt[kWarps];
+    __shared__ uint32_t s_base[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t mine = c0 | (c1 << 16);
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_cnt[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int i = 0; i < kWarps; ++i) {
+            const uint32_t c = s_cnt[i];
+            s_cnt[i] = tot;
+            tot += c;
+        }
+        s_base[0] = (tot & 0xFFFFu) ? atomicAdd(ctr0, tot & 0xFFFFu) : 0u;
+        s_base[1] = (tot >> 16) && ctr1 ? atomicAdd(ctr1, tot >> 16) : 0u;
+    }
+    __syncthreads();
+    const uint32_t before = s_cnt[warp] + (incl - mine);
+    const uint2 r = make_uint2(s_base[0] + (before & 0xFFFFu), s_base[1] + (before >> 16));
+    __syncthreads();  // s_cnt / s_base are reused by the next call
+    return r;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// ----------------------------------------------------------- prepare
 // The page the query's own key falls into: the largest p with
 // page_key[p] <= key (0 if none), i.e. where the query's iSAX word would be
 // stored. Two parallel rounds instead of a serial binary search: the block
@@ -264,7 +406,7 @@ __device__ __forceinline__ void load_query(float* s_q, const float* q, int n) {
 // the keys <= key inside that 256-page window. blockDim.x must be 256.
 __device__ __forceinline__ uint32_t locate_page(const uint64_t* __restrict__ page_key,
                                                 const uint64_t* __restrict__ page_dir, uint64_t P, uint64_t key) {
-    __shared__ unsigned s_part[kThreads / 32];
+    __shared__ unsigned s_part[kWarps];
     const uint64_t nd = (P + 255) / 256;
     unsigned c = 0;
     for (uint64_t i = threadIdx.x; i < nd; i += blockDim.x) c += page_dir[i] <= key ? 1u : 0u;
@@ -272,7 +414,7 @@ __device__ __forceinline__ uint32_t locate_page(const uint64_t* __restrict__ pag
     if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = c;
     __syncthreads();
     unsigned dirs = 0;
-    for (int i = 0; i < kThreads / 32; ++i) dirs += s_part[i];
+    for (int i = 0; i < kWarps; ++i) dirs += s_part[i];
     const uint64_t w0 = dirs == 0 ? 0 : static_cast<uint64_t>(dirs - 1) * 256;
     const uint64_t p = w0 + threadIdx.x;
     const int cnt = __syncthreads_count(p < P && page_key[p] <= key);
@@ -288,54 +430,68 @@ __device__ __forceinline__ uint64_t query_key(const unsigned char* qsym, int w) 
     return left >= 64 ? 0 : k << left;
 }
 
-// -------------------------------------------------------------- seed
-// The leaf the query's own iSAX word descends to; an overflow leaf larger
-// than seed_cap is replaced by that page alone. Every entry is refined.
-template <bool VEC>
+// One block per query: resets the slot, prepares the query (PAA, symbols,
+// table) and picks the seed range: the leaf the query's own iSAX word
+// descends to, replaced by that page alone when the leaf is an overflow leaf
+// larger than seed_cap.
 __global__ void __launch_bounds__(kThreads)
-    k_seed(const float* __restrict__ rows, int n, int w, int bits, const double* __restrict__ thr_g,
-           const float* __restrict__ query, const uint32_t* __restrict__ leaf_off,
-           const uint32_t* __restrict__ page_off, const uint32_t* __restrict__ page_leaf,
-           const uint64_t* __restrict__ page_key, const uint64_t* __restrict__ page_dir, uint64_t P,
-           const uint32_t* __restrict__ pos, uint32_t seed_cap, QueryWork* wk, uint32_t* __restrict__ cand_pos,
-           double* __restrict__ cand_sq, float* __restrict__ lut_out) {
+    k_prepare(IndexView ix, SlotView S, const float* __restrict__ queries) {
     extern __shared__ float s_q[];
     __shared__ QueryShared qs;
-    __shared__ uint32_t s_range[2];
-    load_query(s_q, query, n);
-    prepare_query(s_q, n, w, bits, thr_g, qs, nullptr);
-    if (blockIdx.x == gridDim.x - 1) {  // one block publishes the query's table and symbols
-        fill_lut(qs, n, w, bits, lut_out);
-        if (threadIdx.x < w) wk->qsym[threadIdx.x] = qs.qsym[threadIdx.x];
-    }
-    const uint32_t page = locate_page(page_key, page_dir, P, query_key(qs.qsym, w));
+    const int q = blockIdx.x;
+    QueryWork* wk = S.work + q;
+    load_query(s_q, queries + static_cast<uint64_t>(q) * ix.n, ix.n);
+    prepare_query(s_q, ix.n, ix.w, ix.bits, ix.thr, qs);
+    fill_lut(qs, ix.n, ix.w, ix.bits, S.lut + static_cast<uint64_t>(q) * S.lut_len);
+    if (threadIdx.x < kMaxW) wk->qsym[threadIdx.x] = threadIdx.x < ix.w ? qs.qsym[threadIdx.x] : 0;
+    const uint32_t page = locate_page(ix.page_key, ix.page_dir, ix.P, query_key(qs.qsym, ix.w));
     if (threadIdx.x == 0) {
-        const uint32_t leaf = page_leaf[page];
-        uint32_t a = leaf_off[leaf], b = leaf_off[leaf + 1];
-        if (b - a > seed_cap) {
-            a = page_off[page];
-            b = page_off[page + 1];
+        const uint32_t leaf = ix.page_leaf[page];
+        uint32_t a = ix.leaf_off[leaf], b = ix.leaf_off[leaf + 1];
+        if (b - a > ix.seed_cap) {
+            a = ix.page_off[page];
+            b = ix.page_off[page + 1];
         }
-        s_range[0] = a;
-        s_range[1] = b;
-        if (blockIdx.x == 0) {
-            wk->seed_key = page;
-            wk->nseed = b - a;
-            wk->ncand = b - a;
-            wk->seed_begin = a;
-            wk->seed_end = b;
-            wk->stats[kRealDist] += b - a;
-        }
+        wk->bsf_bits = kInfBits;
+        wk->cand = b - a;
+        wk->nseed = b - a;
+        wk->seed_begin = a;
+        wk->seed_end = b;
+        wk->ngroups = 0;
+        wk->nsurv = 0;
+        wk->nsurv_hi = 0;
+        for (int k = 0; k < kNextCount; ++k) wk->next[k] = 0;
+        wk->done_blocks = 0;
+        wk->best_pos = 0xFFFFFFFFu;
+        wk->overflow = (b - a) > S.cap ? 1u : 0u;
+        wk->scan_bound = 0.f;
+        for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
+        wk->stats[kRealDist] = b - a;
     }
-    __syncthreads();
-    const uint32_t a = s_range[0], b = s_range[1];
+}
+
+// -------------------------------------------------------------- seed
+// Grid (x, query): every entry of the seed range is refined; 32 row groups
+// per block.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    k_seed(IndexView ix, SlotView S, const float* __restrict__ queries) {
+    extern __shared__ double s_qd[];
+    const int q = blockIdx.y;
+    QueryWork* wk = S.work + q;
+    const uint32_t a = wk->seed_begin, b = wk->seed_end;
+    constexpr int kGroups = kThreads / kRowLanes;
+    if (wk->overflow || a + static_cast<uint64_t>(blockIdx.x) * kGroups >= b) return;
+    load_query_f64(s_qd, queries + static_cast<uint64_t>(q) * ix.n, ix.n);
+    uint32_t* cand_pos = S.cand_pos + q * S.cap;
+    double* cand_sq = S.cand_sq + q * S.cap;
     const int lane = threadIdx.x & 31;
-    const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
-    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
+    const uint64_t group = static_cast<uint64_t>(blockIdx.x) * kGroups + threadIdx.x / kRowLanes;
+    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * kGroups;
     unsigned long long updates = 0;
     for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
-        const uint32_t p = pos[e];
-        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
+        const uint32_t p = ix.pos[e];
+        const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if ((lane & (kRowLanes - 1)) == 0) {
             cand_pos[e - a] = static_cast<uint32_t>(e);  // index-order entry (finalize maps via pos[])
             updates += publish(wk, s, e - a, cand_sq);
@@ -344,74 +500,35 @@ __global__ void __launch_bounds__(kThreads)
     if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
 }
 
-// ------------------------------------------------------- bound + filter
-// Box bound: per segment the table entry of the query symbol clamped into the
-// box [lo, hi] (0 when the query symbol is inside) — node_lower_bound's
-// region gap (src/query.cpp:102-107) over a box of iSAX words.
-template <int H, bool W16>
-__device__ __forceinline__ float box_bound(const float* s_lut, const uint4* q4, const uint4* lo, const uint4* hi, int w) {
-    uint4 c[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h)
-        c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, lo[h].x), hi[h].x), __vminu4(__vmaxu4(q4[h].y, lo[h].y), hi[h].y),
-                          __vminu4(__vmaxu4(q4[h].z, lo[h].z), hi[h].z), __vminu4(__vmaxu4(q4[h].w, lo[h].w), hi[h].w));
-    return word_bound<W16>(s_lut, c, w);
-}
-
-// Block-wide slot reservation: each thread brings two counts (< 2^16 per
-// block); returns its first slot in each of two global lists, with one
-// atomicAdd per list per block. All threads of the block must call it.
-__device__ __forceinline__ uint2 block_reserve(unsigned c0, unsigned c1, unsigned* ctr0, unsigned* ctr1) {
-    __shared__ uint32_t s_cnt[kThreads / 32];
-    __shared__ uint32_t s_base[2];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t mine = c0 | (c1 << 16);
-    uint32_t incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_cnt[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int i = 0; i < kThreads / 32; ++i) {
-            const uint32_t c = s_cnt[i];
-            s_cnt[i] = tot;
-            tot += c;
-        }
-        s_base[0] = (tot & 0xFFFFu) ? atomicAdd(ctr0, tot & 0xFFFFu) : 0u;
-        s_base[1] = (tot >> 16) && ctr1 ? atomicAdd(ctr1, tot >> 16) : 0u;
-    }
-    __syncthreads();
-    const uint32_t before = s_cnt[warp] + (incl - mine);
-    const uint2 r = make_uint2(s_base[0] + (before & 0xFFFFu), s_base[1] + (before >> 16));
-    __syncthreads();  // s_cnt / s_base are reused by the next call
-    return r;
-}
-
-// Level 1, the flat analog of the tree's internal nodes: one box per group
-// of kGroup consecutive pages. Surviving groups are listed (block-aggregated)
-// for the page level, which then runs balanced over them.
+// ------------------------------------------------------------ groups
+// Level 1 of the box filter, the flat analog of the tree's internal nodes:
+// one box per group of kGroup consecutive pages. Grid (x, query); each
+// thread bounds kGP groups per round; surviving groups are listed per query
+// (block-aggregated) for the page level.
 constexpr int kGP = 4;  // groups / pages per thread per round
 
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
-    k_groups(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ glo, const uint8_t* __restrict__ ghi,
-             uint64_t NG, QueryWork* wk, uint32_t* __restrict__ gsurv) {
+    k_groups(IndexView ix, SlotView S) {
     constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
-    load_prepared(lut_g, wk, w, s_lut, qsym);
+    const int q = blockIdx.y;
+    QueryWork* wk = S.work + q;
+    if (wk->overflow) return;
+    load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
     uint4 q4[H];
 #pragma unroll
     for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
     const float bound = bound_from_bits(wk->bsf_bits);
-    if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        wk->scan_bound = bound;
+        atomicAdd(&wk->stats[kLbNode], static_cast<unsigned long long>(ix.NG));
+    }
+    uint32_t* gsurv = S.gsurv + q * S.NG;
     unsigned long long pruned = 0;
     constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kGP;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < NG;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < ix.NG;
          base += static_cast<uint64_t>(gridDim.x) * kRound) {
         uint4 bl[kGP][H], bh[kGP][H];
 #pragma unroll
@@ -419,16 +536,16 @@ __global__ void __launch_bounds__(kThreads)
             const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                bl[k][h] = g < NG ? ld_stream_u4(glo + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                bh[k][h] = g < NG ? ld_stream_u4(ghi + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bl[k][h] = g < ix.NG ? ld_stream_u4(ix.group_lo + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bh[k][h] = g < ix.NG ? ld_stream_u4(ix.group_hi + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
             }
         }
         unsigned keep = 0;
 #pragma unroll
         for (int k = 0; k < kGP; ++k) {
             const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-            if (g >= NG) continue;
-            if (box_bound<H, W16>(s_lut, q4, bl[k], bh[k], w) <= bound) keep |= 1u << k;
+            if (g >= ix.NG) continue;
+            if (box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w) <= bound) keep |= 1u << k;
             else pruned += 1;
         }
         uint32_t at = block_reserve(__popc(keep), 0, &wk->ngroups, nullptr).x;
@@ -436,50 +553,74 @@ __global__ void __launch_bounds__(kThreads)
         for (int k = 0; k < kGP; ++k)
             if (keep & (1u << k)) gsurv[at++] = static_cast<uint32_t>(base + threadIdx.x + static_cast<uint64_t>(kThreads) * k);
     }
-    for (int o = 16; o > 0; o >>= 1) pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
+    pruned = warp_sum(pruned);
     if ((threadIdx.x & 31) == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&wk->stats[kLbNode], NG);
 }
 
-// Level 2: the pages of the surviving groups, kGP per thread per round.
-// Pages whose bound is within the BSF (and outside the seed range) survive,
-// split into page wave 0 (bound <= split x BSF, front of surv) and wave 1
-// (back of surv); one atomic pair per block and round reserves the slots.
+// ------------------------------------------------------------- bound
+// Level 2: the pages of the surviving groups (persistent, affinity chunks of
+// kThreads x kGP pages). Pages whose bound is within the BSF (and outside the
+// seed range) survive, split into page wave 0 (bound <= split x BSF, front of
+// surv) and wave 1 (back of surv); one atomic pair per block and chunk.
 template <int WS, bool W16>
-__global__ void __launch_bounds__(kThreads)
-    k_bound(const float* __restrict__ lut_g, int w, const uint32_t* __restrict__ gsurv,
-            const uint8_t* __restrict__ lo, const uint8_t* __restrict__ hi, const uint32_t* __restrict__ page_off,
-            uint64_t P, QueryWork* wk, float split, uint2* __restrict__ surv, float* __restrict__ surv_lb) {
+__global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
+    k_bound(IndexView ix, SlotView S, int nq) {
     constexpr int H = WS / 16;
+    constexpr uint32_t kRound = static_cast<uint32_t>(kThreads) * kGP;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
-    load_prepared(lut_g, wk, w, s_lut, qsym);
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
     uint4 q4[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
-    const float bound = wk->scan_bound;
-    const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
-    const float cut = bound * split;  // wave 0: the most promising pages
-    const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
+    float bound = 0.f, cut = 0.f;
+    uint32_t sa = 0, sb = 0;
     unsigned long long pruned = 0, nodes = 0;
-    constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kGP;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < nitems;
-         base += static_cast<uint64_t>(gridDim.x) * kRound) {
+    auto nchunks = [](const QueryWork* wk) { return (wk->ngroups * static_cast<uint32_t>(kGroup) + kRound - 1) / kRound; };
+    auto flush_stats = [&](int q) {
+        pruned = warp_sum(pruned);
+        nodes = warp_sum(nodes);
+        if ((threadIdx.x & 31) == 0) {
+            if (pruned) atomicAdd(&S.work[q].stats[kPruned], pruned);
+            if (nodes) atomicAdd(&S.work[q].stats[kLbNode], nodes);
+        }
+        pruned = nodes = 0;
+    };
+    uint32_t chunk = 0, pre = ~0u;
+    for (int q = -1;;) {
+        q = claim(S.work, nq, kNextBound, cur, chunk, pre, q, nchunks);
+        if (q < 0) break;
+        pre = claim_ahead(S.work, q, kNextBound);
+        QueryWork* wk = S.work + q;
+        if (q != loaded) {
+            if (loaded >= 0) flush_stats(loaded);
+            load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
+#pragma unroll
+            for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+            bound = wk->scan_bound;
+            cut = bound * ix.split;  // wave 0: the most promising pages
+            sa = wk->seed_begin;
+            sb = wk->seed_end;
+            loaded = q;
+        }
+        const uint32_t* gsurv = S.gsurv + q * S.NG;
+        uint2* surv = S.surv + q * S.P;
+        float* surv_lb = S.surv_lb + q * S.P;
+        const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
+        const uint64_t base = static_cast<uint64_t>(chunk) * kRound;
         uint4 bl[kGP][H], bh[kGP][H];
         uint32_t ea[kGP], eb[kGP];
         bool valid[kGP];
 #pragma unroll
         for (int k = 0; k < kGP; ++k) {
             const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-            const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : P;
-            valid[k] = p < P;
+            const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
+            valid[k] = p < ix.P;
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                bl[k][h] = valid[k] ? ld_stream_u4(lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                bh[k][h] = valid[k] ? ld_stream_u4(hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bl[k][h] = valid[k] ? ld_stream_u4(ix.page_lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bh[k][h] = valid[k] ? ld_stream_u4(ix.page_hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
             }
-            ea[k] = valid[k] ? page_off[p] : 0u;
-            eb[k] = valid[k] ? page_off[p + 1] : 0u;
+            ea[k] = valid[k] ? ix.page_off[p] : 0u;
+            eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
         }
         unsigned lowmask = 0, highmask = 0;
         float lbs[kGP];
@@ -488,7 +629,7 @@ __global__ void __launch_bounds__(kThreads)
             lbs[k] = 0.f;
             if (!valid[k]) continue;
             nodes += 1;
-            const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], w);
+            const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
             lbs[k] = lb;
             const bool seeded = ea[k] >= sa && eb[k] <= sb;
             const bool keep = !seeded && lb <= bound;
@@ -504,28 +645,26 @@ __global__ void __launch_bounds__(kThreads)
                 surv_lb[at] = lbs[k];
                 surv[at++] = make_uint2(ea[k], eb[k]);
             } else if (highmask & (1u << k)) {
-                const uint64_t slot = P - 1 - at_hi++;
+                const uint64_t slot = ix.P - 1 - at_hi++;
                 surv_lb[slot] = lbs[k];
                 surv[slot] = make_uint2(ea[k], eb[k]);
             }
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
-        nodes += __shfl_xor_sync(0xFFFFFFFFu, nodes, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
-        if (nodes) atomicAdd(&wk->stats[kLbNode], nodes);
-    }
+    if (loaded >= 0) flush_stats(loaded);
 }
 
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
+constexpr int kTripPerWarp = 4;                      // page triples per warp per chunk
+constexpr uint32_t kTripChunk = kWarps * kTripPerWarp;  // page triples per chunk
 
 // Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
-// upward from ncand, wave B downward from the top of the candidate arrays
-// (nhigh). cut = +inf sends everything to A, cut < 0 everything to B.
+// upward after the seed range, wave B downward from the top of the slot's
+// candidate arrays; both counts are reserved with one 64-bit atomic so a
+// slot that would overflow is detected exactly (the query is then flagged
+// and rerun with a full-size slot; nothing is written out of range).
+// cut = +inf sends everything to A, cut < 0 everything to B.
 __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
                                             float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
@@ -535,70 +674,89 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
         const float lb = valid ? s_lb[i] : 0.f;
         const bool low = valid && lb <= cut;
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
-        uint32_t bl = 0, bh = 0;
-        if (lane == 0) {
-            if (ml) bl = atomicAdd(&wk->ncand, static_cast<unsigned>(__popc(ml)));
-            if (mh) bh = atomicAdd(&wk->nhigh, static_cast<unsigned>(__popc(mh)));
-        }
-        bl = __shfl_sync(0xFFFFFFFFu, bl, 0);
-        bh = __shfl_sync(0xFFFFFFFFu, bh, 0);
+        unsigned long long old = 0;
+        if (lane == 0)
+            old = atomicAdd(&wk->cand, static_cast<unsigned long long>(__popc(ml)) |
+                                           (static_cast<unsigned long long>(__popc(mh)) << 32));
+        old = __shfl_sync(0xFFFFFFFFu, old, 0);
+        const uint64_t bl = old & 0xFFFFFFFFull, bh = old >> 32;
+        if (lane == 0 && bl + __popc(ml) + bh + __popc(mh) > cap) atomicExch(&wk->overflow, 1u);
         const unsigned below = (1u << lane) - 1u;
         if (low) {
             const uint64_t at = bl + __popc(ml & below);
-            cand_pos[at] = s_pos[i];
-            cand_lb[at] = lb;
+            if (at < cap) {
+                cand_pos[at] = s_pos[i];
+                cand_lb[at] = lb;
+            }
         } else if (valid) {
-            const uint64_t at = cap - 1 - (bh + __popc(mh & below));
-            cand_pos[at] = s_pos[i];
-            cand_lb[at] = lb;
+            const uint64_t off = bh + __popc(mh & below);
+            if (off < cap) {
+                cand_pos[cap - 1 - off] = s_pos[i];
+                cand_lb[cap - 1 - off] = lb;
+            }
         }
     }
     __syncwarp();
 }
 
-// One page wave: wave 0 scans the pages whose box bound is within `split`
-// of the seed bound (surv[0, nsurv)), wave 1 the rest (surv[P - nsurv_hi, P)),
-// re-filtered against the BSF that wave 0's refinement tightened — MESSI's
-// LB-ordered leaf processing (src/query.cpp:173-184) at page granularity.
-// Below the page sits one more box level: aligned kRun-entry runs. A warp
-// takes three surviving pages at a time; lane 10j + t bounds run t of page j
-// (a <= 128-entry page touches at most 9 runs) with the same clamped-symbol
-// box bound as the page filter, surviving runs (clipped to their page) queue
-// in shared memory, and the queue drains four runs per step: each half-warp
-// bounds one run's words, one entry per lane. Words of pruned runs are never
-// read. The next triple's ranges and run boxes are in flight while the
-// current one is bounded.
+// One page wave (persistent, affinity chunks of kTripChunk page triples):
+// wave 0 scans surv[0, nsurv), wave 1 surv[P - nsurv_hi, P) re-filtered
+// against the BSF that refinement wave A tightened. Below the page sit two
+// more box levels over the sorted words, aligned kRun-entry runs and
+// kQuad-entry quads, bounded like the page boxes:
+//   pages: a warp takes three surviving pages at a time; lane 10j + t bounds
+//          run t of page j (a <= 128-entry page touches at most 9 runs);
+//   runs:  surviving runs (clipped to their page) queue in shared memory;
+//          eight at a time, lane 4k + u bounds quad u of queued run k;
+//   quads: surviving quads queue likewise; sixteen at a time, each lane
+//          bounds the words of entry u of two queued quads.
+// Only the words of surviving quads are read. Within a warp the next page
+// triple's ranges and run boxes are in flight while the current one is
+// bounded. Candidates are staged per warp and flushed when the stage fills
+// or the block moves to another query.
 template <int WS, bool W16>
-__global__ void __launch_bounds__(kThreads)
-    k_lbscan(const float* __restrict__ lut_g, int w, const uint8_t* __restrict__ words,
-             const uint8_t* __restrict__ run_lo, const uint8_t* __restrict__ run_hi,
-             const uint2* __restrict__ surv, const float* __restrict__ surv_lb,
-             uint64_t P, QueryWork* wk,
-             int wave, float split, uint64_t cap, uint32_t* __restrict__ cand_pos, float* __restrict__ cand_lb) {
-    constexpr int kRunQ = 40;
+__global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
+    k_lbscan(IndexView ix, SlotView S, int nq, int wave) {
+    constexpr int kRing = 64;  // per-warp ring queues (entry ranges), power of two
+    constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
-    __shared__ uint32_t s_pos[kThreads / 32][kStageCap];
-    __shared__ float s_lb[kThreads / 32][kStageCap];
-    __shared__ uint2 s_runq[kThreads / 32][kRunQ];
-    load_prepared(lut_g, wk, w, s_lut, qsym);
-    constexpr int H = WS / 16;
-    uint4 q4[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+    __shared__ uint32_t s_pos[kWarps][kStageCap];
+    __shared__ float s_lb[kWarps][kStageCap];
+    __shared__ uint2 s_rq[kWarps][kRing];  // surviving runs
+    __shared__ uint2 s_qq[kWarps][kRing];  // surviving quads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
     const int grp = lane / 10, t = lane - 10 * grp;  // page of the triple, run of the page (lanes 30, 31 idle)
-    const float bound = bound_from_bits(wk->bsf_bits);
-    // Page wave 0 splits its candidates into refinement waves A and B by their
-    // own bound; page wave 1 (scanned after wave A is refined) feeds wave B.
-    const float cut = wave == 0 ? wk->scan_bound * split : -1.f;
-    const uint32_t nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
-    const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
-    const uint64_t gwarp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
-    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    int cnt = 0, qn = 0;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
+    uint4 q4[H];
+    float bound = 0.f, cut = 0.f;
+    uint32_t nsurv = 0;
+    QueryWork* wk = nullptr;
+    uint32_t* cand_pos = nullptr;
+    float* cand_lb = nullptr;
+    const uint2* surv = nullptr;
+    const float* surv_lb = nullptr;
+    int cnt = 0;
+    uint32_t rh = 0, rt = 0, qh = 0, qt = 0;  // ring heads / tails (warp-uniform)
     unsigned long long scanned = 0, pruned = 0;
+    const int k_next = wave == 0 ? kNextScan0 : kNextScan1;
+    auto nchunks = [wave](const QueryWork* w) -> uint32_t {
+        if (w->overflow) return 0;
+        const uint32_t ns = wave == 0 ? w->nsurv : w->nsurv_hi;
+        return ((ns + 2) / 3 + kTripChunk - 1) / kTripChunk;
+    };
+    auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
+        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
+        cnt = 0;
+        scanned = warp_sum(scanned);
+        pruned = warp_sum(pruned);
+        if (lane == 0) {
+            if (scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
+            if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
+        }
+        scanned = pruned = 0;
+    };
 
     auto stage = [&](bool pass, uint32_t e, float lb) {
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
@@ -611,43 +769,66 @@ __global__ void __launch_bounds__(kThreads)
         cnt += __popc(m);
         __syncwarp();
         if (cnt > kStageCap - 32) {
-            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, cap, cand_pos, cand_lb);
+            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
             cnt = 0;
         }
     };
-    // Bounds the words of the first min(qn, 4) queued runs, then shifts the queue.
-    auto drain = [&]() {
-        const int take = min(qn, 4);
+    // Words of up to 16 queued quads: lane 4k + u takes entry u of quads k and k + 8.
+    auto drain_quads = [&]() {
+        const uint32_t take = min(qt - qh, 16u);
         uint4 wv[2][H];
         uint32_t e[2];
         bool ok[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int q = 2 * k + (lane >> 4);
+            const uint32_t qi = 8 * k + (lane >> 2);
             ok[k] = false;
             e[k] = 0;
-            if (q < take) {
-                const uint2 rr = s_runq[warp][q];
-                e[k] = rr.x + (lane & 15);
+            if (qi < take) {
+                const uint2 rr = s_qq[warp][(qh + qi) & (kRing - 1)];
+                e[k] = rr.x + (lane & 3);
                 ok[k] = e[k] < rr.y;
             }
 #pragma unroll
             for (int h = 0; h < H; ++h)
-                wv[k][h] = ok[k] ? ld_stream_u4(words + static_cast<uint64_t>(e[k]) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                wv[k][h] = ok[k] ? ld_stream_u4(ix.words + static_cast<uint64_t>(e[k]) * WS + 16 * h)
+                                 : make_uint4(0, 0, 0, 0);
         }
+        qh += take;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const float lb = word_bound<W16>(s_lut, wv[k], w);
+            const float lb = word_bound<W16>(s_lut, wv[k], ix.w);
             scanned += ok[k] ? 1 : 0;
             stage(ok[k] && lb <= bound, e[k], lb);
         }
-        const int rest = qn - take;
-        uint2 v = make_uint2(0, 0);
-        if (lane < rest) v = s_runq[warp][take + lane];
+    };
+    // Quads of up to 8 queued runs: lane 4k + u bounds quad u of run k.
+    auto drain_runs = [&]() {
+        const uint32_t take = min(rt - rh, 8u);
+        const uint32_t k = lane >> 2, u = lane & 3;
+        bool ok = false;
+        uint32_t e0 = 0, e1 = 0, qd = 0;
+        if (k < take) {
+            const uint2 rr = s_rq[warp][(rh + k) & (kRing - 1)];
+            qd = (rr.x / kRun) * (kRun / kQuad) + u;  // the run's aligned quads
+            e0 = max(rr.x, qd * kQuad);
+            e1 = min(rr.y, qd * kQuad + kQuad);
+            ok = e0 < e1;
+        }
+        uint4 bl[H], bh[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            bl[h] = ok ? ld_stream_u4(ix.quad_lo + static_cast<uint64_t>(qd) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            bh[h] = ok ? ld_stream_u4(ix.quad_hi + static_cast<uint64_t>(qd) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+        }
+        rh += take;
+        const bool pass = ok && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
+        pruned += ok && !pass ? 1 : 0;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+        if (pass) s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
+        qt += __popc(m);
         __syncwarp();
-        if (lane < rest) s_runq[warp][lane] = v;
-        __syncwarp();
-        qn = rest;
+        while (qt - qh >= 16) drain_quads();
     };
 
     uint32_t na = 0, nb = 0, nrun = 0;
@@ -658,7 +839,7 @@ __global__ void __launch_bounds__(kThreads)
         if (lane < 3) {
             const uint64_t i = 3 * T + lane;
             if (i < nsurv) {
-                const uint64_t slot = wave == 0 ? i : P - 1 - i;
+                const uint64_t slot = wave == 0 ? i : ix.P - 1 - i;
                 if (wave == 0 || surv_lb[slot] <= bound) {
                     const uint2 r = surv[slot];
                     a = r.x;
@@ -674,151 +855,330 @@ __global__ void __launch_bounds__(kThreads)
         nvalid = grp < 3 && na < nb && nrun * kRun < nb;
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            nbl[h] = nvalid ? ld_stream_u4(run_lo + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-            nbh[h] = nvalid ? ld_stream_u4(run_hi + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            nbl[h] = nvalid ? ld_stream_u4(ix.run_lo + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            nbh[h] = nvalid ? ld_stream_u4(ix.run_hi + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
         }
     };
-    if (gwarp < ntrip) fetch(gwarp);
-    for (uint64_t T = gwarp; T < ntrip; T += nwarps) {
-        const uint32_t a = na, b = nb, r = nrun;
-        const bool valid = nvalid;
-        uint4 c[H];
+
+    uint32_t chunk = 0, pre = ~0u;
+    for (int q = -1;;) {
+        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
+        if (q < 0) break;
+        pre = claim_ahead(S.work, q, k_next);
+        if (q != loaded) {
+            if (loaded >= 0) leave_query();
+            wk = S.work + q;
+            load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
 #pragma unroll
-        for (int h = 0; h < H; ++h)
-            c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, nbl[h].x), nbh[h].x),
-                              __vminu4(__vmaxu4(q4[h].y, nbl[h].y), nbh[h].y),
-                              __vminu4(__vmaxu4(q4[h].z, nbl[h].z), nbh[h].z),
-                              __vminu4(__vmaxu4(q4[h].w, nbl[h].w), nbh[h].w));
-        if (T + nwarps < ntrip) fetch(T + nwarps);
-        bool pass = false;
-        if (valid) pass = word_bound<W16>(s_lut, c, w) <= bound;
-        pruned += valid && !pass ? 1 : 0;
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-        if (pass) s_runq[warp][qn + __popc(m & below)] = make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
-        qn += __popc(m);
-        __syncwarp();
-        while (qn >= 4) drain();
-    }
-    while (qn > 0) drain();
-    for (int o = 16; o > 0; o >>= 1) {
-        scanned += __shfl_xor_sync(0xFFFFFFFFu, scanned, o);
-        pruned += __shfl_xor_sync(0xFFFFFFFFu, pruned, o);
-    }
-    // Final flush, one atomic pair per block instead of one per warp.
-    __shared__ uint32_t s_wcnt[kThreads / 32], s_wbase[2];
-    int lo_cnt = 0;
-    for (int i = lane; i < cnt; i += 32) lo_cnt += s_lb[warp][i] <= cut ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
-    if (lane == 0) s_wcnt[warp] = static_cast<uint32_t>(lo_cnt) | (static_cast<uint32_t>(cnt - lo_cnt) << 16);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int i = 0; i < kThreads / 32; ++i) {
-            const uint32_t c2 = s_wcnt[i];
-            s_wcnt[i] = tot;
-            tot += c2;
+            for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+            bound = bound_from_bits(wk->bsf_bits);
+            // Page wave 0 splits its candidates into refinement waves A and B
+            // by their own bound; page wave 1 (scanned after wave A is
+            // refined) feeds wave B.
+            cut = wave == 0 ? wk->scan_bound * ix.split : -1.f;
+            nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
+            cand_pos = S.cand_pos + q * S.cap;
+            cand_lb = S.cand_lb + q * S.cap;
+            surv = S.surv + q * S.P;
+            surv_lb = S.surv_lb + q * S.P;
+            loaded = q;
         }
-        s_wbase[0] = (tot & 0xFFFFu) ? atomicAdd(&wk->ncand, tot & 0xFFFFu) : 0u;
-        s_wbase[1] = (tot >> 16) ? atomicAdd(&wk->nhigh, tot >> 16) : 0u;
-    }
-    __syncthreads();
-    {
-        uint32_t at_lo = s_wbase[0] + (s_wcnt[warp] & 0xFFFFu), at_hi = s_wbase[1] + (s_wcnt[warp] >> 16);
-        for (int i0 = 0; i0 < cnt; i0 += 32) {
-            const int i = i0 + lane;
-            const bool valid = i < cnt;
-            const float lb = valid ? s_lb[warp][i] : 0.f;
-            const bool low = valid && lb <= cut;
-            const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
-            const unsigned below = (1u << lane) - 1u;
-            if (low) {
-                const uint64_t at = at_lo + __popc(ml & below);
-                cand_pos[at] = s_pos[warp][i];
-                cand_lb[at] = lb;
-            } else if (valid) {
-                const uint64_t at = cap - 1 - (at_hi + __popc(mh & below));
-                cand_pos[at] = s_pos[warp][i];
-                cand_lb[at] = lb;
+        const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
+        const uint64_t t0 = static_cast<uint64_t>(chunk) * kTripChunk + warp * kTripPerWarp;
+        const uint64_t t1 = u64min(t0 + kTripPerWarp, ntrip);
+        if (t0 < t1) fetch(t0);
+        for (uint64_t T = t0; T < t1; ++T) {
+            const uint32_t a = na, b = nb, r = nrun;
+            const bool valid = nvalid;
+            uint4 bl[H], bh[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                bl[h] = nbl[h];
+                bh[h] = nbh[h];
             }
-            at_lo += __popc(ml);
-            at_hi += __popc(mh);
+            if (T + 1 < t1) fetch(T + 1);
+            const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
+            pruned += valid && !pass ? 1 : 0;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+            if (pass)
+                s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] =
+                    make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
+            rt += __popc(m);
+            __syncwarp();
+            while (rt - rh >= 8) drain_runs();
         }
+        while (rt != rh) drain_runs();
+        while (qt != qh) drain_quads();
     }
-    if (lane == 0 && scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
-    if (lane == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
+    if (loaded >= 0) leave_query();
 }
 
 // ------------------------------------------------------------ refine
-// One wave: wave 0 = [nseed, ncand), wave 1 = [cap - nhigh, cap).
+// One refinement wave (persistent, affinity chunks of kRefChunk candidates):
+// wave 0 = records [nseed, nA), wave 1 = [cap - nB, cap). Each 8-lane group
+// walks its own candidates of the chunk, the next record prefetched while the
+// current row is refined; a candidate whose bound exceeds the live BSF costs
+// one check.
+constexpr uint32_t kRefPerGroup = 8;
+constexpr uint32_t kRefChunk = (kThreads / kRowLanes) * kRefPerGroup;
+
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    k_refine(const float* __restrict__ rows, int n, const float* __restrict__ query, const uint32_t* __restrict__ pos,
-             QueryWork* wk,
-             const uint32_t* __restrict__ cand_pos, const float* __restrict__ cand_lb,
-             double* __restrict__ cand_sq, int wave, uint64_t cap) {
-    extern __shared__ float s_q[];
-    load_query(s_q, query, n);
-    const uint64_t begin = wave == 0 ? wk->nseed : cap - wk->nhigh;
-    const uint64_t end = wave == 0 ? wk->ncand : cap;
+__global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
+    k_refine(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
+    extern __shared__ double s_qd[];
+    constexpr uint32_t kGroups = kThreads / kRowLanes;
     const int lane = threadIdx.x & 31;
     const bool leader = (lane & (kRowLanes - 1)) == 0;
+    const uint32_t g = threadIdx.x / kRowLanes;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
     unsigned long long refined = 0, updates = 0;
-    // Each 8-lane group walks its own candidates (group-stride), the next
-    // candidate's record prefetched while the current row is refined; a
-    // candidate whose bound exceeds the live BSF costs one check.
-    const uint64_t group = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kRowLanes;
-    const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * blockDim.x / kRowLanes;
-    uint64_t c = begin + group;
-    float nlb = c < end ? cand_lb[c] : 0.f;
-    uint32_t np = c < end ? pos[cand_pos[c]] : 0u;  // candidate records hold index-order entries
-    // Cached pruning bound: refreshed from the BSF each publish observes, so a
-    // skipped candidate costs no memory access (a stale bound only refines more).
-    float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
-    for (; c < end; c += ngroups) {
-        const float lb = nlb;
-        const uint32_t p = np;
-        if (c + ngroups < end) {
-            nlb = cand_lb[c + ngroups];
-            np = pos[cand_pos[c + ngroups]];
+    auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
+        const unsigned long long c = w->cand;
+        if (wave == 0) {
+            begin = w->nseed;
+            end = c & 0xFFFFFFFFull;
+        } else {
+            begin = S.cap - (c >> 32);
+            end = S.cap;
         }
-        if (lb > bnd) {
-            if (leader) cand_sq[c] = INFINITY;
-            continue;
-        }
-        // read the BSF for the next candidate's bound while this row is in flight
-        const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
-        const double s = group_row_sq<VEC>(rows + static_cast<uint64_t>(p) * n, s_q, n, &wk->bsf_bits);
+    };
+    auto nchunks = [&](const QueryWork* w) -> uint32_t {
+        if (w->overflow) return 0;
+        uint64_t b, e;
+        range(w, b, e);
+        return static_cast<uint32_t>((e - b + kRefChunk - 1) / kRefChunk);
+    };
+    auto leave_query = [&](int q) {
         if (leader) {
-            refined += 1;
-            updates += publish(wk, s, c, cand_sq);
+            if (refined) atomicAdd(&S.work[q].stats[kRealDist], refined);
+            if (updates) atomicAdd(&S.work[q].stats[kBsfUpd], updates);
         }
-        bnd = bound_from_bits(min(seen, static_cast<unsigned long long>(__double_as_longlong(s < INFINITY ? s : INFINITY))));
+        refined = updates = 0;
+    };
+    uint32_t chunk = 0, pre = ~0u;
+    const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
+    for (int q = -1;;) {
+        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
+        if (q < 0) break;
+        pre = claim_ahead(S.work, q, k_next);
+        QueryWork* wk = S.work + q;
+        if (q != loaded) {
+            if (loaded >= 0) leave_query(loaded);
+            load_query_f64(s_qd, queries + static_cast<uint64_t>(q) * ix.n, ix.n);
+            loaded = q;
+        }
+        const uint32_t* cand_pos = S.cand_pos + q * S.cap;
+        const float* cand_lb = S.cand_lb + q * S.cap;
+        double* cand_sq = S.cand_sq + q * S.cap;
+        uint64_t begin, end;
+        range(wk, begin, end);
+        const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kRefChunk;
+        const uint64_t c1 = u64min(c0 + kRefChunk, end);
+        uint64_t c = c0 + g;
+        float nlb = c < c1 ? cand_lb[c] : 0.f;
+        uint32_t np = c < c1 ? ix.pos[cand_pos[c]] : 0u;  // candidate records hold index-order entries
+        // Cached pruning bound: refreshed from the BSF each refinement sees,
+        // so a skipped candidate costs no memory access (a stale bound only
+        // refines more).
+        float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+        for (; c < c1; c += kGroups) {
+            const float lb = nlb;
+            const uint32_t p = np;
+            if (c + kGroups < c1) {
+                nlb = cand_lb[c + kGroups];
+                np = ix.pos[cand_pos[c + kGroups]];
+            }
+            if (lb > bnd) {
+                if (leader) cand_sq[c] = INFINITY;
+                continue;
+            }
+            // read the BSF for the next candidate's bound while this row is in flight
+            const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
+            const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
+            if (leader) {
+                refined += 1;
+                updates += publish(wk, s, c, cand_sq);
+            }
+            bnd = bound_from_bits(min(seen, static_cast<unsigned long long>(__double_as_longlong(s < INFINITY ? s : INFINITY))));
+        }
     }
-    if (leader) {
-        if (refined) atomicAdd(&wk->stats[kRealDist], refined);
-        if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+    if (loaded >= 0) leave_query(loaded);
+}
+
+// Refinement with TMA row staging (n % 8 == 0, n <= kTmaMaxN): per chunk of
+// kTmaChunk candidate records the block first keeps those whose bound is
+// within the BSF (compacted in shared memory, row positions gathered by all
+// threads at once); then each 8-lane group walks the kept rows with two
+// shared-memory row buffers: while it sums row j from one buffer, a 1-D bulk
+// copy (cp.async.bulk, mbarrier-tracked) brings row j + 32 into the other, so
+// the row fetch overlaps the FP64 arithmetic instead of stalling it. Sums
+// are the same blocked FP64 sums in squared_l2's order as group_row_sq
+// (whole rows: an abandoned sum only ever exceeds the BSF, so computing it
+// in full changes no answer).
+constexpr int kTmaMaxN = 512;
+constexpr uint32_t kTmaChunk = 512;
+
+// NB = n / 8 blocks per row, a compile-time constant so the row sum unrolls.
+template <int NB>
+__global__ void __launch_bounds__(kThreads, 3)
+    k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
+    constexpr int kGroups = kThreads / kRowLanes;
+    constexpr int n = NB * 8;
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    float* s_rows = reinterpret_cast<float*>(s_dyn);                       // [kGroups][2][n]
+    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // [n]
+    __shared__ __align__(8) uint64_t s_bar[kGroups][2];
+    __shared__ uint32_t s_c[kTmaChunk], s_p[kTmaChunk];
+    __shared__ uint32_t s_m;
+    const int lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
+    const int gbase = lane & ~(kRowLanes - 1);
+    const unsigned gmask = 0xFFu << gbase;
+    const bool leader = j8 == 0;
+    constexpr unsigned row_bytes = static_cast<unsigned>(n) * 4u;
+    if (threadIdx.x < 2 * kGroups) mbar_init(&s_bar[threadIdx.x >> 1][threadIdx.x & 1], 1);
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    unsigned phase = 0;  // bit b: parity of this group's buffer b
+    float* buf0 = s_rows + static_cast<size_t>(g) * 2 * n;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
+    unsigned long long refined = 0, updates = 0;
+    const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
+    auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
+        const unsigned long long c = w->cand;
+        if (wave == 0) {
+            begin = w->nseed;
+            end = c & 0xFFFFFFFFull;
+        } else {
+            begin = S.cap - (c >> 32);
+            end = S.cap;
+        }
+    };
+    auto nchunks = [&](const QueryWork* w) -> uint32_t {
+        if (w->overflow) return 0;
+        uint64_t b, e;
+        range(w, b, e);
+        return static_cast<uint32_t>((e - b + kTmaChunk - 1) / kTmaChunk);
+    };
+    auto leave_query = [&](int q) {
+        if (leader) {
+            if (refined) atomicAdd(&S.work[q].stats[kRealDist], refined);
+            if (updates) atomicAdd(&S.work[q].stats[kBsfUpd], updates);
+        }
+        refined = updates = 0;
+    };
+    auto issue = [&](int b, uint32_t p) {  // leader: row p -> this group's buffer b
+        fence_proxy_async_smem();
+        mbar_expect_tx(&s_bar[g][b], row_bytes);
+        tma_copy_1d(buf0 + b * n, ix.rows + static_cast<uint64_t>(p) * n, row_bytes, &s_bar[g][b]);
+    };
+    uint32_t chunk = 0, pre = ~0u;
+    for (int q = -1;;) {
+        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
+        if (q < 0) break;
+        pre = claim_ahead(S.work, q, k_next);
+        QueryWork* wk = S.work + q;
+        if (q != loaded) {
+            if (loaded >= 0) leave_query(loaded);
+            load_query_f64(s_qd, queries + static_cast<uint64_t>(q) * n, n);
+            loaded = q;
+        }
+        const uint32_t* cand_pos = S.cand_pos + q * S.cap;
+        const float* cand_lb = S.cand_lb + q * S.cap;
+        double* cand_sq = S.cand_sq + q * S.cap;
+        uint64_t begin, end;
+        range(wk, begin, end);
+        const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kTmaChunk;
+        const uint64_t c1 = u64min(c0 + kTmaChunk, end);
+        // Phase 1: keep the records whose bound is within the BSF.
+        if (threadIdx.x == 0) s_m = 0;
+        __syncthreads();
+        const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+        for (uint32_t i0 = 0; i0 < kTmaChunk; i0 += kThreads) {
+            const uint64_t c = c0 + i0 + threadIdx.x;
+            const bool in = c < c1;
+            const bool keep = in && cand_lb[c] <= bnd;
+            if (in && !keep) cand_sq[c] = INFINITY;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+            uint32_t base = 0;
+            if (lane == 0 && m) base = atomicAdd(&s_m, static_cast<unsigned>(__popc(m)));
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (keep) {
+                const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
+                s_c[slot] = static_cast<uint32_t>(c);
+                s_p[slot] = ix.pos[cand_pos[c]];  // candidate records hold index-order entries
+            }
+        }
+        __syncthreads();
+        const uint32_t m = s_m;
+        // Phase 2: the kept rows, double-buffered per group.
+        if (leader && static_cast<uint32_t>(g) < m) issue(0, s_p[g]);
+        int b = 0;
+        for (uint32_t j = g; j < m; j += kGroups, b ^= 1) {
+            if (leader && j + kGroups < m) issue(b ^ 1, s_p[j + kGroups]);
+            const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
+            mbar_wait(&s_bar[g][b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+            const float* row = buf0 + b * n;
+            constexpr int kT = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
+            double blk[kT];
+#pragma unroll
+            for (int t = 0; t < kT; ++t) {
+                const int k = j8 + kRowLanes * t;
+                blk[t] = 0.0;
+                if (k < NB) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(row + 8 * k);
+                    const float4 x1 = *reinterpret_cast<const float4*>(row + 8 * k + 4);
+                    const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                    blk[t] = block_sq(x, s_qd + 8 * k, 8);
+                }
+            }
+            // left to right over the blocks: block 8t + i lives in lane gbase + i, slot t
+            double sum = 0.0;
+#pragma unroll
+            for (int t = 0; t < kT; ++t)
+#pragma unroll
+                for (int i = 0; i < kRowLanes; ++i) {
+                    const double v = __shfl_sync(gmask, blk[t], gbase + i);
+                    if (kRowLanes * t + i < NB) sum = __dadd_rn(sum, v);
+                }
+            __syncwarp(gmask);  // the group is done with buffer b before it is refilled
+            if (leader) {
+                const uint32_t c = s_c[j];
+                cand_sq[c] = sum;
+                refined += 1;
+                const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
+                if (sb < seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
+            }
+        }
     }
+    if (loaded >= 0) leave_query(loaded);
 }
 
 // ----------------------------------------------------------- finalize
-// Lowest position among the candidates whose sqrt(sum) equals the best
-// distance; the last block to finish writes the result and resets `wk`.
+// Grid (x, query): lowest position among the candidates whose sqrt(sum)
+// equals the best distance; the last block of a query writes its result
+// (flagged when the slot overflowed).
 __global__ void __launch_bounds__(kThreads)
-    k_finalize(QueryWork* wk, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ cand_pos,
-               const double* __restrict__ cand_sq, int seed_only,
-               uint64_t cap, DevResult* out, uint64_t P, uint64_t pos_offset) {
+    k_finalize(IndexView ix, SlotView S, int seed_only, DevResult* __restrict__ results) {
+    const int q = blockIdx.y;
+    QueryWork* wk = S.work + q;
     const double best = bsf_of(wk->bsf_bits);
     const double dist = sqrt(best);
     const double lim = best * kSlack;
-    const uint64_t lo_end = seed_only ? wk->nseed : wk->ncand;
-    const uint64_t hi_n = seed_only ? 0 : wk->nhigh;
+    const bool overflow = wk->overflow != 0;
+    const unsigned long long cand = wk->cand;
+    const uint64_t lo_end = seed_only ? wk->nseed : (cand & 0xFFFFFFFFull);
+    const uint64_t hi_n = seed_only ? 0 : (cand >> 32);
+    const uint32_t* cand_pos = S.cand_pos + q * S.cap;
+    const double* cand_sq = S.cand_sq + q * S.cap;
     uint32_t mine = 0xFFFFFFFFu;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < lo_end + hi_n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t c = i < lo_end ? i : cap - 1 - (i - lo_end);
-        const double s = cand_sq[c];
-        if (s <= lim && sqrt(s) == dist) mine = min(mine, pos[cand_pos[c]]);
-    }
+    if (!overflow)
+        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < lo_end + hi_n;
+             i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+            const uint64_t c = i < lo_end ? i : S.cap - 1 - (i - lo_end);
+            const double s = cand_sq[c];
+            if (s <= lim && sqrt(s) == dist) mine = min(mine, ix.pos[cand_pos[c]]);
+        }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
     if ((threadIdx.x & 31) == 0 && mine != 0xFFFFFFFFu) atomicMin(&wk->best_pos, mine);
@@ -830,22 +1190,16 @@ __global__ void __launch_bounds__(kThreads)
     if (!last || threadIdx.x != 0) return;
     __threadfence();
     const unsigned best_pos = atomicAdd(&wk->best_pos, 0u);
+    DevResult* out = results + q;
     out->distance = dist;
-    out->position = static_cast<uint32_t>(best_pos + pos_offset);
-    out->reserved = 0;
+    out->position = static_cast<uint32_t>(best_pos + ix.pos_offset);
+    out->flags = overflow ? kResultOverflow : 0u;
     out->stats[kLbNode] = wk->stats[kLbNode];
     out->stats[kLbEntry] = wk->stats[kLbEntry] + wk->nseed;
     out->stats[kRealDist] = wk->stats[kRealDist];
     out->stats[kBsfUpd] = wk->stats[kBsfUpd];
     out->stats[kPruned] = wk->stats[kPruned];
-    out->stats[kQueueIns] = wk->ncand - wk->nseed + wk->nhigh;
-    reset_work(wk);  // for the next query on this stream
-    __threadfence();
-    wk->done_blocks = 0;
-}
-
-unsigned cap_grid(uint64_t want, int sms, int per_sm) {
-    return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, static_cast<uint64_t>(sms) * per_sm)));
+    out->stats[kQueueIns] = (cand & 0xFFFFFFFFull) - wk->nseed + (cand >> 32);
 }
 
 template <typename K>
@@ -857,11 +1211,15 @@ int blocks_per_sm(K kernel, size_t smem) {
 
 }  // namespace
 
-void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approximate) {
+void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
+                  DevResult* results) {
+    if (nq == 0) return;
+    if (nq > slots.n) throw std::logic_error("search_batch: batch larger than its slots");
     cudaStream_t st = ix.stream;
     const int n = ix.n, w = ix.w;
     const size_t lut_bytes = static_cast<size_t>(w) * 256 * sizeof(float);
     const size_t q_bytes = static_cast<size_t>(n) * sizeof(float);
+    const size_t qd_bytes = static_cast<size_t>(n) * sizeof(double);
     const bool vec = (n % 8) == 0 && (reinterpret_cast<uintptr_t>(ix.rows) % 32) == 0;
     const bool w16 = w == 16;
     auto refine = vec ? k_refine<true> : k_refine<false>;
@@ -869,34 +1227,61 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
     auto lbscan = ix.ws == 16 ? (w16 ? k_lbscan<16, true> : k_lbscan<16, false>) : k_lbscan<32, false>;
     auto bound = ix.ws == 16 ? (w16 ? k_bound<16, true> : k_bound<16, false>) : k_bound<32, false>;
     auto groups = ix.ws == 16 ? (w16 ? k_groups<16, true> : k_groups<16, false>) : k_groups<32, false>;
-    TSG_CUDA(cudaFuncSetAttribute(groups, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     // Per-device function attributes (cheap; set on every call so each device is covered).
-    TSG_CUDA(cudaFuncSetAttribute(refine, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    TSG_CUDA(cudaFuncSetAttribute(seed, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    TSG_CUDA(cudaFuncSetAttribute(lbscan, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    TSG_CUDA(cudaFuncSetAttribute(bound, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    const uint32_t seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
-    // With several query lanes, each kernel gets a share of the GPU so kernels
-    // of different queries co-reside (TSG_GRID_SHARE: 1/share of the
-    // resident-block capacity; default 2 when lanes run concurrently).
-    const int share_env = std::getenv("TSG_GRID_SHARE") ? std::atoi(std::getenv("TSG_GRID_SHARE")) : 0;
-    const int share = std::max(1, share_env > 0 ? share_env : (ix.nlanes > 1 && !ix.profile ? 2 : 1));
-    const unsigned group_grid = cap_grid((ix.NG + kThreads * kGP - 1) / (kThreads * kGP), ix.sms,
-                                         std::max(1, std::min(6, blocks_per_sm(groups, lut_bytes)) / share));
-    // (the page level's size is only known on the device: a resident-capacity grid)
-    const unsigned bound_grid = cap_grid((ix.P + kThreads * kGP - 1) / (kThreads * kGP), ix.sms,
-                                         std::max(1, std::min(6, blocks_per_sm(bound, lut_bytes)) / share));
-    const unsigned seed_grid = cap_grid((std::min<uint64_t>(seed_cap, ix.N) * kRowLanes + kThreads - 1) / kThreads,
-                                        ix.sms, blocks_per_sm(seed, q_bytes));
-    const unsigned scan_grid = static_cast<unsigned>(std::max(ix.sms, ix.sms * blocks_per_sm(lbscan, lut_bytes) / share));
-    const unsigned refine_grid = static_cast<unsigned>(std::max(ix.sms, ix.sms * blocks_per_sm(refine, q_bytes) / share));
-    const uint64_t cap = ix.cand_cap;
-    // Profiling runs one lane so per-kernel times are not overlapped.
-    const int nl = ix.profile ? 1 : std::max(1, std::min<int>(ix.nlanes, static_cast<int>(nq)));
+    // TMA-staged refinement for the row lengths it is instantiated for.
+    auto refine_tma = n == 256 ? k_refine_tma<32> : n == 128 ? k_refine_tma<16> : n == 96 ? k_refine_tma<12>
+                    : n == 64 ? k_refine_tma<8> : n == 512 ? k_refine_tma<64> : nullptr;
+    const bool tma = vec && refine_tma && !std::getenv("TSG_NO_TMA_REFINE");
+    const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * 2 * n * 4 + static_cast<size_t>(n) * 8;
+    if (tma) TSG_CUDA(cudaFuncSetAttribute(refine_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024));
+    for (const void* f : {reinterpret_cast<const void*>(refine), reinterpret_cast<const void*>(seed),
+                          reinterpret_cast<const void*>(lbscan), reinterpret_cast<const void*>(bound),
+                          reinterpret_cast<const void*>(groups), reinterpret_cast<const void*>(k_prepare)})
+        TSG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+
+    IndexView iv{};
+    iv.rows = ix.rows;
+    iv.n = n;
+    iv.w = w;
+    iv.bits = ix.bits;
+    iv.thr = ix.thr;
+    iv.words = ix.words;
+    iv.pos = ix.pos;
+    iv.leaf_off = ix.leaf_off;
+    iv.page_off = ix.page_off;
+    iv.page_leaf = ix.page_leaf;
+    iv.page_key = ix.page_key;
+    iv.page_dir = ix.page_dir;
+    iv.P = ix.P;
+    iv.page_lo = ix.page_lo;
+    iv.page_hi = ix.page_hi;
+    iv.group_lo = ix.group_lo;
+    iv.group_hi = ix.group_hi;
+    iv.NG = ix.NG;
+    iv.run_lo = ix.run_lo;
+    iv.run_hi = ix.run_hi;
+    iv.quad_lo = ix.quad_lo;
+    iv.quad_hi = ix.quad_hi;
+    iv.seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
+    iv.split = ix.refine_split;
+    iv.pos_offset = ix.pos_offset;
+    SlotView sv{slots.work, slots.lut, slots.gsurv, slots.surv, slots.surv_lb, slots.cand_pos, slots.cand_lb,
+                slots.cand_sq, slots.cap, ix.P, ix.NG, w * 256};
+
+    const int sms = ix.sms;
+    const unsigned seed_x = (iv.seed_cap + kThreads / kRowLanes - 1) / (kThreads / kRowLanes);
+    const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>((ix.NG + kThreads * kGP - 1) / (kThreads * kGP),
+                              static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
+    const unsigned bound_grid = static_cast<unsigned>(sms * blocks_per_sm(bound, lut_bytes));
+    const unsigned scan_grid = static_cast<unsigned>(sms * blocks_per_sm(lbscan, lut_bytes));
+    const unsigned refine_grid = tma ? static_cast<unsigned>(sms * blocks_per_sm(refine_tma, tma_bytes))
+                                     : static_cast<unsigned>(sms * blocks_per_sm(refine, qd_bytes));
+    const unsigned fin_x = std::max(1u, std::min(256u, static_cast<unsigned>(sms * 32 / nq)));
 
     // Optional per-kernel timing: events around every launch, summed after the batch.
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
-    auto mark = [&](cudaStream_t ls, int slot, auto&& launch) {
+    auto mark = [&](int slot, auto&& launch) {
         if (!ix.profile) {
             launch();
             return;
@@ -904,111 +1289,48 @@ void search_batch(DevIndex& ix, const float* d_queries, uint32_t nq, bool approx
         cudaEvent_t a, b;
         TSG_CUDA(cudaEventCreate(&a));
         TSG_CUDA(cudaEventCreate(&b));
-        TSG_CUDA(cudaEventRecord(a, ls));
+        TSG_CUDA(cudaEventRecord(a, st));
         launch();
-        TSG_CUDA(cudaEventRecord(b, ls));
+        TSG_CUDA(cudaEventRecord(b, st));
         marks.push_back({slot, {a, b}});
     };
-
-    // Fork (every lane starts after the work already queued on the index
-    // stream), the queries round-robin over the lanes, join.
-    auto enqueue = [&]() {
-        TSG_CUDA(cudaEventRecord(ix.lanes[0].done, st));
-        for (int k = 0; k < nl; ++k) {
-            DevIndex::Lane& L = ix.lanes[k];
-            if (k > 0) TSG_CUDA(cudaStreamWaitEvent(L.stream, ix.lanes[0].done, 0));
-            k_reset<<<1, 1, 0, L.stream>>>(L.work);
+    const int inq = static_cast<int>(nq);
+    mark(2, [&] {
+        k_prepare<<<nq, kThreads, q_bytes, st>>>(iv, sv, d_queries);
+        TSG_LAUNCHED();
+        seed<<<dim3(seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
+        TSG_LAUNCHED();
+    });
+    if (!approximate) {
+        mark(1, [&] {
+            groups<<<dim3(group_x, nq), kThreads, lut_bytes, st>>>(iv, sv);
             TSG_LAUNCHED();
-        }
-        for (uint32_t qi = 0; qi < nq; ++qi) {
-            const DevIndex::Lane& L = ix.lanes[qi % nl];
-            cudaStream_t ls = L.stream;
-            const float* q = d_queries + static_cast<uint64_t>(qi) * n;
-            mark(ls, 2, [&] {
-                seed<<<seed_grid, kThreads, q_bytes, ls>>>(ix.rows, n, w, ix.bits, ix.thr, q, ix.leaf_off, ix.page_off,
-                                                           ix.page_leaf, ix.page_key, ix.page_dir, ix.P, ix.pos, seed_cap,
-                                                           L.work, L.cand_pos, L.cand_sq, L.lut);
-            });
+            bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq);
             TSG_LAUNCHED();
-            if (!approximate) {
-                mark(ls, 1, [&] {
-                    groups<<<group_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.group_lo, ix.group_hi, ix.NG, L.work,
-                                                                    L.gsurv);
-                    TSG_LAUNCHED();
-                    bound<<<bound_grid, kThreads, lut_bytes, ls>>>(L.lut, w, L.gsurv, ix.page_lo, ix.page_hi, ix.page_off,
-                                                                   ix.P, L.work, ix.refine_split, L.surv, L.surv_lb);
-                });
+        });
+        for (int wave = 0; wave < 2; ++wave) {
+            mark(4, [&] {
+                lbscan<<<scan_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, wave);
                 TSG_LAUNCHED();
-                for (int wave = 0; wave < 2; ++wave) {
-                    mark(ls, 4, [&] {
-                        lbscan<<<scan_grid, kThreads, lut_bytes, ls>>>(L.lut, w, ix.words, ix.run_lo, ix.run_hi, L.surv, L.surv_lb,
-                                                                       ix.P, L.work, wave, ix.refine_split, cap, L.cand_pos,
-                                                                       L.cand_lb);
-                    });
-                    TSG_LAUNCHED();
-                    mark(ls, wave == 0 ? 3 : 5, [&] {
-                        refine<<<refine_grid, kThreads, q_bytes, ls>>>(ix.rows, n, q, ix.pos, L.work, L.cand_pos, L.cand_lb,
-                                                                       L.cand_sq, wave, cap);
-                    });
-                    TSG_LAUNCHED();
-                }
-            }
-            mark(ls, 6, [&] {
-                k_finalize<<<ix.sms, kThreads, 0, ls>>>(L.work, ix.pos, L.cand_pos, L.cand_sq, approximate ? 1 : 0, cap,
-                                                        ix.results + qi, ix.P, ix.pos_offset);
             });
-            TSG_LAUNCHED();
+            mark(wave == 0 ? 3 : 5, [&] {
+                if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                TSG_LAUNCHED();
+            });
         }
-        // Join: the index stream waits for every lane.
-        for (int k = 1; k < nl; ++k) {
-            TSG_CUDA(cudaEventRecord(ix.lanes[k].done, ix.lanes[k].stream));
-            TSG_CUDA(cudaStreamWaitEvent(st, ix.lanes[k].done, 0));
-        }
-    };
-
-    // TSG_GRAPHS=1: the batch is captured into a CUDA graph (~7 kernels per
-    // query over the lanes' streams as one launch, replayed while the batch
-    // shape and buffers repeat). Measured no faster than direct launches on
-    // c2 (the host enqueue overlaps the GPU), so off by default; it lets ncu
-    // (--graph-profiling graph) measure a whole concurrent batch.
-    const char* genv = std::getenv("TSG_GRAPHS");
-    const bool graph = !ix.profile && genv && genv[0] == '1';
-    if (!graph) {
-        enqueue();
-    } else if (ix.graph && ix.graph_key.queries == d_queries && ix.graph_key.nq == nq &&
-               ix.graph_key.approximate == approximate && ix.graph_key.nlanes == nl) {
-        // Same batch shape and buffers as the captured graph: replay it.
-        TSG_CUDA(cudaGraphLaunch(ix.graph, st));
-        note_launch(ix.graph_key.kernels);
-    } else {
-        TSG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        try {
-            enqueue();
-        } catch (...) {
-            cudaGraph_t g = nullptr;
-            cudaStreamEndCapture(st, &g);
-            if (g) cudaGraphDestroy(g);
-            throw;
-        }
-        cudaGraph_t g = nullptr;
-        TSG_CUDA(cudaStreamEndCapture(st, &g));
-        if (ix.graph) {
-            TSG_CUDA(cudaStreamSynchronize(st));  // the previous batch's graph may still run
-            TSG_CUDA(cudaGraphExecDestroy(ix.graph));
-            ix.graph = nullptr;
-        }
-        TSG_CUDA(cudaGraphInstantiate(&ix.graph, g, 0));
-        TSG_CUDA(cudaGraphDestroy(g));
-        ix.graph_key = {d_queries, nq, approximate, nl, nl + static_cast<int>(nq) * (approximate ? 2 : 8)};
-        TSG_CUDA(cudaGraphLaunch(ix.graph, st));
     }
+    mark(6, [&] {
+        k_finalize<<<dim3(fin_x, nq), kThreads, 0, st>>>(iv, sv, approximate ? 1 : 0, results);
+        TSG_LAUNCHED();
+    });
     if (!marks.empty()) {
         TSG_CUDA(cudaStreamSynchronize(st));
         for (auto& m : marks) {
             float ms = 0.f;
             TSG_CUDA(cudaEventElapsedTime(&ms, m.second.first, m.second.second));
             ix.prof_ms[m.first] += ms;
-            ix.prof_launches[m.first] += 1;
+            ix.prof_launches[m.first] += nq;
             cudaEventDestroy(m.second.first);
             cudaEventDestroy(m.second.second);
         }
