@@ -1024,6 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     constexpr int kGroups = kThreads / kRowLanes;
     constexpr int n = NB * 8;
+    constexpr int kTq = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
     extern __shared__ __align__(128) unsigned char s_dyn[];
     float* s_rows = reinterpret_cast<float*>(s_dyn);                       // [kGroups][2][n]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // [n]
@@ -1034,6 +1035,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int gbase = lane & ~(kRowLanes - 1);
     const unsigned gmask = 0xFFu << gbase;
     const bool leader = j8 == 0;
+    const int hsw = (j8 >> 2) & 1;
     constexpr unsigned row_bytes = static_cast<unsigned>(n) * 4u;
     if (threadIdx.x < 2 * kGroups) mbar_init(&s_bar[threadIdx.x >> 1][threadIdx.x & 1], 1);
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1079,7 +1081,16 @@ __global__ void __launch_bounds__(kThreads, 3)
         QueryWork* wk = S.work + q;
         if (q != loaded) {
             if (loaded >= 0) leave_query(loaded);
-            load_query_f64(s_qd, queries + static_cast<uint64_t>(q) * n, n);
+            // The query widened to double in lane order: element i of lane j8's
+            // t-th block (block j8 + 8t) at [(8t + i) * 8 + j8], so the eight
+            // lanes of a group read eight consecutive doubles (no bank conflicts).
+            const float* qg = queries + static_cast<uint64_t>(q) * n;
+            for (int e = threadIdx.x; e < 8 * 8 * kTq; e += blockDim.x) {
+                const int jj = e & 7, i = (e >> 3) & 7, t = e >> 6;
+                const int k = jj + kRowLanes * t;
+                s_qd[e] = k < NB ? static_cast<double>(qg[8 * k + i]) : 0.0;
+            }
+            __syncthreads();
             loaded = q;
         }
         const uint32_t* cand_pos = S.cand_pos + q * S.cap;
@@ -1119,28 +1130,45 @@ __global__ void __launch_bounds__(kThreads, 3)
             mbar_wait(&s_bar[g][b], (phase >> b) & 1u);
             phase ^= 1u << b;
             const float* row = buf0 + b * n;
-            constexpr int kT = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
+            constexpr int kT = kTq;  // blocks per lane
             double blk[kT];
 #pragma unroll
             for (int t = 0; t < kT; ++t) {
                 const int k = j8 + kRowLanes * t;
                 blk[t] = 0.0;
                 if (k < NB) {
-                    const float4 x0 = *reinterpret_cast<const float4*>(row + 8 * k);
-                    const float4 x1 = *reinterpret_cast<const float4*>(row + 8 * k + 4);
+                    // Lanes 4-7 read the halves in the other order, so the
+                    // group's 16-byte reads of one instruction hit all 32 banks.
+                    const float4 ua = *reinterpret_cast<const float4*>(row + 8 * k + 4 * hsw);
+                    const float4 ub = *reinterpret_cast<const float4*>(row + 8 * k + 4 * (1 - hsw));
+                    const float4 x0 = hsw ? ub : ua, x1 = hsw ? ua : ub;
                     const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                    blk[t] = block_sq(x, s_qd + 8 * k, 8);
+                    double b8 = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const double d = __dsub_rn(static_cast<double>(x[i]), s_qd[(8 * t + i) * 8 + j8]);
+                        b8 = __dadd_rn(b8, __dmul_rn(d, d));
+                    }
+                    blk[t] = b8;
                 }
             }
-            // left to right over the blocks: block 8t + i lives in lane gbase + i, slot t
-            double sum = 0.0;
+            // Left to right over the blocks by the group leader: the block sums
+            // go through the row buffer just consumed (block k at double k).
+            double* sums = reinterpret_cast<double*>(buf0 + b * n);
+            __syncwarp(gmask);  // every lane has read its row slices
 #pragma unroll
             for (int t = 0; t < kT; ++t)
+                if (j8 + kRowLanes * t < NB) sums[j8 + kRowLanes * t] = blk[t];
+            __syncwarp(gmask);
+            double sum = 0.0;
+            if (leader) {
 #pragma unroll
-                for (int i = 0; i < kRowLanes; ++i) {
-                    const double v = __shfl_sync(gmask, blk[t], gbase + i);
-                    if (kRowLanes * t + i < NB) sum = __dadd_rn(sum, v);
+                for (int k = 0; k + 1 < NB; k += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(sums + k);
+                    sum = __dadd_rn(__dadd_rn(sum, v.x), v.y);
                 }
+                if (NB & 1) sum = __dadd_rn(sum, sums[NB - 1]);
+            }
             __syncwarp(gmask);  // the group is done with buffer b before it is refilled
             if (leader) {
                 const uint32_t c = s_c[j];
@@ -1232,7 +1260,8 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     auto refine_tma = n == 256 ? k_refine_tma<32> : n == 128 ? k_refine_tma<16> : n == 96 ? k_refine_tma<12>
                     : n == 64 ? k_refine_tma<8> : n == 512 ? k_refine_tma<64> : nullptr;
     const bool tma = vec && refine_tma && !std::getenv("TSG_NO_TMA_REFINE");
-    const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * 2 * n * 4 + static_cast<size_t>(n) * 8;
+    const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * 2 * n * 4 +
+                             static_cast<size_t>((n / 8 + kRowLanes - 1) / kRowLanes) * 64 * 8;
     if (tma) TSG_CUDA(cudaFuncSetAttribute(refine_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024));
     for (const void* f : {reinterpret_cast<const void*>(refine), reinterpret_cast<const void*>(seed),
                           reinterpret_cast<const void*>(lbscan), reinterpret_cast<const void*>(bound),
