@@ -863,10 +863,17 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     uint32_t chunk = 0, pre = ~0u;
     for (int q = -1;;) {
         q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
-        if (q < 0) break;
-        pre = claim_ahead(S.work, q, k_next);
+        if (q < 0 && loaded < 0) break;  // no work at all for this block
         if (q != loaded) {
-            if (loaded >= 0) leave_query();
+            // The queues carry over between chunks of one query; they are
+            // drained (with the old table still loaded) when the block moves on.
+            if (loaded >= 0) {
+                while (rt != rh) drain_runs();
+                while (qt != qh) drain_quads();
+                leave_query();
+            }
+            if (q < 0) break;
+            __syncthreads();  // every warp is done with the old table
             wk = S.work + q;
             load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
 #pragma unroll
@@ -883,6 +890,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             surv_lb = S.surv_lb + q * S.P;
             loaded = q;
         }
+        pre = claim_ahead(S.work, q, k_next);
         const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
         const uint64_t t0 = static_cast<uint64_t>(chunk) * kTripChunk + warp * kTripPerWarp;
         const uint64_t t1 = u64min(t0 + kTripPerWarp, ntrip);
@@ -897,7 +905,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
                 bh[h] = nbh[h];
             }
             if (T + 1 < t1) fetch(T + 1);
-            const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
+            const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;  // run box
             pruned += valid && !pass ? 1 : 0;
             const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
             if (pass)
@@ -907,10 +915,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             __syncwarp();
             while (rt - rh >= 8) drain_runs();
         }
-        while (rt != rh) drain_runs();
-        while (qt != qh) drain_quads();
     }
-    if (loaded >= 0) leave_query();
 }
 
 // ------------------------------------------------------------ refine
