@@ -69,7 +69,7 @@ struct DevIndex {
     float* queries = nullptr;      // staging for host queries
     uint32_t queries_cap = 0;
     int sms = 148;
-    float refine_split = 0.5f;     // wave-0 page-bound fraction of the seed bound (TSG_REFINE_SPLIT)
+    float refine_split = 0.3f;     // wave-0 page-bound fraction of the seed bound (TSG_REFINE_SPLIT)
     // per-kernel profiling (tsg_profile_enable)
     bool profile = false;
     double prof_ms[8] = {0};
