@@ -355,6 +355,19 @@ __device__ __forceinline__ int claim(QueryWork* work, int nq, int k, int& cur, u
     return r;
 }
 
+// Thread 0: the first query from `cur` on whose chunk counter `k` has work
+// left (-1 if none); takes no chunk (the block's warps claim their own).
+template <typename NChunks>
+__device__ __forceinline__ int select_query(QueryWork* work, int nq, int k, int cur, NChunks nchunks) {
+    int q = cur;
+    for (int tries = 0; tries < nq; ++tries) {
+        QueryWork* wk = work + q;
+        if (ld_volatile_u32(&wk->next[k]) < nchunks(wk)) return q;
+        q = q + 1 == nq ? 0 : q + 1;
+    }
+    return -1;
+}
+
 // Thread 0 reserves the block's next chunk of query q (read by the next claim).
 __device__ __forceinline__ uint32_t claim_ahead(QueryWork* work, int q, int k) {
     return threadIdx.x == 0 ? atomicAdd(&work[q].next[k], 1u) : ~0u;
@@ -656,8 +669,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
-constexpr int kTripPerWarp = 4;                      // page triples per warp per chunk
-constexpr uint32_t kTripChunk = kWarps * kTripPerWarp;  // page triples per chunk
+#ifndef TSG_TRIP_PER_WARP
+#define TSG_TRIP_PER_WARP 8
+#endif
+constexpr int kTripPerWarp = TSG_TRIP_PER_WARP;      // page triples per warp per chunk
 
 // Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
 // upward after the seed range, wave B downward from the top of the slot's
@@ -699,7 +714,7 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
     __syncwarp();
 }
 
-// One page wave (persistent, affinity chunks of kTripChunk page triples):
+// One page wave (persistent; warps claim chunks of kTripPerWarp page triples):
 // wave 0 scans surv[0, nsurv), wave 1 surv[P - nsurv_hi, P) re-filtered
 // against the BSF that refinement wave A tightened. Below the page sit two
 // more box levels over the sorted words, aligned kRun-entry runs and
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
     const int grp = lane / 10, t = lane - 10 * grp;  // page of the triple, run of the page (lanes 30, 31 idle)
-    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
     float bound = 0.f, cut = 0.f;
     uint32_t nsurv = 0;
@@ -744,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     auto nchunks = [wave](const QueryWork* w) -> uint32_t {
         if (w->overflow) return 0;
         const uint32_t ns = wave == 0 ? w->nsurv : w->nsurv_hi;
-        return ((ns + 2) / 3 + kTripChunk - 1) / kTripChunk;
+        return ((ns + 2) / 3 + kTripPerWarp - 1) / kTripPerWarp;
     };
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
         if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
@@ -860,61 +875,68 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         }
     };
 
-    uint32_t chunk = 0, pre = ~0u;
-    for (int q = -1;;) {
-        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
-        if (q < 0 && loaded < 0) break;  // no work at all for this block
-        if (q != loaded) {
-            // The queues carry over between chunks of one query; they are
-            // drained (with the old table still loaded) when the block moves on.
-            if (loaded >= 0) {
-                while (rt != rh) drain_runs();
-                while (qt != qh) drain_quads();
-                leave_query();
-            }
-            if (q < 0) break;
-            __syncthreads();  // every warp is done with the old table
-            wk = S.work + q;
-            load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
+    // Query loop (block level; the only barriers): pick a query with chunks
+    // left, load its table; then every warp claims chunks of it on its own
+    // (lane 0, the next claim issued while the current chunk runs) until it
+    // is exhausted, drains its queues and flushes its stage.
+    __shared__ int s_sel;
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous table
+        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
+        __syncthreads();
+        const int q = s_sel;
+        if (q < 0) break;
+        cur = q;
+        wk = S.work + q;
+        load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
 #pragma unroll
-            for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
-            bound = bound_from_bits(wk->bsf_bits);
-            // Page wave 0 splits its candidates into refinement waves A and B
-            // by their own bound; page wave 1 (scanned after wave A is
-            // refined) feeds wave B.
-            cut = wave == 0 ? wk->scan_bound * ix.split : -1.f;
-            nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
-            cand_pos = S.cand_pos + q * S.cap;
-            cand_lb = S.cand_lb + q * S.cap;
-            surv = S.surv + q * S.P;
-            surv_lb = S.surv_lb + q * S.P;
-            loaded = q;
-        }
-        pre = claim_ahead(S.work, q, k_next);
+        for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+        bound = bound_from_bits(wk->bsf_bits);
+        // Page wave 0 splits its candidates into refinement waves A and B by
+        // their own bound; page wave 1 (scanned after wave A is refined)
+        // feeds wave B.
+        cut = wave == 0 ? wk->scan_bound * ix.split : -1.f;
+        nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
+        cand_pos = S.cand_pos + q * S.cap;
+        cand_lb = S.cand_lb + q * S.cap;
+        surv = S.surv + q * S.P;
+        surv_lb = S.surv_lb + q * S.P;
         const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
-        const uint64_t t0 = static_cast<uint64_t>(chunk) * kTripChunk + warp * kTripPerWarp;
-        const uint64_t t1 = u64min(t0 + kTripPerWarp, ntrip);
-        if (t0 < t1) fetch(t0);
-        for (uint64_t T = t0; T < t1; ++T) {
-            const uint32_t a = na, b = nb, r = nrun;
-            const bool valid = nvalid;
-            uint4 bl[H], bh[H];
+        const uint32_t nch = nchunks(wk);
+        uint32_t chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
+        chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+        while (chunk < nch) {
+            uint32_t pre = 0;
+            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
+            const uint64_t t0 = static_cast<uint64_t>(chunk) * kTripPerWarp;
+            const uint64_t t1 = u64min(t0 + kTripPerWarp, ntrip);
+            if (t0 < t1) fetch(t0);
+            for (uint64_t T = t0; T < t1; ++T) {
+                const uint32_t a = na, b = nb, r = nrun;
+                const bool valid = nvalid;
+                uint4 bl[H], bh[H];
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                bl[h] = nbl[h];
-                bh[h] = nbh[h];
+                for (int h = 0; h < H; ++h) {
+                    bl[h] = nbl[h];
+                    bh[h] = nbh[h];
+                }
+                if (T + 1 < t1) fetch(T + 1);
+                const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;  // run box
+                pruned += valid && !pass ? 1 : 0;
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+                if (pass)
+                    s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] =
+                        make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
+                rt += __popc(m);
+                __syncwarp();
+                while (rt - rh >= 8) drain_runs();
             }
-            if (T + 1 < t1) fetch(T + 1);
-            const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;  // run box
-            pruned += valid && !pass ? 1 : 0;
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-            if (pass)
-                s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] =
-                    make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
-            rt += __popc(m);
-            __syncwarp();
-            while (rt - rh >= 8) drain_runs();
+            chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
         }
+        while (rt != rh) drain_runs();
+        while (qt != qh) drain_quads();
+        leave_query();
     }
 }
 
@@ -1010,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
     if (loaded >= 0) leave_query(loaded);
 }
 
-// Refinement with TMA row staging (n % 8 == 0, n <= kTmaMaxN): per chunk of
+// Refinement with TMA row staging (n % 8 == 0, n in {64, 96, 128, 256, 512}): per chunk of
 // kTmaChunk candidate records the block first keeps those whose bound is
 // within the BSF (compacted in shared memory, row positions gathered by all
 // threads at once); then each 8-lane group walks the kept rows with two
@@ -1020,8 +1042,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
 // are the same blocked FP64 sums in squared_l2's order as group_row_sq
 // (whole rows: an abandoned sum only ever exceeds the BSF, so computing it
 // in full changes no answer).
-constexpr int kTmaMaxN = 512;
-constexpr uint32_t kTmaChunk = 512;
+#ifndef TSG_TMA_CHUNK
+#define TSG_TMA_CHUNK 512
+#endif
+constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;
 
 // NB = n / 8 blocks per row, a compile-time constant so the row sum unrolls.
 template <int NB>
