@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
 #ifndef TSG_TRIP_PER_WARP
-#define TSG_TRIP_PER_WARP 8
+#define TSG_TRIP_PER_WARP 4
 #endif
 constexpr int kTripPerWarp = TSG_TRIP_PER_WARP;      // page triples per warp per chunk
 
@@ -1032,35 +1032,38 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
     if (loaded >= 0) leave_query(loaded);
 }
 
-// Refinement with TMA row staging (n % 8 == 0, n in {64, 96, 128, 256, 512}): per chunk of
-// kTmaChunk candidate records the block first keeps those whose bound is
-// within the BSF (compacted in shared memory, row positions gathered by all
-// threads at once); then each 8-lane group walks the kept rows with two
-// shared-memory row buffers: while it sums row j from one buffer, a 1-D bulk
-// copy (cp.async.bulk, mbarrier-tracked) brings row j + 32 into the other, so
-// the row fetch overlaps the FP64 arithmetic instead of stalling it. Sums
-// are the same blocked FP64 sums in squared_l2's order as group_row_sq
-// (whole rows: an abandoned sum only ever exceeds the BSF, so computing it
-// in full changes no answer).
+// Refinement with TMA row staging (n % 8 == 0, n in {64, 96, 128, 256, 512}).
+// Blocks pick a query (barriers only when switching); each warp then claims
+// chunks of kTmaChunk candidate records of it on its own: lanes keep the
+// records whose bound is within the BSF (ballot compaction into the warp's
+// list, row positions gathered by all 32 lanes at once), and the warp's four
+// 8-lane groups walk the kept rows with two shared-memory row buffers each:
+// while a group sums row j from one buffer, a 1-D bulk copy (cp.async.bulk,
+// mbarrier-tracked) brings its next row into the other, so the row fetch
+// overlaps the FP64 arithmetic. Sums are the blocked FP64 sums in
+// squared_l2's order (whole rows: an abandoned sum only ever exceeds the
+// BSF, so computing it in full changes no answer).
 #ifndef TSG_TMA_CHUNK
-#define TSG_TMA_CHUNK 512
+#define TSG_TMA_CHUNK 64
 #endif
-constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;
+constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;  // candidate records per warp chunk
 
 // NB = n / 8 blocks per row, a compile-time constant so the row sum unrolls.
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 3)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     constexpr int kGroups = kThreads / kRowLanes;
+    constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
     constexpr int kTq = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
     extern __shared__ __align__(128) unsigned char s_dyn[];
-    float* s_rows = reinterpret_cast<float*>(s_dyn);                       // [kGroups][2][n]
-    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // [n]
+    float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][2][n]
+    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // lane-ordered query
     __shared__ __align__(8) uint64_t s_bar[kGroups][2];
-    __shared__ uint32_t s_c[kTmaChunk], s_p[kTmaChunk];
-    __shared__ uint32_t s_m;
-    const int lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
+    __shared__ uint32_t s_c[kWarps][kTmaChunk], s_p[kWarps][kTmaChunk];
+    __shared__ int s_sel;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
+    const int wg = lane / kRowLanes;  // group within the warp
     const int gbase = lane & ~(kRowLanes - 1);
     const unsigned gmask = 0xFFu << gbase;
     const bool leader = j8 == 0;
@@ -1071,7 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     __syncthreads();
     unsigned phase = 0;  // bit b: parity of this group's buffer b
     float* buf0 = s_rows + static_cast<size_t>(g) * 2 * n;
-    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     unsigned long long refined = 0, updates = 0;
     const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
     auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
@@ -1090,125 +1093,123 @@ __global__ void __launch_bounds__(kThreads, 3)
         range(w, b, e);
         return static_cast<uint32_t>((e - b + kTmaChunk - 1) / kTmaChunk);
     };
-    auto leave_query = [&](int q) {
-        if (leader) {
-            if (refined) atomicAdd(&S.work[q].stats[kRealDist], refined);
-            if (updates) atomicAdd(&S.work[q].stats[kBsfUpd], updates);
-        }
-        refined = updates = 0;
-    };
     auto issue = [&](int b, uint32_t p) {  // leader: row p -> this group's buffer b
         fence_proxy_async_smem();
         mbar_expect_tx(&s_bar[g][b], row_bytes);
         tma_copy_1d(buf0 + b * n, ix.rows + static_cast<uint64_t>(p) * n, row_bytes, &s_bar[g][b]);
     };
-    uint32_t chunk = 0, pre = ~0u;
-    for (int q = -1;;) {
-        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous query
+        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
+        __syncthreads();
+        const int q = s_sel;
         if (q < 0) break;
-        pre = claim_ahead(S.work, q, k_next);
+        cur = q;
         QueryWork* wk = S.work + q;
-        if (q != loaded) {
-            if (loaded >= 0) leave_query(loaded);
-            // The query widened to double in lane order: element i of lane j8's
-            // t-th block (block j8 + 8t) at [(8t + i) * 8 + j8], so the eight
-            // lanes of a group read eight consecutive doubles (no bank conflicts).
-            const float* qg = queries + static_cast<uint64_t>(q) * n;
-            for (int e = threadIdx.x; e < 8 * 8 * kTq; e += blockDim.x) {
-                const int jj = e & 7, i = (e >> 3) & 7, t = e >> 6;
-                const int k = jj + kRowLanes * t;
-                s_qd[e] = k < NB ? static_cast<double>(qg[8 * k + i]) : 0.0;
-            }
-            __syncthreads();
-            loaded = q;
+        // The query widened to double in lane order: element i of lane j8's
+        // t-th block (block j8 + 8t) at [(8t + i) * 8 + j8], so the eight
+        // lanes of a group read eight consecutive doubles (no bank conflicts).
+        const float* qg = queries + static_cast<uint64_t>(q) * n;
+        for (int e = threadIdx.x; e < 8 * 8 * kTq; e += blockDim.x) {
+            const int jj = e & 7, i = (e >> 3) & 7, t = e >> 6;
+            const int k = jj + kRowLanes * t;
+            s_qd[e] = k < NB ? static_cast<double>(qg[8 * k + i]) : 0.0;
         }
+        __syncthreads();
         const uint32_t* cand_pos = S.cand_pos + q * S.cap;
         const float* cand_lb = S.cand_lb + q * S.cap;
         double* cand_sq = S.cand_sq + q * S.cap;
         uint64_t begin, end;
         range(wk, begin, end);
-        const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kTmaChunk;
-        const uint64_t c1 = u64min(c0 + kTmaChunk, end);
-        // Phase 1: keep the records whose bound is within the BSF.
-        if (threadIdx.x == 0) s_m = 0;
-        __syncthreads();
-        const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
-        for (uint32_t i0 = 0; i0 < kTmaChunk; i0 += kThreads) {
-            const uint64_t c = c0 + i0 + threadIdx.x;
-            const bool in = c < c1;
-            const bool keep = in && cand_lb[c] <= bnd;
-            if (in && !keep) cand_sq[c] = INFINITY;
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
-            uint32_t base = 0;
-            if (lane == 0 && m) base = atomicAdd(&s_m, static_cast<unsigned>(__popc(m)));
-            base = __shfl_sync(0xFFFFFFFFu, base, 0);
-            if (keep) {
-                const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
-                s_c[slot] = static_cast<uint32_t>(c);
-                s_p[slot] = ix.pos[cand_pos[c]];  // candidate records hold index-order entries
+        const uint32_t nch = nchunks(wk);
+        uint32_t chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
+        chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+        while (chunk < nch) {
+            uint32_t pre = 0;
+            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
+            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kTmaChunk;
+            const uint64_t c1 = u64min(c0 + kTmaChunk, end);
+            // Phase 1 (warp): keep the records whose bound is within the BSF.
+            const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            uint32_t m = 0;
+#pragma unroll
+            for (uint32_t i0 = 0; i0 < kTmaChunk; i0 += 32) {
+                const uint64_t c = c0 + i0 + lane;
+                const bool in = c < c1;
+                const bool keep = in && cand_lb[c] <= bnd;
+                if (in && !keep) cand_sq[c] = INFINITY;
+                const unsigned mk = __ballot_sync(0xFFFFFFFFu, keep);
+                if (keep) {
+                    const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
+                    s_c[warp][slot] = static_cast<uint32_t>(c);
+                    s_p[warp][slot] = ix.pos[cand_pos[c]];  // candidate records hold index-order entries
+                }
+                m += __popc(mk);
             }
-        }
-        __syncthreads();
-        const uint32_t m = s_m;
-        // Phase 2: the kept rows, double-buffered per group.
-        if (leader && static_cast<uint32_t>(g) < m) issue(0, s_p[g]);
-        int b = 0;
-        for (uint32_t j = g; j < m; j += kGroups, b ^= 1) {
-            if (leader && j + kGroups < m) issue(b ^ 1, s_p[j + kGroups]);
-            const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
-            mbar_wait(&s_bar[g][b], (phase >> b) & 1u);
-            phase ^= 1u << b;
-            const float* row = buf0 + b * n;
-            constexpr int kT = kTq;  // blocks per lane
-            double blk[kT];
+            __syncwarp();
+            // Phase 2: the kept rows, double-buffered per group.
+            if (leader && static_cast<uint32_t>(wg) < m) issue(0, s_p[warp][wg]);
+            int b = 0;
+            for (uint32_t j = wg; j < m; j += kWarpGroups, b ^= 1) {
+                if (leader && j + kWarpGroups < m) issue(b ^ 1, s_p[warp][j + kWarpGroups]);
+                const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
+                mbar_wait(&s_bar[g][b], (phase >> b) & 1u);
+                phase ^= 1u << b;
+                const float* row = buf0 + b * n;
+                double blk[kTq];
 #pragma unroll
-            for (int t = 0; t < kT; ++t) {
-                const int k = j8 + kRowLanes * t;
-                blk[t] = 0.0;
-                if (k < NB) {
-                    // Lanes 4-7 read the halves in the other order, so the
-                    // group's 16-byte reads of one instruction hit all 32 banks.
-                    const float4 ua = *reinterpret_cast<const float4*>(row + 8 * k + 4 * hsw);
-                    const float4 ub = *reinterpret_cast<const float4*>(row + 8 * k + 4 * (1 - hsw));
-                    const float4 x0 = hsw ? ub : ua, x1 = hsw ? ua : ub;
-                    const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-                    double b8 = 0.0;
+                for (int t = 0; t < kTq; ++t) {
+                    const int k = j8 + kRowLanes * t;
+                    blk[t] = 0.0;
+                    if (k < NB) {
+                        // Lanes 4-7 read the halves in the other order, so the
+                        // group's 16-byte reads of one instruction hit all 32 banks.
+                        const float4 ua = *reinterpret_cast<const float4*>(row + 8 * k + 4 * hsw);
+                        const float4 ub = *reinterpret_cast<const float4*>(row + 8 * k + 4 * (1 - hsw));
+                        const float4 x0 = hsw ? ub : ua, x1 = hsw ? ua : ub;
+                        const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                        double b8 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const double d = __dsub_rn(static_cast<double>(x[i]), s_qd[(8 * t + i) * 8 + j8]);
-                        b8 = __dadd_rn(b8, __dmul_rn(d, d));
+                        for (int i = 0; i < 8; ++i) {
+                            const double d = __dsub_rn(static_cast<double>(x[i]), s_qd[(8 * t + i) * 8 + j8]);
+                            b8 = __dadd_rn(b8, __dmul_rn(d, d));
+                        }
+                        blk[t] = b8;
                     }
-                    blk[t] = b8;
                 }
-            }
-            // Left to right over the blocks by the group leader: the block sums
-            // go through the row buffer just consumed (block k at double k).
-            double* sums = reinterpret_cast<double*>(buf0 + b * n);
-            __syncwarp(gmask);  // every lane has read its row slices
+                // Left to right over the blocks by the group leader: the block
+                // sums go through the row buffer just consumed (block k at double k).
+                double* sums = reinterpret_cast<double*>(buf0 + b * n);
+                __syncwarp(gmask);  // every lane has read its row slices
 #pragma unroll
-            for (int t = 0; t < kT; ++t)
-                if (j8 + kRowLanes * t < NB) sums[j8 + kRowLanes * t] = blk[t];
-            __syncwarp(gmask);
-            double sum = 0.0;
-            if (leader) {
+                for (int t = 0; t < kTq; ++t)
+                    if (j8 + kRowLanes * t < NB) sums[j8 + kRowLanes * t] = blk[t];
+                __syncwarp(gmask);
+                if (leader) {
+                    double sum = 0.0;
 #pragma unroll
-                for (int k = 0; k + 1 < NB; k += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(sums + k);
-                    sum = __dadd_rn(__dadd_rn(sum, v.x), v.y);
+                    for (int k = 0; k + 1 < NB; k += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(sums + k);
+                        sum = __dadd_rn(__dadd_rn(sum, v.x), v.y);
+                    }
+                    if (NB & 1) sum = __dadd_rn(sum, sums[NB - 1]);
+                    cand_sq[s_c[warp][j]] = sum;
+                    refined += 1;
+                    const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
+                    if (sb < seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
                 }
-                if (NB & 1) sum = __dadd_rn(sum, sums[NB - 1]);
+                __syncwarp(gmask);  // the group is done with buffer b before it is refilled
             }
-            __syncwarp(gmask);  // the group is done with buffer b before it is refilled
-            if (leader) {
-                const uint32_t c = s_c[j];
-                cand_sq[c] = sum;
-                refined += 1;
-                const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
-                if (sb < seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
-            }
+            __syncwarp();  // the warp's list is reused by the next chunk
+            chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
         }
+        if (leader) {
+            if (refined) atomicAdd(&wk->stats[kRealDist], refined);
+            if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+        }
+        refined = updates = 0;
     }
-    if (loaded >= 0) leave_query(loaded);
 }
 
 // ----------------------------------------------------------- finalize
