@@ -59,6 +59,29 @@ def peaks():
     return 6650.0, "fallback"
 
 
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "round1b_ncu_summary.json")
+NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tma.ncu-rep"],
+               "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
+
+
+def ncu_traffic(kernel, nq):
+    """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per batch (all its launches of one
+    batch: both waves for lbscan / refine), from the committed `ncu --set full` capture of the c2
+    bench command (profiles/ncu_round1b.sh); None when the capture does not match this run."""
+    if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
+        return None
+    with open(NCU_SUMMARY) as f:
+        reps = json.load(f)["reports"]
+    total = 0.0
+    for name in NCU_REPORTS[kernel]:
+        recs = reps.get(name)
+        if not recs:
+            return None
+        total += sum(r.get("dram_read_MB", 0.0) + r.get("dram_write_MB", 0.0) for r in recs)
+    per = "launch" if kernel == "summarise" else f"batch of {nq} queries (all of the batch's launches)"
+    return {"bytes": round(total * 1e6), "per": per, "source": os.path.relpath(NCU_SUMMARY, ROOT)}
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -304,7 +327,7 @@ def run_ours(args):
                 for r in res:
                     s = r.stats
                     stats += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
-                              s.pruned_subtrees, s.queue_insertions)
+                              s.pruned_subtrees, s.queue_insertions, r.box_calcs)
         return max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
 
     # warm-up
@@ -316,7 +339,7 @@ def run_ours(args):
     # Each call is synchronous (results come back to the host per batch): the
     # event pair measures the K batches plus the per-batch result D2H.
     launches0 = tg.launch_count()
-    stats_acc = np.zeros(6, np.float64)
+    stats_acc = np.zeros(7, np.float64)
     answers = []
     with Clocks(local) as clk:
         elapsed = timed(False, stats_acc, answers)
@@ -345,17 +368,23 @@ def run_ours(args):
     P = bs.pages
     # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize
     groups = {"bound": [1], "seed": [2], "lbscan": [4], "refine": [3, 5], "finalize": [6]}
-    lb_entries, refined, cands = stats_acc[1], stats_acc[2], stats_acc[5]
-    group_bytes = {  # algorithmic bytes over the profiled pass (SURVEY §8(d) per-unit figures x units)
-        "bound": nqt * P * (2 * ws + 8),            # two 16-byte page boxes + offsets per page
-        "lbscan": lb_entries * ws + cands * 12,     # words of surviving pages + candidate records
-        "refine": refined * 4 * n + cands * 16,     # candidate rows (full length; abandonment reads less)
+    lb_nodes, lb_entries, refined, cands, boxes = stats_acc[0], stats_acc[1], stats_acc[2], stats_acc[5], stats_acc[6]
+    NG = (P + 7) // 8
+    group_bytes = {  # algorithmic bytes over the timed pass (per-unit figures of DESIGN.md §4 x the counters)
+        # every group box (2 x 16 B) + the pages of surviving groups (2 x 16 B boxes + 8 B offsets)
+        "bound": nqt * NG * 2 * ws + max(lb_nodes - nqt * NG, 0) * (2 * ws + 8),
+        # run / quad boxes (2 x 16 B) + words of surviving quads + candidate records (pos + bound)
+        "lbscan": boxes * 2 * ws + lb_entries * ws + cands * 8,
+        # kept candidate rows (full length) + their records (bound, entry, pos gather, sum)
+        "refine": refined * 4 * n + cands * 20,
     }
     group_ms = {g: sum(prof_ms[k] for k in ks) for g, ks in groups.items()}
     dom = max(group_ms, key=group_ms.get)
     dom_ms = group_ms[dom] / nqt  # per query (each group runs once per query per rank)
     dom_bytes = group_bytes.get(dom, 0.0) / nqt
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    # DRAM bytes per batch of the same kernel from the committed ncu capture (c2, 1 GPU only)
+    traffic = ncu_traffic(dom, nq) if args.config == "c2" and world == 1 and nq == 100 else None
 
     # build K1 roofline: read 4n, write the 16-byte word + 8-byte sort key per series
     k1_bytes = count * (4 * n + 16 + 8) / world
@@ -387,7 +416,10 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                          "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "frac": round(achieved / hbm, 4),
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_batch": round(dom_bytes * nq),
+                         "batch_queries": nq,
                          "share_of_query_time": round(share, 4),
                          "per_kernel_ms": {g: round(v, 3) for g, v in group_ms.items()},
                          "per_kernel_us_per_query": {g: round(v * 1e3 / nqt, 2) for g, v in group_ms.items()},
@@ -398,7 +430,8 @@ def run_ours(args):
                                    "leaves": round(bs.leaves_ms, 3)},
                       "roofline": {"bound": "hbm", "kernel": "summarise (K1)", "achieved": round(k1_gbs, 1),
                                    "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                                   "frac": round(k1_gbs / hbm, 4), "traffic": None,
+                                   "frac": round(k1_gbs / hbm, 4),
+                                   "traffic": ncu_traffic("summarise", nq) if args.config == "c2" and world == 1 else None,
                                    "algorithmic_bytes_per_series": 4 * n + 24},
                       "whole_build_frac": round(algo_build / build_dev_s / 1e9 / hbm / world, 4),
                       "leaves": bs.leaves, "pages": P, "root_children": bs.root_children, "max_depth": bs.max_depth,

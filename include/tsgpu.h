@@ -101,7 +101,7 @@ typedef struct tsg_search_stats {
 typedef struct tsg_result {
     double distance;
     uint32_t position;
-    uint32_t reserved;
+    uint32_t box_calcs;  /* sub-page (run / quad) box bounds evaluated (saturates at 2^32-1) */
     tsg_search_stats stats;
 } tsg_result;
 

@@ -49,7 +49,7 @@ class tsg_search_stats(C.Structure):
 
 
 class tsg_result(C.Structure):
-    _fields_ = [("distance", C.c_double), ("position", C.c_uint32), ("reserved", C.c_uint32),
+    _fields_ = [("distance", C.c_double), ("position", C.c_uint32), ("box_calcs", C.c_uint32),
                 ("stats", tsg_search_stats)]
 
 

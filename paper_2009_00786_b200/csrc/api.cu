@@ -288,7 +288,7 @@ void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, Dev
 void to_result(const DevResult& d, tsg_result& r) {
     r.distance = d.distance;
     r.position = d.position;
-    r.reserved = 0;
+    r.box_calcs = static_cast<uint32_t>(std::min<unsigned long long>(d.boxes, 0xFFFFFFFFull));
     r.stats.lb_node_calcs = d.stats[0];
     r.stats.lb_entry_calcs = d.stats[1];
     r.stats.real_dist_calcs = d.stats[2];
@@ -306,8 +306,10 @@ void merge_into(tsg_result& acc, const tsg_result& r, bool first) {
     }
     if (first) {
         acc.stats = r.stats;
+        acc.box_calcs = r.box_calcs;
         return;
     }
+    acc.box_calcs = static_cast<uint32_t>(std::min<uint64_t>(0xFFFFFFFFull, uint64_t{acc.box_calcs} + r.box_calcs));
     acc.stats.lb_node_calcs += r.stats.lb_node_calcs;
     acc.stats.lb_entry_calcs += r.stats.lb_entry_calcs;
     acc.stats.real_dist_calcs += r.stats.real_dist_calcs;

@@ -98,6 +98,7 @@ struct QueryWork {
     unsigned int best_pos;
     unsigned int overflow;              // candidates outgrew the slot: rerun in the big slot
     float scan_bound;                   // BSF bound the page/word filters used
+    unsigned long long boxes;           // run / quad box bounds evaluated
     unsigned long long stats[6];  // SearchStats order
     unsigned char qsym[32];
 };
@@ -109,6 +110,7 @@ struct DevResult {
     uint32_t position;
     uint32_t flags;
     unsigned long long stats[6];
+    unsigned long long boxes;
 };
 
 // K1

@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->best_pos = 0xFFFFFFFFu;
         wk->overflow = (b - a) > S.cap ? 1u : 0u;
         wk->scan_bound = 0.f;
+        wk->boxes = 0;
         for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
         wk->stats[kRealDist] = b - a;
     }
@@ -754,7 +755,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     const float* surv_lb = nullptr;
     int cnt = 0;
     uint32_t rh = 0, rt = 0, qh = 0, qt = 0;  // ring heads / tails (warp-uniform)
-    unsigned long long scanned = 0, pruned = 0;
+    unsigned long long scanned = 0, pruned = 0, boxes = 0;
     const int k_next = wave == 0 ? kNextScan0 : kNextScan1;
     auto nchunks = [wave](const QueryWork* w) -> uint32_t {
         if (w->overflow) return 0;
@@ -766,11 +767,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         cnt = 0;
         scanned = warp_sum(scanned);
         pruned = warp_sum(pruned);
+        boxes = warp_sum(boxes);
         if (lane == 0) {
             if (scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
             if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
+            if (boxes) atomicAdd(&wk->boxes, boxes);
         }
-        scanned = pruned = 0;
+        scanned = pruned = boxes = 0;
     };
 
     auto stage = [&](bool pass, uint32_t e, float lb) {
@@ -839,6 +842,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         rh += take;
         const bool pass = ok && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
         pruned += ok && !pass ? 1 : 0;
+        boxes += ok ? 1 : 0;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
         if (pass) s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
         qt += __popc(m);
@@ -924,6 +928,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
                 if (T + 1 < t1) fetch(T + 1);
                 const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;  // run box
                 pruned += valid && !pass ? 1 : 0;
+                boxes += valid ? 1 : 0;
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
                 if (pass)
                     s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] =
@@ -1258,6 +1263,7 @@ __global__ void __launch_bounds__(kThreads)
     out->stats[kBsfUpd] = wk->stats[kBsfUpd];
     out->stats[kPruned] = wk->stats[kPruned];
     out->stats[kQueueIns] = (cand & 0xFFFFFFFFull) - wk->nseed + (cand >> 32);
+    out->boxes = wk->boxes;
 }
 
 template <typename K>

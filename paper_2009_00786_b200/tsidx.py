@@ -116,6 +116,7 @@ class SearchResult:
     distance: float
     position: int
     stats: SearchStats
+    box_calcs: int = 0  # sub-page (run / quad) box bounds evaluated (device extension of SearchStats)
 
 
 @dataclasses.dataclass
@@ -147,7 +148,7 @@ def _stats_from_c(s: _lib.tsg_build_stats) -> BuildStats:
 
 def _result_from_c(r: _lib.tsg_result) -> SearchResult:
     st = SearchStats(**{f: getattr(r.stats, f) for f, _ in _lib.tsg_search_stats._fields_})
-    return SearchResult(float(r.distance), int(r.position), st)
+    return SearchResult(float(r.distance), int(r.position), st, int(r.box_calcs))
 
 
 class Context:

@@ -62,24 +62,40 @@ def read_report(path):
     return out
 
 
+SETUP = ("k_generate",)  # input generation: untimed setup
+QUERY = ("k_prepare", "k_seed", "k_groups", "k_bound", "k_lbscan", "k_refine", "k_refine_tma", "k_finalize")
+
+
 def read_launches(path):
-    per = defaultdict(lambda: {"launches": 0, "total_us": 0.0})
+    per = defaultdict(lambda: {"launches": 0, "total_us": 0.0, "dram_MB": 0.0})
     with open(path) as f:
         lines = [l for l in f if l.startswith('"')]
     rows = list(csv.reader(lines))
     hdr = rows[0]
     ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     for r in rows[1:]:
-        if r[mi] != "gpu__time_duration.sum":
-            continue
         name = r[ki].replace("void ", "").replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
-        name = name.split("(")[0].split("<")[0].strip()
-        v = float(r[vi].replace(",", "")) * UNIT_SCALE.get(r[ui], 1.0)
-        per[name]["launches"] += 1
-        per[name]["total_us"] += v
-    tot = sum(p["total_us"] for p in per.values()) or 1.0
-    return {k: {**v, "total_us": round(v["total_us"], 1), "share": round(v["total_us"] / tot, 4)}
-            for k, v in sorted(per.items(), key=lambda kv: -kv[1]["total_us"])}
+        name = name.split("(")[0].split("<")[0].strip().split("::")[-1]
+        try:
+            v = float(r[vi].replace(",", ""))
+        except ValueError:
+            continue
+        if r[mi] == "gpu__time_duration.sum":
+            per[name]["launches"] += 1
+            per[name]["total_us"] += v * UNIT_SCALE.get(r[ui], 1.0)
+        elif r[mi].startswith("dram__bytes"):
+            per[name]["dram_MB"] += v * UNIT_SCALE.get(r[ui], 1e-6)
+    tot = sum(p["total_us"] for k, p in per.items() if k not in SETUP) or 1.0
+    qtot = sum(p["total_us"] for k, p in per.items() if k in QUERY) or 1.0
+    out = {}
+    for k, v in sorted(per.items(), key=lambda kv: -kv[1]["total_us"]):
+        rec = {"launches": v["launches"], "total_us": round(v["total_us"], 1), "dram_MB": round(v["dram_MB"], 1)}
+        if k not in SETUP:
+            rec["share_excl_setup"] = round(v["total_us"] / tot, 4)
+        if k in QUERY:
+            rec["share_of_query"] = round(v["total_us"] / qtot, 4)
+        out[k] = rec
+    return out
 
 
 def main():
@@ -103,9 +119,9 @@ def main():
             lines.append("- " + ", ".join(f"{k}={v}" for k, v in r.items()))
         lines.append("")
     if launches:
-        lines.append("## launch list (gpu__time_duration.sum, cold-cache, serialised)")
+        lines.append("## launch list (gpu__time_duration.sum + DRAM bytes, cold-cache, serialised)")
         for k, v in summary["launch_list"].items():
-            lines.append(f"- {k}: {v['launches']} launches, {v['total_us']} us, share {v['share']}")
+            lines.append(f"- {k}: " + ", ".join(f"{a}={b}" for a, b in v.items()))
     with open(os.path.join(here, f"{rnd}_ncu_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
