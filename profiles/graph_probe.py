@@ -1,9 +1,8 @@
-"""One c2 query batch as a CUDA graph, for whole-batch ncu metrics.
+"""One c2 query batch for ncu (profiles/ncu_kernels.sh, ncu_full_kernel.sh).
 
-The lanes' kernels run concurrently, which per-kernel ncu replay serialises;
-with TSG_GRAPHS=1 the batch is one graph and `ncu --graph-profiling graph
---profile-from-start off` measures it as a single workload (profiles/ncu_graph.sh).
-The profiler range brackets a replay of the captured graph only.
+Builds the c2 index (device-generated data), runs one warm-up batch, then
+brackets a second batch with cudaProfilerStart/Stop, so
+`ncu --profile-from-start off` sees only that batch's nine launches.
 """
 import os
 import sys
@@ -18,10 +17,10 @@ NQ = int(os.environ.get("PROBE_NQ", 100))
 rows = tg.generate_device("rw", N, 256, 1)
 index = tg.build_index(rows, tg.IndexConfig(n=256))
 queries = tg.generate_device("rw", NQ, 256, 2, begin=N)
-tg.exact_search_batch(index, queries)  # capture + first launch
+tg.exact_search_batch(index, queries)  # warm-up
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-res = tg.exact_search_batch(index, queries)  # replay
+res = tg.exact_search_batch(index, queries)  # profiled
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("first answer", res[0].distance, res[0].position)
