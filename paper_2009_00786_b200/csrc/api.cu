@@ -9,6 +9,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -244,7 +245,10 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     const uint64_t fixed = per_slot_fixed * s.batch_max;
     const uint64_t cand_budget = budget > fixed ? budget - fixed : 0;
     const uint64_t min_cap = std::min<uint64_t>(N, std::max<uint64_t>(1u << 20, 2 * s.leaf_cap));
-    const uint64_t cap = std::min<uint64_t>(N, std::max<uint64_t>(min_cap, cand_budget / (16ull * s.batch_max)));
+    uint64_t cap = std::min<uint64_t>(N, std::max<uint64_t>(min_cap, cand_budget / (16ull * s.batch_max)));
+    // TSG_SLOT_CAP (tests): smaller slots, to exercise the full-size rerun of overflowing queries
+    if (const char* e = std::getenv("TSG_SLOT_CAP"))
+        cap = std::min<uint64_t>(cap, std::max<uint64_t>(std::strtoull(e, nullptr, 10), std::min<uint64_t>(N, 2 * s.leaf_cap)));
     alloc_slots(s, s.batch, s.batch_max, cap);
 }
 

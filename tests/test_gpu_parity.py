@@ -161,9 +161,9 @@ def test_duplicates_overflow_leaves(oracle):
         assert r.distance == 0.0 and r.position == p
 
 
-def test_finalist_overflow_ties(oracle):
-    """More exact ties than finalize's finalist slots (4096 per lane): the
-    rescan of every candidate record must still return the lowest position."""
+def test_many_exact_ties(oracle):
+    """7500 exact duplicates of three series, shuffled: every batch slot's
+    finalize must still return the lowest position among thousands of ties."""
     protos = oracle.generate(3, 64, 4242, znorm=False)
     rows = np.concatenate([oracle.generate(1000, 64, 4243, znorm=False), np.tile(protos, (2500, 1))])
     rng = np.random.default_rng(5)
@@ -309,3 +309,35 @@ def test_exact_matches_scan_c5_noisy_queries(oracle, sigma):
     _, res = check_against_scan(oracle, rows, queries, tg.IndexConfig())
     if sigma <= 0.01:  # near-duplicates find their source row
         assert sum(int(r.position) == int(s) for r, s in zip(res, src)) >= 8
+
+
+def test_slot_overflow_reruns_full_size(oracle, monkeypatch):
+    """Queries whose candidates outgrow a batch slot are rerun alone in a full-size slot."""
+    monkeypatch.setenv("TSG_SLOT_CAP", "64")  # read when the index is built
+    rows = oracle.generate(6000, 64, 515)
+    cfg = tg.IndexConfig(n=64, w=8, max_card_bits=2, leaf_capacity=20)  # coarse words: many candidates
+    index = tg.build_index(rows, cfg)
+    queries = np.concatenate([oracle.generate(5, 64, 516), rows[[3, 4000]] + np.float32(0.3)]).astype(np.float32)
+    check_against_scan(oracle, rows, queries, cfg, index=index)
+
+
+def test_many_batches_one_call(oracle):
+    """More queries than batch slots in one call: consecutive batches reuse the slots."""
+    rows = oracle.generate(4000, 96, 517)
+    rng = np.random.default_rng(3)
+    queries = np.concatenate([oracle.generate(150, 96, 518),
+                              rows[rng.integers(0, 4000, 150)] + 0.05 * rng.standard_normal((150, 96)).astype(np.float32)])
+    cfg = tg.IndexConfig(n=96, w=16, leaf_capacity=50)
+    check_against_scan(oracle, rows, queries.astype(np.float32), cfg)
+
+
+def test_approximate_batch_matches_single(oracle):
+    rows = oracle.generate(3000, 128, 519)
+    index = tg.build_index(rows, tg.IndexConfig(n=128, w=16, leaf_capacity=30))
+    qs = oracle.generate(8, 128, 520)
+    for q in qs:
+        a = tg.approximate_search(index, q)
+        e = tg.exact_search(index, q)
+        assert a.distance >= e.distance
+        d, p = oracle.scan_nn(rows, q, 0)
+        assert e.position == p and e.distance == d
