@@ -1130,29 +1130,46 @@ __global__ void __launch_bounds__(kThreads, 3)
         uint32_t chunk = 0;
         if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
         chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+        // The current chunk's records (bound, entry) are loaded one chunk ahead,
+        // while the previous chunk's rows are being refined.
+        constexpr int kPer = kTmaChunk / 32;
+        float rlb[kPer];
+        uint32_t rcp[kPer];
+        auto load_records = [&](uint32_t ch, float* lbv, uint32_t* cpv) {
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const uint64_t c = begin + static_cast<uint64_t>(ch) * kTmaChunk + 32 * k + lane;
+                const bool in = ch < nch && c < end;
+                lbv[k] = in ? cand_lb[c] : INFINITY;
+                cpv[k] = in ? cand_pos[c] : 0u;
+            }
+        };
+        load_records(chunk, rlb, rcp);
         while (chunk < nch) {
             uint32_t pre = 0;
-            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
+            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);
             const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kTmaChunk;
             const uint64_t c1 = u64min(c0 + kTmaChunk, end);
             // Phase 1 (warp): keep the records whose bound is within the BSF.
             const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
             uint32_t m = 0;
 #pragma unroll
-            for (uint32_t i0 = 0; i0 < kTmaChunk; i0 += 32) {
-                const uint64_t c = c0 + i0 + lane;
+            for (int k = 0; k < kPer; ++k) {
+                const uint64_t c = c0 + 32 * k + lane;
                 const bool in = c < c1;
-                const bool keep = in && cand_lb[c] <= bnd;
+                const bool keep = in && rlb[k] <= bnd;
                 if (in && !keep) cand_sq[c] = INFINITY;
                 const unsigned mk = __ballot_sync(0xFFFFFFFFu, keep);
                 if (keep) {
                     const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
                     s_c[warp][slot] = static_cast<uint32_t>(c);
-                    s_p[warp][slot] = ix.pos[cand_pos[c]];  // candidate records hold index-order entries
+                    s_p[warp][slot] = ix.pos[rcp[k]];  // candidate records hold index-order entries
                 }
                 m += __popc(mk);
             }
             __syncwarp();
+            const uint32_t next = __shfl_sync(0xFFFFFFFFu, pre, 0);
+            load_records(next, rlb, rcp);  // in flight during phase 2
             // Phase 2: the kept rows, double-buffered per group.
             if (leader && static_cast<uint32_t>(wg) < m) issue(0, s_p[warp][wg]);
             int b = 0;
@@ -1207,7 +1224,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 __syncwarp(gmask);  // the group is done with buffer b before it is refilled
             }
             __syncwarp();  // the warp's list is reused by the next chunk
-            chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
+            chunk = next;
         }
         if (leader) {
             if (refined) atomicAdd(&wk->stats[kRealDist], refined);
