@@ -137,6 +137,19 @@ tsg_status tsg_index_build_device(tsg_ctx* ctx, const float* dev_rows, uint64_t 
                                   uint64_t position_offset, tsg_index** out,
                                   tsg_build_stats* stats);
 
+/* Build straight from a headerless float32 file (count x length, row-major)
+ * <- tsidx::load_dataset(path, length) (src/dataset.cpp:87-117) followed by
+ * tsidx::build_index (src/index.cpp:258-318). The series count comes from the
+ * file size (load_dataset's checks and messages: TSG_INVALID_ARGUMENT for
+ * length 0, TSG_RUNTIME for a missing file or a size that is not a positive
+ * multiple of length * 4). Each device reads its range of the file in
+ * ~128 MB chunks through pinned buffers while K1 summarises the chunks that
+ * already arrived (disk, PCIe and K1 overlap); no host copy of the dataset
+ * is kept. stats->h2d_ns = wall time of the streaming phase. */
+tsg_status tsg_index_build_file(tsg_ctx* ctx, const char* path, uint64_t length,
+                                const tsg_config* cfg, uint64_t position_offset,
+                                tsg_index** out, tsg_build_stats* stats);
+
 tsg_status tsg_index_free(tsg_index* index);
 
 tsg_status tsg_index_info(const tsg_index* index, uint64_t* count, uint64_t* length,

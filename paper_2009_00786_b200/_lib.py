@@ -20,7 +20,7 @@ EXPORTS = (
     "tsg_index_build", "tsg_index_build_device", "tsg_index_free", "tsg_index_info", "tsg_search",
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
-    "tsg_generate_series",
+    "tsg_generate_series", "tsg_index_build_file",
 )
 
 
@@ -77,6 +77,8 @@ def lib() -> C.CDLL:
                                   C.POINTER(tsg_build_stats)]),
         "tsg_index_build_device": (i32, [vp, vp, u64, u64, C.POINTER(tsg_config), u64, C.POINTER(vp),
                                          C.POINTER(tsg_build_stats)]),
+        "tsg_index_build_file": (i32, [vp, C.c_char_p, u64, C.POINTER(tsg_config), u64, C.POINTER(vp),
+                                       C.POINTER(tsg_build_stats)]),
         "tsg_index_free": (i32, [vp]),
         "tsg_index_info": (i32, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(tsg_config),
                                  C.POINTER(tsg_build_stats)]),

@@ -4,9 +4,14 @@
 // search: tsidx::exact_search (src/query.cpp:258-298)  -> tsg_search
 // Validation messages follow IndexConfig::validate (src/config.cpp:22-35),
 // build_index (src/index.cpp:259-266) and QueryState (src/query.cpp:84-87).
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -202,8 +207,84 @@ double* upload_thresholds(int bits) {
 }
 
 // Builds one shard on its device. rows: host (copied) or device (borrowed).
+// Source of a shard's rows for build_shard: a file range streamed while K1 runs.
+struct FileRows {
+    const char* path = nullptr;
+    uint64_t first = 0;  // first series of the shard in the file
+};
+
+// Streams series [src.first, src.first + N) of a headerless f32 file into
+// s.rows: chunks of ~128 MB are read (parallel preads) into one of three
+// pinned buffers, copied to HBM on the shard stream and summarised (K1)
+// behind the copy, so disk/page-cache reads, PCIe and K1 overlap.
+RowFeeder file_feeder(DevIndex& s, const FileRows& src, uint64_t* wall_ns) {
+    return [&s, src, wall_ns](const std::function<void(uint64_t, uint64_t)>& sum_chunk) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const uint64_t row_bytes = static_cast<uint64_t>(s.n) * sizeof(float);
+        const uint64_t chunk_rows = std::max<uint64_t>(1, (128ull << 20) / row_bytes);
+        const uint64_t chunk_bytes = chunk_rows * row_bytes;
+        constexpr int kBufs = 3, kReaders = 8;
+        const int fd = ::open(src.path, O_RDONLY);
+        if (fd < 0) throw std::runtime_error(std::string("load_dataset: cannot open ") + src.path);
+        struct Closer {
+            int fd;
+            ~Closer() { ::close(fd); }
+        } closer{fd};
+        ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+        std::array<void*, kBufs> buf{};
+        std::array<cudaEvent_t, kBufs> copied{};
+        struct Pinned {
+            std::array<void*, kBufs>& b;
+            std::array<cudaEvent_t, kBufs>& e;
+            cudaStream_t st;
+            ~Pinned() {
+                cudaStreamSynchronize(st);
+                for (auto p : b)
+                    if (p) cudaFreeHost(p);
+                for (auto x : e)
+                    if (x) cudaEventDestroy(x);
+            }
+        } pinned{buf, copied, s.stream};
+        for (int i = 0; i < kBufs; ++i) {
+            TSG_CUDA(cudaHostAlloc(&buf[i], chunk_bytes, cudaHostAllocDefault));
+            TSG_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+        }
+        uint64_t i = 0;
+        for (uint64_t first = 0; first < s.N; first += chunk_rows, ++i) {
+            const int b = static_cast<int>(i % kBufs);
+            const uint64_t cnt = std::min(chunk_rows, s.N - first);
+            const uint64_t bytes = cnt * row_bytes;
+            if (i >= kBufs) TSG_CUDA(cudaEventSynchronize(copied[b]));  // the buffer's last copy is done
+            const uint64_t off = (src.first + first) * row_bytes;
+            std::atomic<bool> short_read{false};
+            auto read_part = [&](int r) {
+                const uint64_t lo = bytes * r / kReaders, hi = bytes * (r + 1) / kReaders;
+                for (uint64_t p = lo; p < hi;) {
+                    const ssize_t got = ::pread(fd, static_cast<char*>(buf[b]) + p, hi - p, static_cast<off_t>(off + p));
+                    if (got <= 0) {
+                        short_read = true;
+                        return;
+                    }
+                    p += static_cast<uint64_t>(got);
+                }
+            };
+            std::vector<std::thread> readers;
+            for (int r = 1; r < kReaders; ++r) readers.emplace_back(read_part, r);
+            read_part(0);
+            for (auto& t : readers) t.join();
+            if (short_read) throw std::runtime_error(std::string("load_dataset: short read from ") + src.path);
+            TSG_CUDA(cudaMemcpyAsync(s.rows + first * s.n, buf[b], bytes, cudaMemcpyHostToDevice, s.stream));
+            TSG_CUDA(cudaEventRecord(copied[b], s.stream));
+            sum_chunk(first, cnt);
+        }
+        TSG_CUDA(cudaStreamSynchronize(s.stream));
+        *wall_ns = static_cast<uint64_t>(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    };
+}
+
 void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, const tsg_config& cfg,
-                 uint64_t pos_offset, uint64_t* h2d_ns, double ms[3]) {
+                 uint64_t pos_offset, uint64_t* h2d_ns, double ms[3], const FileRows* file = nullptr) {
     DeviceGuard g(s.device);
     check_device(s.device);
     TSG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
@@ -215,7 +296,11 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     s.ws = word_stride(cfg.w);
     s.leaf_cap = cfg.leaf_capacity;
     s.pos_offset = pos_offset;
-    if (host_rows) {
+    if (file) {  // rows arrive from the file while K1 runs (below)
+        TSG_CUDA(cudaMalloc(&s.rows, N * cfg.n * sizeof(float)));
+        s.own_rows = true;
+        *h2d_ns = 0;
+    } else if (host_rows) {
         const auto t0 = std::chrono::steady_clock::now();
         TSG_CUDA(cudaMalloc(&s.rows, N * cfg.n * sizeof(float)));
         s.own_rows = true;
@@ -230,7 +315,12 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     }
     s.thr = upload_thresholds(s.bits);
     if (const char* e = std::getenv("TSG_REFINE_SPLIT")) s.refine_split = static_cast<float>(std::atof(e));
-    build_layout(s, &ms[0], &ms[1], &ms[2]);
+    if (file) {
+        const RowFeeder feeder = file_feeder(s, *file, h2d_ns);
+        build_layout(s, &ms[0], &ms[1], &ms[2], &feeder);
+    } else {
+        build_layout(s, &ms[0], &ms[1], &ms[2]);
+    }
     // Search workspace: batch_max query slots (TSG_BATCH, default 128). Each
     // slot holds up to `cap` candidate records: as many as the shard has
     // entries when memory allows, else a share of ~45% of the free memory
@@ -367,7 +457,8 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
 }
 
 tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, uint64_t length,
-                    const tsg_config* cfg, uint64_t position_offset, tsg_index** out, tsg_build_stats* stats) {
+                    const tsg_config* cfg, uint64_t position_offset, tsg_index** out, tsg_build_stats* stats,
+                    const char* path = nullptr) {
     return guarded([&] {
         if (!ctx || !out) fail("build_index: null argument");
         *out = nullptr;
@@ -378,7 +469,7 @@ tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, 
             fail("build_index: dataset length " + std::to_string(length) + " does not match config.n " +
                  std::to_string(cfg->n));
         if (count > 0xFFFFFFFFull) fail("build_index: more than 2^32-1 series");
-        if (!rows) fail("build_index: null rows");
+        if (!rows && !path) fail("build_index: null rows");
         if (position_offset + count - 1 > 0xFFFFFFFFull) fail("build_index: positions exceed 2^32-1");
         if (!host && ctx->devices.size() != 1) fail("tsg_index_build_device: device rows need a single-device context");
 
@@ -400,8 +491,14 @@ tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, 
                 const uint64_t b = count * k / G, e = count * (k + 1) / G;
                 ix->shard_first[k] = b;
                 ix->shards[k].device = ctx->devices[k];
-                build_shard(ix->shards[k], rows + b * length, host, e - b, *cfg, position_offset + b, &h2d[k],
-                            ms[k].data());
+                if (path) {
+                    const FileRows fr{path, b};
+                    build_shard(ix->shards[k], nullptr, true, e - b, *cfg, position_offset + b, &h2d[k], ms[k].data(),
+                                &fr);
+                } else {
+                    build_shard(ix->shards[k], rows + b * length, host, e - b, *cfg, position_offset + b, &h2d[k],
+                                ms[k].data());
+                }
             } catch (...) {
                 errs[k] = std::current_exception();
             }
@@ -506,6 +603,27 @@ tsg_status tsg_close(tsg_ctx* ctx) {
 tsg_status tsg_index_build(tsg_ctx* ctx, const float* host_rows, uint64_t count, uint64_t length,
                            const tsg_config* cfg, uint64_t position_offset, tsg_index** out, tsg_build_stats* stats) {
     return do_build(ctx, host_rows, true, count, length, cfg, position_offset, out, stats);
+}
+
+tsg_status tsg_index_build_file(tsg_ctx* ctx, const char* path, uint64_t length, const tsg_config* cfg,
+                                uint64_t position_offset, tsg_index** out, tsg_build_stats* stats) {
+    // load_dataset's checks and messages (src/dataset.cpp:87-100), then build_index's.
+    uint64_t count = 0;
+    const tsg_status st = guarded([&] {
+        if (!path) fail("load_dataset: null path");
+        if (length == 0) fail("load_dataset: length must be positive");
+        struct stat sb {};
+        if (::stat(path, &sb) != 0)
+            throw std::runtime_error(std::string("load_dataset: cannot stat ") + path + ": " + std::strerror(errno));
+        const uint64_t bytes = static_cast<uint64_t>(sb.st_size), series_bytes = length * sizeof(float);
+        if (bytes == 0 || bytes % series_bytes != 0)
+            throw std::runtime_error(std::string("load_dataset: ") + path + " holds " + std::to_string(bytes) +
+                                     " bytes, not a positive multiple of " + std::to_string(series_bytes) +
+                                     " (length " + std::to_string(length) + " * 4)");
+        count = bytes / series_bytes;
+    });
+    if (st != TSG_OK) return st;
+    return do_build(ctx, nullptr, true, count, length, cfg, position_offset, out, stats, path);
 }
 
 tsg_status tsg_index_build_device(tsg_ctx* ctx, const float* dev_rows, uint64_t count, uint64_t length,

@@ -250,7 +250,7 @@ T d2h(const T* p, cudaStream_t st) {
 
 }  // namespace
 
-void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf) {
+void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf, const RowFeeder* feeder) {
     const uint64_t N = ix.N;
     cudaStream_t st = ix.stream;
     const int sms = ix.sms;
@@ -309,7 +309,12 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf)
 
     // K1 summarise
     TSG_CUDA(cudaEventRecord(ev[0], st));
-    summarise(ix.rows, N, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>(), nullptr, keys_in.as<uint64_t>(), st);
+    auto sum_chunk = [&](uint64_t first, uint64_t count) {
+        summarise(ix.rows + first * ix.n, count, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>() + first * ix.ws,
+                  nullptr, keys_in.as<uint64_t>() + first, st);
+    };
+    if (feeder) (*feeder)(sum_chunk);  // rows stream in; K1 runs per chunk behind them
+    else sum_chunk(0, N);
     TSG_CUDA(cudaEventRecord(ev[1], st));
 
     // K2 organise: stable sort by the significant key bits, carrying positions.

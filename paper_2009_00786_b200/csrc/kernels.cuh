@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <functional>
 
 namespace tsg {
 
@@ -117,9 +118,16 @@ struct DevResult {
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
                uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream);
 
-// K2 + K3: sort, gather, leaves, pages, boxes. Fills the index arrays of
-// `ix` (rows/thr/N/n/w/bits/leaf_cap must be set). Device ms per phase.
-void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, double* ms_leaves);
+// Streams the shard's rows into ix.rows chunk by chunk: for each chunk it
+// enqueues the rows' arrival on ix.stream and then calls sum_chunk(first,
+// count), which enqueues K1 for those rows on the same stream.
+using RowFeeder = std::function<void(const std::function<void(uint64_t, uint64_t)>& sum_chunk)>;
+
+// K1 + K2 + K3: summarise, sort, gather, leaves, pages, boxes. Fills the
+// index arrays of `ix` (rows/thr/N/n/w/bits/leaf_cap must be set; with a
+// feeder the rows arrive while K1 runs). Device ms per phase.
+void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, double* ms_leaves,
+                  const RowFeeder* feeder = nullptr);
 
 // Query pipeline for nq device queries in slots [0, nq) of `slots`; writes
 // results[0..nq). Queries flagged kResultOverflow must be rerun with a slot

@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import dataclasses
 import enum
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -271,6 +272,45 @@ def build_index(dataset, config: IndexConfig = None, devices: Sequence[int] = (0
     check(lib().tsg_index_build(ctx.handle, arr.ctypes.data, arr.shape[0], arr.shape[1], C.byref(cfg),
                                 position_offset, C.byref(h), C.byref(st)))
     return Index(h, arr, config, _stats_from_c(st), ctx)
+
+
+def build_index_from_file(path, config: IndexConfig = None, devices: Sequence[int] = (0,),
+                          position_offset: int = 0) -> Index:
+    """tsidx::load_dataset(path, config.n) + tsidx::build_index, streamed: each
+    device reads its range of the headerless float32 file in chunks while K1
+    summarises the chunks already in HBM (no host copy of the dataset). The
+    index's ``data()`` is a read-only memory map of the file."""
+    config = config or IndexConfig()
+    cfg = config.to_c()
+    st = _lib.tsg_build_stats()
+    h = C.c_void_p()
+    ctx = _context(devices)
+    check(lib().tsg_index_build_file(ctx.handle, os.fsencode(os.fspath(path)), config.n, C.byref(cfg),
+                                     position_offset, C.byref(h), C.byref(st)))
+    data = np.memmap(path, dtype=np.float32, mode="r").reshape(-1, config.n)
+    return Index(h, data, config, _stats_from_c(st), ctx)
+
+
+def load_dataset(path, length: int) -> np.ndarray:
+    """tsidx::load_dataset (src/dataset.cpp:87-110): a headerless float32 file
+    of count x length values, with the reference's checks and messages."""
+    if length <= 0:
+        raise InvalidArgument("load_dataset: length must be positive")
+    path = os.fspath(path)
+    try:
+        size = os.stat(path).st_size
+    except OSError as e:
+        raise TsgError(f"load_dataset: cannot stat {path}: {e.strerror}") from None
+    series_bytes = length * 4
+    if size == 0 or size % series_bytes != 0:
+        raise TsgError(f"load_dataset: {path} holds {size} bytes, not a positive multiple of "
+                       f"{series_bytes} (length {length} * 4)")
+    return np.fromfile(path, dtype=np.float32).reshape(-1, length)
+
+
+def save_dataset(path, rows) -> None:
+    """tsidx::save_dataset (src/dataset.cpp:112-117): the values, row-major, no header."""
+    np.ascontiguousarray(np.asarray(rows, dtype=np.float32)).tofile(os.fspath(path))
 
 
 def _check_measure(measure: Measure, n: int) -> None:

@@ -6,6 +6,7 @@ import ctypes as C
 import os
 import re
 
+import numpy as np
 import pytest
 
 from paper_2009_00786_b200 import _lib
@@ -82,3 +83,22 @@ def test_no_gpu_fails_loudly():
         pytest.skip("a GPU is visible")
     assert st == _lib.TSG_CUDA
     assert "no CUDA device" in _lib.lib().tsg_last_error().decode()
+
+
+def test_dataset_file_roundtrip_and_errors(tmp_path):
+    """load_dataset / save_dataset with the reference's checks (test_data.cpp:94-113)."""
+    import paper_2009_00786_b200 as tg
+
+    rows = np.random.default_rng(0).standard_normal((7, 33)).astype(np.float32)
+    path = tmp_path / "ds.f32"
+    tg.save_dataset(path, rows)
+    back = tg.load_dataset(path, 33)
+    assert back.shape == (7, 33) and np.array_equal(back.view(np.uint32), rows.view(np.uint32))
+    bad = tmp_path / "bad.f32"
+    bad.write_bytes(b"0123456789")
+    with pytest.raises(tg.TsgError, match="10 bytes"):
+        tg.load_dataset(bad, 33)
+    with pytest.raises(tg.TsgError):
+        tg.load_dataset(tmp_path / "missing.f32", 8)
+    with pytest.raises(tg.InvalidArgument, match="length must be positive"):
+        tg.load_dataset(path, 0)

@@ -341,3 +341,32 @@ def test_approximate_batch_matches_single(oracle):
         assert a.distance >= e.distance
         d, p = oracle.scan_nn(rows, q, 0)
         assert e.position == p and e.distance == d
+
+
+def test_build_from_file_equals_build_from_memory(oracle, tmp_path):
+    """load_dataset + build_index streamed from a file (chunks overlapped with K1)
+    gives the same index and answers as the in-memory build; several chunks."""
+    rows = oracle.generate(600_000, 128, 521)  # ~307 MB: three 128 MB chunks
+    path = tmp_path / "c.f32"
+    tg.save_dataset(path, rows)
+    cfg = tg.IndexConfig(n=128, w=16, leaf_capacity=500)
+    a = tg.build_index_from_file(path, cfg)
+    b = tg.build_index(rows, cfg)
+    ea, eb = a.export(), b.export()
+    for x, y in zip(ea, eb):
+        assert np.array_equal(x, y)
+    assert a.build_stats().leaves == b.build_stats().leaves
+    qs = np.concatenate([oracle.generate(6, 128, 522), rows[[5, 599_999]] + np.float32(0.01)]).astype(np.float32)
+    ra, rb = tg.exact_search_batch(a, qs), tg.exact_search_batch(b, qs)
+    for x, y in zip(ra, rb):
+        assert x.position == y.position and x.distance == y.distance
+    assert np.array_equal(a.data()[599_999], rows[599_999])
+
+
+def test_build_from_file_errors(tmp_path):
+    bad = tmp_path / "bad.f32"
+    bad.write_bytes(b"0123456789")
+    with pytest.raises(tg.TsgError, match="10 bytes"):
+        tg.build_index_from_file(bad, tg.IndexConfig(n=32, w=16))
+    with pytest.raises(tg.TsgError, match="cannot stat"):
+        tg.build_index_from_file(tmp_path / "missing.f32", tg.IndexConfig(n=32, w=16))
