@@ -71,6 +71,11 @@ class Oracle:
         _sig(lib, "orc_squared_l2", f64, _f32p, _f32p, u64, f64)
         _sig(lib, "orc_scan_nn", None, _f32p, u64, u64, _f32p, C.c_uint, C.POINTER(f64), C.POINTER(u32))
         _sig(lib, "orc_cmin", u64, _u8p, u64, i32, i32, u64, _f64p, f64)
+        _sig(lib, "orc_keogh_envelope", None, _f32p, u64, i32, i32, _f32p, _f32p, _f64p, _f64p)
+        _sig(lib, "orc_lb_keogh", f64, _f32p, _f32p, _f32p, u64)
+        _sig(lib, "orc_mindist_envelope_isax", f64, _f64p, _f64p, _u8p, _u8p, i32, u64)
+        _sig(lib, "orc_dtw", f64, _f32p, _f32p, u64, i32, f64)
+        _sig(lib, "orc_scan_nn_dtw", None, _f32p, u64, u64, _f32p, i32, C.c_uint, C.POINTER(f64), C.POINTER(u32))
 
     def breakpoints(self, bits: int) -> np.ndarray:
         out = np.empty((1 << bits) - 1, np.float64)
@@ -150,6 +155,37 @@ class Oracle:
         self.lib.orc_scan_nn(rows, rows.shape[0], rows.shape[1], q, threads, C.byref(d), C.byref(p))
         return d.value, p.value
 
+    # ---- DTW ----
+    def keogh_envelope(self, q, window: int, w: int):
+        q = np.ascontiguousarray(q, np.float32)
+        n = q.size
+        up, lo = np.empty(n, np.float32), np.empty(n, np.float32)
+        upaa, lpaa = np.empty(w, np.float64), np.empty(w, np.float64)
+        self.lib.orc_keogh_envelope(q, n, window, w, up, lo, upaa, lpaa)
+        return up, lo, upaa, lpaa
+
+    def lb_keogh(self, q, window: int, c) -> float:
+        up, lo, _, _ = self.keogh_envelope(q, window, 1)
+        return self.lib.orc_lb_keogh(up, lo, np.ascontiguousarray(c, np.float32), up.size)
+
+    def mindist_envelope(self, q, window: int, w: int, sym, bits: int = 8) -> float:
+        _, _, upaa, lpaa = self.keogh_envelope(q, window, w)
+        sym = np.ascontiguousarray(sym, np.uint8)
+        cb = np.full(w, bits, np.uint8)
+        return self.lib.orc_mindist_envelope_isax(lpaa, upaa, sym, cb, w, np.asarray(q).size)
+
+    def dtw(self, a, b, window: int, cutoff: float = -1.0) -> float:
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        return self.lib.orc_dtw(a, b, a.size, window, cutoff)
+
+    def scan_nn_dtw(self, rows, q, window: int, threads: int = 0):
+        rows = np.ascontiguousarray(rows, np.float32)
+        q = np.ascontiguousarray(q, np.float32)
+        d, p = f64(), u32()
+        self.lib.orc_scan_nn_dtw(rows, rows.shape[0], rows.shape[1], q, window, threads, C.byref(d), C.byref(p))
+        return d.value, p.value
+
     def cmin(self, words: np.ndarray, qpaa: np.ndarray, n: int, d_nn: float, bits: int = 8) -> int:
         words = np.ascontiguousarray(words, np.uint8)
         return int(self.lib.orc_cmin(words, words.shape[0], words.shape[1], bits, n,
@@ -197,6 +233,12 @@ class Reference:
         _sig(lib, "ref_build_generated", i32, u64, u64, u64, i32, i32, i32, u64, u64, C.c_uint,
              C.POINTER(C.c_void_p), _u64p, C.POINTER(u64))
         _sig(lib, "ref_series_window", i32, u64, u64, u64, u64, i32, _f32p)
+        _sig(lib, "ref_dtw", i32, _f32p, _f32p, u64, i32, f64, C.POINTER(f64))
+        _sig(lib, "ref_keogh_envelope", i32, _f32p, u64, i32, i32, _f32p, _f32p, _f64p, _f64p)
+        _sig(lib, "ref_lb_keogh", i32, _f32p, u64, i32, i32, _f32p, C.POINTER(f64))
+        _sig(lib, "ref_mindist_envelope_isax", i32, _f32p, u64, i32, i32, _u8p, i32, C.POINTER(f64))
+        _sig(lib, "ref_scan_nn_dtw", i32, C.c_void_p, _f32p, i32, C.c_uint, C.POINTER(f64), C.POINTER(u32))
+        _sig(lib, "ref_exact_search_dtw", i32, C.c_void_p, _f32p, i32, C.POINTER(f64), C.POINTER(u32))
 
     def build_generated(self, count, n, seed, znorm=True, w=16, bits=8, leaf_capacity=2000, chunk=20000,
                         workers=0):
@@ -273,6 +315,46 @@ class Reference:
         finally:
             self.lib.ref_dataset_free(h)
 
+    # ---- DTW ----
+    def dtw(self, a, b, window: int, cutoff: float = -1.0) -> float:
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        out = f64()
+        self._check(self.lib.ref_dtw(a, b, a.size, window, cutoff, C.byref(out)))
+        return out.value
+
+    def keogh_envelope(self, q, window: int, w: int):
+        q = np.ascontiguousarray(q, np.float32)
+        n = q.size
+        up, lo = np.empty(n, np.float32), np.empty(n, np.float32)
+        upaa, lpaa = np.empty(w, np.float64), np.empty(w, np.float64)
+        self._check(self.lib.ref_keogh_envelope(q, n, window, w, up, lo, upaa, lpaa))
+        return up, lo, upaa, lpaa
+
+    def lb_keogh(self, q, window: int, c) -> float:
+        q = np.ascontiguousarray(q, np.float32)
+        out = f64()
+        self._check(self.lib.ref_lb_keogh(q, q.size, window, 1, np.ascontiguousarray(c, np.float32), C.byref(out)))
+        return out.value
+
+    def mindist_envelope(self, q, window: int, w: int, sym, bits: int = 8) -> float:
+        q = np.ascontiguousarray(q, np.float32)
+        out = f64()
+        self._check(self.lib.ref_mindist_envelope_isax(q, q.size, window, w, np.ascontiguousarray(sym, np.uint8),
+                                                       bits, C.byref(out)))
+        return out.value
+
+    def scan_nn_dtw(self, rows, q, window: int, threads: int = 0):
+        rows = np.ascontiguousarray(rows, np.float32)
+        h = self.lib.ref_dataset_new(rows, rows.shape[0], rows.shape[1])
+        try:
+            d, p = f64(), u32()
+            self._check(self.lib.ref_scan_nn_dtw(h, np.ascontiguousarray(q, np.float32), window, threads,
+                                                 C.byref(d), C.byref(p)))
+            return d.value, p.value
+        finally:
+            self.lib.ref_dataset_free(h)
+
     def dataset(self, rows):
         return RefDataset(self, rows)
 
@@ -329,6 +411,12 @@ class RefIndex:
                                                       workers, queues, mode, C.byref(d), C.byref(p),
                                                       st, C.byref(ns)))
         return d.value, p.value, dict(zip(SEARCH_STAT_FIELDS, map(int, st))), ns.value
+
+    def exact_search_dtw(self, q, window: int):
+        d, p = f64(), u32()
+        self.ref._check(self.ref.lib.ref_exact_search_dtw(self.h, np.ascontiguousarray(q, np.float32), window,
+                                                          C.byref(d), C.byref(p)))
+        return d.value, p.value
 
     def approximate_search(self, q):
         d, p = f64(), u32()

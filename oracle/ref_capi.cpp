@@ -345,4 +345,60 @@ int ref_approximate_search(void* h, const float* query, double* dist, std::uint3
     });
 }
 
+
+// ---- DTW: dtw, keogh_envelope, lb_keogh, mindist_envelope_isax
+// (src/metrics.cpp:112-202) and the DTW forms of scan_nn / exact_search.
+int ref_dtw(const float* a, const float* b, std::uint64_t n, int window, double cutoff, double* out) {
+    return guarded([&] {
+        *out = cutoff < 0 ? tsidx_ref::dtw({a, n}, {b, n}, window) : tsidx_ref::dtw({a, n}, {b, n}, window, cutoff);
+    });
+}
+
+int ref_keogh_envelope(const float* q, std::uint64_t n, int window, int w, float* upper, float* lower,
+                       double* upper_paa, double* lower_paa) {
+    return guarded([&] {
+        auto env = tsidx_ref::keogh_envelope({q, n}, window, w);
+        std::copy(env.upper.begin(), env.upper.end(), upper);
+        std::copy(env.lower.begin(), env.lower.end(), lower);
+        std::copy(env.upper_paa.begin(), env.upper_paa.end(), upper_paa);
+        std::copy(env.lower_paa.begin(), env.lower_paa.end(), lower_paa);
+    });
+}
+
+int ref_lb_keogh(const float* q, std::uint64_t n, int window, int w, const float* candidate, double* out) {
+    return guarded([&] {
+        auto env = tsidx_ref::keogh_envelope({q, n}, window, w);
+        *out = tsidx_ref::lb_keogh(env, {candidate, n});
+    });
+}
+
+int ref_mindist_envelope_isax(const float* q, std::uint64_t n, int window, int w, const std::uint8_t* symbols,
+                              int bits, double* out) {
+    return guarded([&] {
+        auto env = tsidx_ref::keogh_envelope({q, n}, window, w);
+        std::vector<std::uint8_t> cb(static_cast<std::size_t>(w), static_cast<std::uint8_t>(bits));
+        tsidx_ref::SaxWordView view{{symbols, static_cast<std::size_t>(w)}, cb};
+        *out = tsidx_ref::mindist_envelope_isax(env, view, n);
+    });
+}
+
+int ref_scan_nn_dtw(void* data, const float* query, int window, unsigned threads, double* dist,
+                    std::uint32_t* pos) {
+    return guarded([&] {
+        auto& ds = static_cast<RefData*>(data)->ds;
+        auto r = tsidx_ref::scan_nn(ds, {query, ds.length}, tsidx_ref::Measure::dtw(window), threads);
+        *dist = r.distance;
+        *pos = r.position;
+    });
+}
+
+int ref_exact_search_dtw(void* h, const float* query, int window, double* dist, std::uint32_t* pos) {
+    return guarded([&] {
+        auto& idx = *static_cast<RefIndex*>(h)->index;
+        auto r = tsidx_ref::exact_search(idx, {query, idx.config().n}, tsidx_ref::Measure::dtw(window), {});
+        *dist = r.distance;
+        *pos = r.position;
+    });
+}
+
 }  // extern "C"

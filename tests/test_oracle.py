@@ -167,3 +167,54 @@ def test_oracle_equals_reference_random(oracle, reference):
         cb = np.full(w, b, np.uint8)
         word = oracle.summarise(rows[3:4], w, b)[0]
         assert oracle.mindist(qp, word, cb, n) == reference.mindist(qp, word, cb, n)
+
+
+# ---- DTW: the restatement against the compiled reference ----
+
+def test_dtw_matches_reference(oracle, reference):
+    rng = np.random.default_rng(11)
+    for n, r in ((8, 0), (8, 1), (16, 3), (64, 6), (96, 95), (128, 12), (33, 5)):
+        for trial in range(6):
+            a = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+            b = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+            want = reference.dtw(a, b, r)
+            assert oracle.dtw(a, b, r) == want
+            assert oracle.dtw(b, a, r) == want  # symmetric, bit for bit
+            assert reference.dtw(b, a, r) == want
+            cut = want * (0.7 + 0.6 * (trial % 2))
+            assert oracle.dtw(a, b, r, cut) == reference.dtw(a, b, r, cut)
+    a = rng.standard_normal(40).astype(np.float32)
+    assert oracle.dtw(a, a, 4) == 0.0
+    # window 0 is the Euclidean distance summed sequentially
+    b = rng.standard_normal(40).astype(np.float32)
+    assert oracle.dtw(a, b, 0) == pytest.approx(np.sqrt(((a.astype(np.float64) - b) ** 2).sum()), rel=1e-15)
+
+
+def test_envelope_bounds_match_reference(oracle, reference):
+    rng = np.random.default_rng(12)
+    for n, r, w in ((64, 6, 16), (96, 10, 16), (128, 0, 8), (256, 25, 16), (60, 59, 5)):
+        q = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+        mine, theirs = oracle.keogh_envelope(q, r, w), reference.keogh_envelope(q, r, w)
+        for x, y in zip(mine, theirs):
+            assert np.array_equal(x, y)
+        c = np.cumsum(rng.standard_normal(n)).astype(np.float32)
+        assert oracle.lb_keogh(q, r, c) == reference.lb_keogh(q, r, c)
+        sym = oracle.summarise(c[None, :], w)[0]
+        assert oracle.mindist_envelope(q, r, w, sym) == reference.mindist_envelope(q, r, w, sym)
+        # soundness: both bounds are below the DTW distance
+        d = oracle.dtw(q, c, r)
+        assert oracle.lb_keogh(q, r, c) <= d + 1e-9 and oracle.mindist_envelope(q, r, w, sym) <= d + 1e-9
+
+
+def test_scan_nn_dtw_matches_reference(oracle, reference):
+    rows = oracle.generate(400, 64, 31)
+    qs = oracle.generate(4, 64, 32)
+    for r in (0, 3, 12):
+        for q in qs:
+            assert oracle.scan_nn_dtw(rows, q, r, threads=3) == reference.scan_nn_dtw(rows, q, r, threads=5)
+    # the reference index agrees on the answer
+    idx = reference.build_index(rows, w=16, leaf_capacity=20)
+    for q in qs:
+        d, p = idx.exact_search_dtw(q, 6)
+        dd, pp = oracle.scan_nn_dtw(rows, q, 6)
+        assert p == pp and d == pytest.approx(dd, rel=1e-12)
