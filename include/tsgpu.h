@@ -152,6 +152,25 @@ tsg_status tsg_index_build_file(tsg_ctx* ctx, const char* path, uint64_t length,
 
 tsg_status tsg_index_free(tsg_index* index);
 
+/* tsidx::Measure (include/tsidx/query.hpp): Euclidean, or DTW under a
+ * Sakoe-Chiba band of half-width `window` (0 <= window < n; the device path
+ * supports window <= 255). */
+enum { TSG_MEASURE_ED = 0, TSG_MEASURE_DTW = 1 };
+typedef struct tsg_measure {
+    int32_t kind;
+    int32_t window;
+} tsg_measure;
+
+/* exact_search / approximate_search with a Measure (query.hpp:133-151) for nq
+ * queries (host, or device when queries_on_device != 0). DTW follows
+ * calculate_real_distance_leaf's DTW branch (src/query.cpp:138-145): envelope
+ * bound on nodes and entries (mindist_envelope_isax), LB_Keogh, then banded DTW
+ * with abandonment; answers equal scan_nn(Measure::dtw(window)) with ties to the
+ * lowest position. Invalid window -> TSG_INVALID_ARGUMENT ("dtw window must be
+ * in [0, n)"). */
+tsg_status tsg_search_measure(tsg_index* index, const float* queries, int queries_on_device, uint32_t nq,
+                              const tsg_measure* measure, int approximate, tsg_result* out);
+
 tsg_status tsg_index_info(const tsg_index* index, uint64_t* count, uint64_t* length,
                           tsg_config* cfg, tsg_build_stats* stats);
 

@@ -20,8 +20,14 @@ EXPORTS = (
     "tsg_index_build", "tsg_index_build_device", "tsg_index_free", "tsg_index_info", "tsg_search",
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
-    "tsg_generate_series", "tsg_index_build_file",
+    "tsg_generate_series", "tsg_index_build_file", "tsg_search_measure",
 )
+
+TSG_MEASURE_ED, TSG_MEASURE_DTW = 0, 1
+
+
+class tsg_measure(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("window", C.c_int32)]
 
 
 class tsg_config(C.Structure):
@@ -80,6 +86,7 @@ def lib() -> C.CDLL:
         "tsg_index_build_file": (i32, [vp, C.c_char_p, u64, C.POINTER(tsg_config), u64, C.POINTER(vp),
                                        C.POINTER(tsg_build_stats)]),
         "tsg_index_free": (i32, [vp]),
+        "tsg_search_measure": (i32, [vp, vp, i32, u32, C.POINTER(tsg_measure), i32, C.POINTER(tsg_result)]),
         "tsg_index_info": (i32, [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(tsg_config),
                                  C.POINTER(tsg_build_stats)]),
         "tsg_search": (i32, [vp, vp, u32, C.POINTER(tsg_result)]),

@@ -143,7 +143,7 @@ namespace {
 void free_slots(DevIndex::Slots& t) {
     for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.gsurv),
                     static_cast<void*>(t.surv), static_cast<void*>(t.surv_lb), static_cast<void*>(t.cand_pos),
-                    static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq)})
+                    static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq), static_cast<void*>(t.env)})
         cudaFree(p);
     t = DevIndex::Slots{};
 }
@@ -162,6 +162,7 @@ void alloc_slots(const DevIndex& s, DevIndex::Slots& t, uint32_t n, uint64_t cap
     TSG_CUDA(cudaMalloc(&t.cand_pos, n * cap * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&t.cand_lb, n * cap * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.cand_sq, n * cap * sizeof(double)));
+    TSG_CUDA(cudaMalloc(&t.env, n * 2ull * s.n * sizeof(float)));
 }
 
 void free_shard(DevIndex& s) {
@@ -361,18 +362,18 @@ void ensure_queries(DevIndex& s, uint32_t nq) {
 // All nq device queries of one shard: batches of batch_max through the batch
 // slots, then any query that outgrew its slot again, alone, in the full-size
 // slot (allocated on first use). Results land in host_out.
-void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out) {
+void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out, int window) {
     ensure_results(s, nq);
     for (uint32_t off = 0; off < nq; off += s.batch_max) {
         const uint32_t b = std::min(s.batch_max, nq - off);
-        search_batch(s, s.batch, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off);
+        search_batch(s, s.batch, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off, window);
     }
     TSG_CUDA(cudaMemcpyAsync(host_out, s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
     TSG_CUDA(cudaStreamSynchronize(s.stream));
     for (uint32_t q = 0; q < nq; ++q) {
         if (!(host_out[q].flags & kResultOverflow)) continue;
         if (!s.big.n) alloc_slots(s, s.big, 1, s.N);
-        search_batch(s, s.big, dq + static_cast<uint64_t>(q) * s.n, 1, approximate, s.results + q);
+        search_batch(s, s.big, dq + static_cast<uint64_t>(q) * s.n, 1, approximate, s.results + q, window);
         TSG_CUDA(cudaMemcpyAsync(host_out + q, s.results + q, sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
         TSG_CUDA(cudaStreamSynchronize(s.stream));
         if (host_out[q].flags & kResultOverflow) throw std::logic_error("search: a full-size slot overflowed");
@@ -412,7 +413,8 @@ void merge_into(tsg_result& acc, const tsg_result& r, bool first) {
     acc.stats.queue_insertions += r.stats.queue_insertions;
 }
 
-void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg_result* out, bool approximate) {
+void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg_result* out, bool approximate,
+                int window = -1) {
     if (!ix) fail("search: null index");
     if (nq == 0) return;
     if (!queries || !out) fail("search: null buffer");
@@ -429,7 +431,7 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
                                      cudaMemcpyHostToDevice, s.stream));
             dq = s.queries;
         }
-        search_all(s, dq, nq, approximate, per[k].data());
+        search_all(s, dq, nq, approximate, per[k].data(), window);
     };
     if (ix->shards.size() == 1) {
         work(0);
@@ -661,6 +663,28 @@ tsg_status tsg_search_device(tsg_index* ix, const float* dev_queries, uint32_t n
 
 tsg_status tsg_approximate_search(tsg_index* ix, const float* host_query, tsg_result* out) {
     return guarded([&] { run_search(ix, host_query, true, 1, out, true); });
+}
+
+// Measure-aware search (exact_search / approximate_search with a Measure,
+// query.hpp:133-151): Euclidean, or DTW with a Sakoe-Chiba window (QueryState's
+// window check, src/query.cpp:88-90, same message).
+tsg_status tsg_search_measure(tsg_index* ix, const float* queries, int queries_on_device, uint32_t nq,
+                              const tsg_measure* m, int approximate, tsg_result* out) {
+    return guarded([&] {
+        if (!m) fail("exact_search: null measure");
+        int window = -1;
+        if (m->kind == TSG_MEASURE_DTW) {
+            if (!ix) fail("search: null index");
+            if (m->window < 0 || static_cast<uint64_t>(m->window) >= ix->cfg.n) fail("dtw window must be in [0, n)");
+            if (m->window > kMaxDtwWindow)
+                fail("dtw window " + std::to_string(m->window) + " above the device limit " +
+                     std::to_string(kMaxDtwWindow));
+            window = m->window;
+        } else if (m->kind != TSG_MEASURE_ED) {
+            fail("exact_search: unknown measure kind");
+        }
+        run_search(ix, queries, queries_on_device == 0, nq, out, approximate != 0, window);
+    });
 }
 
 tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length, int w, int bits, uint8_t* dev_words,

@@ -62,6 +62,7 @@ struct DevIndex {
         uint32_t* cand_pos = nullptr;   // [n][cap] candidate entries: refinement wave A front, B back
         float* cand_lb = nullptr;       // [n][cap]
         double* cand_sq = nullptr;      // [n][cap]
+        float* env = nullptr;           // [n][2][len] DTW: the query's upper / lower Keogh envelope
     };
     Slots batch, big;
     uint32_t batch_max = 128;       // queries per batch (TSG_BATCH)
@@ -132,8 +133,11 @@ void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, doubl
 // Query pipeline for nq device queries in slots [0, nq) of `slots`; writes
 // results[0..nq). Queries flagged kResultOverflow must be rerun with a slot
 // of capacity N (api.cu's search_all does that).
+// window < 0: Euclidean; window >= 0: DTW with that Sakoe-Chiba window
+// (Measure::dtw, src/query.cpp:88-92,138-145).
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
-                  struct DevResult* results);
+                  struct DevResult* results, int window = -1);
+constexpr int kMaxDtwWindow = 255;  // the device DTW keeps a band diagonal in registers (8 cells per lane)
 
 // Input generators (not on the timed path), see generate.cu.
 enum GenKind {

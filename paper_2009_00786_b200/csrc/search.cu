@@ -88,6 +88,7 @@ struct IndexView {
     uint32_t seed_cap;
     float split;
     uint64_t pos_offset;
+    int window;  // < 0: Euclidean; >= 0: DTW with this Sakoe-Chiba window
 };
 
 struct SlotView {
@@ -99,6 +100,7 @@ struct SlotView {
     uint32_t* cand_pos;
     float* cand_lb;
     double* cand_sq;
+    float* env;  // [slots][2][n] DTW envelopes (upper, lower)
     uint64_t cap, P, NG;
     int lut_len;
 };
@@ -142,6 +144,27 @@ __device__ __forceinline__ void fill_lut(const QueryShared& qs, int n, int w, in
         double gap = 0.0;
         if (x < lo) gap = lo - x;
         else if (x > hi) gap = x - hi;
+        out[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
+    }
+}
+
+// DTW: the same table for the envelope band [lower_paa, upper_paa]
+// (mindist_envelope_isax, src/metrics.cpp:48-70,194-196): per segment the
+// squared gap from the band to each symbol's region, times n/w, rounded down.
+// It is zero exactly on the symbols between those of lower_paa and
+// upper_paa, so box bounds clamp the lower_paa symbol into the box.
+__device__ __forceinline__ void fill_lut_band(const double* thr, const double* lo_paa, const double* hi_paa, int n,
+                                              int w, int bits, float* out) {
+    const unsigned card = 1u << bits;
+    const double scale = static_cast<double>(n) / static_cast<double>(w);
+    for (int idx = threadIdx.x; idx < w * 256; idx += blockDim.x) {
+        const int s = idx >> 8, v = idx & 255;
+        const unsigned prefix = static_cast<unsigned>(v) >> (8 - bits);
+        const double lo = prefix == 0 ? -INFINITY : thr[prefix - 1];
+        const double hi = prefix == card - 1 ? INFINITY : thr[prefix];
+        double gap = 0.0;
+        if (hi_paa[s] < lo) gap = lo - hi_paa[s];
+        else if (lo_paa[s] > hi) gap = lo_paa[s] - hi;
         out[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
     }
 }
@@ -455,8 +478,46 @@ __global__ void __launch_bounds__(kThreads)
     QueryWork* wk = S.work + q;
     load_query(s_q, queries + static_cast<uint64_t>(q) * ix.n, ix.n);
     prepare_query(s_q, ix.n, ix.w, ix.bits, ix.thr, qs);
-    fill_lut(qs, ix.n, ix.w, ix.bits, S.lut + static_cast<uint64_t>(q) * S.lut_len);
-    if (threadIdx.x < kMaxW) wk->qsym[threadIdx.x] = threadIdx.x < ix.w ? qs.qsym[threadIdx.x] : 0;
+    if (ix.window < 0) {
+        fill_lut(qs, ix.n, ix.w, ix.bits, S.lut + static_cast<uint64_t>(q) * S.lut_len);
+        if (threadIdx.x < kMaxW) wk->qsym[threadIdx.x] = threadIdx.x < ix.w ? qs.qsym[threadIdx.x] : 0;
+    } else {
+        // keogh_envelope (src/metrics.cpp:72-91,167-177): window max / min (exact,
+        // so a direct scan equals the reference's deque), then the bands' PAA.
+        float* up = s_q + ix.n;
+        float* lo = s_q + 2 * ix.n;
+        float* env = S.env + static_cast<uint64_t>(q) * 2 * ix.n;
+        const int r = ix.window;
+        for (int i = threadIdx.x; i < ix.n; i += blockDim.x) {
+            const int a = max(0, i - r), b = min(ix.n - 1, i + r);
+            float hi = s_q[a], lw = s_q[a];
+            for (int j = a + 1; j <= b; ++j) {
+                hi = fmaxf(hi, s_q[j]);
+                lw = fminf(lw, s_q[j]);
+            }
+            up[i] = hi;
+            lo[i] = lw;
+            env[i] = hi;
+            env[ix.n + i] = lw;
+        }
+        __syncthreads();
+        __shared__ double s_bpaa[2][kMaxW];
+        const int seg = ix.n / ix.w;
+        if (threadIdx.x < 2 * ix.w) {
+            const int g = threadIdx.x % ix.w, which = threadIdx.x / ix.w;  // 0: upper, 1: lower
+            const float* src = which == 0 ? up : lo;
+            double sum = 0.0;
+            for (int j = 0; j < seg; ++j) sum = __dadd_rn(sum, static_cast<double>(src[g * seg + j]));
+            s_bpaa[which][g] = __ddiv_rn(sum, static_cast<double>(seg));
+        }
+        __syncthreads();
+        fill_lut_band(qs.thr, s_bpaa[1], s_bpaa[0], ix.n, ix.w, ix.bits, S.lut + static_cast<uint64_t>(q) * S.lut_len);
+        // box bounds clamp the symbol of lower_paa (the band's first zero-gap symbol)
+        if (threadIdx.x < kMaxW)
+            wk->qsym[threadIdx.x] = threadIdx.x < ix.w
+                ? static_cast<unsigned char>(symbol_of(qs.thr, ix.bits, s_bpaa[1][threadIdx.x]) << (8 - ix.bits))
+                : 0;
+    }
     const uint32_t page = locate_page(ix.page_key, ix.page_dir, ix.P, query_key(qs.qsym, ix.w));
     if (threadIdx.x == 0) {
         const uint32_t leaf = ix.page_leaf[page];
@@ -480,7 +541,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->scan_bound = 0.f;
         wk->boxes = 0;
         for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
-        wk->stats[kRealDist] = b - a;
+        wk->stats[kRealDist] = ix.window < 0 ? b - a : 0;  // DTW seeds count the DTWs that ran
     }
 }
 
@@ -1234,6 +1295,227 @@ __global__ void __launch_bounds__(kThreads, 3)
     }
 }
 
+// --------------------------------------------------------------- DTW
+// Banded DTW (src/metrics.cpp:112-164) by one warp along anti-diagonals: the
+// cells of diagonal k = i + j inside the band |j - i| <= r are independent,
+// so lane l holds band offsets u = j - i + r = 2 (l + 32 t) + p (p = parity
+// of k + r, t < M slots) and each step reads its up / left neighbours from
+// diagonal k - 1 by shuffles and its diagonal neighbour from k - 2 in its own
+// registers. Every cell is min(up, diagonal, left) + (a_i - b_j)^2 in FP64
+// (product rounded, then the sum) — the reference's recurrence, so the value
+// is bit-identical (min is exact; dtw is symmetric bit for bit). Abandonment:
+// every warping path meets diagonal k or k + 1 and cell values only grow
+// along a path, so once both diagonals exceed cutoff_sq the distance does
+// too (sound; the reference abandons per row). Returns the squared distance
+// or +inf. r + 1 <= 32 M.
+template <int M>
+__device__ double warp_dtw_sq(const float* __restrict__ sa, const float* __restrict__ b, int n, int r,
+                              double cutoff_sq) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned kFull = 0xFFFFFFFFu;
+    double p1[M], p2[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) p1[t] = p2[t] = INFINITY;
+    double prev_min = INFINITY;
+    for (int k = 0; k < 2 * n - 1; ++k) {
+        const int p = (k + r) & 1;
+        double cur[M];
+        double cmin = INFINITY;
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            const double dn = __shfl_down_sync(kFull, p1[t], 1);
+            const double wrap_up = __shfl_sync(kFull, p1[t + 1 < M ? t + 1 : t], 0);
+            const double upn = __shfl_up_sync(kFull, p1[t], 1);
+            const double wrap_lo = __shfl_sync(kFull, p1[t > 0 ? t - 1 : 0], 31);
+            const double up = p == 0 ? p1[t] : (lane == 31 ? (t + 1 < M ? wrap_up : INFINITY) : dn);
+            const double left = p == 1 ? p1[t] : (lane == 0 ? (t > 0 ? wrap_lo : INFINITY) : upn);
+            const int u = 2 * (lane + 32 * t) + p;
+            const int delta = u - r;
+            const int i2 = k - delta;
+            const int i = i2 >> 1, j = (k + delta) >> 1;
+            double cell = INFINITY;
+            if (u <= 2 * r && i2 >= 0 && i < n && j >= 0 && j < n) {
+                const double best = (i == 0 && j == 0) ? 0.0 : fmin(fmin(up, left), p2[t]);
+                const double d = __dsub_rn(static_cast<double>(sa[i]), static_cast<double>(__ldg(b + j)));
+                cell = __dadd_rn(best, __dmul_rn(d, d));
+            }
+            cur[t] = cell;
+            cmin = fmin(cmin, cell);
+        }
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+            p2[t] = p1[t];
+            p1[t] = cur[t];
+        }
+        if ((k & 7) == 7) {
+            double m2 = fmin(cmin, prev_min);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m2 = fmin(m2, __shfl_xor_sync(kFull, m2, o));
+            if (m2 > cutoff_sq) return INFINITY;
+        }
+        prev_min = cmin;
+    }
+    // cell (n - 1, n - 1): diagonal 2n - 2, u = r
+    const int idx = (r - (r & 1)) / 2;
+    double v = INFINITY;
+#pragma unroll
+    for (int t = 0; t < M; ++t)
+        if (t == (idx >> 5)) v = p1[t];
+    return __shfl_sync(kFull, v, idx & 31);
+}
+
+// LB_Keogh (src/metrics.cpp:179-192), squared, by one warp (any summation
+// order: it is only a filter, compared with the same 1e-9 slack as the BSF).
+__device__ __forceinline__ double warp_lb_keogh_sq(const float* __restrict__ up, const float* __restrict__ lo,
+                                                   const float* __restrict__ c, int n) {
+    double sum = 0.0;
+    for (int i = threadIdx.x & 31; i < n; i += 32) {
+        const double v = __ldg(c + i);
+        double d = 0.0;
+        if (v > up[i]) d = v - up[i];
+        else if (v < lo[i]) d = lo[i] - v;
+        sum += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    return sum;
+}
+
+// One candidate row under DTW by a warp: LB_Keogh against the live BSF, then
+// the banded DTW abandoning at it (calculate_real_distance_leaf's DTW branch,
+// src/query.cpp:138-145). Returns the squared distance or +inf; `refined`
+// tells whether the DTW ran.
+template <int M>
+__device__ double warp_dtw_candidate(const float* s_q, const float* s_up, const float* s_lo, const float* row, int n,
+                                     int r, const QueryWork* wk, bool& refined) {
+    const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
+    refined = false;
+    if (warp_lb_keogh_sq(s_up, s_lo, row, n) > cut) return INFINITY;
+    refined = true;
+    return warp_dtw_sq<M>(s_q, row, n, r, cut);
+}
+
+// Query + envelope into shared memory: [query | upper | lower], n floats each.
+__device__ __forceinline__ void load_query_env(float* s, const float* q, const float* env, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        s[i] = q[i];
+        s[n + i] = env[i];
+        s[2 * n + i] = env[n + i];
+    }
+    __syncthreads();
+}
+
+// DTW seed: every row of the seed range, one warp per row. Grid (x, query).
+template <int M>
+__global__ void __launch_bounds__(kThreads)
+    k_seed_dtw(IndexView ix, SlotView S, const float* __restrict__ queries) {
+    extern __shared__ float s_qe[];
+    const int q = blockIdx.y;
+    QueryWork* wk = S.work + q;
+    const uint32_t a = wk->seed_begin, b = wk->seed_end;
+    if (wk->overflow || a + static_cast<uint64_t>(blockIdx.x) * kWarps >= b) return;
+    const int n = ix.n;
+    load_query_env(s_qe, queries + static_cast<uint64_t>(q) * n, S.env + static_cast<uint64_t>(q) * 2 * n, n);
+    uint32_t* cand_pos = S.cand_pos + q * S.cap;
+    double* cand_sq = S.cand_sq + q * S.cap;
+    const int lane = threadIdx.x & 31;
+    unsigned long long updates = 0, refined = 0;
+    for (uint64_t e = a + static_cast<uint64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5); e < b;
+         e += static_cast<uint64_t>(gridDim.x) * kWarps) {
+        const uint32_t p = ix.pos[e];
+        bool ran;
+        const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(p) * n,
+                                                n, ix.window, wk, ran);
+        if (lane == 0) {
+            cand_pos[e - a] = static_cast<uint32_t>(e);
+            updates += publish(wk, sq, e - a, cand_sq);
+            refined += ran ? 1 : 0;
+        }
+    }
+    if (lane == 0) {
+        if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+        if (refined) atomicAdd(&wk->stats[kRealDist], refined);
+    }
+}
+
+// DTW refinement wave: blocks pick a query (barriers only when switching),
+// warps claim chunks of 32 candidate records, keep those whose word bound is
+// within the BSF, and refine them one at a time (LB_Keogh, then DTW).
+template <int M>
+__global__ void __launch_bounds__(kThreads)
+    k_refine_dtw(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
+    extern __shared__ float s_qe[];
+    __shared__ int s_sel;
+    const int n = ix.n;
+    const int lane = threadIdx.x & 31;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
+    const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
+    auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
+        const unsigned long long c = w->cand;
+        if (wave == 0) {
+            begin = w->nseed;
+            end = c & 0xFFFFFFFFull;
+        } else {
+            begin = S.cap - (c >> 32);
+            end = S.cap;
+        }
+    };
+    auto nchunks = [&](const QueryWork* w) -> uint32_t {
+        if (w->overflow) return 0;
+        uint64_t b, e;
+        range(w, b, e);
+        return static_cast<uint32_t>((e - b + 31) / 32);
+    };
+    unsigned long long refined = 0, updates = 0;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
+        __syncthreads();
+        const int q = s_sel;
+        if (q < 0) break;
+        cur = q;
+        QueryWork* wk = S.work + q;
+        load_query_env(s_qe, queries + static_cast<uint64_t>(q) * n, S.env + static_cast<uint64_t>(q) * 2 * n, n);
+        const uint32_t* cand_pos = S.cand_pos + q * S.cap;
+        const float* cand_lb = S.cand_lb + q * S.cap;
+        double* cand_sq = S.cand_sq + q * S.cap;
+        uint64_t begin, end;
+        range(wk, begin, end);
+        const uint32_t nch = nchunks(wk);
+        for (;;) {
+            uint32_t chunk = 0;
+            if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
+            chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+            if (chunk >= nch) break;
+            const uint64_t c = begin + static_cast<uint64_t>(chunk) * 32 + lane;
+            const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            const bool in = c < end;
+            const bool keep = in && cand_lb[c] <= bnd;
+            if (in && !keep) cand_sq[c] = INFINITY;
+            const uint32_t p = keep ? ix.pos[cand_pos[c]] : 0u;
+            unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+            while (m) {
+                const int src = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
+                const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
+                bool ran;
+                const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n,
+                                                        ix.rows + static_cast<uint64_t>(pp) * n, n, ix.window, wk, ran);
+                if (lane == 0) {
+                    refined += ran ? 1 : 0;
+                    updates += publish(wk, sq, cc, cand_sq);
+                }
+            }
+        }
+        if (lane == 0) {
+            if (refined) atomicAdd(&wk->stats[kRealDist], refined);
+            if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+        }
+        refined = updates = 0;
+    }
+}
+
 // ----------------------------------------------------------- finalize
 // Grid (x, query): lowest position among the candidates whose sqrt(sum)
 // equals the best distance; the last block of a query writes its result
@@ -1293,7 +1575,7 @@ int blocks_per_sm(K kernel, size_t smem) {
 }  // namespace
 
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
-                  DevResult* results) {
+                  DevResult* results, int window) {
     if (nq == 0) return;
     if (nq > slots.n) throw std::logic_error("search_batch: batch larger than its slots");
     cudaStream_t st = ix.stream;
@@ -1319,7 +1601,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     for (const void* f : {reinterpret_cast<const void*>(refine), reinterpret_cast<const void*>(seed),
                           reinterpret_cast<const void*>(lbscan), reinterpret_cast<const void*>(bound),
                           reinterpret_cast<const void*>(groups), reinterpret_cast<const void*>(k_prepare)})
-        TSG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        TSG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
 
     IndexView iv{};
     iv.rows = ix.rows;
@@ -1347,8 +1629,17 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
     iv.split = ix.refine_split;
     iv.pos_offset = ix.pos_offset;
+    iv.window = window;
     SlotView sv{slots.work, slots.lut, slots.gsurv, slots.surv, slots.surv_lb, slots.cand_pos, slots.cand_lb,
-                slots.cand_sq, slots.cap, ix.P, ix.NG, w * 256};
+                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256};
+    // DTW kernels, by band-diagonal registers per lane (window <= 32 M - 1).
+    const bool dtw = window >= 0;
+    if (window > kMaxDtwWindow) throw std::invalid_argument("exact_search: dtw window above the device limit");
+    const int dtw_m = window < 32 ? 1 : window < 64 ? 2 : window < 128 ? 4 : 8;
+    auto seed_dtw = dtw_m == 1 ? k_seed_dtw<1> : dtw_m == 2 ? k_seed_dtw<2> : dtw_m == 4 ? k_seed_dtw<4> : k_seed_dtw<8>;
+    auto refine_dtw = dtw_m == 1 ? k_refine_dtw<1> : dtw_m == 2 ? k_refine_dtw<2> : dtw_m == 4 ? k_refine_dtw<4>
+                                                                                     : k_refine_dtw<8>;
+    const size_t qe_bytes = 3ull * n * sizeof(float);
 
     const int sms = ix.sms;
     const unsigned seed_x = (iv.seed_cap + kThreads / kRowLanes - 1) / (kThreads / kRowLanes);
@@ -1360,6 +1651,12 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const unsigned refine_grid = tma ? static_cast<unsigned>(sms * blocks_per_sm(refine_tma, tma_bytes))
                                      : static_cast<unsigned>(sms * blocks_per_sm(refine, qd_bytes));
     const unsigned fin_x = std::max(1u, std::min(256u, static_cast<unsigned>(sms * 32 / nq)));
+    if (dtw) {
+        TSG_CUDA(cudaFuncSetAttribute(seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        TSG_CUDA(cudaFuncSetAttribute(refine_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    }
+    const unsigned seed_dtw_x = (iv.seed_cap + kWarps - 1) / kWarps;
+    const unsigned refine_dtw_grid = dtw ? static_cast<unsigned>(sms * blocks_per_sm(refine_dtw, qe_bytes)) : 0u;
 
     // Optional per-kernel timing: events around every launch, summed after the batch.
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
@@ -1378,9 +1675,10 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     };
     const int inq = static_cast<int>(nq);
     mark(2, [&] {
-        k_prepare<<<nq, kThreads, q_bytes, st>>>(iv, sv, d_queries);
+        k_prepare<<<nq, kThreads, dtw ? qe_bytes : q_bytes, st>>>(iv, sv, d_queries);
         TSG_LAUNCHED();
-        seed<<<dim3(seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
+        if (dtw) seed_dtw<<<dim3(seed_dtw_x, nq), kThreads, qe_bytes, st>>>(iv, sv, d_queries);
+        else seed<<<dim3(seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
         TSG_LAUNCHED();
     });
     if (!approximate) {
@@ -1396,7 +1694,8 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                 TSG_LAUNCHED();
             });
             mark(wave == 0 ? 3 : 5, [&] {
-                if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, qe_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 TSG_LAUNCHED();
             });

@@ -66,11 +66,15 @@ tsg_ctx* default_context() {
 }
 
 void check_measure(const Measure& m, std::size_t n) {
-    if (m.kind == MeasureKind::dtw) {
-        if (m.window < 0 || static_cast<std::size_t>(m.window) >= n)
-            throw std::invalid_argument("dtw window must be in [0, n)");
-        throw std::invalid_argument("exact_search: the device path answers Euclidean (Measure::ed()) queries only");
-    }
+    if (m.kind == MeasureKind::dtw && (m.window < 0 || static_cast<std::size_t>(m.window) >= n))
+        throw std::invalid_argument("dtw window must be in [0, n)");
+}
+
+tsg_measure measure_of(const Measure& m) {
+    tsg_measure c{};
+    c.kind = m.kind == MeasureKind::dtw ? TSG_MEASURE_DTW : TSG_MEASURE_ED;
+    c.window = m.window;
+    return c;
 }
 
 SearchStats stats_of(const tsg_search_stats& s) {
@@ -278,7 +282,8 @@ SearchResult exact_search(const Index& index, std::span<const float> query, Meas
         throw std::invalid_argument("query length " + std::to_string(query.size()) +
                                     " does not match the index series length " + std::to_string(index.config().n));
     tsg_result r{};
-    throw_status(tsg_search(index.handle(), query.data(), 1, &r));
+    const tsg_measure m = measure_of(measure);
+    throw_status(tsg_search_measure(index.handle(), query.data(), 0, 1, &m, 0, &r));
     return {r.distance, r.position, stats_of(r.stats)};
 }
 
@@ -290,7 +295,8 @@ std::vector<SearchResult> exact_search_batch(const Index& index, std::span<const
                                     std::to_string(n));
     const std::size_t nq = queries.size() / n;
     std::vector<tsg_result> raw(nq);
-    if (nq) throw_status(tsg_search(index.handle(), queries.data(), static_cast<uint32_t>(nq), raw.data()));
+    const tsg_measure m = measure_of(measure);
+    if (nq) throw_status(tsg_search_measure(index.handle(), queries.data(), 0, static_cast<uint32_t>(nq), &m, 0, raw.data()));
     std::vector<SearchResult> out;
     out.reserve(nq);
     for (const auto& r : raw) out.push_back({r.distance, r.position, stats_of(r.stats)});
@@ -303,7 +309,8 @@ ApproxResult approximate_search(const Index& index, std::span<const float> query
         throw std::invalid_argument("query length " + std::to_string(query.size()) +
                                     " does not match the index series length " + std::to_string(index.config().n));
     tsg_result r{};
-    throw_status(tsg_approximate_search(index.handle(), query.data(), &r));
+    const tsg_measure m = measure_of(measure);
+    throw_status(tsg_search_measure(index.handle(), query.data(), 0, 1, &m, 1, &r));
     return {r.distance, r.position};
 }
 

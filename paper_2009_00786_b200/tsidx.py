@@ -314,10 +314,13 @@ def save_dataset(path, rows) -> None:
 
 
 def _check_measure(measure: Measure, n: int) -> None:
-    if measure.kind == MeasureKind.dtw:
-        if measure.window < 0 or measure.window >= n:
-            raise InvalidArgument("dtw window must be in [0, n)")
-        raise InvalidArgument("exact_search: the device path answers Euclidean (Measure.ed()) queries only")
+    if measure.kind == MeasureKind.dtw and (measure.window < 0 or measure.window >= n):
+        raise InvalidArgument("dtw window must be in [0, n)")
+
+
+def _measure_c(measure: Measure) -> "_lib.tsg_measure":
+    return _lib.tsg_measure(_lib.TSG_MEASURE_DTW if measure.kind == MeasureKind.dtw else _lib.TSG_MEASURE_ED,
+                            measure.window)
 
 
 def _query_array(index: Index, query) -> np.ndarray:
@@ -330,11 +333,16 @@ def _query_array(index: Index, query) -> np.ndarray:
 
 
 def exact_search(index: Index, query, measure: Measure = Measure.ed(), options: SearchOptions = None) -> SearchResult:
-    """tsidx::exact_search (Euclidean). options.workers/queues/mode are accepted and ignored."""
+    """tsidx::exact_search: Euclidean or DTW (Measure.dtw(window)). options.workers/queues/mode are
+    accepted and ignored."""
     _check_measure(measure, index.config().n)
     q = _query_array(index, query)
     out = (_lib.tsg_result * 1)()
-    check(lib().tsg_search(index.handle, q.ctypes.data, 1, out))
+    if measure.kind == MeasureKind.euclidean:
+        check(lib().tsg_search(index.handle, q.ctypes.data, 1, out))
+    else:
+        m = _measure_c(measure)
+        check(lib().tsg_search_measure(index.handle, q.ctypes.data, 0, 1, C.byref(m), 0, out))
     return _result_from_c(out[0])
 
 
@@ -342,18 +350,25 @@ def exact_search_batch(index: Index, queries, measure: Measure = Measure.ed()) -
     """Exact 1-NN for a (nq, n) block of queries in one call (queries answered in order)."""
     _check_measure(measure, index.config().n)
     n = index.config().n
+    m = _measure_c(measure)
     if _is_cuda_tensor(queries):
         t = queries.contiguous()
         if t.dim() != 2 or t.shape[1] != n:
             raise InvalidArgument(f"query length {tuple(t.shape)} does not match the index series length {n}")
         out = (_lib.tsg_result * t.shape[0])()
-        check(lib().tsg_search_device(index.handle, C.c_void_p(t.data_ptr()), t.shape[0], out))
+        if measure.kind == MeasureKind.euclidean:
+            check(lib().tsg_search_device(index.handle, C.c_void_p(t.data_ptr()), t.shape[0], out))
+        else:
+            check(lib().tsg_search_measure(index.handle, C.c_void_p(t.data_ptr()), 1, t.shape[0], C.byref(m), 0, out))
         return [_result_from_c(r) for r in out]
     q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
     if q.ndim != 2 or q.shape[1] != n:
         raise InvalidArgument(f"query length {q.shape} does not match the index series length {n}")
     out = (_lib.tsg_result * q.shape[0])()
-    check(lib().tsg_search(index.handle, q.ctypes.data, q.shape[0], out))
+    if measure.kind == MeasureKind.euclidean:
+        check(lib().tsg_search(index.handle, q.ctypes.data, q.shape[0], out))
+    else:
+        check(lib().tsg_search_measure(index.handle, q.ctypes.data, 0, q.shape[0], C.byref(m), 0, out))
     return [_result_from_c(r) for r in out]
 
 
@@ -362,7 +377,8 @@ def approximate_search(index: Index, query, measure: Measure = Measure.ed()) -> 
     _check_measure(measure, index.config().n)
     q = _query_array(index, query)
     out = (_lib.tsg_result * 1)()
-    check(lib().tsg_approximate_search(index.handle, q.ctypes.data, out))
+    m = _measure_c(measure)
+    check(lib().tsg_search_measure(index.handle, q.ctypes.data, 0, 1, C.byref(m), 1, out))
     return _result_from_c(out[0])
 
 

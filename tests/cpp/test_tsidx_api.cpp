@@ -111,7 +111,16 @@ int main() {
     CHECK(throws<std::invalid_argument>([&] { exact_search(index, wrong); }));
     std::vector<float> zq(256, 0.f);
     CHECK(throws<std::invalid_argument>([&] { exact_search(index, zq, Measure::dtw(300)); }));
-    CHECK(throws<std::invalid_argument>([&] { exact_search(index, zq, Measure::dtw(10)); }));
+    // DTW: the banded DTW distance never exceeds the Euclidean one
+    // (the diagonal is a warping path); window 0 is the sequentially summed ED.
+    for (std::size_t k = 0; k < 3; ++k) {
+        const auto q = queries.series(k);
+        const SearchResult ed = exact_search(index, q);
+        const SearchResult d10 = exact_search(index, q, Measure::dtw(10));
+        const SearchResult d0 = exact_search(index, q, Measure::dtw(0));
+        CHECK(d10.distance <= ed.distance * (1 + 1e-12));
+        CHECK(std::abs(d0.distance - ed.distance) <= 1e-9 * ed.distance);
+    }
 
     // dataset file round trip + padding (src/dataset.cpp:87-137)
     const auto path = std::filesystem::temp_directory_path() / "tsidx_b200_roundtrip.f32";

@@ -370,3 +370,37 @@ def test_build_from_file_errors(tmp_path):
         tg.build_index_from_file(bad, tg.IndexConfig(n=32, w=16))
     with pytest.raises(tg.TsgError, match="cannot stat"):
         tg.build_index_from_file(tmp_path / "missing.f32", tg.IndexConfig(n=32, w=16))
+
+
+# ---- DTW: exact search under Measure::dtw(window) ----------------
+
+@pytest.mark.parametrize("count,n,w,leaf,window", [
+    (3000, 64, 16, 20, 0), (3000, 64, 16, 20, 6), (2500, 64, 16, 200, 31), (2000, 96, 16, 50, 40),
+    (1500, 128, 16, 30, 100), (1200, 60, 5, 10, 12), (1000, 256, 16, 64, 25), (800, 32, 8, 2000, 31),
+])
+def test_dtw_exact_matches_scan(oracle, count, n, w, leaf, window):
+    rng = np.random.default_rng(count + n + window)
+    rows = oracle.generate(count, n, 800 + n)
+    queries = np.concatenate([oracle.generate(4, n, 900 + n + window),
+                              rows[rng.integers(0, count, 3)] + 0.1 * rng.standard_normal((3, n)).astype(np.float32)])
+    index = tg.build_index(rows, tg.IndexConfig(n=n, w=w, leaf_capacity=leaf))
+    res = tg.exact_search_batch(index, queries.astype(np.float32), tg.Measure.dtw(window))
+    for k, q in enumerate(queries.astype(np.float32)):
+        d, p = oracle.scan_nn_dtw(rows, q, window)
+        assert res[k].position == p, (k, res[k].position, p, res[k].distance, d)
+        assert res[k].distance == d, (k, res[k].distance, d)
+        one = tg.exact_search(index, q, tg.Measure.dtw(window))
+        assert one.position == p and one.distance == d
+        a = tg.approximate_search(index, q, tg.Measure.dtw(window))
+        assert a.distance >= d
+
+
+def test_dtw_members_and_limits(oracle):
+    rows = oracle.generate(1500, 64, 1301, znorm=False)
+    index = tg.build_index(rows, tg.IndexConfig(n=64, w=16, leaf_capacity=20))
+    for m in (3, 777, 1499):
+        r = tg.exact_search(index, rows[m], tg.Measure.dtw(5))
+        assert r.distance == 0.0 and r.position == m
+    big = tg.build_index(oracle.generate(300, 512, 1302), tg.IndexConfig(n=512, w=16))
+    with pytest.raises(tg.InvalidArgument):
+        tg.exact_search(big, np.zeros(512, np.float32), tg.Measure.dtw(256))  # above the device band limit
