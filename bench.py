@@ -176,18 +176,27 @@ def ref_inputs(name, count, n, nq_total, sigma, sample_cap):
     return idx, qs, count, gen_ns
 
 
-def cpu_baseline(name, count_full, n, sigma, sample, queries):
+def cpu_baseline(name, count_full, n, sigma, sample, queries, dtw=-1):
     """The unmodified reference (oracle/_ref) on this host's cores, on a
     bounded sample of the workload (the first `sample` series of the same
-    dataset): reference build_index + exact_search (mq, 24 queues, all cores)."""
+    dataset): reference build_index + exact_search (mq, 24 queues, all cores).
+    With dtw >= 0: exact_search(Measure::dtw(dtw)) on a 1M-series sample."""
     from oracle.oracle import Reference
 
     cores = Reference().hardware_concurrency()
+    if dtw >= 0:
+        sample = min(sample, 1_000_000)
+        queries = min(queries, 5)
     idx, qs, used, _ = ref_inputs(name, min(sample, count_full), n, queries, sigma, sample)
     t = []
     for q in qs:
-        d, p, st, ns = idx.exact_search(q)
-        t.append(ns)
+        if dtw >= 0:
+            t0 = time.perf_counter_ns()
+            idx.exact_search_dtw(q, dtw)
+            t.append(time.perf_counter_ns() - t0)
+        else:
+            d, p, st, ns = idx.exact_search(q)
+            t.append(ns)
     qps = len(t) / (sum(t) * 1e-9)
     build_ns = idx.build_stats["build_ns"]
     return {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "reference",
@@ -296,11 +305,13 @@ def run_ours(args):
     build_dev_s = max_over_ranks(bs.build_ns * 1e-9)
     k1_s = max_over_ranks(bs.summarise_ms * 1e-3)
 
+    measure = tg.Measure.dtw(args.dtw) if args.dtw >= 0 else tg.Measure.ed()
+
     def step(batch, host):
         if host:
-            res = tg.exact_search_batch(index, qhost[batch * nq:(batch + 1) * nq])
+            res = tg.exact_search_batch(index, qhost[batch * nq:(batch + 1) * nq], measure)
         else:
-            res = tg.exact_search_batch(index, qdev[batch * nq:(batch + 1) * nq])
+            res = tg.exact_search_batch(index, qdev[batch * nq:(batch + 1) * nq], measure)
         rec = np.array([(r.distance, r.position) for r in res], dtype=np.float64)
         if world > 1:  # the cross-GPU exchange: all-gather of (distance, position) over NCCL
             rec = allgather_merge(rec, device=f"cuda:{local}")
@@ -396,13 +407,14 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                cpu = cpu_baseline(args.config, count, n, args.sigma, args.cpu_sample, args.cpu_queries)
+                cpu = cpu_baseline(args.config, count, n, args.sigma, args.cpu_sample, args.cpu_queries, args.dtw)
             except Exception as ex:  # reported, not hidden
                 cpu = {"error": str(ex)}
         clocks = clk.summary()
         share = group_ms[dom] / max(sum(group_ms.values()), 1e-12)
         line = {
-            "metric": METRIC, "value": round(qps, 3), "unit": "queries/s", "n_gpus": world,
+            "metric": METRIC if args.dtw < 0 else METRIC.replace("exact 1-NN", f"exact 1-NN DTW(window {args.dtw})"),
+            "value": round(qps, 3), "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed * 1e3 / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
@@ -513,6 +525,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per step (default: the config's 100)")
     ap.add_argument("--sigma", type=float, default=0.1, help="c5 query noise")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtw", type=int, default=-1, help="search under Measure::dtw(window) (SURVEY 8(f)#4)")
     ap.add_argument("--ingest", type=int, default=0,
                     help="instead of the search bench: build from a file of this many series (SURVEY 8(f)#3)")
     args = ap.parse_args()

@@ -1323,12 +1323,21 @@ __device__ double warp_dtw_sq(const float* __restrict__ sa, const float* __restr
         double cmin = INFINITY;
 #pragma unroll
         for (int t = 0; t < M; ++t) {
-            const double dn = __shfl_down_sync(kFull, p1[t], 1);
-            const double wrap_up = __shfl_sync(kFull, p1[t + 1 < M ? t + 1 : t], 0);
-            const double upn = __shfl_up_sync(kFull, p1[t], 1);
-            const double wrap_lo = __shfl_sync(kFull, p1[t > 0 ? t - 1 : 0], 31);
-            const double up = p == 0 ? p1[t] : (lane == 31 ? (t + 1 < M ? wrap_up : INFINITY) : dn);
-            const double left = p == 1 ? p1[t] : (lane == 0 ? (t > 0 ? wrap_lo : INFINITY) : upn);
+            // On a diagonal of parity 0 the up neighbour is this lane's own cell
+            // of diagonal k - 1 and the left one is lane - 1's; on parity 1 the
+            // left one is this lane's and the up one lane + 1's (p is uniform).
+            double up, left;
+            if (p == 0) {
+                up = p1[t];
+                const double upn = __shfl_up_sync(kFull, p1[t], 1);
+                const double wrap = M > 1 ? __shfl_sync(kFull, p1[t > 0 ? t - 1 : 0], 31) : INFINITY;
+                left = lane == 0 ? (t > 0 ? wrap : INFINITY) : upn;
+            } else {
+                left = p1[t];
+                const double dn = __shfl_down_sync(kFull, p1[t], 1);
+                const double wrap = M > 1 ? __shfl_sync(kFull, p1[t + 1 < M ? t + 1 : t], 0) : INFINITY;
+                up = lane == 31 ? (t + 1 < M ? wrap : INFINITY) : dn;
+            }
             const int u = 2 * (lane + 32 * t) + p;
             const int delta = u - r;
             const int i2 = k - delta;
