@@ -152,13 +152,14 @@ void free_slots(DevIndex::Slots& t) {
 void alloc_slots(const DevIndex& s, DevIndex::Slots& t, uint32_t n, uint64_t cap) {
     t.n = n;
     t.cap = cap;
-    const uint64_t P = std::max<uint64_t>(s.P, 1), NG = std::max<uint64_t>(s.NG, 1);
+    const uint64_t NG = std::max<uint64_t>(s.NG, 1);
     TSG_CUDA(cudaMalloc(&t.work, n * sizeof(QueryWork)));
     TSG_CUDA(cudaMemset(t.work, 0, n * sizeof(QueryWork)));
     TSG_CUDA(cudaMalloc(&t.lut, n * static_cast<size_t>(s.w) * 256 * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.gsurv, n * NG * sizeof(uint32_t)));
-    TSG_CUDA(cudaMalloc(&t.surv, n * P * sizeof(uint2)));
-    TSG_CUDA(cudaMalloc(&t.surv_lb, n * P * sizeof(float)));
+    t.rcap = std::max<uint64_t>(s.R + s.P, 1);  // a page touches its runs; boundary runs count once per page
+    TSG_CUDA(cudaMalloc(&t.surv, n * t.rcap * sizeof(uint2)));
+    TSG_CUDA(cudaMalloc(&t.surv_lb, n * t.rcap * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.cand_pos, n * cap * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&t.cand_lb, n * cap * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.cand_sq, n * cap * sizeof(double)));
@@ -331,7 +332,8 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     size_t free_b = 0, total_b = 0;
     TSG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t per_slot_fixed = sizeof(QueryWork) + static_cast<uint64_t>(s.w) * 1024 +
-                                    std::max<uint64_t>(s.NG, 1) * 4 + std::max<uint64_t>(s.P, 1) * 12;
+                                    std::max<uint64_t>(s.NG, 1) * 4 + (s.R + s.P + 1) * 12 +
+                                    static_cast<uint64_t>(s.n) * 8;
     const uint64_t budget = static_cast<uint64_t>(0.45 * static_cast<double>(free_b));
     const uint64_t fixed = per_slot_fixed * s.batch_max;
     const uint64_t cand_budget = budget > fixed ? budget - fixed : 0;

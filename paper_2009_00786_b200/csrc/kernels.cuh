@@ -57,8 +57,9 @@ struct DevIndex {
         struct QueryWork* work = nullptr;  // [n]
         float* lut = nullptr;           // [n][w][256] squared-gap tables
         uint32_t* gsurv = nullptr;      // [n][NG] surviving page groups
-        uint2* surv = nullptr;          // [n][P] surviving pages' entry ranges: wave 0 front, wave 1 back
-        float* surv_lb = nullptr;       // [n][P] their box bounds
+        uint64_t rcap = 0;              // run-list capacity per slot (every run of the shard)
+        uint2* surv = nullptr;          // [n][rcap] surviving runs' entry ranges: wave 0 front, wave 1 back
+        float* surv_lb = nullptr;       // [n][rcap] their box bounds
         uint32_t* cand_pos = nullptr;   // [n][cap] candidate entries: refinement wave A front, B back
         float* cand_lb = nullptr;       // [n][cap]
         double* cand_sq = nullptr;      // [n][cap]
@@ -93,8 +94,9 @@ struct QueryWork {
     unsigned int nseed;
     unsigned int seed_begin, seed_end;  // index range refined as the seed
     unsigned int ngroups;               // surviving page groups
-    unsigned int nsurv;                 // surviving pages, wave 0 (bound <= split x seed bound)
-    unsigned int nsurv_hi;              // surviving pages, wave 1 (stored from the back of surv)
+    // surviving runs: wave 0 (low 32 bits, bound <= split x seed bound, front of
+    // the run list) and wave 1 (high 32 bits, back of the list)
+    unsigned long long runs;
     unsigned int next[kNextCount];      // work-chunk counters of the persistent kernels
     unsigned int done_blocks;           // finalize's last-block counter
     unsigned int best_pos;

@@ -103,6 +103,7 @@ struct SlotView {
     float* env;  // [slots][2][n] DTW envelopes (upper, lower)
     uint64_t cap, P, NG;
     int lut_len;
+    uint64_t rcap;  // run-list capacity per slot
 };
 
 __device__ __forceinline__ double bsf_of(unsigned long long bits) {
@@ -532,8 +533,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->seed_begin = a;
         wk->seed_end = b;
         wk->ngroups = 0;
-        wk->nsurv = 0;
-        wk->nsurv_hi = 0;
+        wk->runs = 0;
         for (int k = 0; k < kNextCount; ++k) wk->next[k] = 0;
         wk->done_blocks = 0;
         wk->best_pos = 0xFFFFFFFFu;
@@ -633,10 +633,52 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ------------------------------------------------------------- bound
-// Level 2: the pages of the surviving groups (persistent, affinity chunks of
-// kThreads x kGP pages). Pages whose bound is within the BSF (and outside the
-// seed range) survive, split into page wave 0 (bound <= split x BSF, front of
-// surv) and wave 1 (back of surv); one atomic pair per block and chunk.
+// Levels 2 and 3: the pages of the surviving groups, then the aligned
+// kRun-entry runs of the surviving pages (persistent, affinity chunks of
+// kThreads x kGP pages). A page survives when its bound is within the BSF
+// (and it is not inside the seed range); its runs are then bounded by all
+// threads of the block at once (the chunk's surviving pages are compacted in
+// shared memory and each thread takes (page, run) items), and every run within
+// the BSF is listed, clipped to its page: run wave 0 (bound <= split x BSF,
+// front of the slot's run list) or wave 1 (back). Survivors are staged per
+// warp and written with one 64-bit atomic per flush (both waves' counts).
+constexpr int kRunsPerPage = kPage / kRun + 1;  // an unaligned page touches at most 9 runs
+constexpr int kRunStage = 128;
+
+__device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, const float* s_l, int cnt, int lane,
+                                           float cut, uint64_t rcap, uint2* __restrict__ surv,
+                                           float* __restrict__ surv_lb) {
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+        const int i = i0 + lane;
+        const bool valid = i < cnt;
+        const float lb = valid ? s_l[i] : 0.f;
+        const bool low = valid && lb <= cut;
+        const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
+        unsigned long long old = 0;
+        if (lane == 0)
+            old = atomicAdd(&wk->runs, static_cast<unsigned long long>(__popc(ml)) |
+                                           (static_cast<unsigned long long>(__popc(mh)) << 32));
+        old = __shfl_sync(0xFFFFFFFFu, old, 0);
+        if (lane == 0 && (old & 0xFFFFFFFFull) + __popc(ml) + (old >> 32) + __popc(mh) > rcap)
+            atomicExch(&wk->overflow, 1u);  // cannot happen with rcap = R + P; never write out of range
+        const unsigned below = (1u << lane) - 1u;
+        if (low) {
+            const uint64_t at = (old & 0xFFFFFFFFull) + __popc(ml & below);
+            if (at < rcap) {
+                surv[at] = s_r[i];
+                surv_lb[at] = lb;
+            }
+        } else if (valid) {
+            const uint64_t off = (old >> 32) + __popc(mh & below);
+            if (off < rcap) {
+                surv[rcap - 1 - off] = s_r[i];
+                surv_lb[rcap - 1 - off] = lb;
+            }
+        }
+    }
+    __syncwarp();
+}
+
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     k_bound(IndexView ix, SlotView S, int nq) {
@@ -644,41 +686,53 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     constexpr uint32_t kRound = static_cast<uint32_t>(kThreads) * kGP;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
+    __shared__ uint2 s_pages[kRound];            // the chunk's surviving pages
+    __shared__ uint2 s_r[kWarps][kRunStage];     // staged surviving runs
+    __shared__ float s_l[kWarps][kRunStage];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
     uint4 q4[H];
     float bound = 0.f, cut = 0.f;
     uint32_t sa = 0, sb = 0;
-    unsigned long long pruned = 0, nodes = 0;
+    unsigned long long pruned = 0, nodes = 0, boxes = 0;
+    int cnt = 0;
     auto nchunks = [](const QueryWork* wk) { return (wk->ngroups * static_cast<uint32_t>(kGroup) + kRound - 1) / kRound; };
-    auto flush_stats = [&](int q) {
+    auto leave_query = [&](int q) {
+        QueryWork* w = S.work + q;
+        if (cnt) flush_runs(w, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, S.surv + q * S.rcap,
+                            S.surv_lb + q * S.rcap);
+        cnt = 0;
         pruned = warp_sum(pruned);
         nodes = warp_sum(nodes);
-        if ((threadIdx.x & 31) == 0) {
-            if (pruned) atomicAdd(&S.work[q].stats[kPruned], pruned);
-            if (nodes) atomicAdd(&S.work[q].stats[kLbNode], nodes);
+        boxes = warp_sum(boxes);
+        if (lane == 0) {
+            if (pruned) atomicAdd(&w->stats[kPruned], pruned);
+            if (nodes) atomicAdd(&w->stats[kLbNode], nodes);
+            if (boxes) atomicAdd(&w->boxes, boxes);
         }
-        pruned = nodes = 0;
+        pruned = nodes = boxes = 0;
     };
     uint32_t chunk = 0, pre = ~0u;
     for (int q = -1;;) {
         q = claim(S.work, nq, kNextBound, cur, chunk, pre, q, nchunks);
+        if (q != loaded && loaded >= 0) leave_query(loaded);
         if (q < 0) break;
         pre = claim_ahead(S.work, q, kNextBound);
         QueryWork* wk = S.work + q;
         if (q != loaded) {
-            if (loaded >= 0) flush_stats(loaded);
             load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
 #pragma unroll
             for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
             bound = wk->scan_bound;
-            cut = bound * ix.split;  // wave 0: the most promising pages
+            cut = bound * ix.split;  // wave 0: the most promising runs
             sa = wk->seed_begin;
             sb = wk->seed_end;
             loaded = q;
         }
         const uint32_t* gsurv = S.gsurv + q * S.NG;
-        uint2* surv = S.surv + q * S.P;
-        float* surv_lb = S.surv_lb + q * S.P;
+        uint2* surv = S.surv + q * S.rcap;
+        float* surv_lb = S.surv_lb + q * S.rcap;
         const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
         const uint64_t base = static_cast<uint64_t>(chunk) * kRound;
         uint4 bl[kGP][H], bh[kGP][H];
@@ -697,44 +751,85 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
             ea[k] = valid[k] ? ix.page_off[p] : 0u;
             eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
         }
-        unsigned lowmask = 0, highmask = 0;
-        float lbs[kGP];
+        unsigned keep = 0;
 #pragma unroll
         for (int k = 0; k < kGP; ++k) {
-            lbs[k] = 0.f;
             if (!valid[k]) continue;
             nodes += 1;
             const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
-            lbs[k] = lb;
             const bool seeded = ea[k] >= sa && eb[k] <= sb;
-            const bool keep = !seeded && lb <= bound;
-            lowmask |= (keep && lb <= cut) ? (1u << k) : 0u;
-            highmask |= (keep && lb > cut) ? (1u << k) : 0u;
-            pruned += (!keep && !seeded) ? 1 : 0;
+            if (!seeded && lb <= bound) keep |= 1u << k;
+            else if (!seeded) pruned += 1;
         }
-        const uint2 at0 = block_reserve(__popc(lowmask), __popc(highmask), &wk->nsurv, &wk->nsurv_hi);
-        uint32_t at = at0.x, at_hi = at0.y;
+        // compact the chunk's surviving pages into shared memory
+        __shared__ uint32_t s_wsum[kWarps];
+        __shared__ uint32_t s_total;
+        const uint32_t mine = __popc(keep);
+        uint32_t incl = mine;
 #pragma unroll
-        for (int k = 0; k < kGP; ++k) {
-            if (lowmask & (1u << k)) {
-                surv_lb[at] = lbs[k];
-                surv[at++] = make_uint2(ea[k], eb[k]);
-            } else if (highmask & (1u << k)) {
-                const uint64_t slot = ix.P - 1 - at_hi++;
-                surv_lb[slot] = lbs[k];
-                surv[slot] = make_uint2(ea[k], eb[k]);
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int i = 0; i < kWarps; ++i) {
+                const uint32_t c = s_wsum[i];
+                s_wsum[i] = tot;
+                tot += c;
+            }
+            s_total = tot;
+        }
+        __syncthreads();
+        uint32_t at = s_wsum[warp] + incl - mine;
+#pragma unroll
+        for (int k = 0; k < kGP; ++k)
+            if (keep & (1u << k)) s_pages[at++] = make_uint2(ea[k], eb[k]);
+        __syncthreads();
+        // their runs: (page, run) items over all threads
+        const uint32_t nrun_items = s_total * kRunsPerPage;
+        for (uint32_t j0 = 0; j0 < nrun_items; j0 += kThreads) {
+            const uint32_t j = j0 + threadIdx.x;
+            bool ok = false;
+            uint32_t e0 = 0, e1 = 0;
+            uint64_t r = 0;
+            if (j < nrun_items) {
+                const uint2 pg = s_pages[j / kRunsPerPage];
+                r = pg.x / kRun + j % kRunsPerPage;
+                e0 = max(pg.x, static_cast<uint32_t>(r * kRun));
+                e1 = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
+                ok = e0 < e1;
+            }
+            uint4 rl[H], rh[H];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                rl[h] = ok ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                rh[h] = ok ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            }
+            const float lb = ok ? box_bound<H, W16>(s_lut, q4, rl, rh, ix.w) : INFINITY;
+            const bool pass = ok && lb <= bound;
+            boxes += ok ? 1 : 0;
+            pruned += ok && !pass ? 1 : 0;
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+            if (pass) {
+                const int slot = cnt + __popc(m & below);
+                s_r[warp][slot] = make_uint2(e0, e1);
+                s_l[warp][slot] = lb;
+            }
+            cnt += __popc(m);
+            __syncwarp();
+            if (cnt > kRunStage - 32) {
+                flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
+                cnt = 0;
             }
         }
     }
-    if (loaded >= 0) flush_stats(loaded);
 }
 
 // ------------------------------------------------------------ lbscan
 constexpr int kStageCap = 256;
-#ifndef TSG_TRIP_PER_WARP
-#define TSG_TRIP_PER_WARP 4
-#endif
-constexpr int kTripPerWarp = TSG_TRIP_PER_WARP;      // page triples per warp per chunk
 
 // Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
 // upward after the seed range, wave B downward from the top of the slot's
@@ -776,21 +871,18 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
     __syncwarp();
 }
 
-// One page wave (persistent; warps claim chunks of kTripPerWarp page triples):
-// wave 0 scans surv[0, nsurv), wave 1 surv[P - nsurv_hi, P) re-filtered
-// against the BSF that refinement wave A tightened. Below the page sit two
-// more box levels over the sorted words, aligned kRun-entry runs and
-// kQuad-entry quads, bounded like the page boxes:
-//   pages: a warp takes three surviving pages at a time; lane 10j + t bounds
-//          run t of page j (a <= 128-entry page touches at most 9 runs);
-//   runs:  surviving runs (clipped to their page) queue in shared memory;
-//          eight at a time, lane 4k + u bounds quad u of queued run k;
-//   quads: surviving quads queue likewise; sixteen at a time, each lane
-//          bounds the words of entry u of two queued quads.
-// Only the words of surviving quads are read. Within a warp the next page
-// triple's ranges and run boxes are in flight while the current one is
-// bounded. Candidates are staged per warp and flushed when the stage fills
-// or the block moves to another query.
+// One run wave (persistent; warps claim chunks of 32 listed runs): wave 0
+// scans the front of the slot's run list, wave 1 the back, re-filtered
+// against the BSF that refinement wave A tightened. Below the run sit the
+// aligned kQuad-entry quads, bounded like the other boxes:
+//   runs:  a lane takes one listed run (clipped to its page); those still
+//          within the BSF queue in shared memory;
+//   quads: eight queued runs at a time, lane 4k + u bounds quad u of run k;
+//          surviving quads queue likewise;
+//   words: sixteen queued quads at a time, each lane bounds the words of
+//          entry u of two queued quads.
+// Only the words of surviving quads are read. Candidates are staged per warp
+// and flushed when the stage fills or the block moves to another query.
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     k_lbscan(IndexView ix, SlotView S, int nq, int wave) {
@@ -804,11 +896,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     __shared__ uint2 s_qq[kWarps][kRing];  // surviving quads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
-    const int grp = lane / 10, t = lane - 10 * grp;  // page of the triple, run of the page (lanes 30, 31 idle)
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
     float bound = 0.f, cut = 0.f;
-    uint32_t nsurv = 0;
     QueryWork* wk = nullptr;
     uint32_t* cand_pos = nullptr;
     float* cand_lb = nullptr;
@@ -820,8 +910,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     const int k_next = wave == 0 ? kNextScan0 : kNextScan1;
     auto nchunks = [wave](const QueryWork* w) -> uint32_t {
         if (w->overflow) return 0;
-        const uint32_t ns = wave == 0 ? w->nsurv : w->nsurv_hi;
-        return ((ns + 2) / 3 + kTripPerWarp - 1) / kTripPerWarp;
+        const unsigned long long r = w->runs;
+        const uint32_t ns = static_cast<uint32_t>(wave == 0 ? (r & 0xFFFFFFFFull) : (r >> 32));
+        return (ns + 31) / 32;
     };
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
         if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
@@ -911,35 +1002,6 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         while (qt - qh >= 16) drain_quads();
     };
 
-    uint32_t na = 0, nb = 0, nrun = 0;
-    bool nvalid = false;
-    uint4 nbl[H], nbh[H];
-    auto fetch = [&](uint64_t T) {
-        uint32_t a = 0, b = 0;
-        if (lane < 3) {
-            const uint64_t i = 3 * T + lane;
-            if (i < nsurv) {
-                const uint64_t slot = wave == 0 ? i : ix.P - 1 - i;
-                if (wave == 0 || surv_lb[slot] <= bound) {
-                    const uint2 r = surv[slot];
-                    a = r.x;
-                    b = r.y;
-                } else {
-                    pruned += 1;
-                }
-            }
-        }
-        na = __shfl_sync(0xFFFFFFFFu, a, min(grp, 2));
-        nb = __shfl_sync(0xFFFFFFFFu, b, min(grp, 2));
-        nrun = na / kRun + t;
-        nvalid = grp < 3 && na < nb && nrun * kRun < nb;
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            nbl[h] = nvalid ? ld_stream_u4(ix.run_lo + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-            nbh[h] = nvalid ? ld_stream_u4(ix.run_hi + static_cast<uint64_t>(nrun) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-        }
-    };
-
     // Query loop (block level; the only barriers): pick a query with chunks
     // left, load its table; then every warp claims chunks of it on its own
     // (lane 0, the next claim issued while the current chunk runs) until it
@@ -961,12 +1023,12 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         // their own bound; page wave 1 (scanned after wave A is refined)
         // feeds wave B.
         cut = wave == 0 ? wk->scan_bound * ix.split : -1.f;
-        nsurv = wave == 0 ? wk->nsurv : wk->nsurv_hi;
+        const unsigned long long rr = wk->runs;
+        const uint64_t nruns = wave == 0 ? (rr & 0xFFFFFFFFull) : (rr >> 32);
         cand_pos = S.cand_pos + q * S.cap;
         cand_lb = S.cand_lb + q * S.cap;
-        surv = S.surv + q * S.P;
-        surv_lb = S.surv_lb + q * S.P;
-        const uint64_t ntrip = (static_cast<uint64_t>(nsurv) + 2) / 3;
+        surv = S.surv + q * S.rcap;
+        surv_lb = S.surv_lb + q * S.rcap;
         const uint32_t nch = nchunks(wk);
         uint32_t chunk = 0;
         if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
@@ -974,30 +1036,20 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         while (chunk < nch) {
             uint32_t pre = 0;
             if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
-            const uint64_t t0 = static_cast<uint64_t>(chunk) * kTripPerWarp;
-            const uint64_t t1 = u64min(t0 + kTripPerWarp, ntrip);
-            if (t0 < t1) fetch(t0);
-            for (uint64_t T = t0; T < t1; ++T) {
-                const uint32_t a = na, b = nb, r = nrun;
-                const bool valid = nvalid;
-                uint4 bl[H], bh[H];
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    bl[h] = nbl[h];
-                    bh[h] = nbh[h];
-                }
-                if (T + 1 < t1) fetch(T + 1);
-                const bool pass = valid && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;  // run box
-                pruned += valid && !pass ? 1 : 0;
-                boxes += valid ? 1 : 0;
-                const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-                if (pass)
-                    s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] =
-                        make_uint2(max(a, r * kRun), min(b, r * kRun + kRun));
-                rt += __popc(m);
-                __syncwarp();
-                while (rt - rh >= 8) drain_runs();
+            const uint64_t i = static_cast<uint64_t>(chunk) * 32 + lane;
+            bool pass = false;
+            uint2 run = make_uint2(0, 0);
+            if (i < nruns) {
+                const uint64_t slot = wave == 0 ? i : S.rcap - 1 - i;
+                run = surv[slot];
+                pass = wave == 0 || surv_lb[slot] <= bound;  // wave 1: re-filtered with the tightened BSF
+                pruned += pass ? 0 : 1;
             }
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+            if (pass) s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
+            rt += __popc(m);
+            __syncwarp();
+            while (rt - rh >= 8) drain_runs();
             chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
         }
         while (rt != rh) drain_runs();
@@ -1640,7 +1692,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.pos_offset = ix.pos_offset;
     iv.window = window;
     SlotView sv{slots.work, slots.lut, slots.gsurv, slots.surv, slots.surv_lb, slots.cand_pos, slots.cand_lb,
-                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256};
+                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256, slots.rcap};
     // DTW kernels, by band-diagonal registers per lane (window <= 32 M - 1).
     const bool dtw = window >= 0;
     if (window > kMaxDtwWindow) throw std::invalid_argument("exact_search: dtw window above the device limit");
