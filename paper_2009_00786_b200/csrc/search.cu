@@ -788,41 +788,51 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         for (int k = 0; k < kGP; ++k)
             if (keep & (1u << k)) s_pages[at++] = make_uint2(ea[k], eb[k]);
         __syncthreads();
-        // their runs: (page, run) items over all threads
+        // their runs: (page, run) items over all threads, kRunU per thread per
+        // step with every box load issued before the first bound
+        constexpr int kRunU = 2;
         const uint32_t nrun_items = s_total * kRunsPerPage;
-        for (uint32_t j0 = 0; j0 < nrun_items; j0 += kThreads) {
-            const uint32_t j = j0 + threadIdx.x;
-            bool ok = false;
-            uint32_t e0 = 0, e1 = 0;
-            uint64_t r = 0;
-            if (j < nrun_items) {
-                const uint2 pg = s_pages[j / kRunsPerPage];
-                r = pg.x / kRun + j % kRunsPerPage;
-                e0 = max(pg.x, static_cast<uint32_t>(r * kRun));
-                e1 = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
-                ok = e0 < e1;
-            }
-            uint4 rl[H], rh[H];
+        for (uint32_t j0 = 0; j0 < nrun_items; j0 += kThreads * kRunU) {
+            bool ok[kRunU];
+            uint32_t e0[kRunU], e1[kRunU];
+            uint4 rl[kRunU][H], rh[kRunU][H];
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                rl[h] = ok ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                rh[h] = ok ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            for (int u = 0; u < kRunU; ++u) {
+                const uint32_t j = j0 + threadIdx.x + kThreads * u;
+                ok[u] = false;
+                e0[u] = e1[u] = 0;
+                uint64_t r = 0;
+                if (j < nrun_items) {
+                    const uint2 pg = s_pages[j / kRunsPerPage];
+                    r = pg.x / kRun + j % kRunsPerPage;
+                    e0[u] = max(pg.x, static_cast<uint32_t>(r * kRun));
+                    e1[u] = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
+                    ok[u] = e0[u] < e1[u];
+                }
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    rl[u][h] = ok[u] ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                    rh[u][h] = ok[u] ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                }
             }
-            const float lb = ok ? box_bound<H, W16>(s_lut, q4, rl, rh, ix.w) : INFINITY;
-            const bool pass = ok && lb <= bound;
-            boxes += ok ? 1 : 0;
-            pruned += ok && !pass ? 1 : 0;
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-            if (pass) {
-                const int slot = cnt + __popc(m & below);
-                s_r[warp][slot] = make_uint2(e0, e1);
-                s_l[warp][slot] = lb;
-            }
-            cnt += __popc(m);
-            __syncwarp();
-            if (cnt > kRunStage - 32) {
-                flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
-                cnt = 0;
+#pragma unroll
+            for (int u = 0; u < kRunU; ++u) {
+                const float lb = ok[u] ? box_bound<H, W16>(s_lut, q4, rl[u], rh[u], ix.w) : INFINITY;
+                const bool pass = ok[u] && lb <= bound;
+                boxes += ok[u] ? 1 : 0;
+                pruned += ok[u] && !pass ? 1 : 0;
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
+                if (pass) {
+                    const int slot = cnt + __popc(m & below);
+                    s_r[warp][slot] = make_uint2(e0[u], e1[u]);
+                    s_l[warp][slot] = lb;
+                }
+                cnt += __popc(m);
+                __syncwarp();
+                if (cnt > kRunStage - 32) {
+                    flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
+                    cnt = 0;
+                }
             }
         }
     }
