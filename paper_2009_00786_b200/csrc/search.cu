@@ -648,33 +648,41 @@ constexpr int kRunStage = 128;
 __device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, const float* s_l, int cnt, int lane,
                                            float cut, uint64_t rcap, uint2* __restrict__ surv,
                                            float* __restrict__ surv_lb) {
+    // one 64-bit atomic reserves both waves' slots for the whole stage
+    int lo_cnt = 0;
+    for (int i = lane; i < cnt; i += 32) lo_cnt += s_l[i] <= cut ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
+    unsigned long long old = 0;
+    if (lane == 0) {
+        old = atomicAdd(&wk->runs, static_cast<unsigned long long>(lo_cnt) |
+                                       (static_cast<unsigned long long>(cnt - lo_cnt) << 32));
+        if ((old & 0xFFFFFFFFull) + (old >> 32) + cnt > rcap)
+            atomicExch(&wk->overflow, 1u);  // cannot happen with rcap = R + P; never write out of range
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, 0);
+    uint64_t at_lo = old & 0xFFFFFFFFull, at_hi = old >> 32;
+    const unsigned below = (1u << lane) - 1u;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < cnt;
         const float lb = valid ? s_l[i] : 0.f;
         const bool low = valid && lb <= cut;
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
-        unsigned long long old = 0;
-        if (lane == 0)
-            old = atomicAdd(&wk->runs, static_cast<unsigned long long>(__popc(ml)) |
-                                           (static_cast<unsigned long long>(__popc(mh)) << 32));
-        old = __shfl_sync(0xFFFFFFFFu, old, 0);
-        if (lane == 0 && (old & 0xFFFFFFFFull) + __popc(ml) + (old >> 32) + __popc(mh) > rcap)
-            atomicExch(&wk->overflow, 1u);  // cannot happen with rcap = R + P; never write out of range
-        const unsigned below = (1u << lane) - 1u;
         if (low) {
-            const uint64_t at = (old & 0xFFFFFFFFull) + __popc(ml & below);
+            const uint64_t at = at_lo + __popc(ml & below);
             if (at < rcap) {
                 surv[at] = s_r[i];
                 surv_lb[at] = lb;
             }
         } else if (valid) {
-            const uint64_t off = (old >> 32) + __popc(mh & below);
+            const uint64_t off = at_hi + __popc(mh & below);
             if (off < rcap) {
                 surv[rcap - 1 - off] = s_r[i];
                 surv_lb[rcap - 1 - off] = lb;
             }
         }
+        at_lo += __popc(ml);
+        at_hi += __popc(mh);
     }
     __syncwarp();
 }
@@ -790,7 +798,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         __syncthreads();
         // their runs: (page, run) items over all threads, kRunU per thread per
         // step with every box load issued before the first bound
-        constexpr int kRunU = 2;
+#ifndef TSG_RUN_U
+#define TSG_RUN_U 2
+#endif
+        constexpr int kRunU = TSG_RUN_U;
         const uint32_t nrun_items = s_total * kRunsPerPage;
         for (uint32_t j0 = 0; j0 < nrun_items; j0 += kThreads * kRunU) {
             bool ok[kRunU];
