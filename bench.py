@@ -382,9 +382,10 @@ def run_ours(args):
     lb_nodes, lb_entries, refined, cands, boxes = stats_acc[0], stats_acc[1], stats_acc[2], stats_acc[5], stats_acc[6]
     NG = (P + 7) // 8
     group_bytes = {  # algorithmic bytes over the timed pass (per-unit figures of DESIGN.md §4 x the counters)
-        # every group box (2 x 16 B) + the pages of surviving groups (2 x 16 B boxes + 8 B offsets)
-        "bound": nqt * NG * 2 * ws + max(lb_nodes - nqt * NG, 0) * (2 * ws + 8),
-        # run / quad boxes (2 x 16 B) + words of surviving quads + candidate records (pos + bound)
+        # every group box (2 x 16 B) + pages of surviving groups and runs of surviving pages
+        # (lb_node_calcs - groups; 2 x 16 B boxes, + 8 B offsets for pages: counted as 36 B)
+        "bound": nqt * NG * 2 * ws + max(lb_nodes - nqt * NG, 0) * (2 * ws + 4),
+        # quad boxes (box_calcs, 2 x 16 B) + words of surviving quads + candidate records (pos + bound)
         "lbscan": boxes * 2 * ws + lb_entries * ws + cands * 8,
         # kept candidate rows (full length) + their records (bound, entry, pos gather, sum)
         "refine": refined * 4 * n + cands * 20,

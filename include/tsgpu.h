@@ -101,7 +101,8 @@ typedef struct tsg_search_stats {
 typedef struct tsg_result {
     double distance;
     uint32_t position;
-    uint32_t box_calcs;  /* sub-page (run / quad) box bounds evaluated (saturates at 2^32-1) */
+    uint32_t box_calcs;  /* quad (4-entry) box bounds evaluated (saturates at 2^32-1); group, page and
+                            run boxes count in stats.lb_node_calcs */
     tsg_search_stats stats;
 } tsg_result;
 

@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     uint4 q4[H];
     float bound = 0.f, cut = 0.f;
     uint32_t sa = 0, sb = 0;
-    unsigned long long pruned = 0, nodes = 0, boxes = 0;
+    unsigned long long pruned = 0, nodes = 0;
     int cnt = 0;
     auto nchunks = [](const QueryWork* wk) { return (wk->ngroups * static_cast<uint32_t>(kGroup) + kRound - 1) / kRound; };
     auto leave_query = [&](int q) {
@@ -713,13 +713,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         cnt = 0;
         pruned = warp_sum(pruned);
         nodes = warp_sum(nodes);
-        boxes = warp_sum(boxes);
         if (lane == 0) {
             if (pruned) atomicAdd(&w->stats[kPruned], pruned);
             if (nodes) atomicAdd(&w->stats[kLbNode], nodes);
-            if (boxes) atomicAdd(&w->boxes, boxes);
         }
-        pruned = nodes = boxes = 0;
+        pruned = nodes = 0;
     };
     uint32_t chunk = 0, pre = ~0u;
     for (int q = -1;;) {
@@ -830,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
             for (int u = 0; u < kRunU; ++u) {
                 const float lb = ok[u] ? box_bound<H, W16>(s_lut, q4, rl[u], rh[u], ix.w) : INFINITY;
                 const bool pass = ok[u] && lb <= bound;
-                boxes += ok[u] ? 1 : 0;
+                nodes += ok[u] ? 1 : 0;  // run boxes are node bounds (box_calcs counts quads)
                 pruned += ok[u] && !pass ? 1 : 0;
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
                 if (pass) {

@@ -117,7 +117,7 @@ class SearchResult:
     distance: float
     position: int
     stats: SearchStats
-    box_calcs: int = 0  # sub-page (run / quad) box bounds evaluated (device extension of SearchStats)
+    box_calcs: int = 0  # quad box bounds evaluated (device extension of SearchStats)
 
 
 @dataclasses.dataclass
