@@ -59,7 +59,7 @@ def peaks():
     return 6650.0, "fallback"
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "round1b_ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "round1c_ncu_summary.json")
 NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tma.ncu-rep"],
                "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
 
