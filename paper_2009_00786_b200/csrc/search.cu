@@ -1193,10 +1193,15 @@ __global__ void __launch_bounds__(kThreads, 3)
     constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
     constexpr int kTq = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
+#ifndef TSG_HALF_ROWS
+#define TSG_HALF_ROWS 1
+#endif
+    // half-row fetches keep the lane-ordered query layout when a half is a whole number of 8-block rounds
+    constexpr bool kHalf = TSG_HALF_ROWS && NB % 16 == 0;
     extern __shared__ __align__(128) unsigned char s_dyn[];
     float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][2][n]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // lane-ordered query
-    __shared__ __align__(8) uint64_t s_bar[kGroups][2];
+    __shared__ __align__(8) uint64_t s_bar[kGroups][3];
     __shared__ uint32_t s_c[kWarps][kTmaChunk], s_p[kWarps][kTmaChunk];
     __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const bool leader = j8 == 0;
     const int hsw = (j8 >> 2) & 1;
     constexpr unsigned row_bytes = static_cast<unsigned>(n) * 4u;
-    if (threadIdx.x < 2 * kGroups) mbar_init(&s_bar[threadIdx.x >> 1][threadIdx.x & 1], 1);
+    for (int i = threadIdx.x; i < 3 * kGroups; i += blockDim.x) mbar_init(&s_bar[i / 3][i % 3], 1);
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     unsigned phase = 0;  // bit b: parity of this group's buffer b
@@ -1234,6 +1239,60 @@ __global__ void __launch_bounds__(kThreads, 3)
         fence_proxy_async_smem();
         mbar_expect_tx(&s_bar[g][b], row_bytes);
         tma_copy_1d(buf0 + b * n, ix.rows + static_cast<uint64_t>(p) * n, row_bytes, &s_bar[g][b]);
+    };
+    // Half rows (kHalf): three half-row buffers per group at 0, n/2, n; a row's
+    // first half is fetched one row ahead, its second half only if the sum of
+    // the first half is still within the BSF (squared_l2's abandonment,
+    // metrics.cpp:28, at half-row granularity) — most rows stop there.
+    constexpr int kHB = NB / 2;                       // blocks per half row
+    constexpr int kTh = (kHB + kRowLanes - 1) / kRowLanes;
+    constexpr unsigned half_bytes = row_bytes / 2;
+    auto hbuf = [&](int b) { return buf0 + b * (n / 2); };
+    auto issue_half = [&](int b, uint32_t p, int h) {  // leader: half h of row p -> half buffer b
+        fence_proxy_async_smem();
+        mbar_expect_tx(&s_bar[g][b], half_bytes);
+        tma_copy_1d(hbuf(b), ix.rows + static_cast<uint64_t>(p) * n + h * (n / 2), half_bytes, &s_bar[g][b]);
+    };
+    auto wait_buf = [&](int b) {
+        mbar_wait(&s_bar[g][b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+    };
+    // Block sums of half h of a row in half buffer b, added left to right by the
+    // leader onto `sum` (the leader's value is the one that counts).
+    auto half_sum = [&](int b, int h, double sum) -> double {
+        const float* row = hbuf(b);
+        double blk[kTh];
+#pragma unroll
+        for (int t = 0; t < kTh; ++t) {
+            const int kh = j8 + kRowLanes * t;  // block within the half
+            blk[t] = 0.0;
+            if (kh < kHB) {
+                const float4 ua = *reinterpret_cast<const float4*>(row + 8 * kh + 4 * hsw);
+                const float4 ub = *reinterpret_cast<const float4*>(row + 8 * kh + 4 * (1 - hsw));
+                const float4 x0 = hsw ? ub : ua, x1 = hsw ? ua : ub;
+                const float x[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                const int tf = t + h * kTh;  // lane-ordered query block index (block j8 + 8 tf)
+                double b8 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const double d = __dsub_rn(static_cast<double>(x[i]), s_qd[(8 * tf + i) * 8 + j8]);
+                    b8 = __dadd_rn(b8, __dmul_rn(d, d));
+                }
+                blk[t] = b8;
+            }
+        }
+        double* sums = reinterpret_cast<double*>(hbuf(b));
+        __syncwarp(gmask);  // every lane has read its slices
+#pragma unroll
+        for (int t = 0; t < kTh; ++t)
+            if (j8 + kRowLanes * t < kHB) sums[j8 + kRowLanes * t] = blk[t];
+        __syncwarp(gmask);
+        if (leader) {
+#pragma unroll
+            for (int k = 0; k < kHB; ++k) sum = __dadd_rn(sum, sums[k]);
+        }
+        __syncwarp(gmask);  // the buffer is free again
+        return sum;
     };
     for (;;) {
         __syncthreads();  // every warp is done with the previous query
@@ -1302,6 +1361,55 @@ __global__ void __launch_bounds__(kThreads, 3)
             __syncwarp();
             const uint32_t next = __shfl_sync(0xFFFFFFFFu, pre, 0);
             load_records(next, rlb, rcp);  // in flight during phase 2
+            if constexpr (kHalf) {
+                // Phase 2 (half rows): first halves one row ahead in buffers 0 / 1,
+                // the pending second half in buffer 2, completed one row later.
+                bool pending = false;
+                uint32_t pend_c = 0;
+                double pend_sum = 0.0;
+                unsigned long long pend_seen = 0;
+                if (leader && static_cast<uint32_t>(wg) < m) issue_half(0, s_p[warp][wg], 0);
+                int fb = 0;
+                for (uint32_t j = wg; j < m; j += kWarpGroups, fb ^= 1) {
+                    if (leader && j + kWarpGroups < m) issue_half(fb ^ 1, s_p[warp][j + kWarpGroups], 0);
+                    const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
+                    wait_buf(fb);
+                    const double part = half_sum(fb, 0, 0.0);
+                    if (pending) {  // the previous row's second half
+                        wait_buf(2);
+                        const double sum = half_sum(2, 1, pend_sum);
+                        if (leader) {
+                            cand_sq[pend_c] = sum;
+                            const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
+                            if (sb < pend_seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
+                        }
+                        pending = false;
+                    }
+                    const bool cont = __shfl_sync(gmask, leader && !(part > bsf_of(seen) * kSlack), gbase);
+                    if (leader) refined += 1;
+                    if (cont) {
+                        if (leader) issue_half(2, s_p[warp][j], 1);
+                        pending = true;
+                        pend_c = s_c[warp][j];
+                        pend_sum = part;
+                        pend_seen = seen;
+                    } else if (leader) {
+                        cand_sq[s_c[warp][j]] = INFINITY;  // abandoned after its first half
+                    }
+                }
+                if (pending) {
+                    wait_buf(2);
+                    const double sum = half_sum(2, 1, pend_sum);
+                    if (leader) {
+                        cand_sq[pend_c] = sum;
+                        const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
+                        if (sb < pend_seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
+                    }
+                }
+                __syncwarp();  // the warp's list is reused by the next chunk
+                chunk = next;
+                continue;
+            }
             // Phase 2: the kept rows, double-buffered per group.
             if (leader && static_cast<uint32_t>(wg) < m) issue(0, s_p[warp][wg]);
             int b = 0;
