@@ -143,7 +143,8 @@ namespace {
 void free_slots(DevIndex::Slots& t) {
     for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.gsurv),
                     static_cast<void*>(t.surv), static_cast<void*>(t.surv_lb), static_cast<void*>(t.cand_pos),
-                    static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq), static_cast<void*>(t.env)})
+                    static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq), static_cast<void*>(t.env),
+                    static_cast<void*>(t.dpage), static_cast<void*>(t.dpage_lb)})
         cudaFree(p);
     t = DevIndex::Slots{};
 }
@@ -160,6 +161,8 @@ void alloc_slots(const DevIndex& s, DevIndex::Slots& t, uint32_t n, uint64_t cap
     t.rcap = std::max<uint64_t>(s.R + s.P, 1);  // a page touches its runs; boundary runs count once per page
     TSG_CUDA(cudaMalloc(&t.surv, n * t.rcap * sizeof(uint2)));
     TSG_CUDA(cudaMalloc(&t.surv_lb, n * t.rcap * sizeof(float)));
+    TSG_CUDA(cudaMalloc(&t.dpage, n * std::max<uint64_t>(s.P, 1) * sizeof(uint2)));
+    TSG_CUDA(cudaMalloc(&t.dpage_lb, n * std::max<uint64_t>(s.P, 1) * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.cand_pos, n * cap * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&t.cand_lb, n * cap * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.cand_sq, n * cap * sizeof(double)));
@@ -332,7 +335,7 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     size_t free_b = 0, total_b = 0;
     TSG_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const uint64_t per_slot_fixed = sizeof(QueryWork) + static_cast<uint64_t>(s.w) * 1024 +
-                                    std::max<uint64_t>(s.NG, 1) * 4 + (s.R + s.P + 1) * 12 +
+                                    std::max<uint64_t>(s.NG, 1) * 4 + (s.R + 2 * s.P + 2) * 12 +
                                     static_cast<uint64_t>(s.n) * 8;
     const uint64_t budget = static_cast<uint64_t>(0.45 * static_cast<double>(free_b));
     const uint64_t fixed = per_slot_fixed * s.batch_max;

@@ -60,6 +60,8 @@ struct DevIndex {
         uint64_t rcap = 0;              // run-list capacity per slot (every run of the shard)
         uint2* surv = nullptr;          // [n][rcap] surviving runs' entry ranges: wave 0 front, wave 1 back
         float* surv_lb = nullptr;       // [n][rcap] their box bounds
+        uint2* dpage = nullptr;         // [n][P] deferred pages' entry ranges
+        float* dpage_lb = nullptr;      // [n][P] their box bounds
         uint32_t* cand_pos = nullptr;   // [n][cap] candidate entries: refinement wave A front, B back
         float* cand_lb = nullptr;       // [n][cap]
         double* cand_sq = nullptr;      // [n][cap]
@@ -85,7 +87,7 @@ constexpr int kRun = 16;  // entries per run box (the sub-page filter level)
 constexpr int kQuad = 4;  // entries per quad box (the level below runs)
 
 // Per-query device scratch (reset by the prepare kernel).
-enum WorkCounter { kNextBound = 0, kNextScan0, kNextRefine0, kNextScan1, kNextRefine1, kNextCount };
+enum WorkCounter { kNextBound = 0, kNextScan0, kNextRefine0, kNextBound1, kNextScan1, kNextRefine1, kNextCount };
 struct QueryWork {
     unsigned long long bsf_bits;  // best squared distance so far (double bits)
     // candidate records: wave A (low 32 bits, from the front, after the seed
@@ -97,6 +99,7 @@ struct QueryWork {
     // surviving runs: wave 0 (low 32 bits, bound <= split x seed bound, front of
     // the run list) and wave 1 (high 32 bits, back of the list)
     unsigned long long runs;
+    unsigned int ndefer;                // pages deferred to the second bound pass (bound > split x seed bound)
     unsigned int next[kNextCount];      // work-chunk counters of the persistent kernels
     unsigned int done_blocks;           // finalize's last-block counter
     unsigned int best_pos;

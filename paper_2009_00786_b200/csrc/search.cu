@@ -104,6 +104,8 @@ struct SlotView {
     uint64_t cap, P, NG;
     int lut_len;
     uint64_t rcap;  // run-list capacity per slot
+    uint2* dpage;   // [slots][P] pages deferred to the second bound pass
+    float* dpage_lb;
 };
 
 __device__ __forceinline__ double bsf_of(unsigned long long bits) {
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->seed_end = b;
         wk->ngroups = 0;
         wk->runs = 0;
+        wk->ndefer = 0;
         for (int k = 0; k < kNextCount; ++k) wk->next[k] = 0;
         wk->done_blocks = 0;
         wk->best_pos = 0xFFFFFFFFu;
@@ -689,9 +692,10 @@ __device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, cons
 
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
-    k_bound(IndexView ix, SlotView S, int nq) {
+    k_bound(IndexView ix, SlotView S, int nq, int pass) {
     constexpr int H = WS / 16;
     constexpr uint32_t kRound = static_cast<uint32_t>(kThreads) * kGP;
+    const int k_next = pass == 0 ? kNextBound : kNextBound1;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint2 s_pages[kRound];            // the chunk's surviving pages
@@ -705,7 +709,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     uint32_t sa = 0, sb = 0;
     unsigned long long pruned = 0, nodes = 0;
     int cnt = 0;
-    auto nchunks = [](const QueryWork* wk) { return (wk->ngroups * static_cast<uint32_t>(kGroup) + kRound - 1) / kRound; };
+    auto nchunks = [pass](const QueryWork* wk) -> uint32_t {
+        if (wk->overflow) return 0;
+        const uint32_t items = pass == 0 ? wk->ngroups * static_cast<uint32_t>(kGroup) : wk->ndefer;
+        return (items + kRound - 1) / kRound;
+    };
     auto leave_query = [&](int q) {
         QueryWork* w = S.work + q;
         if (cnt) flush_runs(w, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, S.surv + q * S.rcap,
@@ -721,17 +729,18 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     };
     uint32_t chunk = 0, pre = ~0u;
     for (int q = -1;;) {
-        q = claim(S.work, nq, kNextBound, cur, chunk, pre, q, nchunks);
+        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
         if (q != loaded && loaded >= 0) leave_query(loaded);
         if (q < 0) break;
-        pre = claim_ahead(S.work, q, kNextBound);
+        pre = claim_ahead(S.work, q, k_next);
         QueryWork* wk = S.work + q;
         if (q != loaded) {
             load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
 #pragma unroll
             for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
-            bound = wk->scan_bound;
-            cut = bound * ix.split;  // wave 0: the most promising runs
+            // pass 0: the seed bound; pass 1 (after refinement wave A): the tightened BSF
+            bound = pass == 0 ? wk->scan_bound : bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            cut = pass == 0 ? bound * ix.split : -1.f;  // wave 0: the most promising runs
             sa = wk->seed_begin;
             sb = wk->seed_end;
             loaded = q;
@@ -739,33 +748,62 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         const uint32_t* gsurv = S.gsurv + q * S.NG;
         uint2* surv = S.surv + q * S.rcap;
         float* surv_lb = S.surv_lb + q * S.rcap;
-        const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
         const uint64_t base = static_cast<uint64_t>(chunk) * kRound;
-        uint4 bl[kGP][H], bh[kGP][H];
+        uint2* dpage = S.dpage + q * S.P;
+        float* dpage_lb = S.dpage_lb + q * S.P;
+        unsigned keep = 0, defer = 0;
         uint32_t ea[kGP], eb[kGP];
-        bool valid[kGP];
+        float plb[kGP];
+        if (pass == 0) {
+            // pages of the surviving groups; those beyond split x bound wait for pass 1
+            const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
+            uint4 bl[kGP][H], bh[kGP][H];
+            bool valid[kGP];
 #pragma unroll
-        for (int k = 0; k < kGP; ++k) {
-            const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-            const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
-            valid[k] = p < ix.P;
+            for (int k = 0; k < kGP; ++k) {
+                const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+                const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
+                valid[k] = p < ix.P;
 #pragma unroll
-            for (int h = 0; h < H; ++h) {
-                bl[k][h] = valid[k] ? ld_stream_u4(ix.page_lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                bh[k][h] = valid[k] ? ld_stream_u4(ix.page_hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                for (int h = 0; h < H; ++h) {
+                    bl[k][h] = valid[k] ? ld_stream_u4(ix.page_lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                    bh[k][h] = valid[k] ? ld_stream_u4(ix.page_hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                }
+                ea[k] = valid[k] ? ix.page_off[p] : 0u;
+                eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
             }
-            ea[k] = valid[k] ? ix.page_off[p] : 0u;
-            eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
-        }
-        unsigned keep = 0;
 #pragma unroll
-        for (int k = 0; k < kGP; ++k) {
-            if (!valid[k]) continue;
-            nodes += 1;
-            const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
-            const bool seeded = ea[k] >= sa && eb[k] <= sb;
-            if (!seeded && lb <= bound) keep |= 1u << k;
-            else if (!seeded) pruned += 1;
+            for (int k = 0; k < kGP; ++k) {
+                plb[k] = 0.f;
+                if (!valid[k]) continue;
+                nodes += 1;
+                const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
+                plb[k] = lb;
+                const bool seeded = ea[k] >= sa && eb[k] <= sb;
+                if (!seeded && lb <= cut) keep |= 1u << k;
+                else if (!seeded && lb <= bound) defer |= 1u << k;
+                else if (!seeded) pruned += 1;
+            }
+            uint32_t at = block_reserve(__popc(defer), 0, &wk->ndefer, nullptr).x;
+#pragma unroll
+            for (int k = 0; k < kGP; ++k)
+                if (defer & (1u << k)) {
+                    dpage[at] = make_uint2(ea[k], eb[k]);
+                    dpage_lb[at++] = plb[k];
+                }
+        } else {
+            // the deferred pages, re-tested against the tightened BSF
+            const uint64_t nitems = wk->ndefer;
+#pragma unroll
+            for (int k = 0; k < kGP; ++k) {
+                const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+                const bool in = i < nitems;
+                const uint2 r = in ? dpage[i] : make_uint2(0, 0);
+                ea[k] = r.x;
+                eb[k] = r.y;
+                if (in && dpage_lb[i] <= bound) keep |= 1u << k;
+                else if (in) pruned += 1;
+            }
         }
         // compact the chunk's surviving pages into shared memory
         __shared__ uint32_t s_wsum[kWarps];
@@ -1819,7 +1857,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.pos_offset = ix.pos_offset;
     iv.window = window;
     SlotView sv{slots.work, slots.lut, slots.gsurv, slots.surv, slots.surv_lb, slots.cand_pos, slots.cand_lb,
-                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256, slots.rcap};
+                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256, slots.rcap, slots.dpage, slots.dpage_lb};
     // DTW kernels, by band-diagonal registers per lane (window <= 32 M - 1).
     const bool dtw = window >= 0;
     if (window > kMaxDtwWindow) throw std::invalid_argument("exact_search: dtw window above the device limit");
@@ -1873,10 +1911,15 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         mark(1, [&] {
             groups<<<dim3(group_x, nq), kThreads, lut_bytes, st>>>(iv, sv);
             TSG_LAUNCHED();
-            bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq);
+            bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 0);
             TSG_LAUNCHED();
         });
         for (int wave = 0; wave < 2; ++wave) {
+            if (wave == 1)
+                mark(1, [&] {  // runs of the deferred pages, against the BSF refinement wave A tightened
+                    bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 1);
+                    TSG_LAUNCHED();
+                });
             mark(4, [&] {
                 lbscan<<<scan_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, wave);
                 TSG_LAUNCHED();
