@@ -124,7 +124,8 @@ def test_exact_search_matches_golden(golden, oracle):
 @pytest.mark.parametrize("count,n,w,bits,leaf", [
     (3000, 64, 16, 8, 20), (3000, 64, 16, 8, 2), (3000, 64, 16, 8, 2000), (2500, 64, 8, 4, 7),
     (2000, 96, 16, 8, 50), (2000, 128, 16, 8, 100), (4000, 256, 16, 8, 2000), (1500, 30, 3, 8, 10),
-    (1500, 64, 32, 8, 16), (1000, 60, 5, 2, 4),
+    (1500, 64, 32, 8, 16), (1000, 60, 5, 2, 4), (1200, 512, 16, 8, 40), (800, 1024, 32, 8, 25),
+    (900, 200, 8, 8, 30),
 ])
 def test_exact_matches_scan(oracle, count, n, w, bits, leaf):
     rng = np.random.default_rng(count * 7 + n)
