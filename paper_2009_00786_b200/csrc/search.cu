@@ -1760,13 +1760,23 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t* cand_pos = S.cand_pos + q * S.cap;
     const double* cand_sq = S.cand_sq + q * S.cap;
     uint32_t mine = 0xFFFFFFFFu;
-    if (!overflow)
-        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < lo_end + hi_n;
-             i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-            const uint64_t c = i < lo_end ? i : S.cap - 1 - (i - lo_end);
-            const double s = cand_sq[c];
-            if (s <= lim && sqrt(s) == dist) mine = min(mine, ix.pos[cand_pos[c]]);
+    if (!overflow) {
+        // four records per thread per step, loads first (the scan is latency-bound)
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x, total = lo_end + hi_n;
+        for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < total; i0 += 4 * stride) {
+            double sv[4];
+            uint64_t cv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t i = i0 + u * stride;
+                cv[u] = i < lo_end ? i : S.cap - 1 - (i - lo_end);
+                sv[u] = i < total ? cand_sq[cv[u]] : INFINITY;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (sv[u] <= lim && sqrt(sv[u]) == dist) mine = min(mine, ix.pos[cand_pos[cv[u]]]);
         }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
     if ((threadIdx.x & 31) == 0 && mine != 0xFFFFFFFFu) atomicMin(&wk->best_pos, mine);
