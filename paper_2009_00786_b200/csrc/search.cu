@@ -1590,6 +1590,72 @@ __device__ double warp_dtw_sq(const float* __restrict__ sa, const float* __restr
     return __shfl_sync(kFull, v, idx & 31);
 }
 
+// Two banded DTWs at once by one warp (r < 32, one band cell per lane each):
+// the same recurrence as warp_dtw_sq for rows b0 and b1, interleaved so the
+// two dependency chains hide each other's latency. Each abandons on its own.
+__device__ void warp_dtw_sq_pair(const float* __restrict__ sa, const float* __restrict__ b0,
+                                 const float* __restrict__ b1, int n, int r, double cut0, double cut1, double& out0,
+                                 double& out1) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned kFull = 0xFFFFFFFFu;
+    double p1a = INFINITY, p2a = INFINITY, p1b = INFINITY, p2b = INFINITY;
+    double prev_a = INFINITY, prev_b = INFINITY;
+    bool live_a = true, live_b = true;
+    for (int k = 0; k < 2 * n - 1; ++k) {
+        const int p = (k + r) & 1;
+        double upa, lefta, upb, leftb;
+        if (p == 0) {
+            upa = p1a;
+            upb = p1b;
+            const double la = __shfl_up_sync(kFull, p1a, 1), lb = __shfl_up_sync(kFull, p1b, 1);
+            lefta = lane == 0 ? INFINITY : la;
+            leftb = lane == 0 ? INFINITY : lb;
+        } else {
+            lefta = p1a;
+            leftb = p1b;
+            const double ua = __shfl_down_sync(kFull, p1a, 1), ub = __shfl_down_sync(kFull, p1b, 1);
+            upa = lane == 31 ? INFINITY : ua;
+            upb = lane == 31 ? INFINITY : ub;
+        }
+        const int u = 2 * lane + p;
+        const int delta = u - r;
+        const int i2 = k - delta;
+        const int i = i2 >> 1, j = (k + delta) >> 1;
+        double ca = INFINITY, cb = INFINITY;
+        if (u <= 2 * r && i2 >= 0 && i < n && j >= 0 && j < n) {
+            const double ai = static_cast<double>(sa[i]);
+            const bool origin = i == 0 && j == 0;
+            const double besta = origin ? 0.0 : fmin(fmin(upa, lefta), p2a);
+            const double bestb = origin ? 0.0 : fmin(fmin(upb, leftb), p2b);
+            const double da = __dsub_rn(ai, static_cast<double>(__ldg(b0 + j)));
+            const double db = __dsub_rn(ai, static_cast<double>(__ldg(b1 + j)));
+            ca = __dadd_rn(besta, __dmul_rn(da, da));
+            cb = __dadd_rn(bestb, __dmul_rn(db, db));
+        }
+        p2a = p1a;
+        p1a = ca;
+        p2b = p1b;
+        p1b = cb;
+        if ((k & 7) == 7) {
+            double ma = fmin(ca, prev_a), mb = fmin(cb, prev_b);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ma = fmin(ma, __shfl_xor_sync(kFull, ma, o));
+                mb = fmin(mb, __shfl_xor_sync(kFull, mb, o));
+            }
+            live_a = live_a && !(ma > cut0);
+            live_b = live_b && !(mb > cut1);
+            if (!live_a && !live_b) break;
+        }
+        prev_a = ca;
+        prev_b = cb;
+    }
+    const int idx = (r - (r & 1)) / 2;
+    const double va = __shfl_sync(kFull, p1a, idx), vb = __shfl_sync(kFull, p1b, idx);
+    out0 = live_a ? va : INFINITY;
+    out1 = live_b ? vb : INFINITY;
+}
+
 // LB_Keogh (src/metrics.cpp:179-192), squared, by one warp (any summation
 // order: it is only a filter, compared with the same 1e-9 slack as the BSF).
 __device__ __forceinline__ double warp_lb_keogh_sq(const float* __restrict__ up, const float* __restrict__ lo,
@@ -1720,17 +1786,58 @@ __global__ void __launch_bounds__(kThreads)
             if (in && !keep) cand_sq[c] = INFINITY;
             const uint32_t p = keep ? ix.pos[cand_pos[c]] : 0u;
             unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
-            while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
-                const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
-                bool ran;
-                const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n,
-                                                        ix.rows + static_cast<uint64_t>(pp) * n, n, ix.window, wk, ran);
-                if (lane == 0) {
-                    refined += ran ? 1 : 0;
-                    updates += publish(wk, sq, cc, cand_sq);
+            if constexpr (M == 1) {
+                // LB_Keogh first; the survivors two at a time through the paired DTW
+                unsigned live = 0;
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
+                    const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
+                    const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
+                    if (warp_lb_keogh_sq(s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(pp) * n, n) > cut) {
+                        if (lane == 0) cand_sq[cc] = INFINITY;
+                    } else {
+                        live |= 1u << src;
+                    }
+                }
+                while (live) {
+                    const int s0 = __ffs(live) - 1;
+                    live &= live - 1;
+                    const int s1 = live ? __ffs(live) - 1 : -1;
+                    if (s1 >= 0) live &= live - 1;
+                    const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, p, s0);
+                    const uint64_t c0 = __shfl_sync(0xFFFFFFFFu, c, s0);
+                    const uint32_t p1 = __shfl_sync(0xFFFFFFFFu, p, s1 >= 0 ? s1 : s0);
+                    const uint64_t c1 = __shfl_sync(0xFFFFFFFFu, c, s1 >= 0 ? s1 : s0);
+                    const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
+                    double d0, d1 = INFINITY;
+                    if (s1 >= 0) {
+                        warp_dtw_sq_pair(s_qe, ix.rows + static_cast<uint64_t>(p0) * n,
+                                         ix.rows + static_cast<uint64_t>(p1) * n, n, ix.window, cut, cut, d0, d1);
+                    } else {
+                        d0 = warp_dtw_sq<1>(s_qe, ix.rows + static_cast<uint64_t>(p0) * n, n, ix.window, cut);
+                    }
+                    if (lane == 0) {
+                        refined += s1 >= 0 ? 2 : 1;
+                        updates += publish(wk, d0, c0, cand_sq);
+                        if (s1 >= 0) updates += publish(wk, d1, c1, cand_sq);
+                    }
+                }
+            } else {
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
+                    const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
+                    bool ran;
+                    const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n,
+                                                            ix.rows + static_cast<uint64_t>(pp) * n, n, ix.window, wk,
+                                                            ran);
+                    if (lane == 0) {
+                        refined += ran ? 1 : 0;
+                        updates += publish(wk, sq, cc, cand_sq);
+                    }
                 }
             }
         }
