@@ -525,7 +525,9 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) {
         const uint32_t leaf = ix.page_leaf[page];
         uint32_t a = ix.leaf_off[leaf], b = ix.leaf_off[leaf + 1];
-        if (b - a > ix.seed_cap) {
+        // DTW seeds with the query's page only: every seed row is a full DTW
+        // (nothing to prune against yet), the rest of the leaf goes through the filters.
+        if (b - a > ix.seed_cap || ix.window >= 0) {
             a = ix.page_off[page];
             b = ix.page_off[page + 1];
         }
