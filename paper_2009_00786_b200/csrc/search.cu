@@ -696,194 +696,181 @@ template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     k_bound(IndexView ix, SlotView S, int nq, int pass) {
     constexpr int H = WS / 16;
-    constexpr uint32_t kRound = static_cast<uint32_t>(kThreads) * kGP;
+    constexpr uint32_t kWChunk = 64;  // pages per warp chunk (two per lane)
     const int k_next = pass == 0 ? kNextBound : kNextBound1;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
-    __shared__ uint2 s_pages[kRound];            // the chunk's surviving pages
+    __shared__ uint2 s_pg[kWarps][kWChunk];      // the warp chunk's surviving pages
     __shared__ uint2 s_r[kWarps][kRunStage];     // staged surviving runs
     __shared__ float s_l[kWarps][kRunStage];
+    __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
-    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x), loaded = -1;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
-    float bound = 0.f, cut = 0.f;
-    uint32_t sa = 0, sb = 0;
     unsigned long long pruned = 0, nodes = 0;
     int cnt = 0;
     auto nchunks = [pass](const QueryWork* wk) -> uint32_t {
         if (wk->overflow) return 0;
         const uint32_t items = pass == 0 ? wk->ngroups * static_cast<uint32_t>(kGroup) : wk->ndefer;
-        return (items + kRound - 1) / kRound;
+        return (items + kWChunk - 1) / kWChunk;
     };
-    auto leave_query = [&](int q) {
-        QueryWork* w = S.work + q;
-        if (cnt) flush_runs(w, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, S.surv + q * S.rcap,
-                            S.surv_lb + q * S.rcap);
+    for (;;) {
+        // Query loop (block level; the only barriers): pick a query with
+        // chunks left and load its table; the warps then claim chunks of it
+        // on their own until it is exhausted.
+        __syncthreads();
+        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
+        __syncthreads();
+        const int q = s_sel;
+        if (q < 0) break;
+        cur = q;
+        QueryWork* wk = S.work + q;
+        load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
+#pragma unroll
+        for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
+        // pass 0: the seed bound; pass 1 (after refinement wave A): the tightened BSF
+        const float bound = pass == 0 ? wk->scan_bound : bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+        const float cut = pass == 0 ? bound * ix.split : -1.f;  // wave 0: the most promising runs
+        const uint32_t sa = wk->seed_begin, sb = wk->seed_end;
+        const uint32_t* gsurv = S.gsurv + q * S.NG;
+        uint2* surv = S.surv + q * S.rcap;
+        float* surv_lb = S.surv_lb + q * S.rcap;
+        uint2* dpage = S.dpage + q * S.P;
+        float* dpage_lb = S.dpage_lb + q * S.P;
+        const uint64_t items = pass == 0 ? static_cast<uint64_t>(wk->ngroups) * kGroup : wk->ndefer;
+        const uint32_t nch = nchunks(wk);
+        uint32_t chunk = 0;
+        if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
+        chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+        while (chunk < nch) {
+            uint32_t pre = 0;
+            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
+            // pages: two per lane
+            bool keep[2], defer[2];
+            uint32_t ea[2], eb[2];
+            float plb[2];
+            if (pass == 0) {
+                uint4 bl[2][H], bh[2][H];
+                bool valid[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint64_t i = static_cast<uint64_t>(chunk) * kWChunk + 32 * k + lane;
+                    const uint64_t p = i < items ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
+                    valid[k] = p < ix.P;
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        bl[k][h] = valid[k] ? ld_stream_u4(ix.page_lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                        bh[k][h] = valid[k] ? ld_stream_u4(ix.page_hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                    }
+                    ea[k] = valid[k] ? ix.page_off[p] : 0u;
+                    eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    keep[k] = defer[k] = false;
+                    plb[k] = 0.f;
+                    if (!valid[k]) continue;
+                    nodes += 1;
+                    const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
+                    plb[k] = lb;
+                    const bool seeded = ea[k] >= sa && eb[k] <= sb;
+                    keep[k] = !seeded && lb <= cut;
+                    defer[k] = !seeded && lb > cut && lb <= bound;
+                    pruned += !seeded && lb > bound ? 1 : 0;
+                }
+                // pages beyond split x bound wait for pass 1 (one atomic per warp and chunk)
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, defer[k]);
+                    uint32_t base = 0;
+                    if (lane == 0 && m) base = atomicAdd(&wk->ndefer, static_cast<unsigned>(__popc(m)));
+                    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                    if (defer[k]) {
+                        const uint32_t at = base + __popc(m & below);
+                        dpage[at] = make_uint2(ea[k], eb[k]);
+                        dpage_lb[at] = plb[k];
+                    }
+                }
+            } else {
+                // the deferred pages, re-tested against the tightened BSF
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const uint64_t i = static_cast<uint64_t>(chunk) * kWChunk + 32 * k + lane;
+                    const bool in = i < items;
+                    const uint2 r = in ? dpage[i] : make_uint2(0, 0);
+                    ea[k] = r.x;
+                    eb[k] = r.y;
+                    keep[k] = in && dpage_lb[i] <= bound;
+                    defer[k] = false;
+                    pruned += in && !keep[k] ? 1 : 0;
+                }
+            }
+            // the warp's surviving pages, then their runs (kRunsPerPage items per page)
+            uint32_t np = 0;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const unsigned m = __ballot_sync(0xFFFFFFFFu, keep[k]);
+                if (keep[k]) s_pg[warp][np + __popc(m & below)] = make_uint2(ea[k], eb[k]);
+                np += __popc(m);
+            }
+            __syncwarp();
+            const uint32_t nri = np * kRunsPerPage;
+            for (uint32_t j0 = 0; j0 < nri; j0 += 64) {
+                bool ok[2];
+                uint32_t e0[2], e1[2];
+                uint4 rl[2][H], rh[2][H];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint32_t j = j0 + 32 * u + lane;
+                    ok[u] = false;
+                    e0[u] = e1[u] = 0;
+                    uint64_t r = 0;
+                    if (j < nri) {
+                        const uint2 pg = s_pg[warp][j / kRunsPerPage];
+                        r = pg.x / kRun + j % kRunsPerPage;
+                        e0[u] = max(pg.x, static_cast<uint32_t>(r * kRun));
+                        e1[u] = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
+                        ok[u] = e0[u] < e1[u];
+                    }
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+                        rl[u][h] = ok[u] ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                        rh[u][h] = ok[u] ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float lb = ok[u] ? box_bound<H, W16>(s_lut, q4, rl[u], rh[u], ix.w) : INFINITY;
+                    const bool pass_ = ok[u] && lb <= bound;
+                    nodes += ok[u] ? 1 : 0;  // run boxes are node bounds (box_calcs counts quads)
+                    pruned += ok[u] && !pass_ ? 1 : 0;
+                    const unsigned m = __ballot_sync(0xFFFFFFFFu, pass_);
+                    if (pass_) {
+                        const int slot = cnt + __popc(m & below);
+                        s_r[warp][slot] = make_uint2(e0[u], e1[u]);
+                        s_l[warp][slot] = lb;
+                    }
+                    cnt += __popc(m);
+                    __syncwarp();
+                    if (cnt > kRunStage - 32) {
+                        flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
+                        cnt = 0;
+                    }
+                }
+            }
+            chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
+        }
+        // leave the query: the stage and the counters
+        if (cnt) flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
         cnt = 0;
         pruned = warp_sum(pruned);
         nodes = warp_sum(nodes);
         if (lane == 0) {
-            if (pruned) atomicAdd(&w->stats[kPruned], pruned);
-            if (nodes) atomicAdd(&w->stats[kLbNode], nodes);
+            if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
+            if (nodes) atomicAdd(&wk->stats[kLbNode], nodes);
         }
         pruned = nodes = 0;
-    };
-    uint32_t chunk = 0, pre = ~0u;
-    for (int q = -1;;) {
-        q = claim(S.work, nq, k_next, cur, chunk, pre, q, nchunks);
-        if (q != loaded && loaded >= 0) leave_query(loaded);
-        if (q < 0) break;
-        pre = claim_ahead(S.work, q, k_next);
-        QueryWork* wk = S.work + q;
-        if (q != loaded) {
-            load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
-#pragma unroll
-            for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
-            // pass 0: the seed bound; pass 1 (after refinement wave A): the tightened BSF
-            bound = pass == 0 ? wk->scan_bound : bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
-            cut = pass == 0 ? bound * ix.split : -1.f;  // wave 0: the most promising runs
-            sa = wk->seed_begin;
-            sb = wk->seed_end;
-            loaded = q;
-        }
-        const uint32_t* gsurv = S.gsurv + q * S.NG;
-        uint2* surv = S.surv + q * S.rcap;
-        float* surv_lb = S.surv_lb + q * S.rcap;
-        const uint64_t base = static_cast<uint64_t>(chunk) * kRound;
-        uint2* dpage = S.dpage + q * S.P;
-        float* dpage_lb = S.dpage_lb + q * S.P;
-        unsigned keep = 0, defer = 0;
-        uint32_t ea[kGP], eb[kGP];
-        float plb[kGP];
-        if (pass == 0) {
-            // pages of the surviving groups; those beyond split x bound wait for pass 1
-            const uint64_t nitems = static_cast<uint64_t>(wk->ngroups) * kGroup;
-            uint4 bl[kGP][H], bh[kGP][H];
-            bool valid[kGP];
-#pragma unroll
-            for (int k = 0; k < kGP; ++k) {
-                const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-                const uint64_t p = i < nitems ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
-                valid[k] = p < ix.P;
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    bl[k][h] = valid[k] ? ld_stream_u4(ix.page_lo + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                    bh[k][h] = valid[k] ? ld_stream_u4(ix.page_hi + p * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                }
-                ea[k] = valid[k] ? ix.page_off[p] : 0u;
-                eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
-            }
-#pragma unroll
-            for (int k = 0; k < kGP; ++k) {
-                plb[k] = 0.f;
-                if (!valid[k]) continue;
-                nodes += 1;
-                const float lb = box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w);
-                plb[k] = lb;
-                const bool seeded = ea[k] >= sa && eb[k] <= sb;
-                if (!seeded && lb <= cut) keep |= 1u << k;
-                else if (!seeded && lb <= bound) defer |= 1u << k;
-                else if (!seeded) pruned += 1;
-            }
-            uint32_t at = block_reserve(__popc(defer), 0, &wk->ndefer, nullptr).x;
-#pragma unroll
-            for (int k = 0; k < kGP; ++k)
-                if (defer & (1u << k)) {
-                    dpage[at] = make_uint2(ea[k], eb[k]);
-                    dpage_lb[at++] = plb[k];
-                }
-        } else {
-            // the deferred pages, re-tested against the tightened BSF
-            const uint64_t nitems = wk->ndefer;
-#pragma unroll
-            for (int k = 0; k < kGP; ++k) {
-                const uint64_t i = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-                const bool in = i < nitems;
-                const uint2 r = in ? dpage[i] : make_uint2(0, 0);
-                ea[k] = r.x;
-                eb[k] = r.y;
-                if (in && dpage_lb[i] <= bound) keep |= 1u << k;
-                else if (in) pruned += 1;
-            }
-        }
-        // compact the chunk's surviving pages into shared memory
-        __shared__ uint32_t s_wsum[kWarps];
-        __shared__ uint32_t s_total;
-        const uint32_t mine = __popc(keep);
-        uint32_t incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t tot = 0;
-            for (int i = 0; i < kWarps; ++i) {
-                const uint32_t c = s_wsum[i];
-                s_wsum[i] = tot;
-                tot += c;
-            }
-            s_total = tot;
-        }
-        __syncthreads();
-        uint32_t at = s_wsum[warp] + incl - mine;
-#pragma unroll
-        for (int k = 0; k < kGP; ++k)
-            if (keep & (1u << k)) s_pages[at++] = make_uint2(ea[k], eb[k]);
-        __syncthreads();
-        // their runs: (page, run) items over all threads, kRunU per thread per
-        // step with every box load issued before the first bound
-#ifndef TSG_RUN_U
-#define TSG_RUN_U 2
-#endif
-        constexpr int kRunU = TSG_RUN_U;
-        const uint32_t nrun_items = s_total * kRunsPerPage;
-        for (uint32_t j0 = 0; j0 < nrun_items; j0 += kThreads * kRunU) {
-            bool ok[kRunU];
-            uint32_t e0[kRunU], e1[kRunU];
-            uint4 rl[kRunU][H], rh[kRunU][H];
-#pragma unroll
-            for (int u = 0; u < kRunU; ++u) {
-                const uint32_t j = j0 + threadIdx.x + kThreads * u;
-                ok[u] = false;
-                e0[u] = e1[u] = 0;
-                uint64_t r = 0;
-                if (j < nrun_items) {
-                    const uint2 pg = s_pages[j / kRunsPerPage];
-                    r = pg.x / kRun + j % kRunsPerPage;
-                    e0[u] = max(pg.x, static_cast<uint32_t>(r * kRun));
-                    e1[u] = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
-                    ok[u] = e0[u] < e1[u];
-                }
-#pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    rl[u][h] = ok[u] ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                    rh[u][h] = ok[u] ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kRunU; ++u) {
-                const float lb = ok[u] ? box_bound<H, W16>(s_lut, q4, rl[u], rh[u], ix.w) : INFINITY;
-                const bool pass = ok[u] && lb <= bound;
-                nodes += ok[u] ? 1 : 0;  // run boxes are node bounds (box_calcs counts quads)
-                pruned += ok[u] && !pass ? 1 : 0;
-                const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-                if (pass) {
-                    const int slot = cnt + __popc(m & below);
-                    s_r[warp][slot] = make_uint2(e0[u], e1[u]);
-                    s_l[warp][slot] = lb;
-                }
-                cnt += __popc(m);
-                __syncwarp();
-                if (cnt > kRunStage - 32) {
-                    flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
-                    cnt = 0;
-                }
-            }
-        }
     }
 }
 
