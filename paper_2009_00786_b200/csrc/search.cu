@@ -1228,7 +1228,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     extern __shared__ __align__(128) unsigned char s_dyn[];
     float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][2][n]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // lane-ordered query
-    __shared__ __align__(8) uint64_t s_bar[kGroups][3];
+    __shared__ __align__(8) uint64_t s_bar[kGroups][4];
     __shared__ uint32_t s_c[kWarps][kTmaChunk], s_p[kWarps][kTmaChunk];
     __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
@@ -1238,7 +1238,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     const bool leader = j8 == 0;
     const int hsw = (j8 >> 2) & 1;
     constexpr unsigned row_bytes = static_cast<unsigned>(n) * 4u;
-    for (int i = threadIdx.x; i < 3 * kGroups; i += blockDim.x) mbar_init(&s_bar[i / 3][i % 3], 1);
+    for (int i = threadIdx.x; i < 4 * kGroups; i += blockDim.x) mbar_init(&s_bar[i / 4][i % 4], 1);
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     unsigned phase = 0;  // bit b: parity of this group's buffer b
@@ -1389,22 +1389,24 @@ __global__ void __launch_bounds__(kThreads, 3)
             const uint32_t next = __shfl_sync(0xFFFFFFFFu, pre, 0);
             load_records(next, rlb, rcp);  // in flight during phase 2
             if constexpr (kHalf) {
-                // Phase 2 (half rows): first halves one row ahead in buffers 0 / 1,
-                // the pending second half in buffer 2, completed one row later.
+                // Phase 2 (half rows): first halves two rows ahead in buffers 0-2,
+                // the pending second half in buffer 3, completed one row later.
                 bool pending = false;
                 uint32_t pend_c = 0;
                 double pend_sum = 0.0;
                 unsigned long long pend_seen = 0;
                 if (leader && static_cast<uint32_t>(wg) < m) issue_half(0, s_p[warp][wg], 0);
+                if (leader && static_cast<uint32_t>(wg) + kWarpGroups < m) issue_half(1, s_p[warp][wg + kWarpGroups], 0);
                 int fb = 0;
-                for (uint32_t j = wg; j < m; j += kWarpGroups, fb ^= 1) {
-                    if (leader && j + kWarpGroups < m) issue_half(fb ^ 1, s_p[warp][j + kWarpGroups], 0);
+                for (uint32_t j = wg; j < m; j += kWarpGroups, fb = fb == 2 ? 0 : fb + 1) {
+                    if (leader && j + 2 * kWarpGroups < m)
+                        issue_half(fb == 0 ? 2 : fb - 1, s_p[warp][j + 2 * kWarpGroups], 0);
                     const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
                     wait_buf(fb);
                     const double part = half_sum(fb, 0, 0.0);
                     if (pending) {  // the previous row's second half
-                        wait_buf(2);
-                        const double sum = half_sum(2, 1, pend_sum);
+                        wait_buf(3);
+                        const double sum = half_sum(3, 1, pend_sum);
                         if (leader) {
                             cand_sq[pend_c] = sum;
                             const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
@@ -1415,7 +1417,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                     const bool cont = __shfl_sync(gmask, leader && !(part > bsf_of(seen) * kSlack), gbase);
                     if (leader) refined += 1;
                     if (cont) {
-                        if (leader) issue_half(2, s_p[warp][j], 1);
+                        if (leader) issue_half(3, s_p[warp][j], 1);
                         pending = true;
                         pend_c = s_c[warp][j];
                         pend_sum = part;
@@ -1425,8 +1427,8 @@ __global__ void __launch_bounds__(kThreads, 3)
                     }
                 }
                 if (pending) {
-                    wait_buf(2);
-                    const double sum = half_sum(2, 1, pend_sum);
+                    wait_buf(3);
+                    const double sum = half_sum(3, 1, pend_sum);
                     if (leader) {
                         cand_sq[pend_c] = sum;
                         const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
