@@ -1286,7 +1286,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     };
     // Block sums of half h of a row in half buffer b, added left to right by the
     // leader onto `sum` (the leader's value is the one that counts).
-    auto half_sum = [&](int b, int h, double sum) -> double {
+    // Block sums of half h of the row in half buffer b, written back into that
+    // buffer (block k at double k) for the leader's left-to-right chain.
+    auto half_blocks = [&](int b, int h) {
         const float* row = hbuf(b);
         double blk[kTh];
 #pragma unroll
@@ -1313,8 +1315,12 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
         for (int t = 0; t < kTh; ++t)
             if (j8 + kRowLanes * t < kHB) sums[j8 + kRowLanes * t] = blk[t];
+    };
+    auto half_sum = [&](int b, int h, double sum) -> double {
+        half_blocks(b, h);
         __syncwarp(gmask);
         if (leader) {
+            const double* sums = reinterpret_cast<const double*>(hbuf(b));
 #pragma unroll
             for (int k = 0; k < kHB; ++k) sum = __dadd_rn(sum, sums[k]);
         }
@@ -1402,18 +1408,37 @@ __global__ void __launch_bounds__(kThreads, 3)
                     if (leader && j + 2 * kWarpGroups < m)
                         issue_half(fb == 0 ? 2 : fb - 1, s_p[warp][j + 2 * kWarpGroups], 0);
                     const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
+                    // this row's first half and the previous row's second half: block
+                    // sums by the lanes, then the leader's two left-to-right chains
+                    // interleaved (independent, so their latencies overlap)
                     wait_buf(fb);
-                    const double part = half_sum(fb, 0, 0.0);
-                    if (pending) {  // the previous row's second half
+                    half_blocks(fb, 0);
+                    if (pending) {
                         wait_buf(3);
-                        const double sum = half_sum(3, 1, pend_sum);
-                        if (leader) {
+                        half_blocks(3, 1);
+                    }
+                    __syncwarp(gmask);
+                    double part = 0.0;
+                    if (leader) {
+                        const double* sa = reinterpret_cast<const double*>(hbuf(fb));
+                        const double* sb2 = reinterpret_cast<const double*>(hbuf(3));
+                        double sum = pend_sum;
+                        if (pending) {
+#pragma unroll
+                            for (int k = 0; k < kHB; ++k) {
+                                part = __dadd_rn(part, sa[k]);
+                                sum = __dadd_rn(sum, sb2[k]);
+                            }
                             cand_sq[pend_c] = sum;
                             const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
                             if (sb < pend_seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < kHB; ++k) part = __dadd_rn(part, sa[k]);
                         }
-                        pending = false;
                     }
+                    __syncwarp(gmask);  // both buffers are free again
+                    pending = false;
                     const bool cont = __shfl_sync(gmask, leader && !(part > bsf_of(seen) * kSlack), gbase);
                     if (leader) refined += 1;
                     if (cont) {
