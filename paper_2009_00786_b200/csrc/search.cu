@@ -1213,22 +1213,30 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
 constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;  // candidate records per warp chunk
 
 // NB = n / 8 blocks per row, a compile-time constant so the row sum unrolls.
+#ifndef TSG_MINB_TMA
+#define TSG_MINB_TMA 4
+#endif
+#ifndef TSG_HALF_ROWS
+#define TSG_HALF_ROWS 1
+#endif
+// Half-row refinement applies when a half row is a whole number of 8-block rounds.
+constexpr bool tma_half_rows(int n) { return TSG_HALF_ROWS && (n / 8) % 16 == 0; }
+// Floats of row buffers per 8-lane group: two whole rows, or three half rows.
+constexpr int tma_group_floats(int n) { return tma_half_rows(n) ? 3 * n / 2 : 2 * n; }
 template <int NB>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     constexpr int kGroups = kThreads / kRowLanes;
     constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
     constexpr int kTq = (NB + kRowLanes - 1) / kRowLanes;  // blocks per lane
-#ifndef TSG_HALF_ROWS
-#define TSG_HALF_ROWS 1
-#endif
     // half-row fetches keep the lane-ordered query layout when a half is a whole number of 8-block rounds
-    constexpr bool kHalf = TSG_HALF_ROWS && NB % 16 == 0;
+    constexpr bool kHalf = tma_half_rows(n);
     extern __shared__ __align__(128) unsigned char s_dyn[];
-    float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][2][n]
-    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * 2 * n * 4);  // lane-ordered query
-    __shared__ __align__(8) uint64_t s_bar[kGroups][4];
+    constexpr int kGF = tma_group_floats(n);  // row buffers per group: 2 rows, or 3 half rows
+    float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][kGF]
+    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * kGF * 4);  // lane-ordered query
+    __shared__ __align__(8) uint64_t s_bar[kGroups][3];
     __shared__ uint32_t s_c[kWarps][kTmaChunk], s_p[kWarps][kTmaChunk];
     __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
@@ -1238,11 +1246,11 @@ __global__ void __launch_bounds__(kThreads, 3)
     const bool leader = j8 == 0;
     const int hsw = (j8 >> 2) & 1;
     constexpr unsigned row_bytes = static_cast<unsigned>(n) * 4u;
-    for (int i = threadIdx.x; i < 4 * kGroups; i += blockDim.x) mbar_init(&s_bar[i / 4][i % 4], 1);
+    for (int i = threadIdx.x; i < 3 * kGroups; i += blockDim.x) mbar_init(&s_bar[i / 3][i % 3], 1);
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     unsigned phase = 0;  // bit b: parity of this group's buffer b
-    float* buf0 = s_rows + static_cast<size_t>(g) * 2 * n;
+    float* buf0 = s_rows + static_cast<size_t>(g) * kGF;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     unsigned long long refined = 0, updates = 0;
     const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
@@ -1395,18 +1403,16 @@ __global__ void __launch_bounds__(kThreads, 3)
             const uint32_t next = __shfl_sync(0xFFFFFFFFu, pre, 0);
             load_records(next, rlb, rcp);  // in flight during phase 2
             if constexpr (kHalf) {
-                // Phase 2 (half rows): first halves two rows ahead in buffers 0-2,
-                // the pending second half in buffer 3, completed one row later.
+                // Phase 2 (half rows): first halves one row ahead in buffers 0 / 1,
+                // the pending second half in buffer 2, completed one row later.
                 bool pending = false;
                 uint32_t pend_c = 0;
                 double pend_sum = 0.0;
                 unsigned long long pend_seen = 0;
                 if (leader && static_cast<uint32_t>(wg) < m) issue_half(0, s_p[warp][wg], 0);
-                if (leader && static_cast<uint32_t>(wg) + kWarpGroups < m) issue_half(1, s_p[warp][wg + kWarpGroups], 0);
                 int fb = 0;
-                for (uint32_t j = wg; j < m; j += kWarpGroups, fb = fb == 2 ? 0 : fb + 1) {
-                    if (leader && j + 2 * kWarpGroups < m)
-                        issue_half(fb == 0 ? 2 : fb - 1, s_p[warp][j + 2 * kWarpGroups], 0);
+                for (uint32_t j = wg; j < m; j += kWarpGroups, fb ^= 1) {
+                    if (leader && j + kWarpGroups < m) issue_half(fb ^ 1, s_p[warp][j + kWarpGroups], 0);
                     const unsigned long long seen = ld_volatile_u64(&wk->bsf_bits);
                     // this row's first half and the previous row's second half: block
                     // sums by the lanes, then the leader's two left-to-right chains
@@ -1414,14 +1420,14 @@ __global__ void __launch_bounds__(kThreads, 3)
                     wait_buf(fb);
                     half_blocks(fb, 0);
                     if (pending) {
-                        wait_buf(3);
-                        half_blocks(3, 1);
+                        wait_buf(2);
+                        half_blocks(2, 1);
                     }
                     __syncwarp(gmask);
                     double part = 0.0;
                     if (leader) {
                         const double* sa = reinterpret_cast<const double*>(hbuf(fb));
-                        const double* sb2 = reinterpret_cast<const double*>(hbuf(3));
+                        const double* sb2 = reinterpret_cast<const double*>(hbuf(2));
                         double sum = pend_sum;
                         if (pending) {
 #pragma unroll
@@ -1442,7 +1448,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                     const bool cont = __shfl_sync(gmask, leader && !(part > bsf_of(seen) * kSlack), gbase);
                     if (leader) refined += 1;
                     if (cont) {
-                        if (leader) issue_half(3, s_p[warp][j], 1);
+                        if (leader) issue_half(2, s_p[warp][j], 1);
                         pending = true;
                         pend_c = s_c[warp][j];
                         pend_sum = part;
@@ -1452,8 +1458,8 @@ __global__ void __launch_bounds__(kThreads, 3)
                     }
                 }
                 if (pending) {
-                    wait_buf(3);
-                    const double sum = half_sum(3, 1, pend_sum);
+                    wait_buf(2);
+                    const double sum = half_sum(2, 1, pend_sum);
                     if (leader) {
                         cand_sq[pend_c] = sum;
                         const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
@@ -1954,7 +1960,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     auto refine_tma = n == 256 ? k_refine_tma<32> : n == 128 ? k_refine_tma<16> : n == 96 ? k_refine_tma<12>
                     : n == 64 ? k_refine_tma<8> : n == 512 ? k_refine_tma<64> : nullptr;
     const bool tma = vec && refine_tma && !std::getenv("TSG_NO_TMA_REFINE");
-    const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * 2 * n * 4 +
+    const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * tma_group_floats(n) * 4 +
                              static_cast<size_t>((n / 8 + kRowLanes - 1) / kRowLanes) * 64 * 8;
     if (tma) TSG_CUDA(cudaFuncSetAttribute(refine_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024));
     for (const void* f : {reinterpret_cast<const void*>(refine), reinterpret_cast<const void*>(seed),
