@@ -338,7 +338,7 @@ def run_ours(args):
                 for r in res:
                     s = r.stats
                     stats += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
-                              s.pruned_subtrees, s.queue_insertions, r.box_calcs)
+                              s.pruned_subtrees, s.queue_insertions, r.box_calcs, r.fine_calcs)
         return max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
 
     # warm-up
@@ -350,7 +350,7 @@ def run_ours(args):
     # Each call is synchronous (results come back to the host per batch): the
     # event pair measures the K batches plus the per-batch result D2H.
     launches0 = tg.launch_count()
-    stats_acc = np.zeros(7, np.float64)
+    stats_acc = np.zeros(8, np.float64)
     answers = []
     with Clocks(local) as clk:
         elapsed = timed(False, stats_acc, answers)
@@ -377,9 +377,11 @@ def run_ours(args):
     nqt = args.steps * nq
     ws = 16
     P = bs.pages
-    # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize
-    groups = {"bound": [1], "seed": [2], "lbscan": [4], "refine": [3, 5], "finalize": [6]}
+    # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize, 7 fine
+    groups = {"bound": [1], "seed": [2], "lbscan": [4], "fine": [7], "refine": [3, 5], "finalize": [6]}
     lb_nodes, lb_entries, refined, cands, boxes = stats_acc[0], stats_acc[1], stats_acc[2], stats_acc[5], stats_acc[6]
+    fine_calcs = stats_acc[7]
+    fw = 2 * 16 if (n % 32 == 0 and not os.environ.get("TSG_NO_FINE")) else 0  # fine summary bytes per series (w = 16)
     NG = (P + 7) // 8
     group_bytes = {  # algorithmic bytes over the timed pass (per-unit figures of DESIGN.md §4 x the counters)
         # every group box (2 x 16 B) + pages of surviving groups and runs of surviving pages
@@ -389,6 +391,8 @@ def run_ours(args):
         "lbscan": boxes * 2 * ws + lb_entries * ws + cands * 8,
         # kept candidate rows (full length) + their records (bound, entry, pos gather, sum)
         "refine": refined * 4 * n + cands * 20,
+        # candidate records (bound, entry) + the fine summary rows of those still within the BSF
+        "fine": cands * 8 + fine_calcs * fw,
     }
     group_ms = {g: sum(prof_ms[k] for k in ks) for g, ks in groups.items()}
     dom = max(group_ms, key=group_ms.get)
@@ -399,7 +403,7 @@ def run_ours(args):
     traffic = ncu_traffic(dom, nq) if args.config == "c2" and world == 1 and nq == 100 else None
 
     # build K1 roofline: read 4n, write the 16-byte word + 8-byte sort key per series
-    k1_bytes = count * (4 * n + 16 + 8) / world
+    k1_bytes = count * (4 * n + 16 + 8 + fw) / world
     k1_gbs = k1_bytes / k1_s / 1e9
     algo_build = count * (4 * n + 16 + 4)  # N(4n + w + 4)
 
@@ -445,13 +449,13 @@ def run_ours(args):
                                    "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                                    "frac": round(k1_gbs / hbm, 4),
                                    "traffic": ncu_traffic("summarise", nq) if args.config == "c2" and world == 1 else None,
-                                   "algorithmic_bytes_per_series": 4 * n + 24},
+                                   "algorithmic_bytes_per_series": 4 * n + 24 + fw},
                       "whole_build_frac": round(algo_build / build_dev_s / 1e9 / hbm / world, 4),
                       "leaves": bs.leaves, "pages": P, "root_children": bs.root_children, "max_depth": bs.max_depth,
                       "overflow_leaves": bs.overflow_leaves},
             "search_stats_per_query": {k: round(v / nqt, 2) for k, v in zip(
                 ["lb_node_calcs", "lb_entry_calcs", "real_dist_calcs", "bsf_updates", "pruned_subtrees",
-                 "queue_insertions"], stats_acc)},
+                 "queue_insertions", "box_calcs", "fine_calcs"], stats_acc)},
             # pruning ratio = 1 - refined rows / dataset rows (BASELINE config 5's difficulty measure)
             "pruning_ratio": round(1.0 - stats_acc[2] / nqt / count, 6),
             "query_bytes_gbs": round((lb_entries * ws + refined * 4 * n + nqt * P * (2 * ws + 8)) / elapsed / 1e9, 1),

@@ -104,6 +104,7 @@ typedef struct tsg_result {
     uint32_t box_calcs;  /* quad (4-entry) box bounds evaluated (saturates at 2^32-1); group, page and
                             run boxes count in stats.lb_node_calcs */
     tsg_search_stats stats;
+    uint64_t fine_calcs;  /* fine-summary (2w half-segment) lower bounds evaluated before refinement */
 } tsg_result;
 
 typedef struct tsg_ctx tsg_ctx;
@@ -205,6 +206,15 @@ int tsg_word_stride(int w);
 tsg_status tsg_index_export(const tsg_index* index, uint8_t* words, uint32_t* positions,
                             uint32_t* leaf_offsets, uint32_t* page_offsets, uint8_t* page_lo,
                             uint8_t* page_hi);
+
+/* The fine summary (device extension, a second lower bound in front of
+ * refinement): *fine_width = 2w half-segment symbols per series (0 when the
+ * index has none: 2w > 64, n % 2w != 0, or TSG_NO_FINE at build time) and,
+ * if fine is not NULL, fine[count][stride] in dataset order, stride = the
+ * fine width rounded up to 16 bytes. Symbol = the FP64 mean of the half
+ * segment (the same sums as summarisation) quantised uniformly over
+ * [-2.5, 2.5) in 256 steps (0 / 255 open-ended). */
+tsg_status tsg_index_export_fine(const tsg_index* index, uint32_t* fine_width, uint8_t* fine);
 
 /* Device data generator: rows [begin, begin+count) of the reference's
  * generate_random_walk(., length, seed) (src/dataset.cpp:22-68), optionally

@@ -18,7 +18,7 @@ TSG_OK, TSG_INVALID_ARGUMENT, TSG_RUNTIME, TSG_LOGIC, TSG_CUDA, TSG_NCCL, TSG_OO
 EXPORTS = (
     "tsg_last_error", "tsg_version", "tsg_config_default", "tsg_config_validate", "tsg_open", "tsg_close",
     "tsg_index_build", "tsg_index_build_device", "tsg_index_free", "tsg_index_info", "tsg_search",
-    "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export",
+    "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export", "tsg_index_export_fine",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
     "tsg_generate_series", "tsg_index_build_file", "tsg_search_measure",
 )
@@ -56,7 +56,7 @@ class tsg_search_stats(C.Structure):
 
 class tsg_result(C.Structure):
     _fields_ = [("distance", C.c_double), ("position", C.c_uint32), ("box_calcs", C.c_uint32),
-                ("stats", tsg_search_stats)]
+                ("stats", tsg_search_stats), ("fine_calcs", C.c_uint64)]
 
 
 _lib = None
@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
         "tsg_summarise": (i32, [vp, u64, u64, i32, i32, vp, vp, vp]),
         "tsg_word_stride": (i32, [i32]),
         "tsg_index_export": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+        "tsg_index_export_fine": (i32, [vp, vp, vp]),
         "tsg_generate_random_walk": (i32, [vp, u64, u64, u64, u64, i32, vp]),
         "tsg_launch_count": (u64, []),
         "tsg_generate_series": (i32, [i32, vp, u64, u64, u64, u64, i32, C.c_double, u64, u64, vp]),

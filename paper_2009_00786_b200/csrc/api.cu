@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cerrno>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -141,7 +142,7 @@ struct tsg_index {
 namespace {
 
 void free_slots(DevIndex::Slots& t) {
-    for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.gsurv),
+    for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.fine_lut), static_cast<void*>(t.gsurv),
                     static_cast<void*>(t.surv), static_cast<void*>(t.surv_lb), static_cast<void*>(t.cand_pos),
                     static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq), static_cast<void*>(t.env),
                     static_cast<void*>(t.dpage), static_cast<void*>(t.dpage_lb)})
@@ -157,6 +158,7 @@ void alloc_slots(const DevIndex& s, DevIndex::Slots& t, uint32_t n, uint64_t cap
     TSG_CUDA(cudaMalloc(&t.work, n * sizeof(QueryWork)));
     TSG_CUDA(cudaMemset(t.work, 0, n * sizeof(QueryWork)));
     TSG_CUDA(cudaMalloc(&t.lut, n * static_cast<size_t>(s.w) * 256 * sizeof(float)));
+    if (s.fw) TSG_CUDA(cudaMalloc(&t.fine_lut, n * static_cast<size_t>(s.fw) * 256 * sizeof(float)));
     TSG_CUDA(cudaMalloc(&t.gsurv, n * NG * sizeof(uint32_t)));
     t.rcap = std::max<uint64_t>(s.R + s.P, 1);  // a page touches its runs; boundary runs count once per page
     TSG_CUDA(cudaMalloc(&t.surv, n * t.rcap * sizeof(uint2)));
@@ -174,6 +176,7 @@ void free_shard(DevIndex& s) {
     if (s.own_rows) cudaFree(s.rows);
     cudaFree(s.thr);
     cudaFree(s.words);
+    cudaFree(s.fine);
     cudaFree(s.run_lo);
     cudaFree(s.run_hi);
     cudaFree(s.quad_lo);
@@ -319,6 +322,9 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
         *h2d_ns = 0;
     }
     s.thr = upload_thresholds(s.bits);
+    // Fine summary (TSG_NO_FINE=1 disables it, for A/B measurements).
+    s.fw = std::getenv("TSG_NO_FINE") ? 0 : fine_width(s.n, s.w);
+    s.fws = s.fw ? fine_stride(s.fw) : 0;
     if (const char* e = std::getenv("TSG_REFINE_SPLIT")) s.refine_split = static_cast<float>(std::atof(e));
     if (file) {
         const RowFeeder feeder = file_feeder(s, *file, h2d_ns);
@@ -395,6 +401,7 @@ void to_result(const DevResult& d, tsg_result& r) {
     r.stats.bsf_updates = d.stats[3];
     r.stats.pruned_subtrees = d.stats[4];
     r.stats.queue_insertions = d.stats[5];
+    r.fine_calcs = d.fine_calcs;
 }
 
 // Lexicographic (distance, position) merge of per-shard answers: the
@@ -407,8 +414,10 @@ void merge_into(tsg_result& acc, const tsg_result& r, bool first) {
     if (first) {
         acc.stats = r.stats;
         acc.box_calcs = r.box_calcs;
+        acc.fine_calcs = r.fine_calcs;
         return;
     }
+    acc.fine_calcs += r.fine_calcs;
     acc.box_calcs = static_cast<uint32_t>(std::min<uint64_t>(0xFFFFFFFFull, uint64_t{acc.box_calcs} + r.box_calcs));
     acc.stats.lb_node_calcs += r.stats.lb_node_calcs;
     acc.stats.lb_entry_calcs += r.stats.lb_entry_calcs;
@@ -732,6 +741,17 @@ tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* posit
         if (page_offsets) TSG_CUDA(cudaMemcpy(page_offsets, s.page_off, (s.P + 1) * 4, cudaMemcpyDeviceToHost));
         if (page_lo) TSG_CUDA(cudaMemcpy(page_lo, s.page_lo, s.P * s.ws, cudaMemcpyDeviceToHost));
         if (page_hi) TSG_CUDA(cudaMemcpy(page_hi, s.page_hi, s.P * s.ws, cudaMemcpyDeviceToHost));
+    });
+}
+
+tsg_status tsg_index_export_fine(const tsg_index* ix, uint32_t* fine_width, uint8_t* fine) {
+    return guarded([&] {
+        if (!ix) fail("tsg_index_export_fine: null index");
+        if (ix->shards.size() != 1) fail("tsg_index_export_fine: single-device index only");
+        const DevIndex& s = ix->shards[0];
+        DeviceGuard g(s.device);
+        if (fine_width) *fine_width = static_cast<uint32_t>(s.fw);
+        if (fine && s.fw) TSG_CUDA(cudaMemcpy(fine, s.fine, s.N * s.fws, cudaMemcpyDeviceToHost));
     });
 }
 

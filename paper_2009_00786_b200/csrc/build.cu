@@ -265,6 +265,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(ix.leaf_cap, 0xFFFFFFFFull));
     const uint64_t open_cap = 2 * (N / (static_cast<uint64_t>(cap) + 1)) + 16;
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));
+    if (ix.fw) TSG_CUDA(cudaMalloc(&ix.fine, N * ix.fws));
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&ix.leaf_off, (N + 1) * 4));
     ix.R = (N + kRun - 1) / kRun;
@@ -311,7 +312,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_CUDA(cudaEventRecord(ev[0], st));
     auto sum_chunk = [&](uint64_t first, uint64_t count) {
         summarise(ix.rows + first * ix.n, count, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>() + first * ix.ws,
-                  nullptr, keys_in.as<uint64_t>() + first, st);
+                  nullptr, keys_in.as<uint64_t>() + first, st, ix.fw ? ix.fine + first * ix.fws : nullptr);
     };
     if (feeder) (*feeder)(sum_chunk);  // rows stream in; K1 runs per chunk behind them
     else sum_chunk(0, N);

@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <functional>
 
+#include "common.cuh"
+
 namespace tsg {
 
 // Entries per page: the unit of the leaf-level lower bound and of work
@@ -27,6 +29,10 @@ struct DevIndex {
     bool own_rows = false;
     double* thr = nullptr;    // [256] thresholds for `bits`, +inf padded
     uint8_t* words = nullptr; // [N][ws] index order
+    // Fine summary (fine_width): [N][fws] quantised 2w half-segment means
+    // (fine_quant), dataset order. fw = 0: none.
+    uint8_t* fine = nullptr;
+    int fw = 0, fws = 0;
     uint32_t* pos = nullptr;  // [N] local row of each index entry
     uint32_t* leaf_off = nullptr;  // [L+1]
     uint64_t L = 0;
@@ -56,6 +62,7 @@ struct DevIndex {
         uint64_t cap = 0;               // candidate records per slot
         struct QueryWork* work = nullptr;  // [n]
         float* lut = nullptr;           // [n][w][256] squared-gap tables
+        float* fine_lut = nullptr;      // [n][fw][256] squared-gap tables of the fine summary
         uint32_t* gsurv = nullptr;      // [n][NG] surviving page groups
         uint64_t rcap = 0;              // run-list capacity per slot (every run of the shard)
         uint2* surv = nullptr;          // [n][rcap] surviving runs' entry ranges: wave 0 front, wave 1 back
@@ -87,7 +94,9 @@ constexpr int kRun = 16;  // entries per run box (the sub-page filter level)
 constexpr int kQuad = 4;  // entries per quad box (the level below runs)
 
 // Per-query device scratch (reset by the prepare kernel).
-enum WorkCounter { kNextBound = 0, kNextScan0, kNextRefine0, kNextBound1, kNextScan1, kNextRefine1, kNextCount };
+enum WorkCounter {
+    kNextBound = 0, kNextScan0, kNextRefine0, kNextBound1, kNextScan1, kNextRefine1, kNextFine0, kNextFine1, kNextCount
+};
 struct QueryWork {
     unsigned long long bsf_bits;  // best squared distance so far (double bits)
     // candidate records: wave A (low 32 bits, from the front, after the seed
@@ -107,6 +116,7 @@ struct QueryWork {
     float scan_bound;                   // BSF bound the page/word filters used
     unsigned long long boxes;           // run / quad box bounds evaluated
     unsigned long long stats[6];  // SearchStats order
+    unsigned long long fine_calcs;      // fine-summary lower bounds evaluated
     unsigned char qsym[32];
 };
 
@@ -118,11 +128,14 @@ struct DevResult {
     uint32_t flags;
     unsigned long long stats[6];
     unsigned long long boxes;
+    unsigned long long fine_calcs;
 };
 
-// K1
+// K1. fine (may be null): the fine summary rows (fine_width(n, w) symbols,
+// stride fine_stride) of the same series.
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
-               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream);
+               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream,
+               uint8_t* fine = nullptr);
 
 // Streams the shard's rows into ix.rows chunk by chunk: for each chunk it
 // enqueues the rows' arrival on ix.stream and then calls sum_chunk(first,

@@ -89,6 +89,8 @@ struct IndexView {
     float split;
     uint64_t pos_offset;
     int window;  // < 0: Euclidean; >= 0: DTW with this Sakoe-Chiba window
+    const uint8_t* fine;       // [N][fws] fine summary (dataset order); null: none
+    int fw, fws;
 };
 
 struct SlotView {
@@ -106,6 +108,8 @@ struct SlotView {
     uint64_t rcap;  // run-list capacity per slot
     uint2* dpage;   // [slots][P] pages deferred to the second bound pass
     float* dpage_lb;
+    float* fine_lut;  // [slots][fw][256] fine-summary tables
+    int fine_lut_len;
 };
 
 __device__ __forceinline__ double bsf_of(unsigned long long bits) {
@@ -145,6 +149,35 @@ __device__ __forceinline__ void fill_lut(const QueryShared& qs, int n, int w, in
         const double hi = prefix == card - 1 ? INFINITY : qs.thr[prefix];
         const double x = qs.qpaa[s];
         double gap = 0.0;
+        if (x < lo) gap = lo - x;
+        else if (x > hi) gap = x - hi;
+        out[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
+    }
+}
+
+// The fine summary's table: per fine segment s (2w half segments of n / fw
+// points) and symbol v, the squared gap between the query's fine mean (FP64,
+// the same sums as K1) and v's region (fine_quant) widened by kFineSlack,
+// times n / fw, rounded down. Every entry is <= the exact PAA term, so a sum
+// of entries (rounded down) never exceeds the squared Euclidean distance —
+// the PAA lower-bounding lemma behind mindist_paa_isax (src/metrics.cpp:47-70)
+// at twice the segments.
+__device__ __forceinline__ void fill_fine_lut(const float* s_q, int n, int fw, float* out) {
+    __shared__ double s_fm[kMaxFine];
+    const int h = n / fw;
+    if (threadIdx.x < fw) {
+        double sum = 0.0;
+        for (int j = 0; j < h; ++j) sum = __dadd_rn(sum, static_cast<double>(s_q[threadIdx.x * h + j]));
+        s_fm[threadIdx.x] = __ddiv_rn(sum, static_cast<double>(h));
+    }
+    __syncthreads();
+    const double scale = static_cast<double>(h);
+    for (int idx = threadIdx.x; idx < fw * 256; idx += blockDim.x) {
+        const int s = idx >> 8, v = idx & 255;
+        const double lo = v == 0 ? -INFINITY : kFineLo + v * kFineStep - kFineSlack;
+        const double hi = v == 255 ? INFINITY : kFineLo + (v + 1) * kFineStep + kFineSlack;
+        const double x = s_fm[s];
+        double gap = 0.0;  // a NaN mean keeps 0: never prunes
         if (x < lo) gap = lo - x;
         else if (x > hi) gap = x - hi;
         out[idx] = __double2float_rd(__dmul_rn(__dmul_rn(gap, gap), scale));
@@ -484,6 +517,7 @@ __global__ void __launch_bounds__(kThreads)
     if (ix.window < 0) {
         fill_lut(qs, ix.n, ix.w, ix.bits, S.lut + static_cast<uint64_t>(q) * S.lut_len);
         if (threadIdx.x < kMaxW) wk->qsym[threadIdx.x] = threadIdx.x < ix.w ? qs.qsym[threadIdx.x] : 0;
+        if (ix.fw) fill_fine_lut(s_q, ix.n, ix.fw, S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len);
     } else {
         // keogh_envelope (src/metrics.cpp:72-91,167-177): window max / min (exact,
         // so a direct scan equals the reference's deque), then the bands' PAA.
@@ -545,6 +579,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->overflow = (b - a) > S.cap ? 1u : 0u;
         wk->scan_bound = 0.f;
         wk->boxes = 0;
+        wk->fine_calcs = 0;
         for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
         wk->stats[kRealDist] = ix.window < 0 ? b - a : 0;  // DTW seeds count the DTWs that ran
     }
@@ -573,7 +608,7 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t p = ix.pos[e];
         const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if ((lane & (kRowLanes - 1)) == 0) {
-            cand_pos[e - a] = static_cast<uint32_t>(e);  // index-order entry (finalize maps via pos[])
+            cand_pos[e - a] = p;  // candidate records hold dataset rows
             updates += publish(wk, s, e - a, cand_sq);
         }
     }
@@ -884,13 +919,15 @@ constexpr int kStageCap = 256;
 // and rerun with a full-size slot; nothing is written out of range).
 // cut = +inf sends everything to A, cut < 0 everything to B.
 __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
-                                            float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
+                                            float cut, uint64_t cap, const uint32_t* __restrict__ pos,
+                                            uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
     for (int i0 = 0; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < cnt;
         const float lb = valid ? s_lb[i] : 0.f;
         const bool low = valid && lb <= cut;
+        const uint32_t row = valid ? pos[s_pos[i]] : 0u;  // staged entries -> dataset rows
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
         unsigned long long old = 0;
         if (lane == 0)
@@ -903,13 +940,13 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
         if (low) {
             const uint64_t at = bl + __popc(ml & below);
             if (at < cap) {
-                cand_pos[at] = s_pos[i];
+                cand_pos[at] = row;
                 cand_lb[at] = lb;
             }
         } else if (valid) {
             const uint64_t off = bh + __popc(mh & below);
             if (off < cap) {
-                cand_pos[cap - 1 - off] = s_pos[i];
+                cand_pos[cap - 1 - off] = row;
                 cand_lb[cap - 1 - off] = lb;
             }
         }
@@ -961,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         return (ns + 31) / 32;
     };
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
-        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
+        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, ix.pos, cand_pos, cand_lb);
         cnt = 0;
         scanned = warp_sum(scanned);
         pruned = warp_sum(pruned);
@@ -979,13 +1016,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         if (!m) return;
         if (pass) {
             const int slot = cnt + __popc(m & below);
-            s_pos[warp][slot] = e;  // refine gathers pos[e] off this kernel's path
+            s_pos[warp][slot] = e;  // the flush maps entries to dataset rows
             s_lb[warp][slot] = lb;
         }
         cnt += __popc(m);
         __syncwarp();
         if (cnt > kStageCap - 32) {
-            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
+            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, ix.pos, cand_pos, cand_lb);
             cnt = 0;
         }
     };
@@ -1104,6 +1141,147 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     }
 }
 
+// ------------------------------------------------- fine + refine
+// One refinement wave with the fine summary (persistent, block-to-query
+// affinity like lbscan; the query's [fw][256] fine table and the query row
+// (FP64) in shared memory). Warps claim chunks of 32 K candidate records:
+//   1. lane per record: a record whose bound is within the BSF takes its fine
+//      bound (the fine row of its series, one table entry per fine segment,
+//      __fadd_rd sums) — the larger of the two bounds decides;
+//   2. the survivors (ballot compaction into the warp's list) are refined by
+//      the warp's four 8-lane groups: 256-bit row loads, FP64 blocks added
+//      left to right like squared_l2 (src/metrics.cpp:17-40), abandoned
+//      against the live BSF between 256-float rounds; the BSF is an atomicMin
+//      on the double bits (SharedBsf, src/query.cpp:35-42).
+// Every record gets its squared distance or +inf in cand_sq (finalize).
+#ifndef TSG_FINE_K
+#define TSG_FINE_K 4
+#endif
+constexpr int kFineK = TSG_FINE_K;  // candidate records per lane per chunk
+template <int FW, int K, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    k_fine_refine(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    const int fw = FW > 0 ? FW : ix.fw;
+    float* s_flut = reinterpret_cast<float*>(s_dyn);                                         // [fw][256]
+    double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(fw) * 256 * 4);    // [n]
+    __shared__ int s_sel;
+    __shared__ uint16_t s_c[kWarps][32 * K];  // kept records: offset in the chunk
+    __shared__ uint32_t s_p[kWarps][32 * K];  // and their dataset rows
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wg = lane / kRowLanes;
+    const bool leader = (lane & (kRowLanes - 1)) == 0;
+    int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
+    const int k_next = wave == 0 ? kNextFine0 : kNextFine1;
+    auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
+        const unsigned long long c = w->cand;
+        if (wave == 0) {
+            begin = w->nseed;
+            end = c & 0xFFFFFFFFull;
+        } else {
+            begin = S.cap - (c >> 32);
+            end = S.cap;
+        }
+    };
+    auto nchunks = [&](const QueryWork* w) -> uint32_t {
+        if (w->overflow) return 0;
+        uint64_t b, e;
+        range(w, b, e);
+        return static_cast<uint32_t>((e - b + 32 * K - 1) / (32 * K));
+    };
+    unsigned long long calcs = 0, refined = 0, updates = 0;
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous query
+        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
+        __syncthreads();
+        const int q = s_sel;
+        if (q < 0) break;
+        cur = q;
+        QueryWork* wk = S.work + q;
+        {
+            const float4* src = reinterpret_cast<const float4*>(S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len);
+            float4* dst = reinterpret_cast<float4*>(s_flut);
+            for (int i = threadIdx.x; i < fw * 64; i += blockDim.x) dst[i] = src[i];
+        }
+        load_query_f64(s_qd, queries + static_cast<uint64_t>(q) * ix.n, ix.n);  // syncs
+        const uint32_t* cand_pos = S.cand_pos + q * S.cap;
+        const float* cand_lb = S.cand_lb + q * S.cap;
+        double* cand_sq = S.cand_sq + q * S.cap;
+        uint64_t begin, end;
+        range(wk, begin, end);
+        const uint32_t nch = nchunks(wk);
+        for (;;) {
+            uint32_t chunk = 0;
+            if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
+            chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+            if (chunk >= nch) break;
+            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * (32 * K);
+            float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            bool live[K];
+            uint32_t row[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint64_t c = c0 + 32 * k + lane;
+                live[k] = c < end && cand_lb[c] <= bnd;
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) row[k] = live[k] ? cand_pos[c0 + 32 * k + lane] : 0u;
+            float acc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = 0.f;
+            for (int h = 0; 16 * h < fw; ++h) {
+                uint4 v[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    v[k] = live[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(row[k]) * ix.fws + 16 * h)
+                                   : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int sg = 16 * h + i;
+                    if (FW > 0 || sg < fw) {
+#pragma unroll
+                        for (int k = 0; k < K; ++k) acc[k] = __fadd_rd(acc[k], s_flut[sg * 256 + byte_of(v[k], i)]);
+                    }
+                }
+            }
+            bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                calcs += live[k] ? 1 : 0;
+                const bool keep = live[k] && acc[k] <= bnd;
+                const uint64_t c = c0 + 32 * k + lane;
+                if (c < end && !keep) cand_sq[c] = INFINITY;
+                const unsigned mk = __ballot_sync(0xFFFFFFFFu, keep);
+                if (keep) {
+                    const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
+                    s_c[warp][slot] = static_cast<uint16_t>(32 * k + lane);
+                    s_p[warp][slot] = row[k];
+                }
+                m += __popc(mk);
+            }
+            __syncwarp();
+            for (uint32_t j = wg; j < m; j += 32 / kRowLanes) {
+                const uint64_t c = c0 + s_c[warp][j];
+                const double sq = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(s_p[warp][j]) * ix.n, s_qd, ix.n,
+                                                    &wk->bsf_bits);
+                if (leader) {
+                    refined += 1;
+                    updates += publish(wk, sq, c, cand_sq);
+                }
+            }
+            __syncwarp();  // the warp's list is reused by the next chunk
+        }
+        calcs = warp_sum(calcs);
+        if (lane == 0 && calcs) atomicAdd(&wk->fine_calcs, calcs);
+        if (leader) {
+            if (refined) atomicAdd(&wk->stats[kRealDist], refined);
+            if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+        }
+        calcs = refined = updates = 0;
+    }
+}
+
 // ------------------------------------------------------------ refine
 // One refinement wave (persistent, affinity chunks of kRefChunk candidates):
 // wave 0 = records [nseed, nA), wave 1 = [cap - nB, cap). Each 8-lane group
@@ -1167,7 +1345,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
         const uint64_t c1 = u64min(c0 + kRefChunk, end);
         uint64_t c = c0 + g;
         float nlb = c < c1 ? cand_lb[c] : 0.f;
-        uint32_t np = c < c1 ? ix.pos[cand_pos[c]] : 0u;  // candidate records hold index-order entries
+        uint32_t np = c < c1 ? cand_pos[c] : 0u;  // candidate records hold dataset rows
         // Cached pruning bound: refreshed from the BSF each refinement sees,
         // so a skipped candidate costs no memory access (a stale bound only
         // refines more).
@@ -1177,7 +1355,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
             const uint32_t p = np;
             if (c + kGroups < c1) {
                 nlb = cand_lb[c + kGroups];
-                np = ix.pos[cand_pos[c + kGroups]];
+                np = cand_pos[c + kGroups];
             }
             if (lb > bnd) {
                 if (leader) cand_sq[c] = INFINITY;
@@ -1395,7 +1573,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
                 if (keep) {
                     const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
                     s_c[warp][slot] = static_cast<uint32_t>(c);
-                    s_p[warp][slot] = ix.pos[rcp[k]];  // candidate records hold index-order entries
+                    s_p[warp][slot] = rcp[k];  // candidate records hold dataset rows
                 }
                 m += __popc(mk);
             }
@@ -1741,7 +1919,7 @@ __global__ void __launch_bounds__(kThreads)
         const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(p) * n,
                                                 n, ix.window, wk, ran);
         if (lane == 0) {
-            cand_pos[e - a] = static_cast<uint32_t>(e);
+            cand_pos[e - a] = p;
             updates += publish(wk, sq, e - a, cand_sq);
             refined += ran ? 1 : 0;
         }
@@ -1806,7 +1984,7 @@ __global__ void __launch_bounds__(kThreads)
             const bool in = c < end;
             const bool keep = in && cand_lb[c] <= bnd;
             if (in && !keep) cand_sq[c] = INFINITY;
-            const uint32_t p = keep ? ix.pos[cand_pos[c]] : 0u;
+            const uint32_t p = keep ? cand_pos[c] : 0u;
             unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
             if constexpr (M == 1) {
                 // LB_Keogh first; the survivors two at a time through the paired DTW
@@ -1903,7 +2081,7 @@ __global__ void __launch_bounds__(kThreads)
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (sv[u] <= lim && sqrt(sv[u]) == dist) mine = min(mine, ix.pos[cand_pos[cv[u]]]);
+                if (sv[u] <= lim && sqrt(sv[u]) == dist) mine = min(mine, cand_pos[cv[u]]);
         }
     }
 #pragma unroll
@@ -1928,6 +2106,7 @@ __global__ void __launch_bounds__(kThreads)
     out->stats[kPruned] = wk->stats[kPruned];
     out->stats[kQueueIns] = (cand & 0xFFFFFFFFull) - wk->nseed + (cand >> 32);
     out->boxes = wk->boxes;
+    out->fine_calcs = wk->fine_calcs;
 }
 
 template <typename K>
@@ -1995,8 +2174,13 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.split = ix.refine_split;
     iv.pos_offset = ix.pos_offset;
     iv.window = window;
+    const bool fine = ix.fw > 0 && window < 0;  // the fine bound is Euclidean
+    iv.fine = fine ? ix.fine : nullptr;
+    iv.fw = ix.fw;
+    iv.fws = ix.fws;
     SlotView sv{slots.work, slots.lut, slots.gsurv, slots.surv, slots.surv_lb, slots.cand_pos, slots.cand_lb,
-                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256, slots.rcap, slots.dpage, slots.dpage_lb};
+                slots.cand_sq, slots.env, slots.cap, ix.P, ix.NG, w * 256, slots.rcap, slots.dpage, slots.dpage_lb,
+                slots.fine_lut, ix.fw * 256};
     // DTW kernels, by band-diagonal registers per lane (window <= 32 M - 1).
     const bool dtw = window >= 0;
     if (window > kMaxDtwWindow) throw std::invalid_argument("exact_search: dtw window above the device limit");
@@ -2016,6 +2200,16 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const unsigned refine_grid = tma ? static_cast<unsigned>(sms * blocks_per_sm(refine_tma, tma_bytes))
                                      : static_cast<unsigned>(sms * blocks_per_sm(refine, qd_bytes));
     const unsigned fin_x = std::max(1u, std::min(256u, static_cast<unsigned>(sms * 32 / nq)));
+    auto fine_k = vec ? (ix.fw == 32 ? k_fine_refine<32, kFineK, true> : ix.fw == 64 ? k_fine_refine<64, kFineK, true>
+                                                                          : k_fine_refine<0, kFineK, true>)
+                      : (ix.fw == 32 ? k_fine_refine<32, kFineK, false> : ix.fw == 64 ? k_fine_refine<64, kFineK, false>
+                                                                           : k_fine_refine<0, kFineK, false>);
+    const size_t fine_bytes = static_cast<size_t>(ix.fw) * 256 * sizeof(float) + qd_bytes;
+    unsigned fine_grid = 0;
+    if (fine) {
+        TSG_CUDA(cudaFuncSetAttribute(fine_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        fine_grid = static_cast<unsigned>(sms * blocks_per_sm(fine_k, fine_bytes));
+    }
     if (dtw) {
         TSG_CUDA(cudaFuncSetAttribute(seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
         TSG_CUDA(cudaFuncSetAttribute(refine_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -2064,7 +2258,8 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                 TSG_LAUNCHED();
             });
             mark(wave == 0 ? 3 : 5, [&] {
-                if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, qe_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, qe_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 TSG_LAUNCHED();

@@ -50,6 +50,8 @@ struct SumArgs {
     uint8_t* words;
     uint32_t* root_keys;  // may be null
     uint64_t* sort_keys;  // may be null
+    uint8_t* fine;        // may be null: fine summary rows (fws bytes each)
+    int fw, fws;
 };
 
 // Sort key: the first 64 bits of the plane-major bit string of the word
@@ -82,13 +84,15 @@ __device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const 
     }
 }
 
-template <int STAGES, bool VEC>
-__global__ void __launch_bounds__(kSumThreads)
+// SEG > 0: compile-time segment length of the w = 16 path (n = 16 SEG);
+// VEC: segments are whole float4s.
+template <int STAGES, int SEG, bool VEC, bool FINE>
+__global__ void __launch_bounds__(kSumThreads, 2)
     k_summarise_tma(const __grid_constant__ CUtensorMap tmap, SumArgs a,
                     const double* __restrict__ thr_g) {
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* stages = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // (offset arithmetic on the shared array keeps the shared address space: LDS, not generic loads)
+    unsigned char* stages = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t tile_bytes = static_cast<uint32_t>(a.R) * a.n * 4u;
     const uint32_t stage_stride = (tile_bytes + 1023u) & ~1023u;
     uint64_t* full = reinterpret_cast<uint64_t*>(stages + STAGES * stage_stride);
@@ -133,28 +137,55 @@ __global__ void __launch_bounds__(kSumThreads)
     // Segment mean: sum / seg. For a power-of-two seg, multiplying by the exact
     // reciprocal is the same IEEE result as the division (pure exponent
     // shift, identical rounding), and far cheaper than DDIV's sequence.
-    const bool pow2 = (a.seg & (a.seg - 1)) == 0;
-    const double inv_seg = 1.0 / static_cast<double>(a.seg);
-    auto segment_symbol = [&](const unsigned char* tile, int ser, int g) -> unsigned {
-        const uint32_t f0 = static_cast<uint32_t>(ser * a.n + g * a.seg);
-        double sum = 0.0;
+    const int segl = SEG > 0 ? SEG : a.seg;
+    const bool pow2 = (segl & (segl - 1)) == 0;
+    const double inv_seg = 1.0 / static_cast<double>(segl);
+    // FINE: the same pass also yields the two half-segment sums (the first
+    // half is a prefix of the reference-order sum; the second half is summed
+    // from 0.0 in its own chain) -> two fine symbols packed in *fine2.
+    const int half = segl >> 1;
+    const bool pow2h = (half & (half - 1)) == 0;
+    const double inv_half = 1.0 / static_cast<double>(half);
+    auto segment_symbol = [&](const unsigned char* tile, int ser, int g, unsigned* fine2) -> unsigned {
+        const uint32_t f0 = static_cast<uint32_t>(ser * (SEG > 0 ? 16 * SEG : a.n) + g * segl);
+        double sum = 0.0, sa = 0.0, sb = 0.0;
         if (VEC) {
-            const int nq = a.seg >> 2;
+            const int nq = segl >> 2, nqh = half >> 2;  // FINE && VEC: seg % 8 == 0
+#pragma unroll
             for (int q = 0; q < nq; ++q) {
                 const float4 v = *reinterpret_cast<const float4*>(tile + swz((f0 + 4u * q) * 4u));
                 sum = __dadd_rn(sum, static_cast<double>(v.x));
                 sum = __dadd_rn(sum, static_cast<double>(v.y));
                 sum = __dadd_rn(sum, static_cast<double>(v.z));
                 sum = __dadd_rn(sum, static_cast<double>(v.w));
+                if (FINE) {
+                    if (q >= nqh) {
+                        sb = __dadd_rn(sb, static_cast<double>(v.x));
+                        sb = __dadd_rn(sb, static_cast<double>(v.y));
+                        sb = __dadd_rn(sb, static_cast<double>(v.z));
+                        sb = __dadd_rn(sb, static_cast<double>(v.w));
+                    }
+                    if (q == nqh - 1) sa = sum;
+                }
             }
         } else {
-            for (int j = 0; j < a.seg; ++j) {
+#pragma unroll
+            for (int j = 0; j < segl; ++j) {
                 const float v = *reinterpret_cast<const float*>(tile + swz((f0 + j) * 4u));
                 sum = __dadd_rn(sum, static_cast<double>(v));
+                if (FINE) {
+                    if (j >= half) sb = __dadd_rn(sb, static_cast<double>(v));
+                    if (j == half - 1) sa = sum;
+                }
             }
         }
-        const double mean = pow2 ? __dmul_rn(sum, inv_seg) : __ddiv_rn(sum, static_cast<double>(a.seg));
-        return symbol_fast(thr, bins, a.bits, mean) << (8 - a.bits);
+        if (FINE) {
+            const double ma = pow2h ? __dmul_rn(sa, inv_half) : __ddiv_rn(sa, static_cast<double>(half));
+            const double mb = pow2h ? __dmul_rn(sb, inv_half) : __ddiv_rn(sb, static_cast<double>(half));
+            *fine2 = fine_quant(ma) | (fine_quant(mb) << 8);
+        }
+        const double mean = pow2 ? __dmul_rn(sum, inv_seg) : __ddiv_rn(sum, static_cast<double>(segl));
+        return symbol_step(thr, bins, a.bits, mean) << (8 - a.bits);
     };
 
     int it = 0;
@@ -172,7 +203,8 @@ __global__ void __launch_bounds__(kSumThreads)
             for (int pair = warp; 2 * pair < valid; pair += kConsumerWarps) {
                 const int ser = 2 * pair + half;
                 const bool ok = ser < valid;
-                const unsigned sym = ok ? segment_symbol(tile, ser, g) : 0u;
+                unsigned f2 = 0;
+                const unsigned sym = ok ? segment_symbol(tile, ser, g, &f2) : 0u;
                 uint64_t key = 0;
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
@@ -188,6 +220,14 @@ __global__ void __launch_bounds__(kSumThreads)
                 if (ok && g == 0) {
                     if (a.sort_keys) a.sort_keys[idx] = key;
                     if (a.root_keys) a.root_keys[idx] = static_cast<uint32_t>(key >> 48);
+                }
+                if (FINE) {  // 32 fine bytes per series: lanes g = 0, 8 store 16 each
+                    const unsigned u = f2 | (__shfl_down_sync(0xFFFFFFFFu, f2, 1) << 16);
+                    const unsigned u2 = __shfl_down_sync(0xFFFFFFFFu, u, 2);
+                    const unsigned u4 = __shfl_down_sync(0xFFFFFFFFu, u, 4);
+                    const unsigned u6 = __shfl_down_sync(0xFFFFFFFFu, u, 6);
+                    if (ok && (g & 7) == 0)
+                        *reinterpret_cast<uint4*>(a.fine + idx * a.fws + 2 * g) = make_uint4(u, u2, u4, u6);
                 }
             }
             __syncwarp();
@@ -205,7 +245,11 @@ __global__ void __launch_bounds__(kSumThreads)
         uint8_t* wb = wbuf + (it & 1) * a.R * a.ws;
         for (int idx = tid; idx < valid * a.w; idx += kConsumers) {
             const int ser = idx / a.w, g = idx - ser * a.w;
-            wb[ser * a.ws + g] = static_cast<uint8_t>(segment_symbol(tile, ser, g));
+            unsigned f2 = 0;
+            wb[ser * a.ws + g] = static_cast<uint8_t>(segment_symbol(tile, ser, g, &f2));
+            if (FINE)
+                *reinterpret_cast<uint16_t*>(a.fine + (a.out_base + first + ser) * a.fws + 2 * g) =
+                    static_cast<uint16_t>(f2);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -229,11 +273,22 @@ __global__ void k_summarise_generic(const float* __restrict__ rows, SumArgs a,
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < a.count;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const float* r = rows + i * static_cast<uint64_t>(a.n);
+        const int half = a.seg >> 1;
         for (int g = 0; g < a.w; ++g) {
-            double sum = 0.0;
-            for (int j = 0; j < a.seg; ++j) sum = __dadd_rn(sum, static_cast<double>(r[g * a.seg + j]));
+            double sum = 0.0, sa = 0.0, sb = 0.0;
+            for (int j = 0; j < a.seg; ++j) {
+                const double v = static_cast<double>(r[g * a.seg + j]);
+                sum = __dadd_rn(sum, v);
+                if (j >= half) sb = __dadd_rn(sb, v);
+                if (j == half - 1) sa = sum;
+            }
             const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
             wrow[g] = static_cast<uint8_t>(symbol_fast(thr, bins, a.bits, mean) << (8 - a.bits));
+            if (a.fine) {
+                uint8_t* f = a.fine + (a.out_base + i) * a.fws + 2 * g;
+                f[0] = static_cast<uint8_t>(fine_quant(__ddiv_rn(sa, static_cast<double>(half))));
+                f[1] = static_cast<uint8_t>(fine_quant(__ddiv_rn(sb, static_cast<double>(half))));
+            }
         }
         uint8_t buf[32] __attribute__((aligned(16)));
         for (int k = 0; k < 32; ++k) buf[k] = k < a.w ? wrow[k] : 0;
@@ -266,7 +321,7 @@ size_t tma_smem_bytes(int R, int n, int ws) {
 }  // namespace
 
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
-               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream) {
+               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream, uint8_t* fine) {
     if (count == 0) return;
     SumArgs a{};
     a.n = n;
@@ -277,6 +332,9 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
     a.words = words;
     a.root_keys = root_keys;
     a.sort_keys = sort_keys;
+    a.fw = fine_width(n, w);
+    a.fws = fine_stride(a.fw);
+    a.fine = a.fw ? fine : nullptr;
 
     int dev = 0, sms = 0;
     TSG_CUDA(cudaGetDevice(&dev));
@@ -299,8 +357,16 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
     if (R < 1) R = 1;
     a.R = R;
     const size_t smem = tma_smem_bytes(R, n, a.ws);
-    const bool vec = (a.seg % 4) == 0;
-    auto kern = vec ? k_summarise_tma<kStages, true> : k_summarise_tma<kStages, false>;
+    const bool with_fine = a.fine != nullptr;
+    const bool vec = (a.seg % 4) == 0 && (!with_fine || a.seg % 8 == 0);
+    // compile-time segment lengths of the BASELINE shapes (n = 256, 128, 96 at w = 16)
+    using Kern = void (*)(const CUtensorMap, SumArgs, const double*);
+    Kern kern;
+    if (w == 16 && a.seg == 16) kern = with_fine ? k_summarise_tma<kStages, 16, true, true> : k_summarise_tma<kStages, 16, true, false>;
+    else if (w == 16 && a.seg == 8) kern = with_fine ? k_summarise_tma<kStages, 8, true, true> : k_summarise_tma<kStages, 8, true, false>;
+    else if (w == 16 && a.seg == 6) kern = with_fine ? k_summarise_tma<kStages, 6, false, true> : k_summarise_tma<kStages, 6, false, false>;
+    else if (with_fine) kern = vec ? k_summarise_tma<kStages, 0, true, true> : k_summarise_tma<kStages, 0, false, true>;
+    else kern = vec ? k_summarise_tma<kStages, 0, true, false> : k_summarise_tma<kStages, 0, false, false>;
     TSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
     int per_sm = 0;

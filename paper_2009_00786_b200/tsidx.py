@@ -118,6 +118,7 @@ class SearchResult:
     position: int
     stats: SearchStats
     box_calcs: int = 0  # quad box bounds evaluated (device extension of SearchStats)
+    fine_calcs: int = 0  # fine-summary lower bounds evaluated before refinement (device extension)
 
 
 @dataclasses.dataclass
@@ -149,7 +150,7 @@ def _stats_from_c(s: _lib.tsg_build_stats) -> BuildStats:
 
 def _result_from_c(r: _lib.tsg_result) -> SearchResult:
     st = SearchStats(**{f: getattr(r.stats, f) for f, _ in _lib.tsg_search_stats._fields_})
-    return SearchResult(float(r.distance), int(r.position), st, int(r.box_calcs))
+    return SearchResult(float(r.distance), int(r.position), st, int(r.box_calcs), int(r.fine_calcs))
 
 
 class Context:
@@ -230,6 +231,17 @@ class Index:
         check(lib().tsg_index_export(self._h, words.ctypes.data, pos.ctypes.data, off.ctypes.data,
                                      poff.ctypes.data, lo.ctypes.data, hi.ctypes.data))
         return words, pos, off, poff, lo, hi
+
+    def export_fine(self):
+        """Fine summary rows [count][fine_width] in dataset order (None when the index has none)."""
+        fw = C.c_uint32(0)
+        check(lib().tsg_index_export_fine(self._h, C.byref(fw), None))
+        if fw.value == 0:
+            return None
+        stride = (fw.value + 15) // 16 * 16
+        out = np.empty((len(self._data), stride), np.uint8)
+        check(lib().tsg_index_export_fine(self._h, None, out.ctypes.data))
+        return out[:, :fw.value]
 
     def free(self):
         if getattr(self, "_h", None):

@@ -405,3 +405,56 @@ def test_dtw_members_and_limits(oracle):
     big = tg.build_index(oracle.generate(300, 512, 1302), tg.IndexConfig(n=512, w=16))
     with pytest.raises(tg.InvalidArgument):
         tg.exact_search(big, np.zeros(512, np.float32), tg.Measure.dtw(256))  # above the device band limit
+
+
+# ---- fine summary (second lower bound in front of refinement) ------------------
+
+def fine_symbols_reference(rows, fw):
+    """Uniform quantisation of the half-segment means (sequential FP64 sums) over [-2.5, 2.5)."""
+    count, n = rows.shape
+    h = n // fw
+    x = rows.astype(np.float64).reshape(count, fw, h)
+    s = np.zeros((count, fw))
+    for j in range(h):
+        s = s + x[:, :, j]
+    m = s / h
+    return np.clip(np.floor((m + 2.5) * 51.2), 0, 255).astype(np.int32), m
+
+
+@pytest.mark.parametrize("count,n,w,bits", [(3000, 256, 16, 8), (2000, 128, 16, 8), (2000, 96, 16, 8),
+                                            (1500, 64, 8, 4), (1200, 60, 5, 8), (1000, 128, 32, 8)])
+def test_fine_summary_quantises_half_segment_means(oracle, count, n, w, bits):
+    """Fine summary = the 2w half-segment means quantised in 5/256 steps (boundary cases counted)."""
+    rows = oracle.generate(count, n, 31 * n + w)
+    index = tg.build_index(rows, tg.IndexConfig(n=n, w=w, max_card_bits=bits, leaf_capacity=50))
+    fine = index.export_fine()
+    if n % (2 * w) or 2 * w > 64:
+        assert fine is None
+        return
+    want, m = fine_symbols_reference(rows, 2 * w)
+    assert fine.shape == want.shape
+    diff = fine.astype(np.int32) - want
+    bad = diff != 0
+    # only float rounding at a region boundary may move a symbol, by one
+    assert np.all(np.abs(diff) <= 1)
+    edge = np.abs((m + 2.5) * 51.2 - np.round((m + 2.5) * 51.2)) < 1e-3
+    assert np.all(edge[bad]), int(np.count_nonzero(bad & ~edge))
+
+
+def test_fine_summary_prunes_refinement_without_changing_answers(oracle, monkeypatch):
+    rows = oracle.generate(40000, 256, 1)
+    rng = np.random.default_rng(11)
+    queries = np.concatenate([oracle.generate(12, 256, 2),
+                              rows[rng.integers(0, 40000, 4)] + 0.2 * rng.standard_normal((4, 256)).astype(np.float32),
+                              rows[[5, 17]]]).astype(np.float32)
+    cfg = tg.IndexConfig(n=256, w=16, leaf_capacity=200)
+    _, with_fine = check_against_scan(oracle, rows, queries, cfg)
+    monkeypatch.setenv("TSG_NO_FINE", "1")  # read when the index is built
+    index = tg.build_index(rows, cfg)
+    assert index.export_fine() is None
+    _, without = check_against_scan(oracle, rows, queries, cfg, index=index)
+    for a, b in zip(with_fine, without):
+        assert (a.position, a.distance) == (b.position, b.distance)
+        assert b.fine_calcs == 0
+    assert sum(r.fine_calcs for r in with_fine) > 0
+    assert sum(r.stats.real_dist_calcs for r in with_fine) < sum(r.stats.real_dist_calcs for r in without)
