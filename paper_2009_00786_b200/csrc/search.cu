@@ -364,6 +364,13 @@ __device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, u
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
 }
 
+// L2 prefetch of boxes / words a few steps before they are read (the box
+// filters are bound by load latency; TSG_PREFETCH=0 for A/B builds).
+#ifndef TSG_PREFETCH
+#define TSG_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // -------------------------------------------------------- scheduling
 // Block-level work distribution with query affinity. Each query has a chunk
 // counter per kernel (`k`); a block drains chunks of its current query and,
@@ -910,6 +917,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 }
 
 // ------------------------------------------------------------ lbscan
+
 constexpr int kStageCap = 256;
 
 // Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
@@ -1079,7 +1087,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         pruned += ok && !pass ? 1 : 0;
         boxes += ok ? 1 : 0;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-        if (pass) s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
+        if (pass) {
+            s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
+            if (TSG_PREFETCH) prefetch_l2(ix.words + static_cast<uint64_t>(e0) * WS);  // read when 16 quads queue
+        }
         qt += __popc(m);
         __syncwarp();
         while (qt - qh >= 16) drain_quads();
@@ -1129,7 +1140,14 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
                 pruned += pass ? 0 : 1;
             }
             const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
-            if (pass) s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
+            if (pass) {
+                s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
+                if (TSG_PREFETCH) {  // the run's quad boxes are read a few drains later
+                    const uint64_t qd0 = static_cast<uint64_t>(run.x / kRun) * (kRun / kQuad);
+                    prefetch_l2(ix.quad_lo + qd0 * WS);
+                    prefetch_l2(ix.quad_hi + qd0 * WS);
+                }
+            }
             rt += __popc(m);
             __syncwarp();
             while (rt - rh >= 8) drain_runs();
@@ -1158,8 +1176,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
 #define TSG_FINE_K 4
 #endif
 constexpr int kFineK = TSG_FINE_K;  // candidate records per lane per chunk
+#ifndef TSG_MINB_FINE
+#define TSG_MINB_FINE 2
+#endif
 template <int FW, int K, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
     k_fine_refine(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     extern __shared__ __align__(128) unsigned char s_dyn[];
     const int fw = FW > 0 ? FW : ix.fw;
