@@ -1422,9 +1422,13 @@ constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;  // candidate records per warp chu
 constexpr bool tma_half_rows(int n) { return TSG_HALF_ROWS && (n / 8) % 16 == 0; }
 // Floats of row buffers per 8-lane group: two whole rows, or three half rows.
 constexpr int tma_group_floats(int n) { return tma_half_rows(n) ? 3 * n / 2 : 2 * n; }
-template <int NB>
-__global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
+// FW > 0: the fine summary's bound (fine width FW, the query's [FW][256] table
+// after the query in shared memory) filters the records in phase 1 as well;
+// chunks are then 128 records and the kernel runs at two blocks per SM.
+template <int NB, int FW>
+__global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
+    constexpr uint32_t kChunk = FW > 0 ? 128u : kTmaChunk;
     constexpr int kGroups = kThreads / kRowLanes;
     constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
@@ -1435,8 +1439,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
     constexpr int kGF = tma_group_floats(n);  // row buffers per group: 2 rows, or 3 half rows
     float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][kGF]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * kGF * 4);  // lane-ordered query
+    float* s_flut = reinterpret_cast<float*>(s_qd + 8 * 8 * kTq);                              // [FW][256]
     __shared__ __align__(8) uint64_t s_bar[kGroups][3];
-    __shared__ uint32_t s_c[kWarps][kTmaChunk], s_p[kWarps][kTmaChunk];
+    __shared__ uint32_t s_c[kWarps][kChunk], s_p[kWarps][kChunk];
     __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
     const int wg = lane / kRowLanes;  // group within the warp
@@ -1451,7 +1456,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
     unsigned phase = 0;  // bit b: parity of this group's buffer b
     float* buf0 = s_rows + static_cast<size_t>(g) * kGF;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
-    unsigned long long refined = 0, updates = 0;
+    unsigned long long refined = 0, updates = 0, fine_calcs = 0;
     const int k_next = wave == 0 ? kNextRefine0 : kNextRefine1;
     auto range = [wave, &S](const QueryWork* w, uint64_t& begin, uint64_t& end) {
         const unsigned long long c = w->cand;
@@ -1467,7 +1472,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
         if (w->overflow) return 0;
         uint64_t b, e;
         range(w, b, e);
-        return static_cast<uint32_t>((e - b + kTmaChunk - 1) / kTmaChunk);
+        return static_cast<uint32_t>((e - b + kChunk - 1) / kChunk);
     };
     auto issue = [&](int b, uint32_t p) {  // leader: row p -> this group's buffer b
         fence_proxy_async_smem();
@@ -1551,6 +1556,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
             const int k = jj + kRowLanes * t;
             s_qd[e] = k < NB ? static_cast<double>(qg[8 * k + i]) : 0.0;
         }
+        if (FW > 0) {
+            const float4* src = reinterpret_cast<const float4*>(S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len);
+            for (int i = threadIdx.x; i < FW * 64; i += blockDim.x) reinterpret_cast<float4*>(s_flut)[i] = src[i];
+        }
         __syncthreads();
         const uint32_t* cand_pos = S.cand_pos + q * S.cap;
         const float* cand_lb = S.cand_lb + q * S.cap;
@@ -1563,13 +1572,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
         chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
         // The current chunk's records (bound, entry) are loaded one chunk ahead,
         // while the previous chunk's rows are being refined.
-        constexpr int kPer = kTmaChunk / 32;
+        constexpr int kPer = kChunk / 32;
         float rlb[kPer];
         uint32_t rcp[kPer];
         auto load_records = [&](uint32_t ch, float* lbv, uint32_t* cpv) {
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
-                const uint64_t c = begin + static_cast<uint64_t>(ch) * kTmaChunk + 32 * k + lane;
+                const uint64_t c = begin + static_cast<uint64_t>(ch) * kChunk + 32 * k + lane;
                 const bool in = ch < nch && c < end;
                 lbv[k] = in ? cand_lb[c] : INFINITY;
                 cpv[k] = in ? cand_pos[c] : 0u;
@@ -1579,16 +1588,43 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
         while (chunk < nch) {
             uint32_t pre = 0;
             if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);
-            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kTmaChunk;
-            const uint64_t c1 = u64min(c0 + kTmaChunk, end);
-            // Phase 1 (warp): keep the records whose bound is within the BSF.
+            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kChunk;
+            const uint64_t c1 = u64min(c0 + kChunk, end);
+            // Phase 1 (warp): keep the records whose bound (then fine bound) is within the BSF.
             const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+            bool kp[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) kp[k] = c0 + 32 * k + lane < c1 && rlb[k] <= bnd;
+            if (FW > 0) {
+                float acc[kPer];
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) acc[k] = 0.f;
+#pragma unroll
+                for (int h = 0; h < FW / 16; ++h) {
+                    uint4 v[kPer];
+#pragma unroll
+                    for (int k = 0; k < kPer; ++k)
+                        v[k] = kp[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws + 16 * h)
+                                     : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+#pragma unroll
+                        for (int k = 0; k < kPer; ++k)
+                            acc[k] = __fadd_rd(acc[k], s_flut[(16 * h + i) * 256 + byte_of(v[k], i)]);
+                }
+                const float bnd2 = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
+#pragma unroll
+                for (int k = 0; k < kPer; ++k) {
+                    fine_calcs += kp[k] ? 1 : 0;
+                    kp[k] = kp[k] && acc[k] <= bnd2;
+                }
+            }
             uint32_t m = 0;
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
                 const uint64_t c = c0 + 32 * k + lane;
                 const bool in = c < c1;
-                const bool keep = in && rlb[k] <= bnd;
+                const bool keep = kp[k];
                 if (in && !keep) cand_sq[c] = INFINITY;
                 const unsigned mk = __ballot_sync(0xFFFFFFFFu, keep);
                 if (keep) {
@@ -1729,7 +1765,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_TMA)
             if (refined) atomicAdd(&wk->stats[kRealDist], refined);
             if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
         }
-        refined = updates = 0;
+        if (FW > 0) {
+            fine_calcs = warp_sum(fine_calcs);
+            if (lane == 0 && fine_calcs) atomicAdd(&wk->fine_calcs, fine_calcs);
+        }
+        refined = updates = fine_calcs = 0;
     }
 }
 
@@ -2157,8 +2197,8 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     auto groups = ix.ws == 16 ? (w16 ? k_groups<16, true> : k_groups<16, false>) : k_groups<32, false>;
     // Per-device function attributes (cheap; set on every call so each device is covered).
     // TMA-staged refinement for the row lengths it is instantiated for.
-    auto refine_tma = n == 256 ? k_refine_tma<32> : n == 128 ? k_refine_tma<16> : n == 96 ? k_refine_tma<12>
-                    : n == 64 ? k_refine_tma<8> : n == 512 ? k_refine_tma<64> : nullptr;
+    auto refine_tma = n == 256 ? k_refine_tma<32, 0> : n == 128 ? k_refine_tma<16, 0> : n == 96 ? k_refine_tma<12, 0>
+                    : n == 64 ? k_refine_tma<8, 0> : n == 512 ? k_refine_tma<64, 0> : nullptr;
     const bool tma = vec && refine_tma && !std::getenv("TSG_NO_TMA_REFINE");
     const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * tma_group_floats(n) * 4 +
                              static_cast<size_t>((n / 8 + kRowLanes - 1) / kRowLanes) * 64 * 8;
@@ -2226,6 +2266,19 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                       : (ix.fw == 32 ? k_fine_refine<32, kFineK, false> : ix.fw == 64 ? k_fine_refine<64, kFineK, false>
                                                                            : k_fine_refine<0, kFineK, false>);
     const size_t fine_bytes = static_cast<size_t>(ix.fw) * 256 * sizeof(float) + qd_bytes;
+    // With a 32-wide fine summary and a TMA row length, the fine bound runs inside the
+    // TMA-staged refinement (half-row abandonment, double-buffered rows); TSG_FINE_FUSED=1
+    // selects the simpler fused kernel instead.
+    auto refine_tma_fine = ix.fw != 32 ? nullptr : n == 256 ? k_refine_tma<32, 32> : n == 128 ? k_refine_tma<16, 32>
+                         : n == 96 ? k_refine_tma<12, 32> : n == 64 ? k_refine_tma<8, 32> : n == 512 ? k_refine_tma<64, 32>
+                                                                                      : nullptr;
+    const bool tma_fine = fine && tma && refine_tma_fine && !std::getenv("TSG_FINE_FUSED");
+    const size_t tma_fine_bytes = tma_bytes + 32 * 256 * sizeof(float);
+    unsigned tma_fine_grid = 0;
+    if (tma_fine) {
+        TSG_CUDA(cudaFuncSetAttribute(refine_tma_fine, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+        tma_fine_grid = static_cast<unsigned>(sms * blocks_per_sm(refine_tma_fine, tma_fine_bytes));
+    }
     unsigned fine_grid = 0;
     if (fine) {
         TSG_CUDA(cudaFuncSetAttribute(fine_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -2279,7 +2332,9 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                 TSG_LAUNCHED();
             });
             mark(wave == 0 ? 3 : 5, [&] {
-                if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                if (tma_fine)
+                    refine_tma_fine<<<tma_fine_grid, kThreads, tma_fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                else if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, qe_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
