@@ -94,6 +94,7 @@ constexpr int kRun = 16;  // entries per run box (the sub-page filter level)
 constexpr int kQuad = 4;  // entries per quad box (the level below runs)
 
 // Per-query device scratch (reset by the prepare kernel).
+constexpr unsigned kTieCap = 64;
 enum WorkCounter {
     kNextBound = 0, kNextScan0, kNextRefine0, kNextBound1, kNextScan1, kNextRefine1, kNextFine0, kNextFine1, kNextCount
 };
@@ -118,6 +119,12 @@ struct QueryWork {
     unsigned long long stats[6];  // SearchStats order
     unsigned long long fine_calcs;      // fine-summary lower bounds evaluated
     unsigned char qsym[32];
+    // every refined row whose sum was within the BSF when it finished (a
+    // superset of the answer and its sqrt ties); finalize scans this list,
+    // or all candidate records when more than kTieCap were noted
+    unsigned int nties;
+    unsigned int tie_row[kTieCap];
+    double tie_sq[kTieCap];
 };
 
 constexpr uint32_t kResultOverflow = 1u;  // DevResult.flags: answer invalid, rerun with a full-size slot

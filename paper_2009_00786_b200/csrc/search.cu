@@ -59,7 +59,7 @@ enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
 // Resident blocks per SM the persistent kernels are compiled for (register
 // caps; -D overrides for tuning runs).
 #ifndef TSG_MINB_LBSCAN
-#define TSG_MINB_LBSCAN 4
+#define TSG_MINB_LBSCAN 5
 #endif
 #ifndef TSG_MINB_REFINE
 #define TSG_MINB_REFINE 4
@@ -355,10 +355,25 @@ __device__ __forceinline__ double group_row_sq(const float* __restrict__ row, co
 
 // Publishes a finished sum: candidate record, BSF atomicMin only when it can
 // improve, strict-improvement count.
-__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq) {
+// A finished row whose sum is within the BSF it was compared with (which is
+// >= the final BSF) joins the query's tie list: the answer and every row
+// whose sqrt equals it are always in the list.
+__device__ __forceinline__ void note_tie(QueryWork* wk, double s, uint32_t row, unsigned long long seen) {
+    if (!(s <= bsf_of(seen) * kSlack)) return;
+    const unsigned i = atomicAdd(&wk->nties, 1u);
+    if (i < kTieCap) {
+        wk->tie_sq[i] = s;
+        wk->tie_row[i] = row;
+    }
+}
+
+// row = ~0u: not noted (the seed range, which finalize scans itself).
+__device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, uint64_t c, double* cand_sq,
+                                                      uint32_t row) {
     cand_sq[c] = s;
     const unsigned long long cur = ld_volatile_u64(&wk->bsf_bits);
     if (!(s < INFINITY)) return 0;
+    if (row != ~0u) note_tie(wk, s, row, cur);
     const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(s));
     if (sb >= cur) return 0;
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
@@ -587,6 +602,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->scan_bound = 0.f;
         wk->boxes = 0;
         wk->fine_calcs = 0;
+        wk->nties = 0;
         for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
         wk->stats[kRealDist] = ix.window < 0 ? b - a : 0;  // DTW seeds count the DTWs that ran
     }
@@ -616,7 +632,7 @@ __global__ void __launch_bounds__(kThreads)
         const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if ((lane & (kRowLanes - 1)) == 0) {
             cand_pos[e - a] = p;  // candidate records hold dataset rows
-            updates += publish(wk, s, e - a, cand_sq);
+            updates += publish(wk, s, e - a, cand_sq, ~0u);
         }
     }
     if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
@@ -1288,7 +1304,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
                                                     &wk->bsf_bits);
                 if (leader) {
                     refined += 1;
-                    updates += publish(wk, sq, c, cand_sq);
+                    updates += publish(wk, sq, c, cand_sq, s_p[warp][j]);
                 }
             }
             __syncwarp();  // the warp's list is reused by the next chunk
@@ -1387,7 +1403,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
             const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
             if (leader) {
                 refined += 1;
-                updates += publish(wk, s, c, cand_sq);
+                updates += publish(wk, s, c, cand_sq, p);
             }
             bnd = bound_from_bits(min(seen, static_cast<unsigned long long>(__double_as_longlong(s < INFINITY ? s : INFINITY))));
         }
@@ -1641,7 +1657,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
                 // Phase 2 (half rows): first halves one row ahead in buffers 0 / 1,
                 // the pending second half in buffer 2, completed one row later.
                 bool pending = false;
-                uint32_t pend_c = 0;
+                uint32_t pend_c = 0, pend_p = 0;
                 double pend_sum = 0.0;
                 unsigned long long pend_seen = 0;
                 if (leader && static_cast<uint32_t>(wg) < m) issue_half(0, s_p[warp][wg], 0);
@@ -1671,6 +1687,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
                                 sum = __dadd_rn(sum, sb2[k]);
                             }
                             cand_sq[pend_c] = sum;
+                            note_tie(wk, sum, pend_p, pend_seen);
                             const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
                             if (sb < pend_seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
                         } else {
@@ -1686,6 +1703,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
                         if (leader) issue_half(2, s_p[warp][j], 1);
                         pending = true;
                         pend_c = s_c[warp][j];
+                        pend_p = s_p[warp][j];
                         pend_sum = part;
                         pend_seen = seen;
                     } else if (leader) {
@@ -1697,6 +1715,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
                     const double sum = half_sum(2, 1, pend_sum);
                     if (leader) {
                         cand_sq[pend_c] = sum;
+                        note_tie(wk, sum, pend_p, pend_seen);
                         const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
                         if (sb < pend_seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
                     }
@@ -1752,6 +1771,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
                     }
                     if (NB & 1) sum = __dadd_rn(sum, sums[NB - 1]);
                     cand_sq[s_c[warp][j]] = sum;
+                    note_tie(wk, sum, s_p[warp][j], seen);
                     refined += 1;
                     const unsigned long long sb = static_cast<unsigned long long>(__double_as_longlong(sum));
                     if (sb < seen) updates += atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
@@ -1981,7 +2001,7 @@ __global__ void __launch_bounds__(kThreads)
                                                 n, ix.window, wk, ran);
         if (lane == 0) {
             cand_pos[e - a] = p;
-            updates += publish(wk, sq, e - a, cand_sq);
+            updates += publish(wk, sq, e - a, cand_sq, ~0u);
             refined += ran ? 1 : 0;
         }
     }
@@ -2081,8 +2101,8 @@ __global__ void __launch_bounds__(kThreads)
                     }
                     if (lane == 0) {
                         refined += s1 >= 0 ? 2 : 1;
-                        updates += publish(wk, d0, c0, cand_sq);
-                        if (s1 >= 0) updates += publish(wk, d1, c1, cand_sq);
+                        updates += publish(wk, d0, c0, cand_sq, p0);
+                        if (s1 >= 0) updates += publish(wk, d1, c1, cand_sq, p1);
                     }
                 }
             } else {
@@ -2097,7 +2117,7 @@ __global__ void __launch_bounds__(kThreads)
                                                             ran);
                     if (lane == 0) {
                         refined += ran ? 1 : 0;
-                        updates += publish(wk, sq, cc, cand_sq);
+                        updates += publish(wk, sq, cc, cand_sq, pp);
                     }
                 }
             }
@@ -2111,6 +2131,21 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ----------------------------------------------------------- finalize
+__device__ __forceinline__ void write_result(const IndexView& ix, const QueryWork* wk, DevResult* out, double dist,
+                                             unsigned best_pos, bool overflow, unsigned long long cand) {
+    out->distance = dist;
+    out->position = static_cast<uint32_t>(best_pos + ix.pos_offset);
+    out->flags = overflow ? kResultOverflow : 0u;
+    out->stats[kLbNode] = wk->stats[kLbNode];
+    out->stats[kLbEntry] = wk->stats[kLbEntry] + wk->nseed;
+    out->stats[kRealDist] = wk->stats[kRealDist];
+    out->stats[kBsfUpd] = wk->stats[kBsfUpd];
+    out->stats[kPruned] = wk->stats[kPruned];
+    out->stats[kQueueIns] = (cand & 0xFFFFFFFFull) - wk->nseed + (cand >> 32);
+    out->boxes = wk->boxes;
+    out->fine_calcs = wk->fine_calcs;
+}
+
 // Grid (x, query): lowest position among the candidates whose sqrt(sum)
 // equals the best distance; the last block of a query writes its result
 // (flagged when the slot overflowed).
@@ -2128,6 +2163,26 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t* cand_pos = S.cand_pos + q * S.cap;
     const double* cand_sq = S.cand_sq + q * S.cap;
     uint32_t mine = 0xFFFFFFFFu;
+    const unsigned nties = wk->nties;
+    if (!overflow && nties <= kTieCap) {
+        // every row that can be the answer is in the seed range or the tie list: block 0 decides
+        if (blockIdx.x != 0) return;
+        const unsigned ns = wk->nseed;
+        for (unsigned i = threadIdx.x; i < ns + nties; i += blockDim.x) {
+            const double sv = i < ns ? cand_sq[i] : wk->tie_sq[i - ns];
+            if (sv <= lim && sqrt(sv) == dist) mine = min(mine, i < ns ? cand_pos[i] : wk->tie_row[i - ns]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
+        __shared__ unsigned s_min[kWarps];
+        if ((threadIdx.x & 31) == 0) s_min[threadIdx.x >> 5] = mine;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < kWarps; ++i) mine = min(mine, s_min[i]);
+            write_result(ix, wk, results + q, dist, mine, false, cand);
+        }
+        return;
+    }
     if (!overflow) {
         // four records per thread per step, loads first (the scan is latency-bound)
         const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x, total = lo_end + hi_n;
@@ -2155,19 +2210,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     if (!last || threadIdx.x != 0) return;
     __threadfence();
-    const unsigned best_pos = atomicAdd(&wk->best_pos, 0u);
-    DevResult* out = results + q;
-    out->distance = dist;
-    out->position = static_cast<uint32_t>(best_pos + ix.pos_offset);
-    out->flags = overflow ? kResultOverflow : 0u;
-    out->stats[kLbNode] = wk->stats[kLbNode];
-    out->stats[kLbEntry] = wk->stats[kLbEntry] + wk->nseed;
-    out->stats[kRealDist] = wk->stats[kRealDist];
-    out->stats[kBsfUpd] = wk->stats[kBsfUpd];
-    out->stats[kPruned] = wk->stats[kPruned];
-    out->stats[kQueueIns] = (cand & 0xFFFFFFFFull) - wk->nseed + (cand >> 32);
-    out->boxes = wk->boxes;
-    out->fine_calcs = wk->fine_calcs;
+    write_result(ix, wk, results + q, dist, atomicAdd(&wk->best_pos, 0u), overflow, cand);
 }
 
 template <typename K>
