@@ -108,7 +108,8 @@ struct Range {
 
 struct LeafCounters {
     unsigned long long inner, overflow, max_depth;
-    unsigned int nleaves, nopen;
+    unsigned int nleaves;
+    unsigned int nopen[2];  // open ranges of the even / odd levels (level L reads [L & 1], fills the other)
 };
 
 __device__ __forceinline__ void emit_leaf(LeafCounters* c, uint32_t* leaf_start, uint32_t a, uint32_t depth,
@@ -119,14 +120,14 @@ __device__ __forceinline__ void emit_leaf(LeafCounters* c, uint32_t* leaf_start,
     if (overflow) atomicAdd(&c->overflow, 1ull);
 }
 
-__device__ __forceinline__ void route(LeafCounters* c, uint32_t* leaf_start, Range* next, const uint64_t* keys,
-                                      uint32_t a, uint32_t b, uint32_t depth, uint32_t cap) {
+__device__ __forceinline__ void route(LeafCounters* c, unsigned* nnext, uint32_t* leaf_start, Range* next,
+                                      const uint64_t* keys, uint32_t a, uint32_t b, uint32_t depth, uint32_t cap) {
     if (b - a <= cap) {
         emit_leaf(c, leaf_start, a, depth, false);
     } else if (keys[a] == keys[b - 1]) {
         emit_leaf(c, leaf_start, a, depth, true);  // all key bits equal: cannot split further
     } else {
-        const unsigned k = atomicAdd(&c->nopen, 1u);
+        const unsigned k = atomicAdd(nnext, 1u);
         next[k] = Range{a, b, depth};
     }
 }
@@ -137,14 +138,18 @@ __global__ void k_init_ranges(const uint32_t* __restrict__ bstart, uint64_t nb, 
     GRID_STRIDE(b, nb) {
         const uint32_t lo = bstart[b];
         const uint32_t hi = b + 1 < nb ? bstart[b + 1] : static_cast<uint32_t>(n);
-        route(c, leaf_start, next, keys, lo, hi, 1, cap);
+        route(c, &c->nopen[0], leaf_start, next, keys, lo, hi, 1, cap);
     }
 }
 
 // One level of splitting: each open range splits at the first key bit its
-// first and last entries disagree on (binary search for the boundary).
-__global__ void k_split(const Range* __restrict__ open, unsigned nopen, const uint64_t* __restrict__ keys,
+// first and last entries disagree on (binary search for the boundary). The
+// level's range count is read on the device (fixed grid, no host round trip
+// per level); a level with nothing open returns at once.
+__global__ void k_split(const Range* __restrict__ open, int level, const uint64_t* __restrict__ keys,
                         uint32_t cap, LeafCounters* c, uint32_t* __restrict__ leaf_start, Range* __restrict__ next) {
+    const unsigned nopen = *reinterpret_cast<volatile unsigned*>(&c->nopen[level & 1]);
+    unsigned* nnext = &c->nopen[(level + 1) & 1];
     GRID_STRIDE(r, nopen) {
         const Range it = open[r];
         const uint64_t ka = keys[it.a], kb = keys[it.b - 1];
@@ -156,8 +161,8 @@ __global__ void k_split(const Range* __restrict__ open, unsigned nopen, const ui
             else lo = mid + 1;
         }
         atomicAdd(&c->inner, 1ull);
-        route(c, leaf_start, next, keys, it.a, lo, it.depth + 1, cap);
-        route(c, leaf_start, next, keys, lo, it.b, it.depth + 1, cap);
+        route(c, nnext, leaf_start, next, keys, it.a, lo, it.depth + 1, cap);
+        route(c, nnext, leaf_start, next, keys, lo, it.b, it.depth + 1, cap);
     }
 }
 
@@ -354,11 +359,19 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_LAUNCHED();
     Range* open = ranges_a.as<Range>();
     Range* next = ranges_b.as<Range>();
-    for (int level = 0; level < 70; ++level) {
-        const unsigned nopen = d2h(&C->nopen, st);
-        if (nopen == 0) break;
-        TSG_CUDA(cudaMemsetAsync(&C->nopen, 0, sizeof(unsigned), st));
-        k_split<<<grid_for(nopen, 128, sms), 128, 0, st>>>(open, nopen, keys, cap, C, leaf_start.as<uint32_t>(), next);
+    // A range splits at a key bit below the one its parent split at, so at most
+    // 64 levels follow the root buckets; the host checks for open ranges only
+    // every 8 levels (levels with none open return at once).
+    for (int level = 0; level < 66; ++level) {
+        if (level % 8 == 0 && level > 0) {
+            unsigned both[2];
+            TSG_CUDA(cudaMemcpyAsync(both, C->nopen, sizeof(both), cudaMemcpyDeviceToHost, st));
+            TSG_CUDA(cudaStreamSynchronize(st));
+            if (both[level & 1] == 0) break;
+        }
+        TSG_CUDA(cudaMemsetAsync(&C->nopen[(level + 1) & 1], 0, sizeof(unsigned), st));
+        k_split<<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(open, level, keys, cap, C, leaf_start.as<uint32_t>(),
+                                                               next);
         TSG_LAUNCHED();
         std::swap(open, next);
     }

@@ -2275,6 +2275,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.quad_lo = ix.quad_lo;
     iv.quad_hi = ix.quad_hi;
     iv.seed_cap = static_cast<uint32_t>(std::min<uint64_t>(2 * ix.leaf_cap, 1u << 20));
+    if (const char* e = std::getenv("TSG_SEED_CAP")) iv.seed_cap = static_cast<uint32_t>(std::atoll(e));  // A/B runs
     iv.split = ix.refine_split;
     iv.pos_offset = ix.pos_offset;
     iv.window = window;

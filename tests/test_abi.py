@@ -102,3 +102,32 @@ def test_dataset_file_roundtrip_and_errors(tmp_path):
         tg.load_dataset(tmp_path / "missing.f32", 8)
     with pytest.raises(tg.InvalidArgument, match="length must be positive"):
         tg.load_dataset(path, 0)
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The Python binding's struct layouts equal the C compiler's (sizes and field offsets)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    structs = {"tsg_config": _lib.tsg_config, "tsg_build_stats": _lib.tsg_build_stats,
+               "tsg_search_stats": _lib.tsg_search_stats, "tsg_result": _lib.tsg_result}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tsgpu.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([gcc, "-std=c99", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
