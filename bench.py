@@ -296,6 +296,12 @@ def run_ours(args):
 
     # ---- build (device-timed inside the library with CUDA events) ----
     cfg = tg.IndexConfig(n=n)
+    # untimed warm-up build of a 1M-series prefix: loads every build kernel's module
+    # (lazy loading) before the timed build
+    warm = tg.build_index(rows[: min(shard, 1_000_000)], cfg, devices=(local,))
+    warm.free()
+    del warm
+    torch.cuda.synchronize()
     barrier()
     tb = time.perf_counter()
     index = tg.build_index(rows, cfg, devices=(local,), position_offset=b)

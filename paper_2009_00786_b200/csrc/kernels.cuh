@@ -142,7 +142,7 @@ struct DevResult {
 // stride fine_stride) of the same series.
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
                uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream,
-               uint8_t* fine = nullptr);
+               uint8_t* fine = nullptr, int key_bits = 64);
 
 // Streams the shard's rows into ix.rows chunk by chunk: for each chunk it
 // enqueues the rows' arrival on ix.stream and then calls sum_chunk(first,

@@ -707,6 +707,10 @@ __global__ void __launch_bounds__(kThreads)
 // warp and written with one 64-bit atomic per flush (both waves' counts).
 constexpr int kRunsPerPage = kPage / kRun + 1;  // an unaligned page touches at most 9 runs
 constexpr int kRunStage = 128;
+#ifndef TSG_BOUND_PL
+#define TSG_BOUND_PL 2
+#endif
+constexpr int kBoundPL = TSG_BOUND_PL;  // pages per lane per bound chunk
 
 __device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, const float* s_l, int cnt, int lane,
                                            float cut, uint64_t rcap, uint2* __restrict__ surv,
@@ -754,7 +758,7 @@ template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     k_bound(IndexView ix, SlotView S, int nq, int pass) {
     constexpr int H = WS / 16;
-    constexpr uint32_t kWChunk = 64;  // pages per warp chunk (two per lane)
+    constexpr uint32_t kWChunk = 32 * kBoundPL;  // pages per warp chunk (kBoundPL per lane)
     const int k_next = pass == 0 ? kNextBound : kNextBound1;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
@@ -805,14 +809,14 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
             uint32_t pre = 0;
             if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);  // read after this chunk
             // pages: two per lane
-            bool keep[2], defer[2];
-            uint32_t ea[2], eb[2];
-            float plb[2];
+            bool keep[kBoundPL], defer[kBoundPL];
+            uint32_t ea[kBoundPL], eb[kBoundPL];
+            float plb[kBoundPL];
             if (pass == 0) {
-                uint4 bl[2][H], bh[2][H];
-                bool valid[2];
+                uint4 bl[kBoundPL][H], bh[kBoundPL][H];
+                bool valid[kBoundPL];
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
+                for (int k = 0; k < kBoundPL; ++k) {
                     const uint64_t i = static_cast<uint64_t>(chunk) * kWChunk + 32 * k + lane;
                     const uint64_t p = i < items ? static_cast<uint64_t>(gsurv[i / kGroup]) * kGroup + i % kGroup : ix.P;
                     valid[k] = p < ix.P;
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     eb[k] = valid[k] ? ix.page_off[p + 1] : 0u;
                 }
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
+                for (int k = 0; k < kBoundPL; ++k) {
                     keep[k] = defer[k] = false;
                     plb[k] = 0.f;
                     if (!valid[k]) continue;
@@ -839,7 +843,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                 }
                 // pages beyond split x bound wait for pass 1 (one atomic per warp and chunk)
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
+                for (int k = 0; k < kBoundPL; ++k) {
                     const unsigned m = __ballot_sync(0xFFFFFFFFu, defer[k]);
                     uint32_t base = 0;
                     if (lane == 0 && m) base = atomicAdd(&wk->ndefer, static_cast<unsigned>(__popc(m)));
@@ -853,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
             } else {
                 // the deferred pages, re-tested against the tightened BSF
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
+                for (int k = 0; k < kBoundPL; ++k) {
                     const uint64_t i = static_cast<uint64_t>(chunk) * kWChunk + 32 * k + lane;
                     const bool in = i < items;
                     const uint2 r = in ? dpage[i] : make_uint2(0, 0);
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
             // the warp's surviving pages, then their runs (kRunsPerPage items per page)
             uint32_t np = 0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
+            for (int k = 0; k < kBoundPL; ++k) {
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, keep[k]);
                 if (keep[k]) s_pg[warp][np + __popc(m & below)] = make_uint2(ea[k], eb[k]);
                 np += __popc(m);

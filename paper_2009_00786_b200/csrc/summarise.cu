@@ -52,6 +52,7 @@ struct SumArgs {
     uint64_t* sort_keys;  // may be null
     uint8_t* fine;        // may be null: fine summary rows (fws bytes each)
     int fw, fws;
+    uint64_t key_mask;    // sort keys keep these bits (the sorted key width)
 };
 
 // Sort key: the first 64 bits of the plane-major bit string of the word
@@ -80,7 +81,7 @@ __device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const 
         uint64_t sk;
         word_keys(wrow, a.w, root, sk);
         if (a.root_keys) a.root_keys[idx] = root;
-        if (a.sort_keys) a.sort_keys[idx] = sk;
+        if (a.sort_keys) a.sort_keys[idx] = sk & a.key_mask;
     }
 }
 
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kSumThreads, 2)
                 if (ok && (g & 3) == 0)
                     reinterpret_cast<uint32_t*>(a.words + idx * 16)[g >> 2] = sym | (b1 << 8) | (b2 << 16) | (b3 << 24);
                 if (ok && g == 0) {
-                    if (a.sort_keys) a.sort_keys[idx] = key;
+                    if (a.sort_keys) a.sort_keys[idx] = key & a.key_mask;
                     if (a.root_keys) a.root_keys[idx] = static_cast<uint32_t>(key >> 48);
                 }
                 if (FINE) {  // 32 fine bytes per series: lanes g = 0, 8 store 16 each
@@ -321,7 +322,8 @@ size_t tma_smem_bytes(int R, int n, int ws) {
 }  // namespace
 
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
-               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream, uint8_t* fine) {
+               uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream, uint8_t* fine,
+               int key_bits) {
     if (count == 0) return;
     SumArgs a{};
     a.n = n;
@@ -335,6 +337,7 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
     a.fw = fine_width(n, w);
     a.fws = fine_stride(a.fw);
     a.fine = a.fw ? fine : nullptr;
+    a.key_mask = key_bits >= 64 ? ~0ull : key_bits <= 0 ? 0ull : ~0ull << (64 - key_bits);
 
     int dev = 0, sms = 0;
     TSG_CUDA(cudaGetDevice(&dev));

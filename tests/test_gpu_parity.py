@@ -213,9 +213,9 @@ def test_index_layout_invariants(oracle):
     assert set(off.tolist()) <= set(poff.tolist())  # pages never straddle leaves
     assert np.all(np.diff(poff.astype(np.int64)) <= 128)
     roots = np.array([oracle.root_key(w) for w in words[:, :16]])
-    # plane-major order of the first 64 key bits (root key first)
+    # plane-major order of the first 48 key bits (root key first; the sorted key width, build.cu kSortBits)
     planes = np.unpackbits(words[:, :16], axis=1).reshape(-1, 16, 8).transpose(0, 2, 1).reshape(-1, 128)[:, :64]
-    keys = np.packbits(planes, axis=1).view(">u8").ravel()
+    keys = np.packbits(planes, axis=1).view(">u8").ravel() & np.uint64(0xFFFFFFFFFFFF0000)
     assert np.all(keys[1:] >= keys[:-1])
     for l in range(L):
         a, b = off[l], off[l + 1]
