@@ -1442,13 +1442,16 @@ constexpr uint32_t kTmaChunk = TSG_TMA_CHUNK;  // candidate records per warp chu
 constexpr bool tma_half_rows(int n) { return TSG_HALF_ROWS && (n / 8) % 16 == 0; }
 // Floats of row buffers per 8-lane group: two whole rows, or three half rows.
 constexpr int tma_group_floats(int n) { return tma_half_rows(n) ? 3 * n / 2 : 2 * n; }
+#ifndef TSG_FINE_CHUNK
+#define TSG_FINE_CHUNK 128
+#endif
 // FW > 0: the fine summary's bound (fine width FW, the query's [FW][256] table
 // after the query in shared memory) filters the records in phase 1 as well;
 // chunks are then 128 records and the kernel runs at two blocks per SM.
 template <int NB, int FW>
 __global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
-    constexpr uint32_t kChunk = FW > 0 ? 128u : kTmaChunk;
+    constexpr uint32_t kChunk = FW > 0 ? static_cast<uint32_t>(TSG_FINE_CHUNK) : kTmaChunk;
     constexpr int kGroups = kThreads / kRowLanes;
     constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
