@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kThreads)
         wk->fine_calcs = 0;
         wk->nties = 0;
         for (int k = 0; k < 6; ++k) wk->stats[k] = 0;
-        wk->stats[kRealDist] = ix.window < 0 ? b - a : 0;  // DTW seeds count the DTWs that ran
+        wk->stats[kRealDist] = 0;  // the seed kernels count the rows they refine
     }
 }
 
@@ -626,16 +626,18 @@ __global__ void __launch_bounds__(kThreads)
     const int lane = threadIdx.x & 31;
     const uint64_t group = static_cast<uint64_t>(blockIdx.x) * kGroups + threadIdx.x / kRowLanes;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * kGroups;
-    unsigned long long updates = 0;
+    unsigned long long updates = 0, refined = 0;
     for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
         const uint32_t p = ix.pos[e];
         const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if ((lane & (kRowLanes - 1)) == 0) {
             cand_pos[e - a] = p;  // candidate records hold dataset rows
             updates += publish(wk, s, e - a, cand_sq, ~0u);
+            refined += 1;
         }
     }
     if (updates) atomicAdd(&wk->stats[kBsfUpd], updates);
+    if (refined) atomicAdd(&wk->stats[kRealDist], refined);
 }
 
 // ------------------------------------------------------------ groups
