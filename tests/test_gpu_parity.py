@@ -458,3 +458,18 @@ def test_fine_summary_prunes_refinement_without_changing_answers(oracle, monkeyp
         assert b.fine_calcs == 0
     assert sum(r.fine_calcs for r in with_fine) > 0
     assert sum(r.stats.real_dist_calcs for r in with_fine) < sum(r.stats.real_dist_calcs for r in without)
+
+
+def test_fine_summary_saturating_values_stay_exact(oracle):
+    """Rows far outside the fine quantiser's [-2.5, 2.5) range (scaled, shifted, constant) keep exact answers."""
+    rng = np.random.default_rng(77)
+    base = oracle.generate(6000, 256, 91)
+    rows = np.concatenate([base[:2000] * np.float32(1000.0),          # saturating both ends
+                           base[2000:4000] + np.float32(40.0),        # all in the top open region
+                           np.repeat(rng.standard_normal((40, 1)).astype(np.float32), 256, axis=1),  # constant rows
+                           base[4040:]]).astype(np.float32)
+    queries = np.concatenate([rows[[5, 2500, 4010, 5000]] + np.float32(0.01),
+                              oracle.generate(4, 256, 92) * np.float32(1000.0),
+                              oracle.generate(4, 256, 93)]).astype(np.float32)
+    _, res = check_against_scan(oracle, rows, queries, tg.IndexConfig(n=256, w=16, leaf_capacity=100))
+    assert sum(r.fine_calcs for r in res) > 0
