@@ -186,7 +186,8 @@ void free_shard(DevIndex& s) {
     // page arrays come from the stream-ordered pool (build.cu)
     for (void* p : {static_cast<void*>(s.page_off), static_cast<void*>(s.page_leaf), static_cast<void*>(s.page_key),
                     static_cast<void*>(s.page_lo), static_cast<void*>(s.page_hi), static_cast<void*>(s.page_dir),
-                    static_cast<void*>(s.group_lo), static_cast<void*>(s.group_hi)})
+                    static_cast<void*>(s.group_lo), static_cast<void*>(s.group_hi), static_cast<void*>(s.top_lo),
+                    static_cast<void*>(s.top_hi)})
         if (p) cudaFreeAsync(p, s.stream);
     if (s.stream) cudaStreamSynchronize(s.stream);
     free_slots(s.batch);

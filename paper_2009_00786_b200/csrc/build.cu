@@ -420,6 +420,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     ix.NG = (ix.P + kGroup - 1) / kGroup;
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.group_lo), ix.NG * ix.ws, st));
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.group_hi), ix.NG * ix.ws, st));
+    ix.NT = (ix.NG + kGroup - 1) / kGroup;
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.top_lo), ix.NT * ix.ws, st));
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ix.top_hi), ix.NT * ix.ws, st));
     trace("page-alloc");
     k_page_write<<<grid_for(ix.L, 256, sms), 256, 0, st>>>(ix.leaf_off, ix.L, pbase, ix.page_off, ix.page_leaf);
     TSG_LAUNCHED();
@@ -432,6 +435,9 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_LAUNCHED();
     k_group_box<<<grid_for(ix.NG * (ix.ws / 16), 256, sms), 256, 0, st>>>(ix.page_lo, ix.page_hi, ix.P, ix.NG, ix.ws,
                                                                          ix.group_lo, ix.group_hi);
+    TSG_LAUNCHED();
+    k_group_box<<<grid_for(ix.NT * (ix.ws / 16), 256, sms), 256, 0, st>>>(ix.group_lo, ix.group_hi, ix.NG, ix.NT, ix.ws,
+                                                                         ix.top_lo, ix.top_hi);
     TSG_LAUNCHED();
     trace("pages");
     TSG_CUDA(cudaEventRecord(ev[3], st));

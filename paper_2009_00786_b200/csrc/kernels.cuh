@@ -44,6 +44,9 @@ struct DevIndex {
     uint8_t* group_lo = nullptr;    // [NG][ws] per-segment min symbol of pages [kGroup g, kGroup g + kGroup)
     uint8_t* group_hi = nullptr;    // [NG][ws] per-segment max symbol
     uint64_t NG = 0;                // ceil(P / kGroup)
+    uint8_t* top_lo = nullptr;      // [NT][ws] per-segment min symbol of groups [kGroup t, kGroup t + kGroup)
+    uint8_t* top_hi = nullptr;      // [NT][ws] per-segment max symbol
+    uint64_t NT = 0;                // ceil(NG / kGroup): the level above groups
     uint8_t* run_lo = nullptr;      // [R][ws] per-segment min symbol of entries [kRun r, kRun r + kRun)
     uint8_t* run_hi = nullptr;      // [R][ws] per-segment max symbol
     uint64_t R = 0;                 // ceil(N / kRun)

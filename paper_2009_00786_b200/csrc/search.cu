@@ -82,8 +82,8 @@ struct IndexView {
     const uint64_t* page_key;
     const uint64_t* page_dir;
     uint64_t P;
-    const uint8_t *page_lo, *page_hi, *group_lo, *group_hi;
-    uint64_t NG;
+    const uint8_t *page_lo, *page_hi, *group_lo, *group_hi, *top_lo, *top_hi;
+    uint64_t NG, NT;
     const uint8_t *run_lo, *run_hi, *quad_lo, *quad_hi;
     uint32_t seed_cap;
     float split;
@@ -641,11 +641,13 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ------------------------------------------------------------ groups
-// Level 1 of the box filter, the flat analog of the tree's internal nodes:
-// one box per group of kGroup consecutive pages. Grid (x, query); each
-// thread bounds kGP groups per round; surviving groups are listed per query
+// Levels 1 and 0 of the box filter, the flat analog of the tree's internal
+// nodes: one box per group of kGroup consecutive pages, and one per "top" of
+// kGroup consecutive groups. Grid (x, query); per round a block bounds kGP
+// tops per thread, lists the surviving tops in shared memory, then bounds
+// their groups (one per thread); surviving groups are listed per query
 // (block-aggregated) for the page level.
-constexpr int kGP = 4;  // groups / pages per thread per round
+constexpr int kGP = 4;  // tops per thread per round
 
 template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads)
@@ -653,6 +655,8 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
+    __shared__ uint32_t s_top[kThreads * kGP];
+    __shared__ unsigned s_ntop;
     const int q = blockIdx.y;
     QueryWork* wk = S.work + q;
     if (wk->overflow) return;
@@ -661,40 +665,62 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
     const float bound = bound_from_bits(wk->bsf_bits);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        wk->scan_bound = bound;
-        atomicAdd(&wk->stats[kLbNode], static_cast<unsigned long long>(ix.NG));
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) wk->scan_bound = bound;
     uint32_t* gsurv = S.gsurv + q * S.NG;
-    unsigned long long pruned = 0;
+    unsigned long long pruned = 0, nodes = 0;
     constexpr uint64_t kRound = static_cast<uint64_t>(kThreads) * kGP;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < ix.NG;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRound; base < ix.NT;
          base += static_cast<uint64_t>(gridDim.x) * kRound) {
+        if (threadIdx.x == 0) s_ntop = 0;
+        __syncthreads();
+        // tops: kGP per thread, loads first
         uint4 bl[kGP][H], bh[kGP][H];
 #pragma unroll
         for (int k = 0; k < kGP; ++k) {
-            const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            const uint64_t t = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                bl[k][h] = g < ix.NG ? ld_stream_u4(ix.group_lo + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                bh[k][h] = g < ix.NG ? ld_stream_u4(ix.group_hi + g * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bl[k][h] = t < ix.NT ? ld_stream_u4(ix.top_lo + t * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                bh[k][h] = t < ix.NT ? ld_stream_u4(ix.top_hi + t * WS + 16 * h) : make_uint4(0, 0, 0, 0);
             }
         }
-        unsigned keep = 0;
 #pragma unroll
         for (int k = 0; k < kGP; ++k) {
-            const uint64_t g = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
-            if (g >= ix.NG) continue;
-            if (box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w) <= bound) keep |= 1u << k;
+            const uint64_t t = base + threadIdx.x + static_cast<uint64_t>(kThreads) * k;
+            if (t >= ix.NT) continue;
+            nodes += 1;
+            if (box_bound<H, W16>(s_lut, q4, bl[k], bh[k], ix.w) <= bound) s_top[atomicAdd(&s_ntop, 1u)] = static_cast<uint32_t>(t);
             else pruned += 1;
         }
-        uint32_t at = block_reserve(__popc(keep), 0, &wk->ngroups, nullptr).x;
+        __syncthreads();
+        // groups of the surviving tops: one per thread
+        const unsigned items = s_ntop * kGroup;
+        for (unsigned i0 = 0; i0 < items; i0 += kThreads) {
+            const unsigned i = i0 + threadIdx.x;
+            uint64_t g = ix.NG;
+            if (i < items) g = static_cast<uint64_t>(s_top[i / kGroup]) * kGroup + i % kGroup;
+            bool keep = false;
+            if (g < ix.NG) {
+                uint4 gl[H], gh[H];
 #pragma unroll
-        for (int k = 0; k < kGP; ++k)
-            if (keep & (1u << k)) gsurv[at++] = static_cast<uint32_t>(base + threadIdx.x + static_cast<uint64_t>(kThreads) * k);
+                for (int h = 0; h < H; ++h) {
+                    gl[h] = ld_stream_u4(ix.group_lo + g * WS + 16 * h);
+                    gh[h] = ld_stream_u4(ix.group_hi + g * WS + 16 * h);
+                }
+                nodes += 1;
+                keep = box_bound<H, W16>(s_lut, q4, gl, gh, ix.w) <= bound;
+                pruned += keep ? 0 : 1;
+            }
+            const uint32_t at = block_reserve(keep ? 1u : 0u, 0, &wk->ngroups, nullptr).x;
+            if (keep) gsurv[at] = static_cast<uint32_t>(g);
+        }
     }
     pruned = warp_sum(pruned);
-    if ((threadIdx.x & 31) == 0 && pruned) atomicAdd(&wk->stats[kPruned], pruned);
+    nodes = warp_sum(nodes);
+    if ((threadIdx.x & 31) == 0) {
+        if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
+        if (nodes) atomicAdd(&wk->stats[kLbNode], nodes);
+    }
 }
 
 // ------------------------------------------------------------- bound
@@ -1451,7 +1477,10 @@ constexpr int tma_group_floats(int n) { return tma_half_rows(n) ? 3 * n / 2 : 2 
 // after the query in shared memory) filters the records in phase 1 as well;
 // chunks are then 128 records and the kernel runs at two blocks per SM.
 template <int NB, int FW>
-__global__ void __launch_bounds__(kThreads, FW > 0 ? 2 : TSG_MINB_TMA)
+#ifndef TSG_MINB_TMA_FINE
+#define TSG_MINB_TMA_FINE 2
+#endif
+__global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MINB_TMA)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     constexpr uint32_t kChunk = FW > 0 ? static_cast<uint32_t>(TSG_FINE_CHUNK) : kTmaChunk;
     constexpr int kGroups = kThreads / kRowLanes;
@@ -2279,6 +2308,9 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     iv.group_lo = ix.group_lo;
     iv.group_hi = ix.group_hi;
     iv.NG = ix.NG;
+    iv.top_lo = ix.top_lo;
+    iv.top_hi = ix.top_hi;
+    iv.NT = ix.NT;
     iv.run_lo = ix.run_lo;
     iv.run_hi = ix.run_hi;
     iv.quad_lo = ix.quad_lo;
@@ -2307,7 +2339,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const int sms = ix.sms;
     const unsigned seed_x = (iv.seed_cap + kThreads / kRowLanes - 1) / (kThreads / kRowLanes);
     const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
-        1, std::min<uint64_t>((ix.NG + kThreads * kGP - 1) / (kThreads * kGP),
+        1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
                               static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
     const unsigned bound_grid = static_cast<unsigned>(sms * blocks_per_sm(bound, lut_bytes));
     const unsigned scan_grid = static_cast<unsigned>(sms * blocks_per_sm(lbscan, lut_bytes));
