@@ -314,11 +314,10 @@ def run_ours(args):
     measure = tg.Measure.dtw(args.dtw) if args.dtw >= 0 else tg.Measure.ed()
 
     def step(batch, host):
-        if host:
-            res = tg.exact_search_batch(index, qhost[batch * nq:(batch + 1) * nq], measure)
-        else:
-            res = tg.exact_search_batch(index, qdev[batch * nq:(batch + 1) * nq], measure)
-        rec = np.array([(r.distance, r.position) for r in res], dtype=np.float64)
+        # one C-ABI call per batch; results as a record array (no per-query Python objects)
+        src = qhost if host else qdev
+        res = tg.exact_search_batch_records(index, src[batch * nq:(batch + 1) * nq], measure)
+        rec = np.stack([res["distance"], res["position"].astype(np.float64)], axis=1)
         if world > 1:  # the cross-GPU exchange: all-gather of (distance, position) over NCCL
             rec = allgather_merge(rec, device=f"cuda:{local}")
         return rec, res
@@ -341,10 +340,8 @@ def run_ours(args):
             if answers is not None:
                 answers.append(rec)
             if stats is not None:
-                for r in res:
-                    s = r.stats
-                    stats += (s.lb_node_calcs, s.lb_entry_calcs, s.real_dist_calcs, s.bsf_updates,
-                              s.pruned_subtrees, s.queue_insertions, r.box_calcs, r.fine_calcs)
+                st = res["stats"].astype(np.float64).sum(axis=0)
+                stats += (*st, float(res["box_calcs"].astype(np.float64).sum()), float(res["fine_calcs"].astype(np.float64).sum()))
         return max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
 
     # warm-up

@@ -384,6 +384,48 @@ def exact_search_batch(index: Index, queries, measure: Measure = Measure.ed()) -
     return [_result_from_c(r) for r in out]
 
 
+# numpy view of tsg_result (include/tsgpu.h): one record per query
+RESULT_DTYPE = np.dtype({"names": ["distance", "position", "box_calcs", "stats", "fine_calcs"],
+                         "formats": [np.float64, np.uint32, np.uint32, (np.uint64, 6), np.uint64],
+                         "offsets": [_lib.tsg_result.distance.offset, _lib.tsg_result.position.offset,
+                                     _lib.tsg_result.box_calcs.offset, _lib.tsg_result.stats.offset,
+                                     _lib.tsg_result.fine_calcs.offset],
+                         "itemsize": C.sizeof(_lib.tsg_result)})
+
+
+def _res_ptr(arr: np.ndarray):
+    return C.cast(arr.ctypes.data, C.POINTER(_lib.tsg_result))
+
+
+def exact_search_batch_records(index: Index, queries, measure: Measure = Measure.ed()) -> np.ndarray:
+    """exact_search_batch without per-query Python objects: a structured array (RESULT_DTYPE) over
+    the C ABI's result records (distance, position, box_calcs, stats[6] in SearchStats order,
+    fine_calcs). For batch pipelines where building SearchResult objects would cost host time."""
+    _check_measure(measure, index.config().n)
+    n = index.config().n
+    m = _measure_c(measure)
+    if _is_cuda_tensor(queries):
+        t = queries.contiguous()
+        if t.dim() != 2 or t.shape[1] != n:
+            raise InvalidArgument(f"query length {tuple(t.shape)} does not match the index series length {n}")
+        out = np.empty(t.shape[0], RESULT_DTYPE)
+        if measure.kind == MeasureKind.euclidean:
+            check(lib().tsg_search_device(index.handle, C.c_void_p(t.data_ptr()), t.shape[0], _res_ptr(out)))
+        else:
+            check(lib().tsg_search_measure(index.handle, C.c_void_p(t.data_ptr()), 1, t.shape[0], C.byref(m), 0,
+                                           _res_ptr(out)))
+        return out
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.float32))
+    if q.ndim != 2 or q.shape[1] != n:
+        raise InvalidArgument(f"query length {q.shape} does not match the index series length {n}")
+    out = np.empty(q.shape[0], RESULT_DTYPE)
+    if measure.kind == MeasureKind.euclidean:
+        check(lib().tsg_search(index.handle, q.ctypes.data, q.shape[0], _res_ptr(out)))
+    else:
+        check(lib().tsg_search_measure(index.handle, q.ctypes.data, 0, q.shape[0], C.byref(m), 0, _res_ptr(out)))
+    return out
+
+
 def approximate_search(index: Index, query, measure: Measure = Measure.ed()) -> SearchResult:
     """tsidx::approximate_search: the best series in the query's closest leaf."""
     _check_measure(measure, index.config().n)

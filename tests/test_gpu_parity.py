@@ -473,3 +473,19 @@ def test_fine_summary_saturating_values_stay_exact(oracle):
                               oracle.generate(4, 256, 93)]).astype(np.float32)
     _, res = check_against_scan(oracle, rows, queries, tg.IndexConfig(n=256, w=16, leaf_capacity=100))
     assert sum(r.fine_calcs for r in res) > 0
+
+
+def test_batch_records_equal_batch_results(oracle):
+    """exact_search_batch_records (record array over the C ABI results) == exact_search_batch."""
+    import torch
+
+    rows = oracle.generate(5000, 128, 61)
+    queries = oracle.generate(20, 128, 62)
+    index = tg.build_index(rows, tg.IndexConfig(n=128, leaf_capacity=100))
+    want = tg.exact_search_batch(index, queries)
+    for q in (queries, torch.from_numpy(queries).cuda()):
+        got = tg.exact_search_batch_records(index, q)
+        assert got.dtype == tg.RESULT_DTYPE and len(got) == len(want)
+        for g, w in zip(got, want):
+            assert (float(g["distance"]), int(g["position"])) == (w.distance, w.position)
+            assert int(g["stats"][2]) == w.stats.real_dist_calcs and int(g["fine_calcs"]) == w.fine_calcs
