@@ -131,3 +131,18 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
         assert int(got[name]) == C.sizeof(cls), name
         for f, _ in cls._fields_:
             assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
+
+
+def test_result_record_dtype_matches_the_c_struct():
+    """The record-array view of batch results (exact_search_batch_records) has tsg_result's layout."""
+    from paper_2009_00786_b200.tsidx import RESULT_DTYPE
+
+    assert RESULT_DTYPE.itemsize == C.sizeof(_lib.tsg_result)
+    for name in ("distance", "position", "box_calcs", "stats", "fine_calcs"):
+        assert RESULT_DTYPE.fields[name][1] == getattr(_lib.tsg_result, name).offset, name
+    rec = np.zeros(2, RESULT_DTYPE)
+    raw = (_lib.tsg_result * 2)()
+    raw[1].distance, raw[1].position, raw[1].fine_calcs = 2.5, 7, 9
+    raw[1].stats.real_dist_calcs = 3
+    C.memmove(rec.ctypes.data, raw, C.sizeof(raw))
+    assert (rec[1]["distance"], rec[1]["position"], rec[1]["fine_calcs"], rec[1]["stats"][2]) == (2.5, 7, 9, 3)
