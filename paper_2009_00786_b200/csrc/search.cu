@@ -89,6 +89,7 @@ struct IndexView {
     float split;
     uint64_t pos_offset;
     int window;  // < 0: Euclidean; >= 0: DTW with this Sakoe-Chiba window
+    int rev_keogh;  // DTW refinement also tests the reversed LB_Keogh (per-warp scratch in shared memory)
     const uint8_t* fine;       // [N][fws] fine summary (dataset order); null: none
     int fw, fws;
 };
@@ -1992,6 +1993,44 @@ __device__ __forceinline__ double warp_lb_keogh_sq(const float* __restrict__ up,
     return sum;
 }
 
+#ifndef TSG_REV_KEOGH
+#define TSG_REV_KEOGH 1
+#endif
+constexpr bool kRevKeogh = TSG_REV_KEOGH;
+// The reversed LB_Keogh (the UCR suite's second envelope bound): the query
+// against the candidate's Keogh envelope (window max / min over |j - i| <= r,
+// exact in float), every term from shared memory. DTW is symmetric, so this is
+// a lower bound of the same DTW as the forward LB_Keogh (metrics.cpp:179-192
+// with the roles swapped). w_row: the candidate row already in the warp's
+// scratch; w_up / w_lo: scratch for its envelope.
+__device__ __forceinline__ double warp_lb_keogh_rev_sq(const float* w_row, float* w_up, float* w_lo,
+                                                       const float* s_q, int n, int r) {
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < n; i += 32) {
+        const int a = max(0, i - r), b = min(n - 1, i + r);
+        float hi = w_row[a], lo = w_row[a];
+        for (int j = a + 1; j <= b; ++j) {
+            hi = fmaxf(hi, w_row[j]);
+            lo = fminf(lo, w_row[j]);
+        }
+        w_up[i] = hi;
+        w_lo[i] = lo;
+    }
+    __syncwarp();
+    double sum = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double v = s_q[i];
+        double d = 0.0;
+        if (v > w_up[i]) d = v - w_up[i];
+        else if (v < w_lo[i]) d = w_lo[i] - v;
+        sum += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    __syncwarp();  // the scratch is free again
+    return sum;
+}
+
 // One candidate row under DTW by a warp: LB_Keogh against the live BSF, then
 // the banded DTW abandoning at it (calculate_real_distance_leaf's DTW branch,
 // src/query.cpp:138-145). Returns the squared distance or +inf; `refined`
@@ -2114,7 +2153,15 @@ __global__ void __launch_bounds__(kThreads)
                     const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
                     const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
                     const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
-                    if (warp_lb_keogh_sq(s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(pp) * n, n) > cut) {
+                    bool drop = warp_lb_keogh_sq(s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(pp) * n, n) > cut;
+                    if (!drop && ix.rev_keogh) {  // then the query against the candidate's envelope
+                        float* w_row = s_qe + 3 * n + (threadIdx.x >> 5) * 3 * n;
+                        const float* row = ix.rows + static_cast<uint64_t>(pp) * n;
+                        for (int i = lane; i < n; i += 32) w_row[i] = __ldg(row + i);
+                        __syncwarp();
+                        drop = warp_lb_keogh_rev_sq(w_row, w_row + n, w_row + 2 * n, s_qe, n, ix.window) > cut;
+                    }
+                    if (drop) {
                         if (lane == 0) cand_sq[cc] = INFINITY;
                     } else {
                         live |= 1u << src;
@@ -2374,7 +2421,10 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         TSG_CUDA(cudaFuncSetAttribute(refine_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     }
     const unsigned seed_dtw_x = (iv.seed_cap + kWarps - 1) / kWarps;
-    const unsigned refine_dtw_grid = dtw ? static_cast<unsigned>(sms * blocks_per_sm(refine_dtw, qe_bytes)) : 0u;
+    // refine_dtw: query + envelope, then per-warp scratch for a candidate row and its envelope
+    iv.rev_keogh = kRevKeogh && static_cast<size_t>(kWarps + 1) * qe_bytes <= 96 * 1024 ? 1 : 0;
+    const size_t rdtw_bytes = qe_bytes + (iv.rev_keogh ? static_cast<size_t>(kWarps) * qe_bytes : 0);
+    const unsigned refine_dtw_grid = dtw ? static_cast<unsigned>(sms * blocks_per_sm(refine_dtw, rdtw_bytes)) : 0u;
 
     // Optional per-kernel timing: events around every launch, summed after the batch.
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
@@ -2420,7 +2470,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                 if (tma_fine)
                     refine_tma_fine<<<tma_fine_grid, kThreads, tma_fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, qe_bytes, st>>>(iv, sv, d_queries, inq, wave);
+                else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, rdtw_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
                 TSG_LAUNCHED();
