@@ -2031,6 +2031,25 @@ __device__ __forceinline__ double warp_lb_keogh_rev_sq(const float* w_row, float
     return sum;
 }
 
+// LB_Keogh of one candidate row by an 8-lane group (lane j: elements j, j + 8,
+// ...: each step reads 32 contiguous bytes); every lane of the group returns it.
+__device__ __forceinline__ double group_lb_keogh_sq(const float* __restrict__ up, const float* __restrict__ lo,
+                                                    const float* __restrict__ c, int n) {
+    const int lane = threadIdx.x & 31, j = lane & (kRowLanes - 1), base = lane & ~(kRowLanes - 1);
+    const unsigned gmask = 0xFFu << base;
+    double sum = 0.0;
+    for (int i = j; i < n; i += kRowLanes) {
+        const double v = __ldg(c + i);
+        double d = 0.0;
+        if (v > up[i]) d = v - up[i];
+        else if (v < lo[i]) d = lo[i] - v;
+        sum += d * d;
+    }
+#pragma unroll
+    for (int o = kRowLanes / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(gmask, sum, o);
+    return sum;
+}
+
 // One candidate row under DTW by a warp: LB_Keogh against the live BSF, then
 // the banded DTW abandoning at it (calculate_real_distance_leaf's DTW branch,
 // src/query.cpp:138-145). Returns the squared distance or +inf; `refined`
@@ -2145,16 +2164,36 @@ __global__ void __launch_bounds__(kThreads)
             const uint32_t p = keep ? cand_pos[c] : 0u;
             unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
             if constexpr (M == 1) {
-                // LB_Keogh first; the survivors two at a time through the paired DTW
+                // LB_Keogh first, four candidates at a time (one per 8-lane group); the
+                // reversed LB_Keogh; the survivors two at a time through the paired DTW
+                unsigned fwd = 0;
+                {
+                    const int wgi = lane / kRowLanes;
+                    const bool gl = (lane & (kRowLanes - 1)) == 0;
+                    while (m) {
+                        unsigned t = m;
+                        for (int k = 0; k < wgi && t; ++k) t &= t - 1;
+                        const int srcg = t ? __ffs(t) - 1 : -1;
+                        for (int k = 0; k < 32 / kRowLanes && m; ++k) m &= m - 1;
+                        const uint32_t pg = __shfl_sync(0xFFFFFFFFu, p, srcg >= 0 ? srcg : 0);
+                        const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
+                        const double lbf = group_lb_keogh_sq(s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(pg) * n, n);
+                        const unsigned bit = gl && srcg >= 0 && lbf <= cut ? 1u << srcg : 0u;
+                        const unsigned drop_bit = gl && srcg >= 0 && !(lbf <= cut) ? 1u << srcg : 0u;
+                        fwd |= __reduce_or_sync(0xFFFFFFFFu, bit);
+                        const unsigned dropped = __reduce_or_sync(0xFFFFFFFFu, drop_bit);
+                        if (dropped >> lane & 1u) cand_sq[c] = INFINITY;
+                    }
+                }
                 unsigned live = 0;
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
+                while (fwd) {
+                    const int src = __ffs(fwd) - 1;
+                    fwd &= fwd - 1;
                     const uint32_t pp = __shfl_sync(0xFFFFFFFFu, p, src);
                     const uint64_t cc = __shfl_sync(0xFFFFFFFFu, c, src);
                     const double cut = bsf_of(ld_volatile_u64(&wk->bsf_bits)) * kSlack;
-                    bool drop = warp_lb_keogh_sq(s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(pp) * n, n) > cut;
-                    if (!drop && ix.rev_keogh) {  // then the query against the candidate's envelope
+                    bool drop = false;
+                    if (ix.rev_keogh) {  // the query against the candidate's envelope
                         float* w_row = s_qe + 3 * n + (threadIdx.x >> 5) * 3 * n;
                         const float* row = ix.rows + static_cast<uint64_t>(pp) * n;
                         for (int i = lane; i < n; i += 32) w_row[i] = __ldg(row + i);
