@@ -1484,6 +1484,12 @@ template <int NB, int FW>
 __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MINB_TMA)
     k_refine_tma(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     constexpr uint32_t kChunk = FW > 0 ? static_cast<uint32_t>(TSG_FINE_CHUNK) : kTmaChunk;
+    // Claims are in slices of kSlice records, up to kChunk at a time; near the end
+    // of a query (fewer than kGuideTail slices left) one slice at a time, so the
+    // block's warps reach the query switch together (guided scheduling).
+    constexpr uint32_t kSlice = FW > 0 ? 32u : kChunk;
+    constexpr uint32_t kMaxSl = kChunk / kSlice;
+    constexpr uint32_t kGuideTail = 128;
     constexpr int kGroups = kThreads / kRowLanes;
     constexpr int kWarpGroups = 32 / kRowLanes;
     constexpr int n = NB * 8;
@@ -1527,7 +1533,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
         if (w->overflow) return 0;
         uint64_t b, e;
         range(w, b, e);
-        return static_cast<uint32_t>((e - b + kChunk - 1) / kChunk);
+        return static_cast<uint32_t>((e - b + kSlice - 1) / kSlice);
     };
     auto issue = [&](int b, uint32_t p) {  // leader: row p -> this group's buffer b
         fence_proxy_async_smem();
@@ -1622,29 +1628,37 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
         uint64_t begin, end;
         range(wk, begin, end);
         const uint32_t nch = nchunks(wk);
-        uint32_t chunk = 0;
-        if (lane == 0) chunk = atomicAdd(&wk->next[k_next], 1u);
-        chunk = __shfl_sync(0xFFFFFFFFu, chunk, 0);
+        // lane 0: claim the next slices; returns start | size << 32 (valid in lane 0)
+        auto claim_slices = [&]() -> unsigned long long {
+            const unsigned cur0 = ld_volatile_u32(&wk->next[k_next]);
+            const unsigned want = kMaxSl > 1 && cur0 + kGuideTail < nch ? kMaxSl : 1u;
+            const unsigned st0 = atomicAdd(&wk->next[k_next], want);
+            return static_cast<unsigned long long>(st0) | (static_cast<unsigned long long>(want) << 32);
+        };
+        unsigned long long cl = 0;
+        if (lane == 0) cl = claim_slices();
+        cl = __shfl_sync(0xFFFFFFFFu, cl, 0);
+        uint32_t chunk = static_cast<uint32_t>(cl), csize = static_cast<uint32_t>(cl >> 32);
         // The current chunk's records (bound, entry) are loaded one chunk ahead,
         // while the previous chunk's rows are being refined.
         constexpr int kPer = kChunk / 32;
         float rlb[kPer];
         uint32_t rcp[kPer];
-        auto load_records = [&](uint32_t ch, float* lbv, uint32_t* cpv) {
+        auto load_records = [&](uint32_t ch, uint32_t sz, float* lbv, uint32_t* cpv) {
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
-                const uint64_t c = begin + static_cast<uint64_t>(ch) * kChunk + 32 * k + lane;
-                const bool in = ch < nch && c < end;
+                const uint64_t c = begin + static_cast<uint64_t>(ch) * kSlice + 32 * k + lane;
+                const bool in = ch < nch && 32u * k < sz * kSlice && c < end;
                 lbv[k] = in ? cand_lb[c] : INFINITY;
                 cpv[k] = in ? cand_pos[c] : 0u;
             }
         };
-        load_records(chunk, rlb, rcp);
+        load_records(chunk, csize, rlb, rcp);
         while (chunk < nch) {
-            uint32_t pre = 0;
-            if (lane == 0) pre = atomicAdd(&wk->next[k_next], 1u);
-            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kChunk;
-            const uint64_t c1 = u64min(c0 + kChunk, end);
+            unsigned long long pre = 0;
+            if (lane == 0) pre = claim_slices();
+            const uint64_t c0 = begin + static_cast<uint64_t>(chunk) * kSlice;
+            const uint64_t c1 = u64min(c0 + static_cast<uint64_t>(csize) * kSlice, end);
             // Phase 1 (warp): keep the records whose bound (then fine bound) is within the BSF.
             const float bnd = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
             bool kp[kPer];
@@ -1690,8 +1704,9 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
                 m += __popc(mk);
             }
             __syncwarp();
-            const uint32_t next = __shfl_sync(0xFFFFFFFFu, pre, 0);
-            load_records(next, rlb, rcp);  // in flight during phase 2
+            const unsigned long long ncl = __shfl_sync(0xFFFFFFFFu, pre, 0);
+            const uint32_t next = static_cast<uint32_t>(ncl), nsize = static_cast<uint32_t>(ncl >> 32);
+            load_records(next, nsize, rlb, rcp);  // in flight during phase 2
             if constexpr (kHalf) {
                 // Phase 2 (half rows): first halves one row ahead in buffers 0 / 1,
                 // the pending second half in buffer 2, completed one row later.
@@ -1761,6 +1776,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
                 }
                 __syncwarp();  // the warp's list is reused by the next chunk
                 chunk = next;
+                csize = nsize;
                 continue;
             }
             // Phase 2: the kept rows, double-buffered per group.
@@ -1819,6 +1835,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
             }
             __syncwarp();  // the warp's list is reused by the next chunk
             chunk = next;
+            csize = nsize;
         }
         if (leader) {
             if (refined) atomicAdd(&wk->stats[kRealDist], refined);
