@@ -489,3 +489,36 @@ def test_batch_records_equal_batch_results(oracle):
         for g, w in zip(got, want):
             assert (float(g["distance"]), int(g["position"])) == (w.distance, w.position)
             assert int(g["stats"][2]) == w.stats.real_dist_calcs and int(g["fine_calcs"]) == w.fine_calcs
+
+
+def _torch_bruteforce_nn(rows, q, chunk=1 << 20):
+    """Independent exhaustive 1-NN in torch (FP64 squared distances, chunked): (distance, lowest position)."""
+    import torch
+
+    qd = q.double()
+    best_d, best_p = float("inf"), -1
+    for a in range(0, rows.shape[0], chunk):
+        d = ((rows[a:a + chunk].double() - qd) ** 2).sum(dim=1)
+        v, i = torch.min(d, dim=0)
+        v = float(v)
+        if v < best_d:  # strict: an earlier chunk keeps equal distances (lowest position)
+            best_d, best_p = v, a + int(i)
+    return math.sqrt(best_d), best_p
+
+
+def test_exact_at_scale_matches_bruteforce():
+    """25M-series prefix of config 2 (25.6 GB in HBM): answers equal an independent exhaustive scan."""
+    import torch
+
+    N, n = 25_000_000, 256
+    rows = tg.generate_device("rw", N, n, 1)
+    queries = torch.cat([tg.generate_device("rw", 6, n, 2, begin=N), rows[[123_456, N - 7]] + 0.001])
+    index = tg.build_index(rows, tg.IndexConfig(n=n))
+    res = tg.exact_search_batch(index, queries)
+    for k in range(queries.shape[0]):
+        d, p = _torch_bruteforce_nn(rows, queries[k])
+        assert res[k].position == p, (k, res[k].position, p)
+        assert res[k].distance == pytest.approx(d, rel=1e-12)
+    assert sum(r.stats.real_dist_calcs for r in res) < 0.001 * N * len(res)  # the index pruned >99.9%
+    del index, rows
+    torch.cuda.empty_cache()
