@@ -628,10 +628,31 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t group = static_cast<uint64_t>(blockIdx.x) * kGroups + threadIdx.x / kRowLanes;
     const uint64_t ngroups = static_cast<uint64_t>(gridDim.x) * kGroups;
     unsigned long long updates = 0, refined = 0;
+    // With the fine summary (Euclidean) the seed runs on few blocks per query: rows of the later
+    // rounds first take their fine bound (the query's table read through L1) against the BSF
+    // the earlier rounds found, and most are never read.
+    const bool fine = ix.fine != nullptr && ix.window < 0;
+    const float* flut = fine ? S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len : nullptr;
+    const int j8 = lane & (kRowLanes - 1);
+    const unsigned gmask = 0xFFu << (lane & ~(kRowLanes - 1));
     for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
         const uint32_t p = ix.pos[e];
+        if (fine && e >= a + ngroups) {
+            const uint8_t* f = ix.fine + static_cast<uint64_t>(p) * ix.fws;
+            float acc = 0.f;
+            for (int sg = j8; sg < ix.fw; sg += kRowLanes) acc = __fadd_rd(acc, __ldg(flut + sg * 256 + f[sg]));
+#pragma unroll
+            for (int o = kRowLanes / 2; o > 0; o >>= 1) acc = __fadd_rd(acc, __shfl_xor_sync(gmask, acc, o));
+            if (acc > bound_from_bits(ld_volatile_u64(&wk->bsf_bits))) {
+                if (j8 == 0) {
+                    cand_pos[e - a] = p;
+                    cand_sq[e - a] = INFINITY;
+                }
+                continue;
+            }
+        }
         const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
-        if ((lane & (kRowLanes - 1)) == 0) {
+        if (j8 == 0) {
             cand_pos[e - a] = p;  // candidate records hold dataset rows
             updates += publish(wk, s, e - a, cand_sq, ~0u);
             refined += 1;
@@ -2441,6 +2462,10 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
 
     const int sms = ix.sms;
     const unsigned seed_x = (iv.seed_cap + kThreads / kRowLanes - 1) / (kThreads / kRowLanes);
+    static const unsigned seed_fine_x = [] {  // seed blocks per query with the fine summary (TSG_SEED_BLOCKS)
+        const char* e = std::getenv("TSG_SEED_BLOCKS");
+        return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 8u;
+    }();
     const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
                               static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
@@ -2502,7 +2527,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         k_prepare<<<nq, kThreads, dtw ? qe_bytes : q_bytes, st>>>(iv, sv, d_queries);
         TSG_LAUNCHED();
         if (dtw) seed_dtw<<<dim3(seed_dtw_x, nq), kThreads, qe_bytes, st>>>(iv, sv, d_queries);
-        else seed<<<dim3(seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
+        else seed<<<dim3(fine ? std::min(seed_x, seed_fine_x) : seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
         TSG_LAUNCHED();
     });
     if (!approximate) {
