@@ -380,8 +380,8 @@ def run_ours(args):
     nqt = args.steps * nq
     ws = 16
     P = bs.pages
-    # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize, 7 fine
-    groups = {"bound": [1], "seed": [2], "lbscan": [4], "fine": [7], "refine": [3, 5], "finalize": [6]}
+    # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize
+    groups = {"bound": [1], "seed": [2], "lbscan": [4], "refine": [3, 5], "finalize": [6]}
     lb_nodes, lb_entries, refined, cands, boxes = stats_acc[0], stats_acc[1], stats_acc[2], stats_acc[5], stats_acc[6]
     fine_calcs = stats_acc[7]
     fw = 2 * 16 if (n % 32 == 0 and not os.environ.get("TSG_NO_FINE")) else 0  # fine summary bytes per series (w = 16)
@@ -392,10 +392,9 @@ def run_ours(args):
         "bound": nqt * NG * 2 * ws + max(lb_nodes - nqt * NG, 0) * (2 * ws + 4),
         # quad boxes (box_calcs, 2 x 16 B) + words of surviving quads + candidate records (pos + bound)
         "lbscan": boxes * 2 * ws + lb_entries * ws + cands * 8,
-        # kept candidate rows (full length) + their records (bound, entry, pos gather, sum)
-        "refine": refined * 4 * n + cands * 20,
-        # candidate records (bound, entry) + the fine summary rows of those still within the BSF
-        "fine": cands * 8 + fine_calcs * fw,
+        # candidate records (bound, row, sum) + the fine summary rows of those within the BSF
+        # + the refined rows (full length)
+        "refine": refined * 4 * n + cands * 16 + fine_calcs * fw,
     }
     group_ms = {g: sum(prof_ms[k] for k in ks) for g, ks in groups.items()}
     dom = max(group_ms, key=group_ms.get)
