@@ -67,6 +67,10 @@ enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
 #ifndef TSG_MINB_BOUND
 #define TSG_MINB_BOUND 4
 #endif
+// w = 16 box bounds clamp with the native u16x2 min/max (0: byte-SIMD __vmaxu4 / __vminu4)
+#ifndef TSG_BOX_U16
+#define TSG_BOX_U16 1
+#endif
 
 // ---------------------------------------------------------------- views
 // Kernel-side views of the index and of a slot set (passed by value).
@@ -262,8 +266,47 @@ __device__ __forceinline__ float word_bound(const float* s_lut, const uint4* v, 
 // Box bound: per segment the table entry of the query symbol clamped into the
 // box [lo, hi] (0 when the query symbol is inside) — node_lower_bound's region
 // gap (src/query.cpp:102-107) over a box of iSAX words.
+__device__ __forceinline__ uint32_t vmax_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t vmin_u16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
+// Four segments of a w = 16 box: the even and odd symbols spread into 16-bit
+// lanes (one LOP3 / PRMT each) are clamped with the native u16x2 min/max
+// (one VIMNMX per two segments; __vmaxu4 / __vminu4 are emulated in about
+// seven instructions each), then read back as table byte offsets.
+__device__ __forceinline__ void box_quad16(const float* s_lut, int s0, uint32_t q, uint32_t lo, uint32_t hi, float* t) {
+    const uint32_t ce = vmin_u16x2(vmax_u16x2(q & 0x00FF00FFu, lo & 0x00FF00FFu), hi & 0x00FF00FFu);
+    const uint32_t co = vmin_u16x2(vmax_u16x2(__byte_perm(q, 0, 0x4341), __byte_perm(lo, 0, 0x4341)),
+                                   __byte_perm(hi, 0, 0x4341));
+    const char* b = reinterpret_cast<const char*>(s_lut);
+    // lanes hold symbols <= 255, so the upper lane shifted right by 14 is its
+    // byte offset (the lower lane's bits 14-15 are zero)
+    t[0] = *reinterpret_cast<const float*>(b + (s0 + 0) * 1024 + ((ce << 2) & 0x3FCu));
+    t[1] = *reinterpret_cast<const float*>(b + (s0 + 1) * 1024 + ((co << 2) & 0x3FCu));
+    t[2] = *reinterpret_cast<const float*>(b + (s0 + 2) * 1024 + (ce >> 14));
+    t[3] = *reinterpret_cast<const float*>(b + (s0 + 3) * 1024 + (co >> 14));
+}
+
 template <int H, bool W16>
 __device__ __forceinline__ float box_bound(const float* s_lut, const uint4* q4, const uint4* lo, const uint4* hi, int w) {
+    if constexpr (W16 && TSG_BOX_U16) {
+        float t[16];
+        box_quad16(s_lut, 0, q4[0].x, lo[0].x, hi[0].x, t + 0);
+        box_quad16(s_lut, 4, q4[0].y, lo[0].y, hi[0].y, t + 4);
+        box_quad16(s_lut, 8, q4[0].z, lo[0].z, hi[0].z, t + 8);
+        box_quad16(s_lut, 12, q4[0].w, lo[0].w, hi[0].w, t + 12);
+        float lb = 0.f;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) lb = __fadd_rd(lb, t[s]);  // segment order, as word_bound
+        return lb;
+    }
     uint4 c[H];
 #pragma unroll
     for (int h = 0; h < H; ++h)
