@@ -190,6 +190,7 @@ void free_shard(DevIndex& s) {
                     static_cast<void*>(s.top_hi)})
         if (p) cudaFreeAsync(p, s.stream);
     if (s.stream) cudaStreamSynchronize(s.stream);
+    free_search_graphs(s);
     free_slots(s.batch);
     free_slots(s.big);
     cudaFree(s.results);

@@ -87,6 +87,7 @@ struct DevIndex {
     float refine_split = 0.3f;     // wave-0 page-bound fraction of the seed bound (TSG_REFINE_SPLIT)
     // per-kernel profiling (tsg_profile_enable)
     bool profile = false;
+    void* graphs = nullptr;  // search_batch's CUDA graphs of the batch pipeline (search.cu)
     double prof_ms[8] = {0};
     uint64_t prof_launches[8] = {0};
 };
@@ -163,6 +164,8 @@ void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, doubl
 // of capacity N (api.cu's search_all does that).
 // window < 0: Euclidean; window >= 0: DTW with that Sakoe-Chiba window
 // (Measure::dtw, src/query.cpp:88-92,138-145).
+// Destroys the shard's cached search graphs (free_shard).
+void free_search_graphs(DevIndex& ix);
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
                   struct DevResult* results, int window = -1);
 constexpr int kMaxDtwWindow = 255;  // the device DTW keeps a band diagonal in registers (8 cells per lane)

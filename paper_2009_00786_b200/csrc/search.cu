@@ -37,6 +37,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <stdexcept>
 #include <utility>
 #include <vector>
@@ -2420,12 +2424,80 @@ __global__ void __launch_bounds__(kThreads)
 
 template <typename K>
 int blocks_per_sm(K kernel, size_t smem) {
+    // cached per (device, kernel, shared memory): the driver query costs
+    // microseconds, which a one-query batch would pay on every call
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, size_t>, int> cache;
+    int dev = 0;
+    TSG_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(dev, reinterpret_cast<const void*>(kernel), smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     int b = 0;
     TSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, smem));
-    return std::max(b, 1);
+    b = std::max(b, 1);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = b;
+    return b;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, bytes).
+void set_max_smem(const void* f, int bytes) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, bool> done;
+    int dev = 0;
+    TSG_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(dev, f, bytes);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(key)) return;
+    TSG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done[key] = true;
+}
+
+// The batch pipeline (prepare .. finalize, nine launches, no host round trip)
+// as CUDA graphs, one per batch shape: a one-query batch otherwise pays every
+// launch's latency in series. The graph reads the queries from its own
+// staging rows, filled by its first node (a device copy whose source is
+// re-pointed before each launch), so the caller's query pointer is not part
+// of the key.
+struct SearchGraph {
+    cudaGraph_t graph = nullptr;  // kept: the copy node belongs to it
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t copy = nullptr;
+    uint64_t launches = 0;  // kernel launches per replay (gpu_launches)
+};
+// (slot arrays, slot sizes, results, batch size, mode, window, seed cap, split); the index's own
+// arrays are fixed for the cache's lifetime (it is freed with the shard)
+using GraphKey = std::tuple<const void*, const void*, const void*, const void*, uint64_t, uint64_t, const void*, uint32_t,
+                            int, int, uint32_t, float>;
+struct GraphCache {
+    std::map<GraphKey, SearchGraph> graphs;
+    float* staging = nullptr;  // [staging_rows][n]
+    uint32_t staging_rows = 0;
+};
+constexpr size_t kMaxGraphs = 32;
+
+void clear_graphs(GraphCache& gc) {
+    for (auto& kv : gc.graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
+    gc.graphs.clear();
 }
 
 }  // namespace
+
+void free_search_graphs(DevIndex& ix) {
+    auto* gc = static_cast<GraphCache*>(ix.graphs);
+    if (!gc) return;
+    clear_graphs(*gc);
+    cudaFree(gc->staging);
+    delete gc;
+    ix.graphs = nullptr;
+}
 
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
                   DevResult* results, int window) {
@@ -2450,11 +2522,11 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const bool tma = vec && refine_tma && !std::getenv("TSG_NO_TMA_REFINE");
     const size_t tma_bytes = static_cast<size_t>(kThreads / kRowLanes) * tma_group_floats(n) * 4 +
                              static_cast<size_t>((n / 8 + kRowLanes - 1) / kRowLanes) * 64 * 8;
-    if (tma) TSG_CUDA(cudaFuncSetAttribute(refine_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024));
+    if (tma) set_max_smem(reinterpret_cast<const void*>(refine_tma), 150 * 1024);
     for (const void* f : {reinterpret_cast<const void*>(refine), reinterpret_cast<const void*>(seed),
                           reinterpret_cast<const void*>(lbscan), reinterpret_cast<const void*>(bound),
                           reinterpret_cast<const void*>(groups), reinterpret_cast<const void*>(k_prepare)})
-        TSG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        set_max_smem(f, 100 * 1024);
 
     IndexView iv{};
     iv.rows = ix.rows;
@@ -2532,17 +2604,17 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const size_t tma_fine_bytes = tma_bytes + 32 * 256 * sizeof(float);
     unsigned tma_fine_grid = 0;
     if (tma_fine) {
-        TSG_CUDA(cudaFuncSetAttribute(refine_tma_fine, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024));
+        set_max_smem(reinterpret_cast<const void*>(refine_tma_fine), 180 * 1024);
         tma_fine_grid = static_cast<unsigned>(sms * blocks_per_sm(refine_tma_fine, tma_fine_bytes));
     }
     unsigned fine_grid = 0;
     if (fine) {
-        TSG_CUDA(cudaFuncSetAttribute(fine_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        set_max_smem(reinterpret_cast<const void*>(fine_k), 100 * 1024);
         fine_grid = static_cast<unsigned>(sms * blocks_per_sm(fine_k, fine_bytes));
     }
     if (dtw) {
-        TSG_CUDA(cudaFuncSetAttribute(seed_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-        TSG_CUDA(cudaFuncSetAttribute(refine_dtw, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+        set_max_smem(reinterpret_cast<const void*>(seed_dtw), 100 * 1024);
+        set_max_smem(reinterpret_cast<const void*>(refine_dtw), 100 * 1024);
     }
     const unsigned seed_dtw_x = (iv.seed_cap + kWarps - 1) / kWarps;
     // refine_dtw: query + envelope, then per-warp scratch for a candidate row and its envelope
@@ -2566,45 +2638,95 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         marks.push_back({slot, {a, b}});
     };
     const int inq = static_cast<int>(nq);
-    mark(2, [&] {
-        k_prepare<<<nq, kThreads, dtw ? qe_bytes : q_bytes, st>>>(iv, sv, d_queries);
-        TSG_LAUNCHED();
-        if (dtw) seed_dtw<<<dim3(seed_dtw_x, nq), kThreads, qe_bytes, st>>>(iv, sv, d_queries);
-        else seed<<<dim3(fine ? std::min(seed_x, seed_fine_x) : seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, d_queries);
-        TSG_LAUNCHED();
-    });
-    if (!approximate) {
-        mark(1, [&] {
-            groups<<<dim3(group_x, nq), kThreads, lut_bytes, st>>>(iv, sv);
+    auto pipeline = [&](const float* qsrc) {
+        mark(2, [&] {
+            k_prepare<<<nq, kThreads, dtw ? qe_bytes : q_bytes, st>>>(iv, sv, qsrc);
             TSG_LAUNCHED();
-            bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 0);
+            if (dtw) seed_dtw<<<dim3(seed_dtw_x, nq), kThreads, qe_bytes, st>>>(iv, sv, qsrc);
+            else seed<<<dim3(fine ? std::min(seed_x, seed_fine_x) : seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, qsrc);
             TSG_LAUNCHED();
         });
-        for (int wave = 0; wave < 2; ++wave) {
-            if (wave == 1)
-                mark(1, [&] {  // runs of the deferred pages, against the BSF refinement wave A tightened
-                    bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 1);
+        if (!approximate) {
+            mark(1, [&] {
+                groups<<<dim3(group_x, nq), kThreads, lut_bytes, st>>>(iv, sv);
+                TSG_LAUNCHED();
+                bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 0);
+                TSG_LAUNCHED();
+            });
+            for (int wave = 0; wave < 2; ++wave) {
+                if (wave == 1)
+                    mark(1, [&] {  // runs of the deferred pages, against the BSF refinement wave A tightened
+                        bound<<<bound_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, 1);
+                        TSG_LAUNCHED();
+                    });
+                mark(4, [&] {
+                    lbscan<<<scan_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, wave);
                     TSG_LAUNCHED();
                 });
-            mark(4, [&] {
-                lbscan<<<scan_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, wave);
-                TSG_LAUNCHED();
-            });
-            mark(wave == 0 ? 3 : 5, [&] {
-                if (tma_fine)
-                    refine_tma_fine<<<tma_fine_grid, kThreads, tma_fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                else if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, rdtw_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, d_queries, inq, wave);
-                TSG_LAUNCHED();
-            });
+                mark(wave == 0 ? 3 : 5, [&] {
+                    if (tma_fine)
+                        refine_tma_fine<<<tma_fine_grid, kThreads, tma_fine_bytes, st>>>(iv, sv, qsrc, inq, wave);
+                    else if (fine) fine_k<<<fine_grid, kThreads, fine_bytes, st>>>(iv, sv, qsrc, inq, wave);
+                    else if (dtw) refine_dtw<<<refine_dtw_grid, kThreads, rdtw_bytes, st>>>(iv, sv, qsrc, inq, wave);
+                    else if (tma) refine_tma<<<refine_grid, kThreads, tma_bytes, st>>>(iv, sv, qsrc, inq, wave);
+                    else refine<<<refine_grid, kThreads, qd_bytes, st>>>(iv, sv, qsrc, inq, wave);
+                    TSG_LAUNCHED();
+                });
+            }
         }
+        mark(6, [&] {
+            k_finalize<<<dim3(fin_x, nq), kThreads, 0, st>>>(iv, sv, approximate ? 1 : 0, results);
+            TSG_LAUNCHED();
+        });
+    };
+    static const bool no_graph = std::getenv("TSG_NO_GRAPH") != nullptr;  // A/B: plain stream launches
+    if (ix.profile || no_graph) {
+        pipeline(d_queries);
+    } else {
+        if (!ix.graphs) ix.graphs = new GraphCache;
+        GraphCache& gc = *static_cast<GraphCache*>(ix.graphs);
+        const size_t qbytes = static_cast<size_t>(nq) * n * sizeof(float);
+        if (gc.staging_rows < nq) {  // graphs point at the old staging rows
+            TSG_CUDA(cudaStreamSynchronize(st));
+            clear_graphs(gc);
+            cudaFree(gc.staging);
+            gc.staging = nullptr;
+            gc.staging_rows = std::max(nq, ix.batch_max);
+            TSG_CUDA(cudaMalloc(&gc.staging, static_cast<size_t>(gc.staging_rows) * n * sizeof(float)));
+        }
+        const GraphKey key{slots.work, slots.cand_pos, slots.surv, slots.fine_lut, slots.cap, slots.rcap, results, nq,
+                           approximate ? 1 : 0, window, iv.seed_cap, iv.split};
+        auto it = gc.graphs.find(key);
+        const bool fresh = it == gc.graphs.end();
+        if (fresh) {
+            if (gc.graphs.size() >= kMaxGraphs) clear_graphs(gc);
+            SearchGraph sg;
+            TSG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            TSG_CUDA(cudaMemcpyAsync(gc.staging, d_queries, qbytes, cudaMemcpyDeviceToDevice, st));
+            const uint64_t l0 = launch_count();
+            pipeline(gc.staging);
+            sg.launches = launch_count() - l0;
+            cudaGraph_t g = nullptr;
+            TSG_CUDA(cudaStreamEndCapture(st, &g));
+            size_t count = 0;
+            TSG_CUDA(cudaGraphGetNodes(g, nullptr, &count));
+            std::vector<cudaGraphNode_t> nodes(count);
+            TSG_CUDA(cudaGraphGetNodes(g, nodes.data(), &count));
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType t;
+                TSG_CUDA(cudaGraphNodeGetType(nd, &t));
+                if (t == cudaGraphNodeTypeMemcpy) sg.copy = nd;
+            }
+            if (!sg.copy) throw std::runtime_error("search_batch: captured graph has no query copy node");
+            TSG_CUDA(cudaGraphInstantiate(&sg.exec, g, 0));
+            sg.graph = g;
+            it = gc.graphs.emplace(key, sg).first;
+        }
+        TSG_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy, gc.staging, d_queries, qbytes,
+                                                    cudaMemcpyDeviceToDevice));
+        TSG_CUDA(cudaGraphLaunch(it->second.exec, st));
+        if (!fresh) note_launch(static_cast<int>(it->second.launches));  // capture counted them once
     }
-    mark(6, [&] {
-        k_finalize<<<dim3(fin_x, nq), kThreads, 0, st>>>(iv, sv, approximate ? 1 : 0, results);
-        TSG_LAUNCHED();
-    });
     if (!marks.empty()) {
         TSG_CUDA(cudaStreamSynchronize(st));
         for (auto& m : marks) {
