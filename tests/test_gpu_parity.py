@@ -522,3 +522,25 @@ def test_exact_at_scale_matches_bruteforce():
     assert sum(r.stats.real_dist_calcs for r in res) < 0.001 * N * len(res)  # the index pruned >99.9%
     del index, rows
     torch.cuda.empty_cache()
+
+
+@pytest.mark.gpu
+def test_graph_replays_with_new_query_buffers(oracle):
+    """The batch pipeline runs as a cached CUDA graph keyed by batch shape, not by the query
+    pointer: replays with other device query buffers (same batch size, and a batch-size
+    change in between) must still answer each buffer's own queries exactly."""
+    import torch
+
+    rows = oracle.generate(5000, 128, 611)
+    index = tg.build_index(rows, tg.IndexConfig(n=128, w=16, leaf_capacity=40))
+    rng = np.random.default_rng(612)
+    for it, nq in enumerate([7, 7, 3, 7, 1, 7]):
+        qs = oracle.generate(nq, 128, 700 + it)
+        if it % 2:  # member-derived queries in every other buffer
+            qs = (rows[rng.integers(0, 5000, nq)] + 0.02 * rng.standard_normal((nq, 128))).astype(np.float32)
+        dq = torch.from_numpy(np.ascontiguousarray(qs)).cuda()
+        res = tg.exact_search_batch(index, dq)
+        del dq  # the next buffer may land elsewhere (or at the same address with other contents)
+        for k, q in enumerate(qs):
+            d, p = oracle.scan_nn(rows, q, 0)
+            assert res[k].position == p and res[k].distance == d, (it, k, res[k], d, p)
