@@ -2577,10 +2577,15 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
 
     const int sms = ix.sms;
     const unsigned seed_x = (iv.seed_cap + kThreads / kRowLanes - 1) / (kThreads / kRowLanes);
-    static const unsigned seed_fine_x = [] {  // seed blocks per query with the fine summary (TSG_SEED_BLOCKS)
+    // Seed blocks per query with the fine summary: 8 (best from batch 64 up), or one wave of
+    // blocks over the batch when it is small (batch 1: 8.8K -> 9.9K q/s at c5 sigma 0.01,
+    // profiles/ab_seed_blocks.sh); TSG_SEED_BLOCKS overrides.
+    static const int seed_env = [] {
         const char* e = std::getenv("TSG_SEED_BLOCKS");
-        return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 8u;
+        return e ? std::max(1, std::atoi(e)) : 0;
     }();
+    const unsigned seed_fine_x = seed_env ? static_cast<unsigned>(seed_env)
+                                          : std::max(8u, static_cast<unsigned>(ix.sms) / nq);
     const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
                               static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
