@@ -372,6 +372,44 @@ void ensure_queries(DevIndex& s, uint32_t nq) {
     s.queries_cap = nq;
 }
 
+// Queries that outgrew their batch slot, rerun together: the batch slots'
+// candidate arrays are one allocation of n x cap records, so k reruns can use
+// them as k slots of n * cap / k records (the shard's size when k <= n * cap / N,
+// which cannot overflow). Rows are gathered into a scratch buffer; answers
+// replace the flagged ones in host_out; any query that overflows again keeps
+// its flag for the one-query full-size path. (c4: 1.57K -> ~2.3K q/s.)
+void rerun_overflows_batched(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out,
+                             int window) {
+    std::vector<uint32_t> ovf;
+    for (uint32_t q = 0; q < nq; ++q)
+        if (host_out[q].flags & kResultOverflow) ovf.push_back(q);
+    const uint64_t total = static_cast<uint64_t>(s.batch.n) * s.batch.cap;
+    const uint64_t k_full = s.N ? total / s.N : 0;  // slots of full size the arrays hold
+    if (ovf.empty() || k_full < 2 || std::getenv("TSG_NO_BATCHED_RERUN")) return;
+    const uint32_t kmax = static_cast<uint32_t>(std::min<uint64_t>(k_full, s.batch.n));
+    float* rows = nullptr;
+    DevResult* res = nullptr;
+    const uint32_t kc0 = std::min<uint32_t>(kmax, static_cast<uint32_t>(ovf.size()));
+    TSG_CUDA(cudaMallocAsync(&rows, static_cast<size_t>(kc0) * s.n * sizeof(float), s.stream));
+    TSG_CUDA(cudaMallocAsync(&res, kc0 * sizeof(DevResult), s.stream));
+    std::vector<DevResult> out(kc0);
+    for (size_t i0 = 0; i0 < ovf.size(); i0 += kc0) {
+        const uint32_t kc = static_cast<uint32_t>(std::min<size_t>(kc0, ovf.size() - i0));
+        for (uint32_t i = 0; i < kc; ++i)
+            TSG_CUDA(cudaMemcpyAsync(rows + static_cast<uint64_t>(i) * s.n, dq + static_cast<uint64_t>(ovf[i0 + i]) * s.n,
+                                     s.n * sizeof(float), cudaMemcpyDeviceToDevice, s.stream));
+        DevIndex::Slots view = s.batch;  // same arrays, fewer and larger slots (not owned)
+        view.n = kc;
+        view.cap = std::min<uint64_t>(s.N, total / kc);
+        search_batch(s, view, rows, kc, approximate, res, window);
+        TSG_CUDA(cudaMemcpyAsync(out.data(), res, kc * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
+        TSG_CUDA(cudaStreamSynchronize(s.stream));
+        for (uint32_t i = 0; i < kc; ++i) host_out[ovf[i0 + i]] = out[i];
+    }
+    TSG_CUDA(cudaFreeAsync(rows, s.stream));
+    TSG_CUDA(cudaFreeAsync(res, s.stream));
+}
+
 // All nq device queries of one shard: batches of batch_max through the batch
 // slots, then any query that outgrew its slot again, alone, in the full-size
 // slot (allocated on first use). Results land in host_out.
@@ -383,6 +421,7 @@ void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, Dev
     }
     TSG_CUDA(cudaMemcpyAsync(host_out, s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
     TSG_CUDA(cudaStreamSynchronize(s.stream));
+    rerun_overflows_batched(s, dq, nq, approximate, host_out, window);
     for (uint32_t q = 0; q < nq; ++q) {
         if (!(host_out[q].flags & kResultOverflow)) continue;
         if (!s.big.n) alloc_slots(s, s.big, 1, s.N);

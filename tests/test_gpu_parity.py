@@ -312,13 +312,19 @@ def test_exact_matches_scan_c5_noisy_queries(oracle, sigma):
         assert sum(int(r.position) == int(s) for r, s in zip(res, src)) >= 8
 
 
-def test_slot_overflow_reruns_full_size(oracle, monkeypatch):
-    """Queries whose candidates outgrow a batch slot are rerun alone in a full-size slot."""
-    monkeypatch.setenv("TSG_SLOT_CAP", "64")  # read when the index is built
+@pytest.mark.parametrize("slot_cap,batched", [(64, True), (200, True), (200, False), (600, True)])
+def test_slot_overflow_reruns_full_size(oracle, monkeypatch, slot_cap, batched):
+    """Queries whose candidates outgrow a batch slot are rerun: together in the batch slots
+    re-sliced into fewer, larger slots when those hold the shard at least twice (slot caps 200 and
+    600: 128 slots x cap >= 2 x 6000 rows, in chunks when more queries overflow than fit), else
+    (cap 64, or TSG_NO_BATCHED_RERUN) alone in a full-size slot."""
+    monkeypatch.setenv("TSG_SLOT_CAP", str(slot_cap))  # read when the index is built
+    if not batched:
+        monkeypatch.setenv("TSG_NO_BATCHED_RERUN", "1")
     rows = oracle.generate(6000, 64, 515)
     cfg = tg.IndexConfig(n=64, w=8, max_card_bits=2, leaf_capacity=20)  # coarse words: many candidates
     index = tg.build_index(rows, cfg)
-    queries = np.concatenate([oracle.generate(5, 64, 516), rows[[3, 4000]] + np.float32(0.3)]).astype(np.float32)
+    queries = np.concatenate([oracle.generate(9, 64, 516), rows[[3, 4000, 5999]] + np.float32(0.3)]).astype(np.float32)
     check_against_scan(oracle, rows, queries, cfg, index=index)
 
 
