@@ -415,12 +415,22 @@ void rerun_overflows_batched(DevIndex& s, const float* dq, uint32_t nq, bool app
 // slot (allocated on first use). Results land in host_out.
 void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out, int window) {
     ensure_results(s, nq);
-    for (uint32_t off = 0; off < nq; off += s.batch_max) {
-        const uint32_t b = std::min(s.batch_max, nq - off);
-        search_batch(s, s.batch, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off, window);
+    // Batches run in the slot arrays sliced into eb slots; a call in which more than 5% of the
+    // queries overflow halves eb for the next calls (fewer, larger slots: c4 -> 64 slots), down
+    // to 16. Datasets whose queries fit (c2) keep batch_max.
+    const uint32_t eb = s.eff_batch ? s.eff_batch : s.batch_max;
+    DevIndex::Slots view = s.batch;  // not owned
+    view.n = eb;
+    view.cap = std::min<uint64_t>(s.N, static_cast<uint64_t>(s.batch.n) * s.batch.cap / eb);
+    for (uint32_t off = 0; off < nq; off += eb) {
+        const uint32_t b = std::min(eb, nq - off);
+        search_batch(s, view, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off, window);
     }
     TSG_CUDA(cudaMemcpyAsync(host_out, s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
     TSG_CUDA(cudaStreamSynchronize(s.stream));
+    uint32_t n_ovf = 0;
+    for (uint32_t q = 0; q < nq; ++q) n_ovf += (host_out[q].flags & kResultOverflow) ? 1 : 0;
+    if (static_cast<uint64_t>(n_ovf) * 20 > nq && eb > 16 && !std::getenv("TSG_FIXED_BATCH")) s.eff_batch = eb / 2;
     rerun_overflows_batched(s, dq, nq, approximate, host_out, window);
     for (uint32_t q = 0; q < nq; ++q) {
         if (!(host_out[q].flags & kResultOverflow)) continue;

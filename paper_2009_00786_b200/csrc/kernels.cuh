@@ -79,6 +79,7 @@ struct DevIndex {
     };
     Slots batch, big;
     uint32_t batch_max = 128;       // queries per batch (TSG_BATCH)
+    uint32_t eff_batch = 0;         // queries per batch after overflow feedback (search_all; 0 = batch_max)
     struct DevResult* results = nullptr;  // [results_cap]
     uint32_t results_cap = 0;
     float* queries = nullptr;      // staging for host queries
