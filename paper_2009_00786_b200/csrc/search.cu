@@ -1047,6 +1047,19 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
                                             float cut, uint64_t cap, const uint32_t* __restrict__ pos,
                                             uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
+    // one 64-bit atomic reserves both waves' records for the whole stage (per 32
+    // records it contended on c4, where every warp queues millions per query)
+    int lo_cnt = 0;
+    for (int i = lane; i < cnt; i += 32) lo_cnt += s_lb[i] <= cut ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
+    unsigned long long old = 0;
+    if (lane == 0) {
+        old = atomicAdd(&wk->cand, static_cast<unsigned long long>(lo_cnt) |
+                                       (static_cast<unsigned long long>(cnt - lo_cnt) << 32));
+        if ((old & 0xFFFFFFFFull) + (old >> 32) + cnt > cap) atomicExch(&wk->overflow, 1u);
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, 0);
+    uint64_t bl = old & 0xFFFFFFFFull, bh = old >> 32;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < cnt;
@@ -1054,13 +1067,6 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
         const bool low = valid && lb <= cut;
         const uint32_t row = valid ? pos[s_pos[i]] : 0u;  // staged entries -> dataset rows
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
-        unsigned long long old = 0;
-        if (lane == 0)
-            old = atomicAdd(&wk->cand, static_cast<unsigned long long>(__popc(ml)) |
-                                           (static_cast<unsigned long long>(__popc(mh)) << 32));
-        old = __shfl_sync(0xFFFFFFFFu, old, 0);
-        const uint64_t bl = old & 0xFFFFFFFFull, bh = old >> 32;
-        if (lane == 0 && bl + __popc(ml) + bh + __popc(mh) > cap) atomicExch(&wk->overflow, 1u);
         const unsigned below = (1u << lane) - 1u;
         if (low) {
             const uint64_t at = bl + __popc(ml & below);
@@ -1075,6 +1081,8 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
                 cand_lb[cap - 1 - off] = lb;
             }
         }
+        bl += __popc(ml);
+        bh += __popc(mh);
     }
     __syncwarp();
 }
