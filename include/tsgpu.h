@@ -119,9 +119,37 @@ tsg_status tsg_config_validate(const tsg_config* cfg);
 
 /* Lifecycle. n_gpus devices (devices may be NULL for 0..n_gpus-1). An index
  * built on a context shards its rows across the context's devices in
- * contiguous ranges; search combines the per-device answers. */
+ * contiguous ranges; search combines the per-shard answers:
+ *   - distinct devices: one NCCL communicator over them (ncclCommInitAll);
+ *     per batch an ncclAllReduce(min) of the shards' seed best-so-far
+ *     distances (every shard prunes against the global seed) and one
+ *     ncclAllGather of the per-shard result records, merged on the device
+ *     (lexicographic (distance, position) minimum = scan_nn's tie rule,
+ *     src/scan.cpp:54-59);
+ *   - the same device repeated (e.g. {0, 0}): the same two exchanges over
+ *     device memory (local shards, for tests and over-decomposition);
+ *   - any other mix: TSG_INVALID_ARGUMENT.
+ * NCCL is loaded at run time (the process's libnccl.so.2, else the system's;
+ * TSG_NCCL_LIB overrides); failures map to TSG_NCCL. Free every index of a
+ * context before closing it. */
 tsg_status tsg_open(int n_gpus, const int* devices, tsg_ctx** out);
 tsg_status tsg_close(tsg_ctx* ctx);
+
+/* One process per GPU (torchrun-style). Rank 0 creates an id, the caller
+ * distributes it (any channel), every rank joins its one-device context to the
+ * communicator. An index built on the context is this rank's shard (pass its
+ * first global row as position_offset); tsg_search / tsg_search_device /
+ * tsg_search_measure on it are COLLECTIVE: every rank calls them with the same
+ * nq, and every rank receives the global answers (seed-BSF allreduce inside
+ * the query pipeline, result all-gather + device merge after it). */
+typedef struct tsg_comm_id {
+    uint8_t internal[128];
+} tsg_comm_id;
+tsg_status tsg_comm_unique_id(tsg_comm_id* id);
+tsg_status tsg_comm_init(tsg_ctx* ctx, int nranks, int rank, const tsg_comm_id* id);
+enum { TSG_TRANSPORT_NONE = 0, TSG_TRANSPORT_LOCAL = 1, TSG_TRANSPORT_NCCL = 2 };
+/* transport of the context, its number of shards / ranks, and this process's rank. */
+tsg_status tsg_comm_info(const tsg_ctx* ctx, int* transport, int* nranks, int* rank);
 
 /* Build from HOST rows (count x length float32, row-major). The library
  * copies the rows into HBM; the caller keeps ownership of its buffer.
@@ -238,9 +266,12 @@ tsg_status tsg_generate_series(int kind, float* dev_rows, uint64_t begin, uint64
 uint64_t tsg_launch_count(void);
 
 /* Per-kernel device timing of the search pipeline (CUDA events recorded on
- * the index's stream around every launch). Kernel slots, in pipeline order:
- * 0 prep, 1 leaf_lb, 2 seed, 3 refine(seed leaf), 4 lbscan, 5 refine,
- * 6 finalize, 7 result. ms[8] and launches[8] accumulate until reset. */
+ * the index's stream around every launch; the pipeline then runs without its
+ * CUDA graph). Slots: 0 unused, 1 groups + bound (both page waves), 2 prepare +
+ * seed, 3 refine wave A (fine bound + rows), 4 lbscan (both waves), 5 refine
+ * wave B, 6 finalize, 7 cross-shard seed-BSF exchange. ms[8] (max over the
+ * index's shards) and launches[8] (query-launches, summed) accumulate until
+ * reset. */
 tsg_status tsg_profile_enable(tsg_index* index, int enable);
 tsg_status tsg_profile_read(tsg_index* index, double* ms, uint64_t* launches, int reset);
 

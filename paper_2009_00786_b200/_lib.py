@@ -21,13 +21,20 @@ EXPORTS = (
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export", "tsg_index_export_fine",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
     "tsg_generate_series", "tsg_index_build_file", "tsg_search_measure",
+    "tsg_comm_unique_id", "tsg_comm_init", "tsg_comm_info",
 )
+
+TSG_TRANSPORT_NONE, TSG_TRANSPORT_LOCAL, TSG_TRANSPORT_NCCL = 0, 1, 2
 
 TSG_MEASURE_ED, TSG_MEASURE_DTW = 0, 1
 
 
 class tsg_measure(C.Structure):
     _fields_ = [("kind", C.c_int32), ("window", C.c_int32)]
+
+
+class tsg_comm_id(C.Structure):
+    _fields_ = [("internal", C.c_uint8 * 128)]
 
 
 class tsg_config(C.Structure):
@@ -101,6 +108,9 @@ def lib() -> C.CDLL:
         "tsg_generate_series": (i32, [i32, vp, u64, u64, u64, u64, i32, C.c_double, u64, u64, vp]),
         "tsg_profile_enable": (i32, [vp, i32]),
         "tsg_profile_read": (i32, [vp, C.POINTER(C.c_double), C.POINTER(u64), i32]),
+        "tsg_comm_unique_id": (i32, [C.POINTER(tsg_comm_id)]),
+        "tsg_comm_init": (i32, [vp, i32, i32, C.POINTER(tsg_comm_id)]),
+        "tsg_comm_info": (i32, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -26,13 +26,19 @@
 
 #include "../../include/tsgpu.h"
 #include "common.cuh"
+#include "exchange.cuh"
 #include "kernels.cuh"
 
 namespace tsg {
 
 static std::atomic<uint64_t> g_launches{0};
-void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+static thread_local uint64_t t_launches = 0;
+void note_launch(int n) {
+    g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed);
+    t_launches += static_cast<uint64_t>(n);
+}
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+uint64_t launch_count_thread() { return t_launches; }
 
 namespace {
 
@@ -56,6 +62,9 @@ tsg_status guarded(F&& f) {
     } catch (const OutOfMemory& e) {
         g_error = e.what();
         return TSG_OOM;
+    } catch (const NcclError& e) {
+        g_error = e.what();
+        return TSG_NCCL;
     } catch (const CudaError& e) {
         g_error = e.what();
         return TSG_CUDA;
@@ -125,8 +134,23 @@ struct DeviceGuard {
 
 using namespace tsg;
 
+// Devices and the transport that combines their shards (exchange.cuh):
+// several shards on one device exchange locally; distinct devices of one
+// process use ncclCommInitAll; tsg_comm_init joins a one-device context to a
+// communicator of processes (one shard per rank).
 struct tsg_ctx {
     std::vector<int> devices;
+    Transport transport = kTransportNone;
+    std::vector<CommHandle> comms;  // NCCL: one per device (multi-device) or this process's (multi-process)
+    int nranks = 1, rank = 0;       // multi-process communicator
+    ~tsg_ctx() {
+        for (CommHandle c : comms) {
+            try {
+                nccl_comm_destroy(c);
+            } catch (...) {
+            }
+        }
+    }
 };
 
 struct tsg_index {
@@ -135,6 +159,7 @@ struct tsg_index {
     uint64_t count = 0, length = 0, position_offset = 0;
     std::vector<DevIndex> shards;
     std::vector<uint64_t> shard_first;  // first local row of each shard (relative to position_offset)
+    std::vector<std::unique_ptr<Exchange>> xchgs;  // one endpoint per shard (none for a lone shard)
     tsg_build_stats stats{};
     std::mutex mu;
 };
@@ -194,6 +219,7 @@ void free_shard(DevIndex& s) {
     free_slots(s.batch);
     free_slots(s.big);
     cudaFree(s.results);
+    cudaFree(s.merged);
     cudaFree(s.queries);
     if (s.stream) cudaStreamDestroy(s.stream);
     s = DevIndex{};
@@ -359,8 +385,10 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
 void ensure_results(DevIndex& s, uint32_t nq) {
     if (s.results_cap >= nq) return;
     cudaFree(s.results);
-    s.results = nullptr;
+    cudaFree(s.merged);
+    s.results = s.merged = nullptr;
     TSG_CUDA(cudaMalloc(&s.results, static_cast<size_t>(nq) * sizeof(DevResult)));
+    TSG_CUDA(cudaMalloc(&s.merged, static_cast<size_t>(nq) * sizeof(DevResult)));
     s.results_cap = nq;
 }
 
@@ -378,6 +406,7 @@ void ensure_queries(DevIndex& s, uint32_t nq) {
 // which cannot overflow). Rows are gathered into a scratch buffer; answers
 // replace the flagged ones in host_out; any query that overflows again keeps
 // its flag for the one-query full-size path. (c4: 1.57K -> ~2.3K q/s.)
+// The device results (s.results) are patched too: the cross-shard merge reads them.
 void rerun_overflows_batched(DevIndex& s, const float* dq, uint32_t nq, bool approximate, DevResult* host_out,
                              int window) {
     std::vector<uint32_t> ovf;
@@ -403,6 +432,9 @@ void rerun_overflows_batched(DevIndex& s, const float* dq, uint32_t nq, bool app
         view.cap = std::min<uint64_t>(s.N, total / kc);
         search_batch(s, view, rows, kc, approximate, res, window);
         TSG_CUDA(cudaMemcpyAsync(out.data(), res, kc * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
+        for (uint32_t i = 0; i < kc; ++i)
+            TSG_CUDA(cudaMemcpyAsync(s.results + ovf[i0 + i], res + i, sizeof(DevResult), cudaMemcpyDeviceToDevice,
+                                     s.stream));
         TSG_CUDA(cudaStreamSynchronize(s.stream));
         for (uint32_t i = 0; i < kc; ++i) host_out[ovf[i0 + i]] = out[i];
     }
@@ -417,20 +449,26 @@ void search_all(DevIndex& s, const float* dq, uint32_t nq, bool approximate, Dev
     ensure_results(s, nq);
     // Batches run in the slot arrays sliced into eb slots; a call in which more than 5% of the
     // queries overflow halves eb for the next calls (fewer, larger slots: c4 -> 64 slots), down
-    // to 16. Datasets whose queries fit (c2) keep batch_max.
-    const uint32_t eb = s.eff_batch ? s.eff_batch : s.batch_max;
+    // to 16, and a call without overflows doubles it again (up to batch_max), so one hard query
+    // set does not slow later easy ones. Datasets whose queries fit (c2) keep batch_max. Shards
+    // that exchange BSFs keep batch_max: every shard must run the same batches.
+    const bool xchg = s.xchg != nullptr;
+    const uint32_t eb = (!xchg && s.eff_batch) ? s.eff_batch : s.batch_max;
     DevIndex::Slots view = s.batch;  // not owned
     view.n = eb;
     view.cap = std::min<uint64_t>(s.N, static_cast<uint64_t>(s.batch.n) * s.batch.cap / eb);
     for (uint32_t off = 0; off < nq; off += eb) {
         const uint32_t b = std::min(eb, nq - off);
-        search_batch(s, view, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off, window);
+        search_batch(s, view, dq + static_cast<uint64_t>(off) * s.n, b, approximate, s.results + off, window, xchg);
     }
     TSG_CUDA(cudaMemcpyAsync(host_out, s.results, nq * sizeof(DevResult), cudaMemcpyDeviceToHost, s.stream));
     TSG_CUDA(cudaStreamSynchronize(s.stream));
     uint32_t n_ovf = 0;
     for (uint32_t q = 0; q < nq; ++q) n_ovf += (host_out[q].flags & kResultOverflow) ? 1 : 0;
-    if (static_cast<uint64_t>(n_ovf) * 20 > nq && eb > 16 && !std::getenv("TSG_FIXED_BATCH")) s.eff_batch = eb / 2;
+    if (!xchg && !std::getenv("TSG_FIXED_BATCH")) {
+        if (static_cast<uint64_t>(n_ovf) * 20 > nq && eb > 16) s.eff_batch = eb / 2;
+        else if (n_ovf == 0 && eb < s.batch_max) s.eff_batch = std::min(s.batch_max, eb * 2);
+    }
     rerun_overflows_batched(s, dq, nq, approximate, host_out, window);
     for (uint32_t q = 0; q < nq; ++q) {
         if (!(host_out[q].flags & kResultOverflow)) continue;
@@ -455,29 +493,6 @@ void to_result(const DevResult& d, tsg_result& r) {
     r.fine_calcs = d.fine_calcs;
 }
 
-// Lexicographic (distance, position) merge of per-shard answers: the
-// cross-device step of the sharded search.
-void merge_into(tsg_result& acc, const tsg_result& r, bool first) {
-    if (first || r.distance < acc.distance || (r.distance == acc.distance && r.position < acc.position)) {
-        acc.distance = r.distance;
-        acc.position = r.position;
-    }
-    if (first) {
-        acc.stats = r.stats;
-        acc.box_calcs = r.box_calcs;
-        acc.fine_calcs = r.fine_calcs;
-        return;
-    }
-    acc.fine_calcs += r.fine_calcs;
-    acc.box_calcs = static_cast<uint32_t>(std::min<uint64_t>(0xFFFFFFFFull, uint64_t{acc.box_calcs} + r.box_calcs));
-    acc.stats.lb_node_calcs += r.stats.lb_node_calcs;
-    acc.stats.lb_entry_calcs += r.stats.lb_entry_calcs;
-    acc.stats.real_dist_calcs += r.stats.real_dist_calcs;
-    acc.stats.bsf_updates += r.stats.bsf_updates;
-    acc.stats.pruned_subtrees += r.stats.pruned_subtrees;
-    acc.stats.queue_insertions += r.stats.queue_insertions;
-}
-
 void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg_result* out, bool approximate,
                 int window = -1) {
     if (!ix) fail("search: null index");
@@ -485,7 +500,10 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
     if (!queries || !out) fail("search: null buffer");
     std::lock_guard<std::mutex> lock(ix->mu);
     if (!host && ix->shards.size() != 1) fail("tsg_search_device: device queries need a single-device index");
-    std::vector<std::vector<DevResult>> per(ix->shards.size(), std::vector<DevResult>(nq));
+    const size_t G = ix->shards.size();
+    const bool nccl = G >= 1 && ix->shards[0].xchg && ix->shards[0].xchg->transport() == kTransportNccl;
+    for (auto& x : ix->xchgs) x->reset();
+    std::vector<std::vector<DevResult>> per(G, std::vector<DevResult>(nq));
     auto work = [&](size_t k) {
         DevIndex& s = ix->shards[k];
         DeviceGuard g(s.device);
@@ -497,30 +515,46 @@ void run_search(tsg_index* ix, const float* queries, bool host, uint32_t nq, tsg
             dq = s.queries;
         }
         search_all(s, dq, nq, approximate, per[k].data(), window);
+        if (nccl) {  // every rank: all-gather the shards' records, merge on the device
+            s.xchg->merge_results(s.results, nq, s.merged, s.stream);
+            TSG_CUDA(cudaMemcpyAsync(per[k].data(), s.merged, nq * sizeof(DevResult), cudaMemcpyDeviceToHost,
+                                     s.stream));
+            TSG_CUDA(cudaStreamSynchronize(s.stream));
+        }
     };
-    if (ix->shards.size() == 1) {
+    if (G == 1) {
         work(0);
     } else {
         std::vector<std::thread> th;
-        std::vector<std::exception_ptr> errs(ix->shards.size());
-        for (size_t k = 0; k < ix->shards.size(); ++k)
+        std::vector<std::exception_ptr> errs(G);
+        for (size_t k = 0; k < G; ++k)
             th.emplace_back([&, k] {
                 try {
                     work(k);
                 } catch (...) {
                     errs[k] = std::current_exception();
+                    if (ix->shards[k].xchg) ix->shards[k].xchg->abort();  // peers must not wait on this shard
                 }
             });
         for (auto& t : th) t.join();
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
     }
-    for (uint32_t q = 0; q < nq; ++q)
-        for (size_t k = 0; k < ix->shards.size(); ++k) {
-            tsg_result r{};
-            to_result(per[k][q], r);
-            merge_into(out[q], r, k == 0);
-        }
+    std::vector<DevResult> merged;
+    const DevResult* final_res = per[0].data();
+    if (G > 1 && !nccl) {  // local shards: merge their device records on the first shard's stream
+        DevIndex& s0 = ix->shards[0];
+        DeviceGuard g(s0.device);
+        std::vector<const DevResult*> src;
+        for (auto& s : ix->shards) src.push_back(s.results);
+        merged.resize(nq);
+        merge_results_local(src, nq, merged.data(), s0.stream);
+        final_res = merged.data();
+    }
+    for (uint32_t q = 0; q < nq; ++q) {
+        out[q] = tsg_result{};
+        to_result(final_res[q], out[q]);
+    }
 }
 
 tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, uint64_t length,
@@ -539,6 +573,8 @@ tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, 
         if (!rows && !path) fail("build_index: null rows");
         if (position_offset + count - 1 > 0xFFFFFFFFull) fail("build_index: positions exceed 2^32-1");
         if (!host && ctx->devices.size() != 1) fail("tsg_index_build_device: device rows need a single-device context");
+        if (ctx->transport == kTransportNccl && ctx->devices.size() > 1 && count < ctx->devices.size())
+            fail("build_index: fewer series than devices (every NCCL rank needs a shard)");
 
         auto ix = std::make_unique<tsg_index>();
         ix->ctx = ctx;
@@ -583,6 +619,20 @@ tsg_status do_build(tsg_ctx* ctx, const float* rows, bool host, uint64_t count, 
                     if (s.stream || s.rows) free_shard(s);
                 std::rethrow_exception(e);
             }
+        // cross-shard exchange endpoints (exchange.cuh)
+        if (ctx->transport == kTransportNccl) {
+            for (size_t k = 0; k < G; ++k) {
+                const int nr = ctx->devices.size() > 1 ? static_cast<int>(G) : ctx->nranks;
+                const int rk = ctx->devices.size() > 1 ? static_cast<int>(k) : ctx->rank;
+                DeviceGuard dg(ix->shards[k].device);
+                ix->xchgs.push_back(make_nccl_exchange(ctx->comms[k], nr, rk, ix->shards[k].device));
+            }
+        } else if (G > 1) {
+            DeviceGuard dg(ix->shards[0].device);
+            auto group = make_local_group(static_cast<int>(G), ix->shards[0].device);
+            for (size_t k = 0; k < G; ++k) ix->xchgs.push_back(make_local_exchange(group, static_cast<int>(k)));
+        }
+        for (size_t k = 0; k < ix->xchgs.size(); ++k) ix->shards[k].xchg = ix->xchgs[k].get();
         (void)t0;
         tsg_build_stats st{};
         st.series = count;
@@ -658,6 +708,19 @@ tsg_status tsg_open(int n_gpus, const int* devices, tsg_ctx** out) {
             check_device(d);
             ctx->devices.push_back(d);
         }
+        if (n_gpus > 1) {
+            std::vector<int> u = ctx->devices;
+            std::sort(u.begin(), u.end());
+            const size_t distinct = static_cast<size_t>(std::unique(u.begin(), u.end()) - u.begin());
+            if (distinct == 1) {
+                ctx->transport = kTransportLocal;
+            } else if (distinct == ctx->devices.size()) {
+                ctx->transport = kTransportNccl;
+                ctx->comms = nccl_comm_init_all(ctx->devices);
+            } else {
+                fail("tsg_open: devices must be all distinct (NCCL) or all the same (local shards)");
+            }
+        }
         *out = ctx.release();
     });
 }
@@ -665,6 +728,37 @@ tsg_status tsg_open(int n_gpus, const int* devices, tsg_ctx** out) {
 tsg_status tsg_close(tsg_ctx* ctx) {
     delete ctx;
     return TSG_OK;
+}
+
+tsg_status tsg_comm_unique_id(tsg_comm_id* id) {
+    return guarded([&] {
+        if (!id) fail("tsg_comm_unique_id: null id");
+        nccl_unique_id(id->internal);
+    });
+}
+
+tsg_status tsg_comm_init(tsg_ctx* ctx, int nranks, int rank, const tsg_comm_id* id) {
+    return guarded([&] {
+        if (!ctx || !id) fail("tsg_comm_init: null argument");
+        if (ctx->devices.size() != 1) fail("tsg_comm_init: a multi-process communicator needs a one-device context");
+        if (ctx->transport != kTransportNone) fail("tsg_comm_init: the context already has a communicator");
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail("tsg_comm_init: rank must be in [0, nranks)");
+        DeviceGuard g(ctx->devices[0]);
+        ctx->comms.push_back(nccl_comm_init_rank(nranks, rank, id->internal));
+        ctx->transport = kTransportNccl;
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+    });
+}
+
+tsg_status tsg_comm_info(const tsg_ctx* ctx, int* transport, int* nranks, int* rank) {
+    return guarded([&] {
+        if (!ctx) fail("tsg_comm_info: null context");
+        if (transport) *transport = static_cast<int>(ctx->transport);
+        const bool multi = ctx->devices.size() > 1;
+        if (nranks) *nranks = multi ? static_cast<int>(ctx->devices.size()) : ctx->nranks;
+        if (rank) *rank = multi ? 0 : ctx->rank;
+    });
 }
 
 tsg_status tsg_index_build(tsg_ctx* ctx, const float* host_rows, uint64_t count, uint64_t length,

@@ -36,6 +36,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 // Counts every kernel this library launches (reported as gpu_launches).
 void note_launch(int n = 1);
 uint64_t launch_count();
+uint64_t launch_count_thread();  // launches noted by the calling thread
 
 #define TSG_LAUNCHED() \
     do {                                                        \

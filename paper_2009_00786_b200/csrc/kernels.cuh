@@ -9,6 +9,8 @@
 
 namespace tsg {
 
+class Exchange;
+
 // Entries per page: the unit of the leaf-level lower bound and of work
 // distribution in the LB scan (a leaf is split into ceil(size/kPage) pages).
 constexpr uint32_t kPage = 128;
@@ -89,6 +91,8 @@ struct DevIndex {
     // per-kernel profiling (tsg_profile_enable)
     bool profile = false;
     void* graphs = nullptr;  // search_batch's CUDA graphs of the batch pipeline (search.cu)
+    class Exchange* xchg = nullptr;  // cross-shard exchange endpoint (exchange.cuh; owned by the index)
+    struct DevResult* merged = nullptr;  // [results_cap] NCCL merge output
     double prof_ms[8] = {0};
     uint64_t prof_launches[8] = {0};
 };
@@ -167,8 +171,11 @@ void build_layout(DevIndex& ix, double* ms_summarise, double* ms_organise, doubl
 // (Measure::dtw, src/query.cpp:88-92,138-145).
 // Destroys the shard's cached search graphs (free_shard).
 void free_search_graphs(DevIndex& ix);
+// exchange: this batch takes part in the cross-shard seed-BSF exchange of
+// ix.xchg (every shard runs the same batches; reruns of overflowing queries
+// do not exchange).
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
-                  struct DevResult* results, int window = -1);
+                  struct DevResult* results, int window = -1, bool exchange = false);
 constexpr int kMaxDtwWindow = 255;  // the device DTW keeps a band diagonal in registers (8 cells per lane)
 
 // Input generators (not on the timed path), see generate.cu.

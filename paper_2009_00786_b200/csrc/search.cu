@@ -46,6 +46,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "exchange.cuh"
 #include "kernels.cuh"
 
 namespace tsg {
@@ -2350,8 +2351,11 @@ __global__ void __launch_bounds__(kThreads)
 // ----------------------------------------------------------- finalize
 __device__ __forceinline__ void write_result(const IndexView& ix, const QueryWork* wk, DevResult* out, double dist,
                                              unsigned best_pos, bool overflow, unsigned long long cand) {
-    out->distance = dist;
-    out->position = static_cast<uint32_t>(best_pos + ix.pos_offset);
+    // No row of this shard reaches the BSF (it was imported from another
+    // shard, exchange.cuh): +inf / 0xFFFFFFFF, which loses every merge.
+    const bool none = best_pos == 0xFFFFFFFFu;
+    out->distance = none ? INFINITY : dist;
+    out->position = none ? 0xFFFFFFFFu : static_cast<uint32_t>(best_pos + ix.pos_offset);
     out->flags = overflow ? kResultOverflow : 0u;
     out->stats[kLbNode] = wk->stats[kLbNode];
     out->stats[kLbEntry] = wk->stats[kLbEntry] + wk->nseed;
@@ -2472,21 +2476,39 @@ void set_max_smem(const void* f, int bytes) {
 // re-pointed before each launch), so the caller's query pointer is not part
 // of the key.
 struct SearchGraph {
-    cudaGraph_t graph = nullptr;  // kept: the copy node belongs to it
+    cudaGraph_t graph = nullptr;  // kept: the copy nodes belong to it
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t copy = nullptr;
+    cudaGraphNode_t copy = nullptr;     // caller's queries -> staging rows (source re-pointed per launch)
+    cudaGraphNode_t copy_out = nullptr; // graph-owned results -> caller's results (destination re-pointed)
     uint64_t launches = 0;  // kernel launches per replay (gpu_launches)
 };
-// (slot arrays, slot sizes, results, batch size, mode, window, seed cap, split); the index's own
-// arrays are fixed for the cache's lifetime (it is freed with the shard)
-using GraphKey = std::tuple<const void*, const void*, const void*, const void*, uint64_t, uint64_t, const void*, uint32_t,
-                            int, int, uint32_t, float>;
+// (slot arrays, slot sizes, batch size, mode, window, seed cap, split, seed exchange); the index's
+// own arrays are fixed for the cache's lifetime (it is freed with the shard). The caller's query
+// and result buffers are not part of the key: copy nodes at both ends are re-pointed per launch.
+using GraphKey = std::tuple<const void*, const void*, const void*, const void*, uint64_t, uint64_t, uint32_t, int,
+                            int, uint32_t, float, int>;
 struct GraphCache {
     std::map<GraphKey, SearchGraph> graphs;
-    float* staging = nullptr;  // [staging_rows][n]
+    float* staging = nullptr;      // [staging_rows][n]
+    DevResult* results = nullptr;  // [staging_rows]
     uint32_t staging_rows = 0;
 };
 constexpr size_t kMaxGraphs = 32;
+
+// Ends a capture that an exception interrupted: the stream leaves capture
+// mode, the partial graph is destroyed and the capture's sticky error cleared,
+// so later searches on the shard still work.
+struct CaptureGuard {
+    cudaStream_t st;
+    bool active = true;
+    ~CaptureGuard() {
+        if (!active) return;
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+    }
+};
 
 void clear_graphs(GraphCache& gc) {
     for (auto& kv : gc.graphs) {
@@ -2503,13 +2525,18 @@ void free_search_graphs(DevIndex& ix) {
     if (!gc) return;
     clear_graphs(*gc);
     cudaFree(gc->staging);
+    cudaFree(gc->results);
     delete gc;
     ix.graphs = nullptr;
 }
 
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
-                  DevResult* results, int window) {
+                  DevResult* results, int window, bool exchange) {
     if (nq == 0) return;
+    // the seed-BSF exchange with the other shards (exchange.cuh); TSG_NO_SEED_EXCHANGE=1 for A/B runs
+    static const bool no_seed_x = std::getenv("TSG_NO_SEED_EXCHANGE") != nullptr;
+    Exchange* xc = exchange && !approximate && !no_seed_x ? ix.xchg : nullptr;
+    if (xc) xc->reserve(nq);
     if (nq > slots.n) throw std::logic_error("search_batch: batch larger than its slots");
     cudaStream_t st = ix.stream;
     const int n = ix.n, w = ix.w;
@@ -2651,7 +2678,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         marks.push_back({slot, {a, b}});
     };
     const int inq = static_cast<int>(nq);
-    auto pipeline = [&](const float* qsrc) {
+    auto pipeline = [&](const float* qsrc, DevResult* res) {
         mark(2, [&] {
             k_prepare<<<nq, kThreads, dtw ? qe_bytes : q_bytes, st>>>(iv, sv, qsrc);
             TSG_LAUNCHED();
@@ -2659,6 +2686,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
             else seed<<<dim3(fine ? std::min(seed_x, seed_fine_x) : seed_x, nq), kThreads, qd_bytes, st>>>(iv, sv, qsrc);
             TSG_LAUNCHED();
         });
+        if (xc) mark(7, [&] { xc->seed_bsf(sv.work, nq, st); });
         if (!approximate) {
             mark(1, [&] {
                 groups<<<dim3(group_x, nq), kThreads, lut_bytes, st>>>(iv, sv);
@@ -2688,13 +2716,13 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
             }
         }
         mark(6, [&] {
-            k_finalize<<<dim3(fin_x, nq), kThreads, 0, st>>>(iv, sv, approximate ? 1 : 0, results);
+            k_finalize<<<dim3(fin_x, nq), kThreads, 0, st>>>(iv, sv, approximate ? 1 : 0, res);
             TSG_LAUNCHED();
         });
     };
     static const bool no_graph = std::getenv("TSG_NO_GRAPH") != nullptr;  // A/B: plain stream launches
-    if (ix.profile || no_graph) {
-        pipeline(d_queries);
+    if (ix.profile || no_graph || (xc && !xc->capturable())) {
+        pipeline(d_queries, results);
     } else {
         if (!ix.graphs) ix.graphs = new GraphCache;
         GraphCache& gc = *static_cast<GraphCache*>(ix.graphs);
@@ -2703,24 +2731,30 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
             TSG_CUDA(cudaStreamSynchronize(st));
             clear_graphs(gc);
             cudaFree(gc.staging);
+            cudaFree(gc.results);
             gc.staging = nullptr;
+            gc.results = nullptr;
             gc.staging_rows = std::max(nq, ix.batch_max);
             TSG_CUDA(cudaMalloc(&gc.staging, static_cast<size_t>(gc.staging_rows) * n * sizeof(float)));
+            TSG_CUDA(cudaMalloc(&gc.results, static_cast<size_t>(gc.staging_rows) * sizeof(DevResult)));
         }
-        const GraphKey key{slots.work, slots.cand_pos, slots.surv, slots.fine_lut, slots.cap, slots.rcap, results, nq,
-                           approximate ? 1 : 0, window, iv.seed_cap, iv.split};
+        const GraphKey key{slots.work, slots.cand_pos, slots.surv, slots.fine_lut, slots.cap, slots.rcap, nq,
+                           approximate ? 1 : 0, window, iv.seed_cap, iv.split, xc ? 1 : 0};
         auto it = gc.graphs.find(key);
-        const bool fresh = it == gc.graphs.end();
-        if (fresh) {
+        if (it == gc.graphs.end()) {
             if (gc.graphs.size() >= kMaxGraphs) clear_graphs(gc);
             SearchGraph sg;
+            const uint64_t l0 = launch_count_thread();
             TSG_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            CaptureGuard guard{st};
             TSG_CUDA(cudaMemcpyAsync(gc.staging, d_queries, qbytes, cudaMemcpyDeviceToDevice, st));
-            const uint64_t l0 = launch_count();
-            pipeline(gc.staging);
-            sg.launches = launch_count() - l0;
+            pipeline(gc.staging, gc.results);
+            TSG_CUDA(cudaMemcpyAsync(results, gc.results, nq * sizeof(DevResult), cudaMemcpyDeviceToDevice, st));
             cudaGraph_t g = nullptr;
+            guard.active = false;
             TSG_CUDA(cudaStreamEndCapture(st, &g));
+            sg.graph = g;
+            sg.launches = launch_count_thread() - l0;  // this thread's launches: the pipeline's own
             size_t count = 0;
             TSG_CUDA(cudaGraphGetNodes(g, nullptr, &count));
             std::vector<cudaGraphNode_t> nodes(count);
@@ -2728,17 +2762,30 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
             for (cudaGraphNode_t nd : nodes) {
                 cudaGraphNodeType t;
                 TSG_CUDA(cudaGraphNodeGetType(nd, &t));
-                if (t == cudaGraphNodeTypeMemcpy) sg.copy = nd;
+                if (t != cudaGraphNodeTypeMemcpy) continue;
+                cudaMemcpy3DParms p{};
+                TSG_CUDA(cudaGraphMemcpyNodeGetParams(nd, &p));
+                if (p.dstPtr.ptr == gc.staging) sg.copy = nd;
+                else if (p.srcPtr.ptr == gc.results) sg.copy_out = nd;
             }
-            if (!sg.copy) throw std::runtime_error("search_batch: captured graph has no query copy node");
-            TSG_CUDA(cudaGraphInstantiate(&sg.exec, g, 0));
-            sg.graph = g;
+            if (!sg.copy || !sg.copy_out) {
+                cudaGraphDestroy(g);
+                throw std::runtime_error("search_batch: captured graph lacks its query / result copy node");
+            }
+            const cudaError_t ie = cudaGraphInstantiate(&sg.exec, g, 0);
+            if (ie != cudaSuccess) {
+                cudaGraphDestroy(g);
+                TSG_CUDA(ie);
+            }
             it = gc.graphs.emplace(key, sg).first;
+        } else {
+            note_launch(static_cast<int>(it->second.launches));  // a capture counts its launches once
         }
         TSG_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy, gc.staging, d_queries, qbytes,
                                                     cudaMemcpyDeviceToDevice));
+        TSG_CUDA(cudaGraphExecMemcpyNodeSetParams1D(it->second.exec, it->second.copy_out, results, gc.results,
+                                                    nq * sizeof(DevResult), cudaMemcpyDeviceToDevice));
         TSG_CUDA(cudaGraphLaunch(it->second.exec, st));
-        if (!fresh) note_launch(static_cast<int>(it->second.launches));  // capture counted them once
     }
     if (!marks.empty()) {
         TSG_CUDA(cudaStreamSynchronize(st));

@@ -168,6 +168,22 @@ class Context:
     def handle(self):
         return self._h
 
+    def comm_init(self, nranks: int, rank: int, comm_id: bytes) -> None:
+        """Join this one-device context to a communicator of `nranks` processes (one GPU each,
+        SURVEY 8(e)). Searches on an index built on the context are then collective: every rank
+        calls them with the same queries and receives the global answers."""
+        cid = _lib.tsg_comm_id()
+        if len(comm_id) != 128:
+            raise InvalidArgument("comm_init: the id is 128 bytes (comm_unique_id)")
+        C.memmove(cid.internal, bytes(comm_id), 128)
+        check(self._lib.tsg_comm_init(self._h, nranks, rank, C.byref(cid)))
+
+    def comm_info(self) -> tuple:
+        """(transport, nranks, rank); transport 0 none, 1 local shards, 2 NCCL."""
+        t, n, r = C.c_int(), C.c_int(), C.c_int()
+        check(self._lib.tsg_comm_info(self._h, C.byref(t), C.byref(n), C.byref(r)))
+        return t.value, n.value, r.value
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.tsg_close(self._h)
@@ -175,6 +191,13 @@ class Context:
 
     def __del__(self):
         self.close()
+
+
+def comm_unique_id() -> bytes:
+    """A fresh 128-byte communicator id (rank 0 creates it; the caller distributes it)."""
+    cid = _lib.tsg_comm_id()
+    check(lib().tsg_comm_unique_id(C.byref(cid)))
+    return bytes(cid.internal)
 
 
 _default_ctx: dict = {}
@@ -202,6 +225,10 @@ class Index:
 
     def config(self) -> IndexConfig:
         return self._config
+
+    def device(self) -> int:
+        """The (first) device of the index's context: where device queries must live."""
+        return self._ctx.devices[0]
 
     def data(self):
         return self._data
@@ -256,21 +283,37 @@ def _is_cuda_tensor(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
 
 
-def build_index(dataset, config: IndexConfig = None, devices: Sequence[int] = (0,), position_offset: int = 0) -> Index:
+def _device_tensor(t, what: str, device: int, dims: int = 2):
+    """A CUDA tensor argument checked (float32, `dims`-D, on the index's device) and made
+    contiguous, with torch's current stream of that device synchronised: the library reads it on
+    its own non-blocking stream, so pending writes (t.contiguous(), generators, user kernels) on
+    torch's stream must have finished first."""
+    import torch
+
+    if t.dtype != torch.float32 or t.dim() != dims:
+        raise InvalidArgument(f"{what} must be a {dims}-D float32 tensor")
+    if t.device.index != device:
+        raise InvalidArgument(f"{what} is on cuda:{t.device.index}, the index on cuda:{device}")
+    t = t.contiguous()
+    torch.cuda.current_stream(t.device).synchronize()
+    return t
+
+
+def build_index(dataset, config: IndexConfig = None, devices: Sequence[int] = (0,), position_offset: int = 0,
+                context: "Context" = None) -> Index:
     """tsidx::build_index. ``dataset``: a (count, n) float32 array on the host
     (copied into HBM), or a CUDA tensor already resident on the device
-    (borrowed, zero-copy; single-device only)."""
+    (borrowed, zero-copy; single-device only). ``context`` (instead of
+    ``devices``): a Context, e.g. one joined to a multi-process communicator."""
     config = config or IndexConfig()
     cfg = config.to_c()
     st = _lib.tsg_build_stats()
     h = C.c_void_p()
-    ctx = _context(devices)
+    ctx = context if context is not None else _context(devices)
     if _is_cuda_tensor(dataset):
-        import torch
-
-        if dataset.dtype != torch.float32 or dataset.dim() != 2:
-            raise InvalidArgument("build_index: device dataset must be a 2-D float32 tensor")
-        t = dataset.contiguous()
+        if len(ctx.devices) != 1:
+            raise InvalidArgument("tsg_index_build_device: device rows need a single-device context")
+        t = _device_tensor(dataset, "build_index: device dataset", ctx.devices[0])
         count, length = (t.shape[0], t.shape[1]) if t.numel() else (0, config.n)
         check(lib().tsg_index_build_device(ctx.handle, C.c_void_p(t.data_ptr()), count, length, C.byref(cfg),
                                            position_offset, C.byref(h), C.byref(st)))
@@ -287,7 +330,7 @@ def build_index(dataset, config: IndexConfig = None, devices: Sequence[int] = (0
 
 
 def build_index_from_file(path, config: IndexConfig = None, devices: Sequence[int] = (0,),
-                          position_offset: int = 0) -> Index:
+                          position_offset: int = 0, context: "Context" = None) -> Index:
     """tsidx::load_dataset(path, config.n) + tsidx::build_index, streamed: each
     device reads its range of the headerless float32 file in chunks while K1
     summarises the chunks already in HBM (no host copy of the dataset). The
@@ -296,7 +339,7 @@ def build_index_from_file(path, config: IndexConfig = None, devices: Sequence[in
     cfg = config.to_c()
     st = _lib.tsg_build_stats()
     h = C.c_void_p()
-    ctx = _context(devices)
+    ctx = context if context is not None else _context(devices)
     check(lib().tsg_index_build_file(ctx.handle, os.fsencode(os.fspath(path)), config.n, C.byref(cfg),
                                      position_offset, C.byref(h), C.byref(st)))
     data = np.memmap(path, dtype=np.float32, mode="r").reshape(-1, config.n)
@@ -364,8 +407,8 @@ def exact_search_batch(index: Index, queries, measure: Measure = Measure.ed()) -
     n = index.config().n
     m = _measure_c(measure)
     if _is_cuda_tensor(queries):
-        t = queries.contiguous()
-        if t.dim() != 2 or t.shape[1] != n:
+        t = _device_tensor(queries, "queries", index.device())
+        if t.shape[1] != n:
             raise InvalidArgument(f"query length {tuple(t.shape)} does not match the index series length {n}")
         out = (_lib.tsg_result * t.shape[0])()
         if measure.kind == MeasureKind.euclidean:
@@ -405,8 +448,8 @@ def exact_search_batch_records(index: Index, queries, measure: Measure = Measure
     n = index.config().n
     m = _measure_c(measure)
     if _is_cuda_tensor(queries):
-        t = queries.contiguous()
-        if t.dim() != 2 or t.shape[1] != n:
+        t = _device_tensor(queries, "queries", index.device())
+        if t.shape[1] != n:
             raise InvalidArgument(f"query length {tuple(t.shape)} does not match the index series length {n}")
         out = np.empty(t.shape[0], RESULT_DTYPE)
         if measure.kind == MeasureKind.euclidean:

@@ -113,7 +113,8 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
     if gcc is None:
         pytest.skip("no C compiler")
     structs = {"tsg_config": _lib.tsg_config, "tsg_build_stats": _lib.tsg_build_stats,
-               "tsg_search_stats": _lib.tsg_search_stats, "tsg_result": _lib.tsg_result}
+               "tsg_search_stats": _lib.tsg_search_stats, "tsg_result": _lib.tsg_result,
+               "tsg_comm_id": _lib.tsg_comm_id}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tsgpu.h"', "int main(void) {"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
@@ -146,3 +147,21 @@ def test_result_record_dtype_matches_the_c_struct():
     raw[1].stats.real_dist_calcs = 3
     C.memmove(rec.ctypes.data, raw, C.sizeof(raw))
     assert (rec[1]["distance"], rec[1]["position"], rec[1]["fine_calcs"], rec[1]["stats"][2]) == (2.5, 7, 9, 3)
+
+
+def test_nccl_unique_id_without_a_gpu():
+    """The multi-process communicator id comes from NCCL, loaded at run time (no GPU needed)."""
+    import torch  # noqa: F401  (the process's NCCL: torch's bundled libnccl.so.2)
+
+    a, b = _lib.tsg_comm_id(), _lib.tsg_comm_id()
+    _lib.check(_lib.lib().tsg_comm_unique_id(C.byref(a)))
+    _lib.check(_lib.lib().tsg_comm_unique_id(C.byref(b)))
+    assert bytes(a.internal) != bytes(b.internal)
+    assert any(bytes(a.internal))
+
+
+def test_comm_init_needs_a_context():
+    cid = _lib.tsg_comm_id()
+    st = _lib.lib().tsg_comm_init(None, 2, 0, C.byref(cid))
+    assert st == _lib.TSG_INVALID_ARGUMENT
+    assert "null argument" in _lib.lib().tsg_last_error().decode()
