@@ -8,13 +8,23 @@ seed 2; w=16, 8-bit symbols, leaf capacity 2000).
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
 
 Ours: the dataset (fixed total size) is sharded by contiguous series ranges
-across ranks; each rank answers every query on its shard and a NCCL
-all-gather of the 16-byte (distance, position) records combines them
+across ranks (one process per GPU; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run). Each rank's index joins the library's
+NCCL communicator (tsg_comm_init): per batch the shards' seed best-so-far
+distances are min-allreduced inside the query graph and the per-shard
+(distance, position) records are all-gathered and merged on the device
 (lexicographic minimum = the exact global answer, ties to the lowest
 position). `value` = queries/s with queries already in HBM; `e2e` = the same
 through the public API with host queries (H2D + result D2H inside the timed
 region). Reference arm (`--impl reference`): the unmodified reference
 (oracle/_ref, compiled from /root/reference) on the host cores, rank 0 only.
+
+Parity (both arms): BASELINE's 100 queries (rows 0..99 of the seed-2 query
+stream) are answered outside the timed region and digested as the reference
+CLI's oracle check prints them ("%zu %u %.17g\n": query, position, distance,
+tools/main.cpp:193-210); on c2 the digest is compared with
+tests/golden/c2_answers.txt (the reference's scan_nn over all 100M series,
+oracle/make_c2_golden.py). A mismatch exits nonzero.
 
 Inputs are synthetic (the reference's own seeded generator, BASELINE.json
 configs), generated on the device by the library's generator (bit-identical
@@ -48,6 +58,59 @@ CONFIGS = {
     "c4": {"data": ("c4", 125_000_000, 96, 4), "queries": ("c4", 4, None), "nq": 100, "per_gpu": True},
     "c5": {"data": ("rw", 100_000_000, 256, 1), "queries": ("c5", 5, 0), "nq": 100},
 }
+
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def golden_for(name, count):
+    """(answers text, meta) of the reference's exhaustive answers for this workload, if committed."""
+    if name != "c2" or count != CONFIGS["c2"]["data"][1]:
+        return None, None
+    path = os.path.join(GOLDEN, "c2_answers.txt")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as f, open(os.path.join(GOLDEN, "c2_golden.json")) as g:
+        return f.read(), json.load(g)
+
+
+def answers_text(dist, pos):
+    return "".join("%d %d %.17g\n" % (k, int(p), float(d)) for k, (d, p) in enumerate(zip(dist, pos)))
+
+
+def parity_object(name, count, dist, pos, arm):
+    """The parity check of the BASELINE query set against the committed golden answers."""
+    import hashlib
+
+    text = answers_text(dist, pos)
+    gold, meta = golden_for(name, count)
+    obj = {"queries": len(dist), "rows": f"0..{len(dist) - 1} of the query stream", "arm": arm,
+           "digest": hashlib.sha256(text.encode()).hexdigest(), "format": "%zu %u %.17g (query, position, distance)"}
+    if gold is None:
+        obj["golden"] = None
+        return obj, True
+    gl = [l.split() for l in gold.splitlines()]
+    gpos = np.array([int(x[1]) for x in gl[:len(dist)]])
+    gdist = np.array([float(x[2]) for x in gl[:len(dist)]])
+    rel = np.abs(np.asarray(dist, np.float64) - gdist) / np.maximum(gdist, 1e-300)
+    obj.update({"golden": "tests/golden/c2_answers.txt (reference scan_nn over all series)",
+                "golden_digest": meta["answers_sha256"], "digest_equal": obj["digest"] == meta["answers_sha256"],
+                "positions_equal": int((np.asarray(pos, np.int64) == gpos).sum()),
+                "distances_bitwise_equal": int((np.asarray(dist, np.float64) == gdist).sum()),
+                "max_rel_dist_err": float(rel.max()) if len(rel) else 0.0})
+    ok = obj["positions_equal"] == len(dist) and obj["max_rel_dist_err"] <= 1e-5
+    return obj, ok
+
+
+def cmin_bytes(name, count, n, w=16):
+    """SURVEY 8(d)'s flat-scan query bytes N*w + C_min*4n per query, C_min (words whose LB is below
+    the exact NN distance) averaged over the golden query set (computed by the oracle over all words)."""
+    _, meta = golden_for(name, count)
+    if meta is None:
+        return None
+    cm = float(np.mean(meta["cmin"]))
+    return {"bytes_per_query": count * w + cm * 4 * n, "mean_cmin": cm, "cmin_frac": cm / count,
+            "source": "tests/golden/c2_golden.json (oracle, BASELINE queries rows 0..99)"}
 
 
 def peaks():
@@ -135,6 +198,13 @@ def dist_setup():
     return world, rank, local
 
 
+def config_obj(name, count, n, sigma, nq_par):
+    """The workload description both arms print identically (same keys and values)."""
+    return {"workload": workload_text(name, count, n, sigma),
+            "parity_queries": f"rows 0..{nq_par - 1} of the query stream (BASELINE's {nq_par} queries)",
+            "l2_flush": f"inputs larger than L2 ({count * n * 4 / 1e9:.1f} GB of rows)"}
+
+
 def workload_text(name, count, n, sigma=None):
     spec = CONFIGS[name]
     dkind, _, _, seed = spec["data"]
@@ -220,33 +290,47 @@ def run_reference(args):
         count = args.count
     cores = Reference().hardware_concurrency()
     per_step = args.ref_queries_per_step
-    total = (args.warmup + args.steps) * per_step
+    nq_par = args.batch or spec["nq"]
+    total = max((args.warmup + args.steps) * per_step, nq_par)
     idx, qs, used, gen_ns = ref_inputs(args.config, count, n, total, args.sigma, args.ref_sample)
     build_ns = idx.build_stats["build_ns"]
-    for q in qs[: args.warmup * per_step]:
-        idx.exact_search(q)
+    ans = {}
+    for k, q in enumerate(qs[: args.warmup * per_step]):
+        d, p, _, _ = idx.exact_search(q)
+        ans[k] = (d, p)
     t0 = time.perf_counter()
     times = []
-    for q in qs[args.warmup * per_step:]:
+    for k, q in enumerate(qs[args.warmup * per_step:(args.warmup + args.steps) * per_step]):
         d, p, st, ns = idx.exact_search(q)
         times.append(ns)
+        ans[args.warmup * per_step + k] = (d, p)
     elapsed = time.perf_counter() - t0
     qps = len(times) / elapsed
+    for k in range(nq_par):  # the rest of the parity set, untimed
+        if k not in ans:
+            d, p, _, _ = idx.exact_search(qs[k])
+            ans[k] = (d, p)
+    parity, ok = parity_object(args.config, used, [ans[k][0] for k in range(nq_par)],
+                               [ans[k][1] for k in range(nq_par)], "reference exact_search")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(qps, 4), "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(elapsed * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_text(args.config, used, n, args.sigma),
-                   "queries_per_step": per_step, "l2_flush": f"inputs larger than L2 ({used * n * 4 / 1e9:.1f} GB)"},
+        "config": config_obj(args.config, used, n, args.sigma, nq_par),
+        "step": {"queries_per_step": per_step, "query_rows": f"0..{total - 1} of the query stream",
+                 "timed_query_rows": f"{args.warmup * per_step}..{(args.warmup + args.steps) * per_step - 1}"},
         "cpu_baseline": {"value": round(qps, 4), "unit": "queries/s", "cores": cores, "kind": "reference",
                          "sample": f"{used} of {count} series, {args.steps * per_step} timed queries"},
         "e2e": {"value": round(qps, 4), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "build": {"value": round(used / (build_ns * 1e-9) / 1e6, 3), "unit": "Mseries/s",
                   "build_s": round(build_ns * 1e-9, 3), "generate_s": round(gen_ns * 1e-9, 3)},
         "median_query_ms": round(statistics.median(times) * 1e-6, 3),
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
+    if not ok:
+        sys.exit(f"parity: the reference's answers differ from the golden answers ({parity})")
 
 
 def run_ours(args):
@@ -255,12 +339,18 @@ def run_ours(args):
 
     import paper_2009_00786_b200 as tg
     from paper_2009_00786_b200 import _lib
-    from paper_2009_00786_b200.shard import allgather_merge, shard_range
+    from paper_2009_00786_b200.shard import shard_range
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
+    ctx = tg.Context((local,))
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # the library's own communicator (seed-BSF allreduce + result all-gather inside tsg_search);
+        # torch.distributed only carries its id and the bench's barrier / max-over-ranks
+        cid = [tg.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(cid, src=0)
+        ctx.comm_init(world, rank, cid[0])
 
     def barrier():
         if world > 1:
@@ -289,7 +379,8 @@ def run_ours(args):
     rows = tg.generate_device(dkind, shard, n, seed, begin=b, device=local)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
-    total_batches = args.warmup + args.steps
+    # batch 0: the parity set (BASELINE's queries, rows 0..nq-1); 1..W warm-up; W+1..W+K timed
+    total_batches = 1 + args.warmup + args.steps
     qdev = tg.generate_device(qkind, total_batches * nq, n, qseed, begin=count if qbegin is None else qbegin,
                               device=local, noise=args.sigma, data_count=count, data_seed=seed)
     qhost = qdev.cpu().numpy()
@@ -304,7 +395,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     tb = time.perf_counter()
-    index = tg.build_index(rows, cfg, devices=(local,), position_offset=b)
+    index = tg.build_index(rows, cfg, context=ctx, position_offset=b)
     torch.cuda.synchronize()
     build_wall = max_over_ranks(time.perf_counter() - tb)
     bs = index.build_stats()
@@ -314,13 +405,12 @@ def run_ours(args):
     measure = tg.Measure.dtw(args.dtw) if args.dtw >= 0 else tg.Measure.ed()
 
     def step(batch, host):
-        # one C-ABI call per batch; results as a record array (no per-query Python objects)
+        # one C-ABI call per batch; results as a record array (no per-query Python objects). With
+        # world > 1 the call is collective: the library exchanges seed BSFs and merges the shards'
+        # answers over NCCL, so every rank gets the global answers.
         src = qhost if host else qdev
         res = tg.exact_search_batch_records(index, src[batch * nq:(batch + 1) * nq], measure)
-        rec = np.stack([res["distance"], res["position"].astype(np.float64)], axis=1)
-        if world > 1:  # the cross-GPU exchange: all-gather of (distance, position) over NCCL
-            rec = allgather_merge(rec, device=f"cuda:{local}")
-        return rec, res
+        return res
 
     def timed(host, stats=None, answers=None):
         # CUDA events on the current stream bracket the K batches; each batch
@@ -331,21 +421,24 @@ def run_ours(args):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         kept = []
-        for i in range(args.warmup, total_batches):
+        for i in range(1 + args.warmup, total_batches):
             kept.append(step(i, host=host))
         ev1.record()
         torch.cuda.synchronize()
         barrier()
-        for rec, res in kept:  # bookkeeping outside the timed region
+        for res in kept:  # bookkeeping outside the timed region
             if answers is not None:
-                answers.append(rec)
+                answers.append(res)
             if stats is not None:
                 st = res["stats"].astype(np.float64).sum(axis=0)
                 stats += (*st, float(res["box_calcs"].astype(np.float64).sum()), float(res["fine_calcs"].astype(np.float64).sum()))
         return max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
 
+    # parity set (untimed): BASELINE's queries against the golden answers
+    par = step(0, host=True)
+    parity, parity_ok = parity_object(args.config, count, par["distance"], par["position"], "ours (tsg_search)")
     # warm-up
-    for i in range(args.warmup):
+    for i in range(1, 1 + args.warmup):
         step(i, host=False)
     torch.cuda.synchronize()
 
@@ -380,8 +473,9 @@ def run_ours(args):
     nqt = args.steps * nq
     ws = 16
     P = bs.pages
-    # library profile slots: 1 bound(+filter), 2 seed, 3 refine wave 0, 4 lbscan, 5 refine wave 1, 6 finalize
-    groups = {"bound": [1], "seed": [2], "lbscan": [4], "refine": [3, 5], "finalize": [6]}
+    # library profile slots (include/tsgpu.h): 1 groups + bound, 2 prepare + seed, 3 refine wave A,
+    # 4 lbscan, 5 refine wave B, 6 finalize, 7 cross-shard seed exchange
+    groups = {"bound": [1], "seed": [2], "lbscan": [4], "refine": [3, 5], "finalize": [6], "exchange": [7]}
     lb_nodes, lb_entries, refined, cands, boxes = stats_acc[0], stats_acc[1], stats_acc[2], stats_acc[5], stats_acc[6]
     fine_calcs = stats_acc[7]
     fw = 2 * 16 if (n % 32 == 0 and not os.environ.get("TSG_NO_FINE")) else 0  # fine summary bytes per series (w = 16)
@@ -401,6 +495,20 @@ def run_ours(args):
     dom_ms = group_ms[dom] / nqt  # per query (each group runs once per query per rank)
     dom_bytes = group_bytes.get(dom, 0.0) / nqt
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_ms > 0 else 0.0
+    # lbscan's other roofline: shared-memory table lookups (16 per quad box and per word), against one
+    # conflict-free 32-lane wavefront per SM per clock
+    props = torch.cuda.get_device_properties(local)
+    sm_clock_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+    lookups = (boxes + lb_entries) * ws
+    lbscan_s = group_ms["lbscan"] * 1e-3
+    smem_peak = props.multi_processor_count * sm_clock_mhz * 1e6 * 32
+    smem_roof = {"kernel": "lbscan", "bound": "smem", "unit": "table lookups/s",
+                 "achieved": lookups / lbscan_s if lbscan_s > 0 else 0.0, "peak": smem_peak,
+                 "frac": round(lookups / lbscan_s / smem_peak, 4) if lbscan_s > 0 else 0.0,
+                 "peak_def": f"{props.multi_processor_count} SMs x {sm_clock_mhz:.0f} MHz x 32 lanes "
+                             "(one conflict-free shared wavefront per SM per clock)"}
+    flat = cmin_bytes(args.config, count, n, ws)
     # DRAM bytes per batch of the same kernel from the committed ncu capture (c2, 1 GPU only)
     traffic = ncu_traffic(dom, nq) if args.config == "c2" and world == 1 and nq == 100 else None
 
@@ -425,11 +533,14 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed * 1e3 / args.steps, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": workload_text(args.config, count, n, args.sigma),
-                       "queries_per_step": nq, "query_rows": f"{args.warmup * nq}.. of the query stream",
-                       "sharding": f"{world} contiguous series ranges",
-                       "l2_flush": f"inputs larger than L2 ({count * n * 4 / world / 1e9:.1f} GB rows, "
-                                   f"{count * 16 / world / 1e9:.2f} GB words per GPU)"},
+            "config": config_obj(args.config, count, n, args.sigma, nq),
+            "step": {"queries_per_step": nq, "query_rows": f"0..{total_batches * nq - 1} of the query stream",
+                     "timed_query_rows": f"{(1 + args.warmup) * nq}..{total_batches * nq - 1}",
+                     "sharding": f"{world} contiguous series ranges, one process per GPU"
+                                 + (", library NCCL communicator" if world > 1 else ""),
+                     "per_gpu_bytes": f"{count * n * 4 / world / 1e9:.1f} GB rows, "
+                                      f"{count * 16 / world / 1e9:.2f} GB words"},
+            "parity": parity,
             "e2e": {"value": round(e2e_qps, 3), "unit": "queries/s", "h2d_bytes_per_step": nq * n * 4,
                     "d2h_bytes_per_step": nq * 72},
             "gpu_launches": int(launches),
@@ -442,7 +553,16 @@ def run_ours(args):
                          "share_of_query_time": round(share, 4),
                          "per_kernel_ms": {g: round(v, 3) for g, v in group_ms.items()},
                          "per_kernel_us_per_query": {g: round(v * 1e3 / nqt, 2) for g, v in group_ms.items()},
-                         "profiled_pass_s": round(prof_s, 4)},
+                         "profiled_pass_s": round(prof_s, 4),
+                         "lbscan_smem": smem_roof},
+            "flat_scan_roofline": None if flat is None else {
+                "formula": "SURVEY 8(d): N*w + C_min*4n bytes per query",
+                "bytes_per_query": round(flat["bytes_per_query"]), "mean_cmin": round(flat["mean_cmin"], 1),
+                "cmin_frac": round(flat["cmin_frac"], 7), "source": flat["source"],
+                "equivalent_gbs": round(flat["bytes_per_query"] * qps / 1e9, 1),
+                "equivalent_frac": round(flat["bytes_per_query"] * qps / 1e9 / hbm / world, 3),
+                "note": "what a flat LB scan would have to move per query; the box hierarchy reads ~1% of the "
+                        "words, so this exceeds 1 by design"},
             "build": {"value": round(count / build_dev_s / 1e6, 3), "unit": "Mseries/s",
                       "build_device_s": round(build_dev_s, 4), "build_wall_s": round(build_wall, 3),
                       "phase_ms": {"summarise": round(bs.summarise_ms, 3), "organise": round(bs.organise_ms, 3),
@@ -465,11 +585,12 @@ def run_ours(args):
             "generate_s": round(gen_s, 2),
             "cpu_baseline": cpu,
         }
-        if answers:
-            line["first_answer"] = {"distance": float(answers[0][0, 0]), "position": int(answers[0][0, 1])}
         print(json.dumps(line), flush=True)
+    index.free()
     if world > 1:
         dist.destroy_process_group()
+    if not parity_ok:
+        sys.exit(f"parity: answers differ from the golden answers ({parity})")
 
 
 def run_ingest(args):
@@ -538,6 +659,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.impl == "ours" and not args.ingest:
+        if args.gpus > 1 and world == 0:
+            # one process per GPU: re-launch this command under torch.distributed.run
+            import socket
+
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            sys.exit(subprocess.call(cmd))
+        if world and world != args.gpus:
+            sys.exit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.ingest:
         run_ingest(args)
     elif args.impl == "reference":

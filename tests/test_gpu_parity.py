@@ -550,3 +550,33 @@ def test_graph_replays_with_new_query_buffers(oracle):
         for k, q in enumerate(qs):
             d, p = oracle.scan_nn(rows, q, 0)
             assert res[k].position == p and res[k].distance == d, (it, k, res[k], d, p)
+
+
+def test_headline_config_answers_equal_reference_golden():
+    """north_star's target on the headline config (BASELINE configs[1]): exact 1-NN answers of the 100
+    BASELINE queries over 100M x 256 z-normalised random walks equal the reference's exhaustive
+    answers (tests/golden/c2_answers.txt: the unmodified reference's scan_nn over all 100M series,
+    oracle/make_c2_golden.py) - identical positions, bit-identical distances, same digest."""
+    import json
+    import os
+
+    import torch
+
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    meta = json.load(open(os.path.join(gdir, "c2_golden.json")))
+    golden = open(os.path.join(gdir, "c2_answers.txt")).read()
+    N, n = meta["count"], meta["n"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("needs ~150 GB of free HBM")
+    rows = tg.generate_device("rw", N, n, 1)  # device generator = the reference's bytes (tested above)
+    queries = tg.generate_device("rw", 100, n, 2)
+    index = tg.build_index(rows, tg.IndexConfig(n=n))
+    for host in (False, True):
+        res = tg.exact_search_batch_records(index, queries.cpu().numpy() if host else queries)
+        text = "".join("%d %d %.17g\n" % (k, int(r["position"]), float(r["distance"])) for k, r in enumerate(res))
+        assert hashlib.sha256(text.encode()).hexdigest() == meta["answers_sha256"]
+        assert text == golden
+    index.free()
+    del rows
+    torch.cuda.empty_cache()
