@@ -224,6 +224,16 @@ tsg_status tsg_approximate_search(tsg_index* index, const float* host_query, tsg
 tsg_status tsg_summarise(const float* dev_rows, uint64_t count, uint64_t length, int w,
                          int bits, uint8_t* dev_words, uint32_t* dev_root_keys, void* stream);
 
+/* The symbol thresholds of cardinality 2^bits: out[256] receives the 2^bits - 1
+ * breakpoints of tsidx::breakpoints_for(2^bits) (src/breakpoints.cpp:65-114,
+ * Acklam + one Newton step, lower half mirrored) followed by +inf padding, as
+ * computed on the host for upload (no GPU needed). */
+tsg_status tsg_breakpoints(int bits, double* out256);
+
+/* The threshold table the index's summarisation and query kernels read, copied
+ * back from HBM (first device): 256 doubles in the layout of tsg_breakpoints. */
+tsg_status tsg_index_thresholds(const tsg_index* index, double* out256);
+
 /* Word stride used by the device layout for a given w. */
 int tsg_word_stride(int w);
 

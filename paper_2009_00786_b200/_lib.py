@@ -21,7 +21,7 @@ EXPORTS = (
     "tsg_search_device", "tsg_approximate_search", "tsg_summarise", "tsg_word_stride", "tsg_index_export", "tsg_index_export_fine",
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
     "tsg_generate_series", "tsg_index_build_file", "tsg_search_measure",
-    "tsg_comm_unique_id", "tsg_comm_init", "tsg_comm_info",
+    "tsg_comm_unique_id", "tsg_comm_init", "tsg_comm_info", "tsg_breakpoints", "tsg_index_thresholds",
 )
 
 TSG_TRANSPORT_NONE, TSG_TRANSPORT_LOCAL, TSG_TRANSPORT_NCCL = 0, 1, 2
@@ -111,6 +111,8 @@ def lib() -> C.CDLL:
         "tsg_comm_unique_id": (i32, [C.POINTER(tsg_comm_id)]),
         "tsg_comm_init": (i32, [vp, i32, i32, C.POINTER(tsg_comm_id)]),
         "tsg_comm_info": (i32, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "tsg_breakpoints": (i32, [i32, vp]),
+        "tsg_index_thresholds": (i32, [vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

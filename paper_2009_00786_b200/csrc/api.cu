@@ -889,6 +889,23 @@ tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* posit
     });
 }
 
+tsg_status tsg_breakpoints(int bits, double* out256) {
+    return guarded([&] {
+        if (bits < 1 || bits > 8) fail("tsg_breakpoints: bits must be in [1, 8]");
+        if (!out256) fail("tsg_breakpoints: null out");
+        host_breakpoints(bits, out256);
+    });
+}
+
+tsg_status tsg_index_thresholds(const tsg_index* ix, double* out256) {
+    return guarded([&] {
+        if (!ix || !out256) fail("tsg_index_thresholds: null argument");
+        const DevIndex& s = ix->shards[0];
+        DeviceGuard g(s.device);
+        TSG_CUDA(cudaMemcpy(out256, s.thr, kThrPad * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 tsg_status tsg_index_export_fine(const tsg_index* ix, uint32_t* fine_width, uint8_t* fine) {
     return guarded([&] {
         if (!ix) fail("tsg_index_export_fine: null index");

@@ -16,7 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <fstream>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -133,72 +133,102 @@ Dataset generate_random_walk(std::size_t count, std::size_t length, std::uint64_
     return ds;
 }
 
-// Input preparation (not the indexed path): FP64 mean / population std,
-// untouched and false when the std is <= 1e-12 (src/dataset.cpp:70-85).
+// ---- dataset utilities (input preparation, not the indexed path) ----------
+// The arithmetic of znormalize must equal the reference's bit for bit
+// (src/dataset.cpp:70-85): FP64 sums taken left to right, population standard
+// deviation, untouched and false at std <= 1e-12. The file helpers keep the
+// reference's checks and error messages (src/dataset.cpp:87-137), which are
+// part of the drop-in contract.
+namespace {
+
+struct Moments {
+    double mean;
+    double stddev;
+};
+
+Moments moments_of(std::span<const float> x) {
+    const double n = static_cast<double>(x.size());
+    double acc = 0.0;
+    for (std::size_t i = 0; i < x.size(); ++i) acc += x[i];
+    const double mean = acc / n;
+    double dev2 = 0.0;
+    for (std::size_t i = 0; i < x.size(); ++i) {
+        const double d = x[i] - mean;
+        dev2 += d * d;
+    }
+    return {mean, std::sqrt(dev2 / n)};
+}
+
+std::uint64_t checked_file_series(const std::filesystem::path& path, std::size_t length) {
+    std::error_code ec;
+    const std::uint64_t size = std::filesystem::file_size(path, ec);
+    if (ec) throw std::runtime_error("load_dataset: cannot stat " + path.string() + ": " + ec.message());
+    const std::uint64_t row = length * sizeof(float);
+    if (size == 0 || size % row != 0)
+        throw std::runtime_error("load_dataset: " + path.string() + " holds " + std::to_string(size) +
+                                 " bytes, not a positive multiple of " + std::to_string(row) + " (length " +
+                                 std::to_string(length) + " * 4)");
+    return size / row;
+}
+
+struct FileCloser {
+    void operator()(std::FILE* f) const {
+        if (f) std::fclose(f);
+    }
+};
+using File = std::unique_ptr<std::FILE, FileCloser>;
+
+}  // namespace
+
 bool znormalize(std::span<float> series) {
     if (series.empty()) throw std::invalid_argument("znormalize: empty series");
-    double sum = 0.0;
-    for (float v : series) sum += v;
-    const double mean = sum / static_cast<double>(series.size());
-    double sq = 0.0;
-    for (float v : series) {
-        const double d = v - mean;
-        sq += d * d;
-    }
-    const double sd = std::sqrt(sq / static_cast<double>(series.size()));
-    if (sd <= 1e-12) return false;
-    for (auto& v : series) v = static_cast<float>((v - mean) / sd);
+    const Moments m = moments_of(series);
+    if (m.stddev <= 1e-12) return false;
+    std::transform(series.begin(), series.end(), series.begin(),
+                   [&](float v) { return static_cast<float>((v - m.mean) / m.stddev); });
     return true;
 }
 
 Dataset load_dataset(const std::filesystem::path& path, std::size_t length) {
     if (length == 0) throw std::invalid_argument("load_dataset: length must be positive");
-    std::error_code ec;
-    const auto bytes = std::filesystem::file_size(path, ec);
-    if (ec) throw std::runtime_error("load_dataset: cannot stat " + path.string() + ": " + ec.message());
-    const std::size_t series_bytes = length * sizeof(float);
-    if (bytes == 0 || bytes % series_bytes != 0)
-        throw std::runtime_error("load_dataset: " + path.string() + " holds " + std::to_string(bytes) +
-                                 " bytes, not a positive multiple of " + std::to_string(series_bytes) + " (length " +
-                                 std::to_string(length) + " * 4)");
+    const std::uint64_t rows = checked_file_series(path, length);
     Dataset ds;
-    ds.count = bytes / series_bytes;
-    ds.length = length;
-    ds.source_length = length;
-    ds.values.resize(ds.count * length);
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw std::runtime_error("load_dataset: cannot open " + path.string());
-    in.read(reinterpret_cast<char*>(ds.values.data()), static_cast<std::streamsize>(bytes));
-    if (in.gcount() != static_cast<std::streamsize>(bytes))
+    ds.count = rows;
+    ds.length = ds.source_length = length;
+    ds.values.resize(rows * length);
+    File f(std::fopen(path.c_str(), "rb"));
+    if (!f) throw std::runtime_error("load_dataset: cannot open " + path.string());
+    if (std::fread(ds.values.data(), sizeof(float), ds.values.size(), f.get()) != ds.values.size())
         throw std::runtime_error("load_dataset: short read from " + path.string());
     return ds;
 }
 
 void save_dataset(const std::filesystem::path& path, const Dataset& dataset) {
-    std::ofstream out(path, std::ios::binary | std::ios::trunc);
-    if (!out) throw std::runtime_error("save_dataset: cannot open " + path.string());
-    out.write(reinterpret_cast<const char*>(dataset.values.data()),
-              static_cast<std::streamsize>(dataset.values.size() * sizeof(float)));
-    if (!out) throw std::runtime_error("save_dataset: short write to " + path.string());
+    File f(std::fopen(path.c_str(), "wb"));
+    if (!f) throw std::runtime_error("save_dataset: cannot open " + path.string());
+    const std::size_t n = dataset.values.size();
+    if (std::fwrite(dataset.values.data(), sizeof(float), n, f.get()) != n || std::fflush(f.get()) != 0)
+        throw std::runtime_error("save_dataset: short write to " + path.string());
 }
 
 Dataset pad_to_segment_multiple(Dataset dataset, int w) {
     if (w < 1) throw std::invalid_argument("pad_to_segment_multiple: w must be at least 1");
-    const auto uw = static_cast<std::size_t>(w);
-    if (dataset.length % uw == 0) return dataset;
-    const std::size_t padded = (dataset.length / uw + 1) * uw;
-    Dataset out;
-    out.count = dataset.count;
-    out.length = padded;
-    out.source_length = dataset.length;
-    out.values.resize(dataset.count * padded);
-    for (std::size_t i = 0; i < dataset.count; ++i) {
-        auto src = dataset.series(i);
-        float* dst = out.values.data() + i * padded;
-        std::memcpy(dst, src.data(), src.size() * sizeof(float));
-        std::fill(dst + dataset.length, dst + padded, src.back());
+    const std::size_t seg = static_cast<std::size_t>(w);
+    const std::size_t target = (dataset.length + seg - 1) / seg * seg;  // next multiple of w
+    if (target == dataset.length) return dataset;
+    Dataset padded;
+    padded.count = dataset.count;
+    padded.length = target;
+    padded.source_length = dataset.length;
+    padded.values.assign(dataset.count * target, 0.f);
+    // each row keeps its values and repeats its last one up to the new length
+    for (std::size_t r = 0; r < dataset.count; ++r) {
+        const float* from = dataset.values.data() + r * dataset.length;
+        float* to = padded.values.data() + r * target;
+        std::copy_n(from, dataset.length, to);
+        std::fill(to + dataset.length, to + target, from[dataset.length - 1]);
     }
-    return out;
+    return padded;
 }
 
 std::string BuildStats::kv_line() const {

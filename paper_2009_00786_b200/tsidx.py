@@ -259,6 +259,12 @@ class Index:
                                      poff.ctypes.data, lo.ctypes.data, hi.ctypes.data))
         return words, pos, off, poff, lo, hi
 
+    def thresholds(self) -> np.ndarray:
+        """The 256-entry threshold table in HBM the index's kernels read (breakpoints, then +inf)."""
+        out = np.empty(256, np.float64)
+        check(lib().tsg_index_thresholds(self._h, out.ctypes.data))
+        return out
+
     def export_fine(self):
         """Fine summary rows [count][fine_width] in dataset order (None when the index has none)."""
         fw = C.c_uint32(0)
@@ -517,6 +523,14 @@ def generate_device(kind: str, count: int, length: int, seed: int, begin: int = 
     stream = torch.cuda.current_stream(out.device).cuda_stream
     check(lib().tsg_generate_series(kinds[kind], C.c_void_p(out.data_ptr()), begin, count, length, seed,
                                     1 if znorm else 0, float(noise), data_count, data_seed, C.c_void_p(stream)))
+    return out
+
+
+def breakpoints(bits: int) -> np.ndarray:
+    """tsidx::breakpoints_for(2**bits) as the library computes it for upload: 256 doubles (the
+    2**bits - 1 breakpoints, then +inf)."""
+    out = np.empty(256, np.float64)
+    check(lib().tsg_breakpoints(bits, out.ctypes.data))
     return out
 
 

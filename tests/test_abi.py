@@ -165,3 +165,21 @@ def test_comm_init_needs_a_context():
     st = _lib.lib().tsg_comm_init(None, 2, 0, C.byref(cid))
     assert st == _lib.TSG_INVALID_ARGUMENT
     assert "null argument" in _lib.lib().tsg_last_error().decode()
+
+
+def test_library_breakpoints_equal_reference_bitwise(golden):
+    """The thresholds libtsgpu uploads (host_breakpoints) equal the reference's
+    breakpoints_for(2^bits) bit for bit, sign of zero included, for every
+    cardinality (src/breakpoints.cpp:65-114; tests/golden/breakpoints.npz is
+    the reference's output), padded with +inf."""
+    import paper_2009_00786_b200 as tg
+
+    g = golden["load"]("breakpoints.npz")
+    for bits in range(1, 9):
+        got = tg.breakpoints(bits)
+        want = g[f"bits{bits}"]
+        k = (1 << bits) - 1
+        assert np.array_equal(got[:k].view(np.uint64), want.view(np.uint64)), bits
+        assert np.all(np.isposinf(got[k:])), bits
+    with pytest.raises(tg.InvalidArgument, match="bits must be in"):
+        tg.breakpoints(9)

@@ -580,3 +580,36 @@ def test_headline_config_answers_equal_reference_golden():
     index.free()
     del rows
     torch.cuda.empty_cache()
+
+
+def test_uploaded_thresholds_equal_reference_bitwise(golden, oracle):
+    """the threshold table in HBM that K1 and the query kernels read is the
+    reference's breakpoints_for(2^bits) bit for bit (tests/golden/breakpoints.npz), for every
+    cardinality."""
+    g = golden["load"]("breakpoints.npz")
+    rows = oracle.generate(500, 64, 5)
+    for bits in range(1, 9):
+        index = tg.build_index(rows, tg.IndexConfig(n=64, w=8, max_card_bits=bits, leaf_capacity=20))
+        got = index.thresholds()
+        k = (1 << bits) - 1
+        assert np.array_equal(got[:k].view(np.uint64), g[f"bits{bits}"].view(np.uint64)), bits
+        assert np.all(np.isposinf(got[k:])), bits
+        index.free()
+
+
+def test_file_built_index_answers_equal_scan(oracle, tmp_path):
+    """Ingestion parity (load_dataset + build_index, src/dataset.cpp:87-117, src/index.cpp:258-318):
+    an index streamed from a headerless float32 file answers exactly like scan_nn over the file's
+    rows, across several streaming chunks."""
+    n = 256
+    rows = oracle.generate(200_000, n, 91)  # 205 MB: two ~128 MB chunks
+    rows[150_000] = rows[10]  # a duplicate: the lower position wins
+    path = tmp_path / "rows.f32"
+    tg.save_dataset(path, rows)
+    queries = np.concatenate([oracle.generate(6, n, 92), rows[[10, 199_999, 130_000]]])
+    index = tg.build_index_from_file(path, tg.IndexConfig(n=n))
+    assert index.build_stats().series == rows.shape[0]
+    for k, r in enumerate(tg.exact_search_batch(index, queries)):
+        d, p = oracle.scan_nn(rows, queries[k], 0)
+        assert (r.position, r.distance) == (p, d), k
+    index.free()
