@@ -553,6 +553,7 @@ def run_ours(args):
                          "share_of_query_time": round(share, 4),
                          "per_kernel_ms": {g: round(v, 3) for g, v in group_ms.items()},
                          "per_kernel_us_per_query": {g: round(v * 1e3 / nqt, 2) for g, v in group_ms.items()},
+                         "per_slot_us_per_query": [round(v * 1e3 / nqt, 2) for v in prof_ms],
                          "profiled_pass_s": round(prof_s, 4),
                          "lbscan_smem": smem_roof},
             "flat_scan_roofline": None if flat is None else {

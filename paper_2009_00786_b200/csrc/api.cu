@@ -170,6 +170,7 @@ void free_slots(DevIndex::Slots& t) {
     for (void* p : {static_cast<void*>(t.work), static_cast<void*>(t.lut), static_cast<void*>(t.fine_lut), static_cast<void*>(t.gsurv),
                     static_cast<void*>(t.surv), static_cast<void*>(t.surv_lb), static_cast<void*>(t.cand_pos),
                     static_cast<void*>(t.cand_lb), static_cast<void*>(t.cand_sq), static_cast<void*>(t.env),
+
                     static_cast<void*>(t.dpage), static_cast<void*>(t.dpage_lb)})
         cudaFree(p);
     t = DevIndex::Slots{};
@@ -325,6 +326,14 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
     check_device(s.device);
     TSG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     TSG_CUDA(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, s.device));
+    if (const char* e = std::getenv("TSG_L2_FETCH")) {  // A/B: L2 fetch granularity hint (bytes)
+        TSG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e))));
+    }
+    if (std::getenv("TSG_PRINT_L2_FETCH")) {
+        size_t v = 0;
+        TSG_CUDA(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity));
+        std::fprintf(stderr, "tsg: cudaLimitMaxL2FetchGranularity = %zu\n", v);
+    }
     s.N = N;
     s.n = static_cast<int>(cfg.n);
     s.w = cfg.w;
@@ -913,7 +922,13 @@ tsg_status tsg_index_export_fine(const tsg_index* ix, uint32_t* fine_width, uint
         const DevIndex& s = ix->shards[0];
         DeviceGuard g(s.device);
         if (fine_width) *fine_width = static_cast<uint32_t>(s.fw);
-        if (fine && s.fw) TSG_CUDA(cudaMemcpy(fine, s.fine, s.N * s.fws, cudaMemcpyDeviceToHost));
+        if (fine && s.fw) {  // stored in index order: back to dataset order for the caller
+            std::vector<uint8_t> idx(s.N * s.fws);
+            std::vector<uint32_t> pos(s.N);
+            TSG_CUDA(cudaMemcpy(idx.data(), s.fine, s.N * s.fws, cudaMemcpyDeviceToHost));
+            TSG_CUDA(cudaMemcpy(pos.data(), s.pos, s.N * 4, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < s.N; ++i) std::memcpy(fine + static_cast<uint64_t>(pos[i]) * s.fws, &idx[i * s.fws], s.fws);
+        }
     });
 }
 

@@ -51,13 +51,22 @@ __global__ void k_iota(uint32_t* v, uint64_t n) {
     GRID_STRIDE(i, n) v[i] = static_cast<uint32_t>(i);
 }
 
-// words[i] = words_orig[pos[i]] (16- or 32-byte rows), and the two lowest
-// box levels: bytewise min / max over each aligned kQuad-entry quad and
-// kRun-entry run of the sorted words (one shuffle tree: offsets 1, 2 give
-// the quads, 4, 8 continue to the runs; a warp's 32 entries are two runs).
+// words[i] = words_orig[pos[i]] (16- or 32-byte rows), the fine summary
+// likewise (fine[i] = fine_orig[pos[i]], fws-byte rows, when present: the
+// query side then reads candidates' fine rows by index entry, next to each
+// other, and maps an entry to its dataset row only when the row is refined),
+// and the two lowest box levels: bytewise min / max over each aligned
+// kQuad-entry quad and kRun-entry run of the sorted words (one shuffle tree:
+// offsets 1, 2 give the quads, 4, 8 continue to the runs; a warp's 32 entries
+// are two runs).
+// src_stride: K1's output stride of words and fine rows; with the fine summary
+// both share one 64-byte record per series (word at 0, fine row at 16), so
+// each entry's gather touches one 64-byte block instead of two scattered ones.
 __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* __restrict__ pos,
                                uint8_t* __restrict__ dst, uint8_t* __restrict__ run_lo, uint8_t* __restrict__ run_hi,
-                               uint8_t* __restrict__ quad_lo, uint8_t* __restrict__ quad_hi, uint64_t n, int ws) {
+                               uint8_t* __restrict__ quad_lo, uint8_t* __restrict__ quad_hi, uint64_t n, int ws,
+                               const uint8_t* __restrict__ fine_src, uint8_t* __restrict__ fine_dst, int fws,
+                               int src_stride, int fine_src_stride) {
     static_assert(kRun == 16 && kQuad == 4, "quad / run boxes are 4- / 16-lane reductions");
     const int lane = threadIdx.x & 31;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -65,10 +74,14 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
         const uint64_t i = w0 + lane;
         const bool in = i < n;
         const uint64_t p = in ? pos[i] : 0;
+        if (fine_src && in)
+            for (int h = 0; h < fws / 16; ++h)
+                *reinterpret_cast<uint4*>(fine_dst + i * fws + 16 * h) =
+                    *reinterpret_cast<const uint4*>(fine_src + p * fine_src_stride + 16 * h);
         for (int h = 0; h < ws / 16; ++h) {
             uint4 x = make_uint4(0, 0, 0, 0);
             if (in) {
-                x = *reinterpret_cast<const uint4*>(src + p * ws + 16 * h);
+                x = *reinterpret_cast<const uint4*>(src + p * src_stride + 16 * h);
                 *reinterpret_cast<uint4*>(dst + i * ws + 16 * h) = x;
             }
             uint4 mn = in ? x : make_uint4(~0u, ~0u, ~0u, ~0u), mx = x;
@@ -289,7 +302,11 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_CUDA(cudaMalloc(&ix.quad_lo, ix.Q * ix.ws));
     TSG_CUDA(cudaMalloc(&ix.quad_hi, ix.Q * ix.ws));
     // pos_in / bstart are reused for the L+1 page counts / bases (L <= N).
-    DevBuf words_orig(N * ix.ws), keys_in(N * 8), keys_out(N * 8), pos_in((N + 1) * 4), flags(N), bstart((N + 1) * 4),
+    // K1 output: words and fine rows interleaved in 64-byte records when both fit (w <= 16, fine
+    // width 32), else separate arrays.
+    const bool rec64 = ix.fw && ix.ws == 16 && ix.fws == 32;
+    const int wst = rec64 ? 64 : ix.ws, fst = rec64 ? 64 : ix.fws;
+    DevBuf words_orig(N * static_cast<uint64_t>(wst)), fine_orig(ix.fw && !rec64 ? N * ix.fws : 0), keys_in(N * 8), keys_out(N * 8), pos_in((N + 1) * 4), flags(N), bstart((N + 1) * 4),
         nsel(8),
         leaf_start(N * 4), ranges_a(open_cap * sizeof(Range)), ranges_b(open_cap * sizeof(Range)),
         ctr(sizeof(LeafCounters));
@@ -325,8 +342,10 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     // K1 summarise
     TSG_CUDA(cudaEventRecord(ev[0], st));
     auto sum_chunk = [&](uint64_t first, uint64_t count) {
-        summarise(ix.rows + first * ix.n, count, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>() + first * ix.ws,
-                  nullptr, keys_in.as<uint64_t>() + first, st, ix.fw ? ix.fine + first * ix.fws : nullptr, key_bits);
+        uint8_t* fine_out = !ix.fw ? nullptr : rec64 ? words_orig.as<uint8_t>() + first * 64 + 16
+                                                      : fine_orig.as<uint8_t>() + first * ix.fws;
+        summarise(ix.rows + first * ix.n, count, ix.n, ix.w, ix.bits, ix.thr, words_orig.as<uint8_t>() + first * wst,
+                  nullptr, keys_in.as<uint64_t>() + first, st, fine_out, key_bits, rec64 ? 64 : 0);
     };
     if (feeder) (*feeder)(sum_chunk);  // rows stream in; K1 runs per chunk behind them
     else sum_chunk(0, N);
@@ -338,7 +357,10 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
                                              pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
     k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, ix.run_lo,
-                                                          ix.run_hi, ix.quad_lo, ix.quad_hi, N, ix.ws);
+                                                          ix.run_hi, ix.quad_lo, ix.quad_hi, N, ix.ws,
+                                                          !ix.fw ? nullptr : rec64 ? words_orig.as<uint8_t>() + 16
+                                                                                   : fine_orig.as<uint8_t>(),
+                                                          ix.fine, ix.fws, wst, fst);
     TSG_LAUNCHED();
     TSG_CUDA(cudaEventRecord(ev[2], st));
 

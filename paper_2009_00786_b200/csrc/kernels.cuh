@@ -32,7 +32,7 @@ struct DevIndex {
     double* thr = nullptr;    // [256] thresholds for `bits`, +inf padded
     uint8_t* words = nullptr; // [N][ws] index order
     // Fine summary (fine_width): [N][fws] quantised 2w half-segment means
-    // (fine_quant), dataset order. fw = 0: none.
+    // (fine_quant), index order (row i = the series of entry i). fw = 0: none.
     uint8_t* fine = nullptr;
     int fw = 0, fws = 0;
     uint32_t* pos = nullptr;  // [N] local row of each index entry
@@ -148,10 +148,11 @@ struct DevResult {
 };
 
 // K1. fine (may be null): the fine summary rows (fine_width(n, w) symbols,
-// stride fine_stride) of the same series.
+// stride fine_stride) of the same series. record_stride > 0: words and fine
+// rows are written with that stride (interleaved records, the build's layout).
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
                uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream,
-               uint8_t* fine = nullptr, int key_bits = 64);
+               uint8_t* fine = nullptr, int key_bits = 64, int record_stride = 0);
 
 // Streams the shard's rows into ix.rows chunk by chunk: for each chunk it
 // enqueues the rows' arrival on ix.stream and then calls sum_chunk(first,

@@ -45,6 +45,8 @@
 #include <utility>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "exchange.cuh"
 #include "kernels.cuh"
@@ -99,7 +101,7 @@ struct IndexView {
     uint64_t pos_offset;
     int window;  // < 0: Euclidean; >= 0: DTW with this Sakoe-Chiba window
     int rev_keogh;  // DTW refinement also tests the reversed LB_Keogh (per-warp scratch in shared memory)
-    const uint8_t* fine;       // [N][fws] fine summary (dataset order); null: none
+    const uint8_t* fine;       // [N][fws] fine summary (index order); null: none
     int fw, fws;
 };
 
@@ -434,6 +436,16 @@ __device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, u
 #define TSG_PREFETCH 1
 #endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// Prefetch of exactly `bytes` (a multiple of 16, 16-byte aligned) into L2 with the bulk-copy unit:
+// unlike prefetch.global.L2 it does not pull the neighbouring sectors of the line.
+__device__ __forceinline__ void prefetch_l2_bytes(const void* p, unsigned bytes) {
+#if TSG_PREFETCH == 2
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+#else
+    (void)bytes;
+    prefetch_l2(p);
+#endif
+}
 
 // -------------------------------------------------------- scheduling
 // Block-level work distribution with query affinity. Each query has a chunk
@@ -686,14 +698,14 @@ __global__ void __launch_bounds__(kThreads)
     for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
         const uint32_t p = ix.pos[e];
         if (fine && e >= a + ngroups) {
-            const uint8_t* f = ix.fine + static_cast<uint64_t>(p) * ix.fws;
+            const uint8_t* f = ix.fine + e * ix.fws;  // fine rows are in index order
             float acc = 0.f;
             for (int sg = j8; sg < ix.fw; sg += kRowLanes) acc = __fadd_rd(acc, __ldg(flut + sg * 256 + f[sg]));
 #pragma unroll
             for (int o = kRowLanes / 2; o > 0; o >>= 1) acc = __fadd_rd(acc, __shfl_xor_sync(gmask, acc, o));
             if (acc > bound_from_bits(ld_volatile_u64(&wk->bsf_bits))) {
                 if (j8 == 0) {
-                    cand_pos[e - a] = p;
+                    cand_pos[e - a] = static_cast<uint32_t>(e);
                     cand_sq[e - a] = INFINITY;
                 }
                 continue;
@@ -701,7 +713,7 @@ __global__ void __launch_bounds__(kThreads)
         }
         const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if (j8 == 0) {
-            cand_pos[e - a] = p;  // candidate records hold dataset rows
+            cand_pos[e - a] = static_cast<uint32_t>(e);  // candidate records hold index entries
             updates += publish(wk, s, e - a, cand_sq, ~0u);
             refined += 1;
         }
@@ -1045,8 +1057,7 @@ constexpr int kStageCap = 256;
 // and rerun with a full-size slot; nothing is written out of range).
 // cut = +inf sends everything to A, cut < 0 everything to B.
 __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
-                                            float cut, uint64_t cap, const uint32_t* __restrict__ pos,
-                                            uint32_t* __restrict__ cand_pos,
+                                            float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
     // one 64-bit atomic reserves both waves' records for the whole stage (per 32
     // records it contended on c4, where every warp queues millions per query)
@@ -1066,7 +1077,7 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
         const bool valid = i < cnt;
         const float lb = valid ? s_lb[i] : 0.f;
         const bool low = valid && lb <= cut;
-        const uint32_t row = valid ? pos[s_pos[i]] : 0u;  // staged entries -> dataset rows
+        const uint32_t row = valid ? s_pos[i] : 0u;  // index entries (mapped to rows only when refined)
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
         const unsigned below = (1u << lane) - 1u;
         if (low) {
@@ -1132,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         return (ns + 31) / 32;
     };
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
-        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, ix.pos, cand_pos, cand_lb);
+        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
         cnt = 0;
         scanned = warp_sum(scanned);
         pruned = warp_sum(pruned);
@@ -1156,7 +1167,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         cnt += __popc(m);
         __syncwarp();
         if (cnt > kStageCap - 32) {
-            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, ix.pos, cand_pos, cand_lb);
+            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
             cnt = 0;
         }
     };
@@ -1215,7 +1226,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
         if (pass) {
             s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
-            if (TSG_PREFETCH) prefetch_l2(ix.words + static_cast<uint64_t>(e0) * WS);  // read when 16 quads queue
+            if (TSG_PREFETCH) prefetch_l2_bytes(ix.words + static_cast<uint64_t>(e0) * WS, (e1 - e0) * WS);  // read when 16 quads queue
         }
         qt += __popc(m);
         __syncwarp();
@@ -1270,8 +1281,8 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
                 s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
                 if (TSG_PREFETCH) {  // the run's quad boxes are read a few drains later
                     const uint64_t qd0 = static_cast<uint64_t>(run.x / kRun) * (kRun / kQuad);
-                    prefetch_l2(ix.quad_lo + qd0 * WS);
-                    prefetch_l2(ix.quad_hi + qd0 * WS);
+                    prefetch_l2_bytes(ix.quad_lo + qd0 * WS, (kRun / kQuad) * WS);
+                    prefetch_l2_bytes(ix.quad_hi + qd0 * WS, (kRun / kQuad) * WS);
                 }
             }
             rt += __popc(m);
@@ -1284,6 +1295,32 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         leave_query();
     }
 }
+
+// ------------------------------------------------- fine table in shared memory
+// The fine summary's [fw][256] table as the TMA refinement kernel keeps it:
+// the float table (default), or half precision rounded DOWN from it
+// (TSG_FINE_LUT_HALF=1: entries stay <= the exact terms, sums stay lower
+// bounds, half the shared memory). Measured on c2 (profiles/ab_refine3.sh):
+// three blocks per SM with the half table and 64- or 128-record chunks are
+// 2-3% slower than two blocks per SM with the float table - the refinement
+// waits on gathered rows, not on occupancy.
+#ifndef TSG_FINE_LUT_HALF
+#define TSG_FINE_LUT_HALF 0
+#endif
+#if TSG_FINE_LUT_HALF
+using FineLutT = __half;
+__device__ __forceinline__ void store_fine_lut4(FineLutT* d, float4 v) {
+    d[0] = __float2half_rd(v.x);
+    d[1] = __float2half_rd(v.y);
+    d[2] = __float2half_rd(v.z);
+    d[3] = __float2half_rd(v.w);
+}
+__device__ __forceinline__ float fine_lut_at(const FineLutT* t, int i) { return __half2float(t[i]); }
+#else
+using FineLutT = float;
+__device__ __forceinline__ void store_fine_lut4(FineLutT* d, float4 v) { *reinterpret_cast<float4*>(d) = v; }
+__device__ __forceinline__ float fine_lut_at(const FineLutT* t, int i) { return t[i]; }
+#endif
 
 // ------------------------------------------------- fine + refine
 // One refinement wave with the fine summary (persistent, block-to-query
@@ -1314,7 +1351,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(fw) * 256 * 4);    // [n]
     __shared__ int s_sel;
     __shared__ uint16_t s_c[kWarps][32 * K];  // kept records: offset in the chunk
-    __shared__ uint32_t s_p[kWarps][32 * K];  // and their dataset rows
+    __shared__ uint32_t s_p[kWarps][32 * K];  // and their dataset rows (pos of the entry)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int wg = lane / kRowLanes;
     const bool leader = (lane & (kRowLanes - 1)) == 0;
@@ -1372,7 +1409,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
                 live[k] = c < end && cand_lb[c] <= bnd;
             }
 #pragma unroll
-            for (int k = 0; k < K; ++k) row[k] = live[k] ? cand_pos[c0 + 32 * k + lane] : 0u;
+            for (int k = 0; k < K; ++k) row[k] = live[k] ? cand_pos[c0 + 32 * k + lane] : 0u;  // index entries
             float acc[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) acc[k] = 0.f;
@@ -1403,7 +1440,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
                 if (keep) {
                     const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
                     s_c[warp][slot] = static_cast<uint16_t>(32 * k + lane);
-                    s_p[warp][slot] = row[k];
+                    s_p[warp][slot] = ix.pos[row[k]];
                 }
                 m += __popc(mk);
             }
@@ -1428,6 +1465,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
         calcs = refined = updates = 0;
     }
 }
+
 
 // ------------------------------------------------------------ refine
 // One refinement wave (persistent, affinity chunks of kRefChunk candidates):
@@ -1492,7 +1530,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
         const uint64_t c1 = u64min(c0 + kRefChunk, end);
         uint64_t c = c0 + g;
         float nlb = c < c1 ? cand_lb[c] : 0.f;
-        uint32_t np = c < c1 ? cand_pos[c] : 0u;  // candidate records hold dataset rows
+        uint32_t np = c < c1 ? ix.pos[cand_pos[c]] : 0u;  // candidate records hold index entries
         // Cached pruning bound: refreshed from the BSF each refinement sees,
         // so a skipped candidate costs no memory access (a stale bound only
         // refines more).
@@ -1502,7 +1540,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_REFINE)
             const uint32_t p = np;
             if (c + kGroups < c1) {
                 nlb = cand_lb[c + kGroups];
-                np = cand_pos[c + kGroups];
+                np = ix.pos[cand_pos[c + kGroups]];
             }
             if (lb > bnd) {
                 if (leader) cand_sq[c] = INFINITY;
@@ -1577,7 +1615,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
     constexpr int kGF = tma_group_floats(n);  // row buffers per group: 2 rows, or 3 half rows
     float* s_rows = reinterpret_cast<float*>(s_dyn);                                           // [kGroups][kGF]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(kGroups) * kGF * 4);  // lane-ordered query
-    float* s_flut = reinterpret_cast<float*>(s_qd + 8 * 8 * kTq);                              // [FW][256]
+    FineLutT* s_flut = reinterpret_cast<FineLutT*>(s_qd + 8 * 8 * kTq);                        // [FW][256]
     __shared__ __align__(8) uint64_t s_bar[kGroups][3];
     __shared__ uint32_t s_c[kWarps][kChunk], s_p[kWarps][kChunk];
     __shared__ int s_sel;
@@ -1696,7 +1734,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
         }
         if (FW > 0) {
             const float4* src = reinterpret_cast<const float4*>(S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len);
-            for (int i = threadIdx.x; i < FW * 64; i += blockDim.x) reinterpret_cast<float4*>(s_flut)[i] = src[i];
+            for (int i = threadIdx.x; i < FW * 64; i += blockDim.x) store_fine_lut4(s_flut + 4 * i, src[i]);
         }
         __syncthreads();
         const uint32_t* cand_pos = S.cand_pos + q * S.cap;
@@ -1750,13 +1788,13 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
                     uint4 v[kPer];
 #pragma unroll
                     for (int k = 0; k < kPer; ++k)
-                        v[k] = kp[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws + 16 * h)
+                        v[k] = kp[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws + 16 * h)  // index order
                                      : make_uint4(0, 0, 0, 0);
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
 #pragma unroll
                         for (int k = 0; k < kPer; ++k)
-                            acc[k] = __fadd_rd(acc[k], s_flut[(16 * h + i) * 256 + byte_of(v[k], i)]);
+                            acc[k] = __fadd_rd(acc[k], fine_lut_at(s_flut, (16 * h + i) * 256 + byte_of(v[k], i)));
                 }
                 const float bnd2 = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
 #pragma unroll
@@ -1776,7 +1814,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
                 if (keep) {
                     const uint32_t slot = m + __popc(mk & ((1u << lane) - 1u));
                     s_c[warp][slot] = static_cast<uint32_t>(c);
-                    s_p[warp][slot] = rcp[k];  // candidate records hold dataset rows
+                    s_p[warp][slot] = ix.pos[rcp[k]];  // candidate records hold index entries
                 }
                 m += __popc(mk);
             }
@@ -2190,7 +2228,7 @@ __global__ void __launch_bounds__(kThreads)
         const double sq = warp_dtw_candidate<M>(s_qe, s_qe + n, s_qe + 2 * n, ix.rows + static_cast<uint64_t>(p) * n,
                                                 n, ix.window, wk, ran);
         if (lane == 0) {
-            cand_pos[e - a] = p;
+            cand_pos[e - a] = static_cast<uint32_t>(e);
             updates += publish(wk, sq, e - a, cand_sq, ~0u);
             refined += ran ? 1 : 0;
         }
@@ -2255,7 +2293,7 @@ __global__ void __launch_bounds__(kThreads)
             const bool in = c < end;
             const bool keep = in && cand_lb[c] <= bnd;
             if (in && !keep) cand_sq[c] = INFINITY;
-            const uint32_t p = keep ? cand_pos[c] : 0u;
+            const uint32_t p = keep ? ix.pos[cand_pos[c]] : 0u;
             unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
             if constexpr (M == 1) {
                 // LB_Keogh first, four candidates at a time (one per 8-lane group); the
@@ -2391,7 +2429,7 @@ __global__ void __launch_bounds__(kThreads)
         const unsigned ns = wk->nseed;
         for (unsigned i = threadIdx.x; i < ns + nties; i += blockDim.x) {
             const double sv = i < ns ? cand_sq[i] : wk->tie_sq[i - ns];
-            if (sv <= lim && sqrt(sv) == dist) mine = min(mine, i < ns ? cand_pos[i] : wk->tie_row[i - ns]);
+            if (sv <= lim && sqrt(sv) == dist) mine = min(mine, i < ns ? ix.pos[cand_pos[i]] : wk->tie_row[i - ns]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
@@ -2418,7 +2456,7 @@ __global__ void __launch_bounds__(kThreads)
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (sv[u] <= lim && sqrt(sv[u]) == dist) mine = min(mine, cand_pos[cv[u]]);
+                if (sv[u] <= lim && sqrt(sv[u]) == dist) mine = min(mine, ix.pos[cand_pos[cv[u]]]);
         }
     }
 #pragma unroll
@@ -2641,7 +2679,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                          : n == 96 ? k_refine_tma<12, 32> : n == 64 ? k_refine_tma<8, 32> : n == 512 ? k_refine_tma<64, 32>
                                                                                       : nullptr;
     const bool tma_fine = fine && tma && refine_tma_fine && !std::getenv("TSG_FINE_FUSED");
-    const size_t tma_fine_bytes = tma_bytes + 32 * 256 * sizeof(float);
+    const size_t tma_fine_bytes = tma_bytes + 32 * 256 * sizeof(FineLutT);
     unsigned tma_fine_grid = 0;
     if (tma_fine) {
         set_max_smem(reinterpret_cast<const void*>(refine_tma_fine), 180 * 1024);

@@ -52,6 +52,7 @@ struct SumArgs {
     uint64_t* sort_keys;  // may be null
     uint8_t* fine;        // may be null: fine summary rows (fws bytes each)
     int fw, fws;
+    int wst, fst;         // output strides of words / fine rows (bytes): ws / fws, or a shared record stride
     uint64_t key_mask;    // sort keys keep these bits (the sorted key width)
 };
 
@@ -72,7 +73,7 @@ __device__ __forceinline__ void word_keys(const uint8_t* sym, int w, uint32_t& r
 }
 
 __device__ __forceinline__ void emit_word(const SumArgs& a, uint64_t idx, const uint8_t* wrow) {
-    uint4* dst = reinterpret_cast<uint4*>(a.words + idx * static_cast<uint64_t>(a.ws));
+    uint4* dst = reinterpret_cast<uint4*>(a.words + idx * static_cast<uint64_t>(a.wst));
     const uint4* src = reinterpret_cast<const uint4*>(wrow);
     dst[0] = src[0];
     if (a.ws == 32) dst[1] = src[1];
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kSumThreads, 2)
                 const unsigned b3 = __shfl_down_sync(0xFFFFFFFFu, sym, 3);
                 const uint64_t idx = a.out_base + first + ser;
                 if (ok && (g & 3) == 0)
-                    reinterpret_cast<uint32_t*>(a.words + idx * 16)[g >> 2] = sym | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                    reinterpret_cast<uint32_t*>(a.words + idx * a.wst)[g >> 2] = sym | (b1 << 8) | (b2 << 16) | (b3 << 24);
                 if (ok && g == 0) {
                     if (a.sort_keys) a.sort_keys[idx] = key & a.key_mask;
                     if (a.root_keys) a.root_keys[idx] = static_cast<uint32_t>(key >> 48);
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kSumThreads, 2)
                     const unsigned u4 = __shfl_down_sync(0xFFFFFFFFu, u, 4);
                     const unsigned u6 = __shfl_down_sync(0xFFFFFFFFu, u, 6);
                     if (ok && (g & 7) == 0)
-                        *reinterpret_cast<uint4*>(a.fine + idx * a.fws + 2 * g) = make_uint4(u, u2, u4, u6);
+                        *reinterpret_cast<uint4*>(a.fine + idx * a.fst + 2 * g) = make_uint4(u, u2, u4, u6);
                 }
             }
             __syncwarp();
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kSumThreads, 2)
             unsigned f2 = 0;
             wb[ser * a.ws + g] = static_cast<uint8_t>(segment_symbol(tile, ser, g, &f2));
             if (FINE)
-                *reinterpret_cast<uint16_t*>(a.fine + (a.out_base + first + ser) * a.fws + 2 * g) =
+                *reinterpret_cast<uint16_t*>(a.fine + (a.out_base + first + ser) * a.fst + 2 * g) =
                     static_cast<uint16_t>(f2);
         }
         __syncwarp();
@@ -286,7 +287,7 @@ __global__ void k_summarise_generic(const float* __restrict__ rows, SumArgs a,
             const double mean = __ddiv_rn(sum, static_cast<double>(a.seg));
             wrow[g] = static_cast<uint8_t>(symbol_fast(thr, bins, a.bits, mean) << (8 - a.bits));
             if (a.fine) {
-                uint8_t* f = a.fine + (a.out_base + i) * a.fws + 2 * g;
+                uint8_t* f = a.fine + (a.out_base + i) * a.fst + 2 * g;
                 f[0] = static_cast<uint8_t>(fine_quant(__ddiv_rn(sa, static_cast<double>(half))));
                 f[1] = static_cast<uint8_t>(fine_quant(__ddiv_rn(sb, static_cast<double>(half))));
             }
@@ -323,7 +324,7 @@ size_t tma_smem_bytes(int R, int n, int ws) {
 
 void summarise(const float* rows, uint64_t count, int n, int w, int bits, const double* d_thr,
                uint8_t* words, uint32_t* root_keys, uint64_t* sort_keys, cudaStream_t stream, uint8_t* fine,
-               int key_bits) {
+               int key_bits, int record_stride) {
     if (count == 0) return;
     SumArgs a{};
     a.n = n;
@@ -337,6 +338,8 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
     a.fw = fine_width(n, w);
     a.fws = fine_stride(a.fw);
     a.fine = a.fw ? fine : nullptr;
+    a.wst = record_stride > 0 ? record_stride : a.ws;
+    a.fst = record_stride > 0 ? record_stride : a.fws;
     a.key_mask = key_bits >= 64 ? ~0ull : key_bits <= 0 ? 0ull : ~0ull << (64 - key_bits);
 
     int dev = 0, sms = 0;

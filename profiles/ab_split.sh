@@ -1,0 +1,7 @@
+#!/bin/bash
+# A/B (round 2): wave split fraction (TSG_REFINE_SPLIT) with the split refinement, and the fused kernel.
+mkdir -p gpurun_out
+for sp in 0.15 0.2 0.3 0.45; do
+  TSG_REFINE_SPLIT=$sp python bench.py --no-cpu-baseline --steps 20 --warmup 5 > gpurun_out/ab_split_$sp.log 2>&1
+done
+TSG_REFINE_FUSED=1 python bench.py --no-cpu-baseline --steps 20 --warmup 5 > gpurun_out/ab_split_fused.log 2>&1
