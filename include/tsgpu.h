@@ -234,6 +234,40 @@ tsg_status tsg_breakpoints(int bits, double* out256);
  * back from HBM (first device): 256 doubles in the layout of tsg_breakpoints. */
 tsg_status tsg_index_thresholds(const tsg_index* index, double* out256);
 
+/* tsidx::ValidationReport (include/tsidx/index.hpp:180-196) of the flat index.
+ * Device meaning: nodes = leaves + inner (split) nodes; the audit checks every
+ * position stored exactly once, every stored word equal to the word recomputed
+ * from its series, key / position order, one root key per leaf, leaf capacity
+ * (overflow leaves only where no key bit can split), page tiling and the exact
+ * min / max of every page / run / quad box (group and top boxes containing
+ * their children), and the fine summary against a recomputation. */
+typedef struct tsg_validation_report {
+    uint64_t nodes;
+    uint64_t inner_nodes;
+    uint64_t leaves;
+    uint64_t empty_leaves;
+    uint64_t overflow_leaves;
+    uint64_t max_depth;
+    uint64_t total_entries;
+    uint64_t leaf_fill_histogram[11]; /* 10% buckets of leaf_capacity, then overflow leaves */
+    uint64_t violation_count;
+    uint32_t n_violations;            /* messages below (the first 20 kinds found) */
+    uint32_t reserved;
+    char violations[20][160];
+    /* device extension */
+    uint64_t pages;
+    uint64_t checked_boxes;
+} tsg_validation_report;
+
+/* <- tsidx::validate_index(const Index&) (src/index.cpp:332-484). */
+tsg_status tsg_index_validate(tsg_index* index, tsg_validation_report* out);
+
+/* Test hook: overwrite n bytes at byte offset `offset` of one of the index's
+ * device arrays (first shard): 0 words, 1 positions, 2 leaf offsets, 3 page
+ * min boxes, 4 quad min boxes, 5 fine summary, 6 run max boxes, 7 group min
+ * boxes. Lets tests prove the audit catches each kind of corruption. */
+tsg_status tsg_index_debug_poke(tsg_index* index, int array, uint64_t offset, const void* bytes, uint64_t n);
+
 /* Word stride used by the device layout for a given w. */
 int tsg_word_stride(int w);
 

@@ -20,6 +20,7 @@
 #pragma once
 
 #include <cstddef>
+#include <array>
 #include <cstdint>
 #include <filesystem>
 #include <limits>
@@ -152,5 +153,25 @@ std::vector<SearchResult> exact_search_batch(const Index& index, std::span<const
 
 ApproxResult approximate_search(const Index& index, std::span<const float> query,
                                 Measure measure = Measure::ed());
+
+// <- tsidx::ValidationReport / validate_index (include/tsidx/index.hpp:180-202):
+// the device audit of the flat index (tsg_index_validate, see include/tsgpu.h).
+struct ValidationReport {
+    std::size_t nodes = 0;
+    std::size_t inner_nodes = 0;
+    std::size_t leaves = 0;
+    std::size_t empty_leaves = 0;
+    std::size_t overflow_leaves = 0;
+    std::size_t max_depth = 0;
+    std::size_t total_entries = 0;
+    std::array<std::size_t, 11> leaf_fill_histogram{};
+    std::vector<std::string> violations;  // first few, see violation_count
+    std::size_t violation_count = 0;
+
+    bool ok() const { return violation_count == 0; }
+    std::string summary() const;
+};
+
+ValidationReport validate_index(const Index& index);
 
 }  // namespace tsidx

@@ -22,6 +22,7 @@ EXPORTS = (
     "tsg_generate_random_walk", "tsg_launch_count", "tsg_profile_enable", "tsg_profile_read",
     "tsg_generate_series", "tsg_index_build_file", "tsg_search_measure",
     "tsg_comm_unique_id", "tsg_comm_init", "tsg_comm_info", "tsg_breakpoints", "tsg_index_thresholds",
+    "tsg_index_validate", "tsg_index_debug_poke",
 )
 
 TSG_TRANSPORT_NONE, TSG_TRANSPORT_LOCAL, TSG_TRANSPORT_NCCL = 0, 1, 2
@@ -58,6 +59,16 @@ class tsg_search_stats(C.Structure):
     _fields_ = [
         ("lb_node_calcs", C.c_uint64), ("lb_entry_calcs", C.c_uint64), ("real_dist_calcs", C.c_uint64),
         ("bsf_updates", C.c_uint64), ("pruned_subtrees", C.c_uint64), ("queue_insertions", C.c_uint64),
+    ]
+
+
+class tsg_validation_report(C.Structure):
+    _fields_ = [
+        ("nodes", C.c_uint64), ("inner_nodes", C.c_uint64), ("leaves", C.c_uint64), ("empty_leaves", C.c_uint64),
+        ("overflow_leaves", C.c_uint64), ("max_depth", C.c_uint64), ("total_entries", C.c_uint64),
+        ("leaf_fill_histogram", C.c_uint64 * 11), ("violation_count", C.c_uint64), ("n_violations", C.c_uint32),
+        ("reserved", C.c_uint32), ("violations", (C.c_char * 160) * 20), ("pages", C.c_uint64),
+        ("checked_boxes", C.c_uint64),
     ]
 
 
@@ -113,6 +124,8 @@ def lib() -> C.CDLL:
         "tsg_comm_info": (i32, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "tsg_breakpoints": (i32, [i32, vp]),
         "tsg_index_thresholds": (i32, [vp, vp]),
+        "tsg_index_validate": (i32, [vp, C.POINTER(tsg_validation_report)]),
+        "tsg_index_debug_poke": (i32, [vp, i32, u64, vp, u64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtsgpu.so")
 BUILD = os.path.join(PKG, "_build")
 
-CU_SOURCES = ["summarise.cu", "build.cu", "search.cu", "generate.cu", "exchange.cu", "api.cu"]
+CU_SOURCES = ["summarise.cu", "build.cu", "search.cu", "generate.cu", "exchange.cu", "audit.cu", "api.cu"]
 # host C++: (file, extra flags). breakpoints.cpp must match the reference's
 # x86-64 arithmetic (no -march, no FMA); tsidx_api.cpp is the C++20 drop-in API.
 CPP_SOURCES = [("breakpoints.cpp", ["-std=c++17"]),

@@ -898,6 +898,41 @@ tsg_status tsg_index_export(const tsg_index* ix, uint8_t* words, uint32_t* posit
     });
 }
 
+tsg_status tsg_index_validate(tsg_index* ix, tsg_validation_report* out) {
+    return guarded([&] {
+        if (!ix || !out) fail("validate_index: null argument");
+        std::lock_guard<std::mutex> lock(ix->mu);
+        std::memset(out, 0, sizeof(*out));
+        for (auto& s : ix->shards) {
+            DeviceGuard g(s.device);
+            audit_index(s, out);
+        }
+    });
+}
+
+tsg_status tsg_index_debug_poke(tsg_index* ix, int array, uint64_t offset, const void* bytes, uint64_t n) {
+    return guarded([&] {
+        if (!ix || !bytes) fail("tsg_index_debug_poke: null argument");
+        DevIndex& s = ix->shards[0];
+        DeviceGuard g(s.device);
+        void* base = nullptr;
+        uint64_t size = 0;
+        switch (array) {
+            case 0: base = s.words; size = s.N * s.ws; break;
+            case 1: base = s.pos; size = s.N * 4; break;
+            case 2: base = s.leaf_off; size = (s.L + 1) * 4; break;
+            case 3: base = s.page_lo; size = s.P * s.ws; break;
+            case 4: base = s.quad_lo; size = s.Q * s.ws; break;
+            case 5: base = s.fine; size = s.fw ? s.N * s.fws : 0; break;
+            case 6: base = s.run_hi; size = s.R * s.ws; break;
+            case 7: base = s.group_lo; size = s.NG * s.ws; break;
+            default: fail("tsg_index_debug_poke: unknown array");
+        }
+        if (!base || offset + n > size) fail("tsg_index_debug_poke: out of range");
+        TSG_CUDA(cudaMemcpy(static_cast<uint8_t*>(base) + offset, bytes, n, cudaMemcpyHostToDevice));
+    });
+}
+
 tsg_status tsg_breakpoints(int bits, double* out256) {
     return guarded([&] {
         if (bits < 1 || bits > 8) fail("tsg_breakpoints: bits must be in [1, 8]");

@@ -289,6 +289,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     int key_bits = std::min(kSortBits, ix.w * ix.bits);
     if (const char* e = std::getenv("TSG_SORT_BITS")) key_bits = std::max(ix.w, std::min(key_bits, std::atoi(e)));
     const int begin_bit = 64 - key_bits;
+    ix.key_bits = key_bits;
     const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(ix.leaf_cap, 0xFFFFFFFFull));
     const uint64_t open_cap = 2 * (N / (static_cast<uint64_t>(cap) + 1)) + 16;
     TSG_CUDA(cudaMalloc(&ix.words, N * ix.ws));

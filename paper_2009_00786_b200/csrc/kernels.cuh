@@ -7,6 +7,8 @@
 
 #include "common.cuh"
 
+struct tsg_validation_report;  // include/tsgpu.h
+
 namespace tsg {
 
 class Exchange;
@@ -26,6 +28,7 @@ struct DevIndex {
     uint64_t N = 0;           // series on this shard
     int n = 0, w = 0, bits = 0, ws = 16;
     uint64_t leaf_cap = 0;
+    int key_bits = 64;        // sort-key bits the build ordered entries by (build.cu)
     uint64_t pos_offset = 0;  // global position of local row 0
     float* rows = nullptr;    // [N][n] original order
     bool own_rows = false;
@@ -178,6 +181,9 @@ void free_search_graphs(DevIndex& ix);
 void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_queries, uint32_t nq, bool approximate,
                   struct DevResult* results, int window = -1, bool exchange = false);
 constexpr int kMaxDtwWindow = 255;  // the device DTW keeps a band diagonal in registers (8 cells per lane)
+
+// validate_index (audit.cu): adds this shard's audit to *out.
+void audit_index(DevIndex& ix, ::tsg_validation_report* out);
 
 // Input generators (not on the timed path), see generate.cu.
 enum GenKind {

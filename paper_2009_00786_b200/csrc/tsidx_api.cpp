@@ -344,4 +344,31 @@ ApproxResult approximate_search(const Index& index, std::span<const float> query
     return {r.distance, r.position};
 }
 
+ValidationReport validate_index(const Index& index) {
+    tsg_validation_report r{};
+    throw_status(tsg_index_validate(index.handle(), &r));
+    ValidationReport out;
+    out.nodes = r.nodes;
+    out.inner_nodes = r.inner_nodes;
+    out.leaves = r.leaves;
+    out.empty_leaves = r.empty_leaves;
+    out.overflow_leaves = r.overflow_leaves;
+    out.max_depth = r.max_depth;
+    out.total_entries = r.total_entries;
+    for (int i = 0; i < 11; ++i) out.leaf_fill_histogram[i] = r.leaf_fill_histogram[i];
+    out.violation_count = r.violation_count;
+    for (uint32_t i = 0; i < r.n_violations; ++i) out.violations.emplace_back(r.violations[i]);
+    return out;
+}
+
+std::string ValidationReport::summary() const {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf),
+                  "validate nodes=%zu inner=%zu leaves=%zu empty_leaves=%zu overflow_leaves=%zu max_depth=%zu "
+                  "entries=%zu violations=%zu",
+                  nodes, inner_nodes, leaves, empty_leaves, overflow_leaves, max_depth, total_entries,
+                  violation_count);
+    return buf;
+}
+
 }  // namespace tsidx

@@ -144,6 +144,41 @@ class BuildStats:
                 f"max_depth={self.max_depth}")
 
 
+@dataclasses.dataclass
+class ValidationReport:
+    """tsidx::ValidationReport (include/tsidx/index.hpp:180-196) of the device index."""
+    nodes: int = 0
+    inner_nodes: int = 0
+    leaves: int = 0
+    empty_leaves: int = 0
+    overflow_leaves: int = 0
+    max_depth: int = 0
+    total_entries: int = 0
+    leaf_fill_histogram: tuple = ()
+    violations: list = dataclasses.field(default_factory=list)
+    violation_count: int = 0
+    pages: int = 0
+    checked_boxes: int = 0
+
+    def ok(self) -> bool:
+        return self.violation_count == 0
+
+    def summary(self) -> str:
+        return (f"validate nodes={self.nodes} inner={self.inner_nodes} leaves={self.leaves} "
+                f"empty_leaves={self.empty_leaves} overflow_leaves={self.overflow_leaves} max_depth={self.max_depth} "
+                f"entries={self.total_entries} violations={self.violation_count}")
+
+
+def validate_index(index: "Index") -> ValidationReport:
+    """tsidx::validate_index (src/index.cpp:332-484): a full audit of the device index (tsg_index_validate)."""
+    r = _lib.tsg_validation_report()
+    check(lib().tsg_index_validate(index.handle, C.byref(r)))
+    return ValidationReport(r.nodes, r.inner_nodes, r.leaves, r.empty_leaves, r.overflow_leaves, r.max_depth,
+                            r.total_entries, tuple(r.leaf_fill_histogram),
+                            [r.violations[i].value.decode() for i in range(r.n_violations)], r.violation_count,
+                            r.pages, r.checked_boxes)
+
+
 def _stats_from_c(s: _lib.tsg_build_stats) -> BuildStats:
     return BuildStats(**{f: getattr(s, f) for f, _ in _lib.tsg_build_stats._fields_})
 
@@ -258,6 +293,11 @@ class Index:
         check(lib().tsg_index_export(self._h, words.ctypes.data, pos.ctypes.data, off.ctypes.data,
                                      poff.ctypes.data, lo.ctypes.data, hi.ctypes.data))
         return words, pos, off, poff, lo, hi
+
+    def debug_poke(self, array: int, offset: int, data: bytes) -> None:
+        """Test hook (tsg_index_debug_poke): overwrite bytes of one device array of the index."""
+        buf = C.create_string_buffer(bytes(data), len(data))
+        check(lib().tsg_index_debug_poke(self._h, array, offset, buf, len(data)))
 
     def thresholds(self) -> np.ndarray:
         """The 256-entry threshold table in HBM the index's kernels read (breakpoints, then +inf)."""

@@ -81,6 +81,11 @@ int main() {
     CHECK(bs.series == 20000);
     CHECK(bs.leaves >= 1 && bs.nodes >= bs.leaves);
     std::printf("%s\n", bs.kv_line().c_str());
+    // validate_index (tools/main.cpp:305-316): the audit passes and agrees with the build
+    const ValidationReport vr = validate_index(index);
+    std::printf("%s\n", vr.summary().c_str());
+    CHECK(vr.ok());
+    CHECK(vr.total_entries == 20000 && vr.leaves == bs.leaves && vr.nodes == bs.nodes);
 
     for (std::size_t k = 0; k < queries.count; ++k) {
         const auto q = queries.series(k);
