@@ -264,8 +264,9 @@ tsg_status tsg_index_validate(tsg_index* index, tsg_validation_report* out);
 
 /* Test hook: overwrite n bytes at byte offset `offset` of one of the index's
  * device arrays (first shard): 0 words, 1 positions, 2 leaf offsets, 3 page
- * min boxes, 4 quad min boxes, 5 fine summary, 6 run max boxes, 7 group min
- * boxes. Lets tests prove the audit catches each kind of corruption. */
+ * min boxes, 4 quad boxes ((min, max) pairs of 2 x word stride bytes, from the
+ * first min), 5 fine summary, 6 run boxes (pairs, from the first max), 7
+ * group min boxes. Lets tests prove the audit catches each kind of corruption. */
 tsg_status tsg_index_debug_poke(tsg_index* index, int array, uint64_t offset, const void* bytes, uint64_t n);
 
 /* Word stride used by the device layout for a given w. */

@@ -203,10 +203,8 @@ void free_shard(DevIndex& s) {
     cudaFree(s.thr);
     cudaFree(s.words);
     cudaFree(s.fine);
-    cudaFree(s.run_lo);
-    cudaFree(s.run_hi);
+    cudaFree(s.run_lo);  // run_hi / quad_hi point into the same pair arrays
     cudaFree(s.quad_lo);
-    cudaFree(s.quad_hi);
     cudaFree(s.pos);
     cudaFree(s.leaf_off);
     // page arrays come from the stream-ordered pool (build.cu)
@@ -922,9 +920,9 @@ tsg_status tsg_index_debug_poke(tsg_index* ix, int array, uint64_t offset, const
             case 1: base = s.pos; size = s.N * 4; break;
             case 2: base = s.leaf_off; size = (s.L + 1) * 4; break;
             case 3: base = s.page_lo; size = s.P * s.ws; break;
-            case 4: base = s.quad_lo; size = s.Q * s.ws; break;
+            case 4: base = s.quad_lo; size = s.Q * 2 * s.ws; break;
             case 5: base = s.fine; size = s.fw ? s.N * s.fws : 0; break;
-            case 6: base = s.run_hi; size = s.R * s.ws; break;
+            case 6: base = s.run_hi; size = s.R * 2 * s.ws - s.ws; break;
             case 7: base = s.group_lo; size = s.NG * s.ws; break;
             default: fail("tsg_index_debug_poke: unknown array");
         }

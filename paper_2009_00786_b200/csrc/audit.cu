@@ -210,7 +210,7 @@ __global__ void k_audit_small_boxes(const uint8_t* __restrict__ words, uint64_t 
         const uint32_t a = static_cast<uint32_t>(r * span);
         const uint64_t end = (r + 1) * span;
         const uint32_t b = static_cast<uint32_t>(end < N ? end : N);
-        if (!box_exact(words, w, ws, a, b, lo + r * ws, hi + r * ws)) report(c, kind, r);
+        if (!box_exact(words, w, ws, a, b, lo + r * 2 * ws, hi + r * 2 * ws)) report(c, kind, r);  // (min, max) pairs
         atomicAdd(&c->boxes, 1ull);
     }
 }

@@ -97,14 +97,14 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
                 mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xFFFFFFFFu, mx.w, o));
                 if (o == 2 && (lane & 3) == 0 && in) {
                     const uint64_t q = i / kQuad;
-                    *reinterpret_cast<uint4*>(quad_lo + q * ws + 16 * h) = mn;
-                    *reinterpret_cast<uint4*>(quad_hi + q * ws + 16 * h) = mx;
+                    *reinterpret_cast<uint4*>(quad_lo + q * 2 * ws + 16 * h) = mn;
+                    *reinterpret_cast<uint4*>(quad_hi + q * 2 * ws + 16 * h) = mx;
                 }
             }
             if ((lane & 15) == 0 && in) {
                 const uint64_t r = i / kRun;
-                *reinterpret_cast<uint4*>(run_lo + r * ws + 16 * h) = mn;
-                *reinterpret_cast<uint4*>(run_hi + r * ws + 16 * h) = mx;
+                *reinterpret_cast<uint4*>(run_lo + r * 2 * ws + 16 * h) = mn;
+                *reinterpret_cast<uint4*>(run_hi + r * 2 * ws + 16 * h) = mx;
             }
         }
     }
@@ -297,11 +297,11 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_CUDA(cudaMalloc(&ix.pos, N * sizeof(uint32_t)));
     TSG_CUDA(cudaMalloc(&ix.leaf_off, (N + 1) * 4));
     ix.R = (N + kRun - 1) / kRun;
-    TSG_CUDA(cudaMalloc(&ix.run_lo, ix.R * ix.ws));
-    TSG_CUDA(cudaMalloc(&ix.run_hi, ix.R * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.run_lo, ix.R * 2 * ix.ws));  // (min, max) pairs
+    ix.run_hi = ix.run_lo + ix.ws;
     ix.Q = (N + kQuad - 1) / kQuad;
-    TSG_CUDA(cudaMalloc(&ix.quad_lo, ix.Q * ix.ws));
-    TSG_CUDA(cudaMalloc(&ix.quad_hi, ix.Q * ix.ws));
+    TSG_CUDA(cudaMalloc(&ix.quad_lo, ix.Q * 2 * ix.ws));  // (min, max) pairs
+    ix.quad_hi = ix.quad_lo + ix.ws;
     // pos_in / bstart are reused for the L+1 page counts / bases (L <= N).
     // K1 output: words and fine rows interleaved in 64-byte records when both fit (w <= 16, fine
     // width 32), else separate arrays.

@@ -52,11 +52,16 @@ struct DevIndex {
     uint8_t* top_lo = nullptr;      // [NT][ws] per-segment min symbol of groups [kGroup t, kGroup t + kGroup)
     uint8_t* top_hi = nullptr;      // [NT][ws] per-segment max symbol
     uint64_t NT = 0;                // ceil(NG / kGroup): the level above groups
-    uint8_t* run_lo = nullptr;      // [R][ws] per-segment min symbol of entries [kRun r, kRun r + kRun)
-    uint8_t* run_hi = nullptr;      // [R][ws] per-segment max symbol
+    // Run and quad boxes are stored as (min, max) pairs, 2 ws bytes per box
+    // (run_hi = run_lo + ws, stride 2 ws): a run's four quad boxes are one
+    // 128-byte line, and B200 fetches a whole 128-byte line from HBM for any
+    // random read (profiles/micro/dram_granularity.cu), so separate min / max
+    // arrays would pull two lines per run, each half used.
+    uint8_t* run_lo = nullptr;      // [R] pairs: per-segment min symbol of entries [kRun r, kRun r + kRun)
+    uint8_t* run_hi = nullptr;      // run_lo + ws: per-segment max symbol (interior pointer)
     uint64_t R = 0;                 // ceil(N / kRun)
-    uint8_t* quad_lo = nullptr;     // [Q][ws] per-segment min symbol of entries [kQuad q, kQuad q + kQuad)
-    uint8_t* quad_hi = nullptr;     // [Q][ws] per-segment max symbol
+    uint8_t* quad_lo = nullptr;     // [Q] pairs: per-segment min symbol of entries [kQuad q, kQuad q + kQuad)
+    uint8_t* quad_hi = nullptr;     // quad_lo + ws: per-segment max symbol (interior pointer)
     uint64_t Q = 0;                 // ceil(N / kQuad)
     uint64_t P = 0;
     uint64_t root_children = 0;

@@ -1007,8 +1007,8 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     }
 #pragma unroll
                     for (int h = 0; h < H; ++h) {
-                        rl[u][h] = ok[u] ? ld_stream_u4(ix.run_lo + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-                        rh[u][h] = ok[u] ? ld_stream_u4(ix.run_hi + r * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                        rl[u][h] = ok[u] ? ld_stream_u4(ix.run_lo + r * 2 * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                        rh[u][h] = ok[u] ? ld_stream_u4(ix.run_hi + r * 2 * WS + 16 * h) : make_uint4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
@@ -1216,8 +1216,8 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         uint4 bl[H], bh[H];
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            bl[h] = ok ? ld_stream_u4(ix.quad_lo + static_cast<uint64_t>(qd) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
-            bh[h] = ok ? ld_stream_u4(ix.quad_hi + static_cast<uint64_t>(qd) * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            bl[h] = ok ? ld_stream_u4(ix.quad_lo + static_cast<uint64_t>(qd) * 2 * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+            bh[h] = ok ? ld_stream_u4(ix.quad_hi + static_cast<uint64_t>(qd) * 2 * WS + 16 * h) : make_uint4(0, 0, 0, 0);
         }
         rh += take;
         const bool pass = ok && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
@@ -1281,8 +1281,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
                 s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
                 if (TSG_PREFETCH) {  // the run's quad boxes are read a few drains later
                     const uint64_t qd0 = static_cast<uint64_t>(run.x / kRun) * (kRun / kQuad);
-                    prefetch_l2_bytes(ix.quad_lo + qd0 * WS, (kRun / kQuad) * WS);
-                    prefetch_l2_bytes(ix.quad_hi + qd0 * WS, (kRun / kQuad) * WS);
+                    prefetch_l2_bytes(ix.quad_lo + qd0 * 2 * WS, (kRun / kQuad) * 2 * WS);  // the run's 128-byte line
                 }
             }
             rt += __popc(m);

@@ -85,9 +85,9 @@ def test_audit_catches_a_broken_leaf(oracle):
 def test_audit_catches_box_corruption(oracle):
     r = _corrupt(oracle, 3, 16 * 2 + 1, bytes([0xFF]))  # a page min above its words
     assert any("page 2: box is not the min / max" in v for v in r.violations), r.violations
-    r = _corrupt(oracle, 4, 16 * 7 + 0, bytes([0xFF]))
+    r = _corrupt(oracle, 4, 32 * 7 + 0, bytes([0xFF]))  # quad boxes are (min, max) pairs
     assert any("quad 7: box is not the min / max" in v for v in r.violations), r.violations
-    r = _corrupt(oracle, 6, 16 * 1 + 9, bytes([0x00]))
+    r = _corrupt(oracle, 6, 32 * 1 + 9, bytes([0x00]))
     assert any("run 1: box is not the min / max" in v for v in r.violations), r.violations
     r = _corrupt(oracle, 7, 16 * 0 + 4, bytes([0xFF]))
     assert any("not contained in its parent" in v for v in r.violations), r.violations
