@@ -333,6 +333,74 @@ def run_reference(args):
         sys.exit(f"parity: the reference's answers differ from the golden answers ({parity})")
 
 
+def timed_batches(tg, index, queries, nq, measure=None, warm=1):
+    """Queries/s of device-resident query batches through the public API (CUDA events), plus the
+    summed per-query statistics and the answers."""
+    import torch
+
+    measure = measure or tg.Measure.ed()
+    nb = queries.shape[0] // nq
+    for b in range(min(warm, nb)):
+        tg.exact_search_batch_records(index, queries[b * nq:(b + 1) * nq], measure)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    res = [tg.exact_search_batch_records(index, queries[b * nq:(b + 1) * nq], measure) for b in range(warm, nb)]
+    ev1.record()
+    torch.cuda.synchronize()
+    sec = ev0.elapsed_time(ev1) * 1e-3
+    rec = np.concatenate(res)
+    return (nb - warm) * nq / sec, rec
+
+
+def other_configs(args, tg, index, count, n, seed):
+    """Secondary BASELINE configs, measured after the headline line's numbers (1 GPU; they are not
+    the headline, and their parity is covered by tests/test_gpu_parity.py at sizes the oracle
+    finishes): config 5's query-difficulty / batch sweep on the c2 index, then configs 3 and 4
+    (the c2 data and index are freed first)."""
+    import torch
+
+    out = {"note": "secondary configs (BASELINE.json configs[2..4]), device-resident queries, CUDA events; "
+                   "not the headline"}
+    sweep = []
+    for sigma in (0.01, 0.1, 0.5, 1.0):
+        for nq in (1, 64, 1024):
+            if nq == 1 and sigma >= 0.5:
+                continue  # hard single queries take seconds each: covered by batch 64 / 1024
+            total = nq * (2 if nq >= 1024 else 4 if nq == 64 else 40)
+            q = tg.generate_device("c5", total, n, 5, begin=0, noise=sigma, data_count=count, data_seed=seed)
+            qps, rec = timed_batches(tg, index, q, nq)
+            refined = float(rec["stats"][:, 2].astype(np.float64).mean())
+            sweep.append({"sigma": sigma, "batch": nq, "queries_per_s": round(qps, 1),
+                          "pruning_ratio": round(1 - refined / count, 6), "refined_rows_per_query": round(refined, 1)})
+            del q
+    out["c5"] = {"workload": workload_text("c5", count, n, "sigma"), "sweep": sweep}
+    return out
+
+
+def other_configs_c3_c4(tg):
+    import torch
+
+    res = {}
+    for name in ("c3", "c4"):
+        dkind, count, n, seed = CONFIGS[name]["data"]
+        qkind, qseed, _ = CONFIGS[name]["queries"]
+        rows = tg.generate_device(dkind, count, n, seed)
+        q = tg.generate_device(qkind, 4 * 100, n, qseed, begin=count)
+        index = tg.build_index(rows, tg.IndexConfig(n=n))
+        bs = index.build_stats()
+        qps, rec = timed_batches(tg, index, q, 100)
+        refined = float(rec["stats"][:, 2].astype(np.float64).mean())
+        res[name] = {"workload": workload_text(name, count, n), "queries_per_s": round(qps, 1),
+                     "build_mseries_s": round(count / (bs.build_ns * 1e-9) / 1e6, 1),
+                     "build_ms": round(bs.build_ns * 1e-6, 2), "pruning_ratio": round(1 - refined / count, 6),
+                     "timed_queries": 300}
+        index.free()
+        del rows, q, index
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -586,6 +654,16 @@ def run_ours(args):
             "generate_s": round(gen_s, 2),
             "cpu_baseline": cpu,
         }
+        if world == 1 and args.config == "c2" and not args.no_other_configs:
+            try:  # secondary configs: reported inside the line, never failing the headline
+                extra = other_configs(args, tg, index, count, n, seed)
+                index.free()
+                del rows, qdev
+                torch.cuda.empty_cache()
+                extra.update(other_configs_c3_c4(tg))
+                line["other_configs"] = extra
+            except Exception as ex:
+                line["other_configs"] = {"error": str(ex)[:300]}
         print(json.dumps(line), flush=True)
     index.free()
     if world > 1:
@@ -654,6 +732,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per step (default: the config's 100)")
     ap.add_argument("--sigma", type=float, default=0.1, help="c5 query noise")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the secondary configs (c5 sweep on the c2 index, c3, c4) reported in other_configs")
     ap.add_argument("--dtw", type=int, default=-1, help="search under Measure::dtw(window) (SURVEY 8(f)#4)")
     ap.add_argument("--ingest", type=int, default=0,
                     help="instead of the search bench: build from a file of this many series (SURVEY 8(f)#3)")

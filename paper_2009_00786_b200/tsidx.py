@@ -320,6 +320,9 @@ class Index:
         if getattr(self, "_h", None):
             self._lib.tsg_index_free(self._h)
             self._h = None
+        if self._keepalive is not None:  # a borrowed device dataset can be released by the caller now
+            self._keepalive = None
+            self._data = None
 
     def __del__(self):
         self.free()
