@@ -122,7 +122,7 @@ def peaks():
     return 6650.0, "fallback"
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "round1h_ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "round2_ncu_summary.json")
 NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tma.ncu-rep"],
                "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
 
@@ -130,7 +130,7 @@ NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tm
 def ncu_traffic(kernel, nq):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per batch (all its launches of one
     batch: both waves for lbscan / refine), from the committed `ncu --set full` capture of the c2
-    bench command (profiles/ncu_round1h.sh); None when the capture does not match this run."""
+    bench command (profiles/ncu_round2.sh); None when the capture does not match this run."""
     if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
         return None
     with open(NCU_SUMMARY) as f:
@@ -580,8 +580,10 @@ def run_ours(args):
     # DRAM bytes per batch of the same kernel from the committed ncu capture (c2, 1 GPU only)
     traffic = ncu_traffic(dom, nq) if args.config == "c2" and world == 1 and nq == 100 else None
 
-    # build K1 roofline: read 4n, write the 16-byte word + 8-byte sort key per series
-    k1_bytes = count * (4 * n + 16 + 8 + fw) / world
+    # build K1 roofline: read 4n, write the 8-byte sort key and the word + fine row (one 64-byte
+    # record per series when the fine summary is 32 wide, else 16-byte word + fine row)
+    k1_rec = 64 if fw == 32 else 16 + fw
+    k1_bytes = count * (4 * n + 8 + k1_rec) / world
     k1_gbs = k1_bytes / k1_s / 1e9
     algo_build = count * (4 * n + 16 + 4)  # N(4n + w + 4)
 
@@ -640,7 +642,7 @@ def run_ours(args):
                                    "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                                    "frac": round(k1_gbs / hbm, 4),
                                    "traffic": ncu_traffic("summarise", nq) if args.config == "c2" and world == 1 else None,
-                                   "algorithmic_bytes_per_series": 4 * n + 24 + fw},
+                                   "algorithmic_bytes_per_series": 4 * n + 8 + k1_rec},
                       "whole_build_frac": round(algo_build / build_dev_s / 1e9 / hbm / world, 4),
                       "leaves": bs.leaves, "pages": P, "root_children": bs.root_children, "max_depth": bs.max_depth,
                       "overflow_leaves": bs.overflow_leaves},

@@ -63,7 +63,8 @@ def read_report(path):
 
 
 SETUP = ("k_generate",)  # input generation: untimed setup
-QUERY = ("k_prepare", "k_seed", "k_groups", "k_bound", "k_lbscan", "k_refine", "k_refine_tma", "k_finalize")
+QUERY = ("k_prepare", "k_seed", "k_groups", "k_bound", "k_lbscan", "k_refine", "k_refine_tma", "k_finalize",
+         "k_pack_bsf", "k_import_bsf", "k_merge_results")
 
 
 def read_launches(path):
