@@ -70,20 +70,31 @@ __global__ void k_gather_words(const uint8_t* __restrict__ src, const uint32_t* 
     static_assert(kRun == 16 && kQuad == 4, "quad / run boxes are 4- / 16-lane reductions");
     const int lane = threadIdx.x & 31;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t w0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u); w0 < n; w0 += stride) {
+    const int H = ws / 16, FH = fine_src ? fws / 16 : 0;  // 16-byte pieces of a word / fine row (<= 2 each)
+    // the next iteration's position is loaded one iteration ahead, and every gathered piece of an
+    // entry is requested before anything is stored (each is one random 128-byte line)
+    uint64_t w0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + (threadIdx.x & ~31u);
+    uint64_t p_next = w0 + lane < n ? pos[w0 + lane] : 0;
+    for (; w0 < n; w0 += stride) {
         const uint64_t i = w0 + lane;
         const bool in = i < n;
-        const uint64_t p = in ? pos[i] : 0;
-        if (fine_src && in)
-            for (int h = 0; h < fws / 16; ++h)
-                *reinterpret_cast<uint4*>(fine_dst + i * fws + 16 * h) =
-                    *reinterpret_cast<const uint4*>(fine_src + p * fine_src_stride + 16 * h);
-        for (int h = 0; h < ws / 16; ++h) {
-            uint4 x = make_uint4(0, 0, 0, 0);
-            if (in) {
-                x = *reinterpret_cast<const uint4*>(src + p * src_stride + 16 * h);
-                *reinterpret_cast<uint4*>(dst + i * ws + 16 * h) = x;
-            }
+        const uint64_t p = p_next;
+        p_next = w0 + stride + lane < n ? pos[w0 + stride + lane] : 0;
+        uint4 wv[2], fv[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            wv[h] = in && h < H ? *reinterpret_cast<const uint4*>(src + p * src_stride + 16 * h) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            if (h < FH && in) fv[h] = *reinterpret_cast<const uint4*>(fine_src + p * fine_src_stride + 16 * h);
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            if (h < FH && in) *reinterpret_cast<uint4*>(fine_dst + i * fws + 16 * h) = fv[h];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h >= H) break;
+            const uint4 x = wv[h];
+            if (in) *reinterpret_cast<uint4*>(dst + i * ws + 16 * h) = x;
             uint4 mn = in ? x : make_uint4(~0u, ~0u, ~0u, ~0u), mx = x;
 #pragma unroll
             for (int o = 1; o < 16; o <<= 1) {

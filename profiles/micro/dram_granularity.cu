@@ -39,6 +39,20 @@ __global__ void k_rand(const uint4* __restrict__ buf, uint64_t n16, uint64_t acc
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+template <int BYTES>
+__global__ void k_rand_write(uint4* __restrict__ buf, uint64_t n16, uint64_t accesses, unsigned* out) {
+    constexpr int V = BYTES >= 16 ? BYTES / 16 : 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < accesses; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t blk = mix(i * 0x9E3779B97F4A7C15ull + 7 * BYTES) % (n16 / V);
+        if (BYTES < 16) {
+            reinterpret_cast<unsigned*>(buf + blk)[0] = (unsigned)i;
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v) buf[blk * V + v] = make_uint4((unsigned)i, v, 0, 0);
+        }
+    }
+}
+
 int main() {
     const uint64_t bytes = 16ull << 30;  // 16 GB: far larger than L2
     uint4* buf;
@@ -51,7 +65,7 @@ int main() {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    auto run = [&](auto kernel, int size) {
+    auto run = [&](auto kernel, int size) {  // (reads and writes alike)
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(a);
             kernel<<<grid, 256>>>(buf, n16, acc, out);
@@ -68,6 +82,11 @@ int main() {
     run(k_rand<32>, 32);
     run(k_rand<64>, 64);
     run(k_rand<128>, 128);
+    run(k_rand_write<4>, 4);
+    run(k_rand_write<16>, 16);
+    run(k_rand_write<32>, 32);
+    run(k_rand_write<64>, 64);
+    run(k_rand_write<128>, 128);
     cudaFree(buf);
     return 0;
 }
