@@ -72,7 +72,7 @@ enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
 #define TSG_MINB_REFINE 4
 #endif
 #ifndef TSG_MINB_BOUND
-#define TSG_MINB_BOUND 4
+#define TSG_MINB_BOUND 5  // 4 until round 2; 5 since the run box pairs (bound 8.31 -> 8.17 us/query, ab_tune2.sh)
 #endif
 // w = 16 box bounds clamp with the native u16x2 min/max (0: byte-SIMD __vmaxu4 / __vminu4)
 #ifndef TSG_BOX_U16
