@@ -613,3 +613,28 @@ def test_file_built_index_answers_equal_scan(oracle, tmp_path):
         d, p = oracle.scan_nn(rows, queries[k], 0)
         assert (r.position, r.distance) == (p, d), k
     index.free()
+
+
+def test_device_inputs_are_checked(oracle):
+    """CUDA-tensor inputs must be float32, 2-D and on the index's device (read by the library on its
+    own stream after torch's current stream is synchronised): anything else fails loudly instead of
+    being reinterpreted."""
+    import torch
+
+    rows = oracle.generate(2000, 64, 3)
+    index = tg.build_index(rows, tg.IndexConfig(n=64, leaf_capacity=50))
+    q = torch.from_numpy(oracle.generate(3, 64, 4)).cuda()
+    with pytest.raises(tg.InvalidArgument, match="float32"):
+        tg.exact_search_batch(index, q.double())
+    with pytest.raises(tg.InvalidArgument, match="float32"):
+        tg.exact_search_batch_records(index, q.half())
+    with pytest.raises(tg.InvalidArgument, match="float32"):
+        tg.build_index(torch.from_numpy(rows).cuda().double(), tg.IndexConfig(n=64))
+    # a non-contiguous view is copied (on torch's stream) and still answers exactly
+    qq = torch.cat([q, q], dim=1)[:, ::2].contiguous()[:, :64]
+    res = tg.exact_search_batch(index, torch.cat([q, q], dim=0)[::2])
+    for k, r in enumerate(res):
+        d, p = oracle.scan_nn(rows, torch.cat([q, q], dim=0)[::2][k].cpu().numpy(), 0)
+        assert (r.position, r.distance) == (p, d)
+    del qq
+    index.free()
