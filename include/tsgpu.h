@@ -10,7 +10,10 @@
  *                               include/tsidx/index.hpp:158, src/index.cpp:258-318
  *   tsg_search               <- tsidx::exact_search(const Index&, span<const float>,
  *                               Measure, SearchOptions)  include/tsidx/query.hpp:150-151,
- *                               src/query.cpp:258-298 (Measure::ed() only)
+ *                               src/query.cpp:258-298 (Measure::ed(); any Measure:
+ *                               tsg_search_measure)
+ *   tsg_index_validate       <- tsidx::validate_index  include/tsidx/index.hpp:202,
+ *                               src/index.cpp:332-484
  *   tsg_approximate_search   <- tsidx::approximate_search  include/tsidx/query.hpp:133-134
  *   tsg_config               <- tsidx::IndexConfig          include/tsidx/config.hpp:12-32
  *   tsg_config_validate      <- IndexConfig::validate       src/config.cpp:22-35

@@ -12,11 +12,13 @@
 //   SearchStats, SearchOptions,
 //   SearchResult, ApproxResult,
 //   exact_search, approximate_search include/tsidx/query.hpp:17-151
+//   ValidationReport, validate_index include/tsidx/index.hpp:180-202
 //
 // Error contract as in the reference: std::invalid_argument for bad
 // configs/inputs, std::logic_error, std::runtime_error for device failures.
-// Differences: Measure::dtw is rejected (the device path is
-// Euclidean), workers/queues/mode options are accepted and ignored, w <= 32.
+// Differences: Measure::dtw is answered on the device for windows
+// <= 255 (larger windows: std::invalid_argument, no CPU fallback),
+// workers/queues/mode options are accepted and ignored, w <= 32.
 #pragma once
 
 #include <cstddef>
