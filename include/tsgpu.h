@@ -82,8 +82,8 @@ typedef struct tsg_build_stats {
     uint64_t pages;           /* leaf pages (<= 128 entries each): the device LB / work unit */
     uint64_t h2d_ns;          /* host->device copy of the rows (0 for device input) */
     double summarise_ms;      /* K1 */
-    double organise_ms;       /* K2 sort + gather */
-    double leaves_ms;         /* K3 leaf partition + boxes */
+    double organise_ms;       /* K2 sort */
+    double leaves_ms;         /* K2 gather (side stream) overlapped with K3 leaves / pages / boxes */
 } tsg_build_stats;
 
 /* tsidx::SearchStats (include/tsidx/query.hpp:17-27). Device meaning:

@@ -322,7 +322,11 @@ void build_shard(DevIndex& s, const float* rows, bool host_rows, uint64_t N, con
                  uint64_t pos_offset, uint64_t* h2d_ns, double ms[3], const FileRows* file = nullptr) {
     DeviceGuard g(s.device);
     check_device(s.device);
-    TSG_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    // the shard's stream has the highest priority: work the library puts on side streams (the
+    // build's gather) yields SMs to it at block granularity
+    int prio_least = 0, prio_greatest = 0;
+    TSG_CUDA(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    TSG_CUDA(cudaStreamCreateWithPriority(&s.stream, cudaStreamNonBlocking, prio_greatest));
     TSG_CUDA(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, s.device));
     if (const char* e = std::getenv("TSG_L2_FETCH")) {  // A/B: L2 fetch granularity hint (bytes)
         TSG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e))));

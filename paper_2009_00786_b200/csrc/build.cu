@@ -385,12 +385,36 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_LAUNCHED();
     TSG_CUDA(cub::DeviceRadixSort::SortPairs(temp.p, tb_sort, keys_in.as<uint64_t>(), keys_out.as<uint64_t>(),
                                              pos_in.as<uint32_t>(), ix.pos, static_cast<int64_t>(N), begin_bit, 64, st));
-    k_gather_words<<<grid_for(N, 256, sms), 256, 0, st>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, ix.run_lo,
-                                                          ix.run_hi, ix.quad_lo, ix.quad_hi, N, ix.ws,
-                                                          !ix.fw ? nullptr : rec64 ? words_orig.as<uint8_t>() + 16
-                                                                                   : fine_orig.as<uint8_t>(),
-                                                          ix.fine, ix.fws, wst, fst);
+    // The gather (bandwidth-bound: one random 128-byte line per entry) runs on a second stream,
+    // overlapped with K3's latency-bound leaf splitting, which needs only the sorted keys; the
+    // page boxes wait for it.
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t sorted_ev = nullptr, gathered_ev = nullptr;
+    TSG_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    TSG_CUDA(cudaEventCreateWithFlags(&sorted_ev, cudaEventDisableTiming));
+    TSG_CUDA(cudaEventCreateWithFlags(&gathered_ev, cudaEventDisableTiming));
+    struct StreamGuard {
+        cudaStream_t s;
+        cudaEvent_t a, b;
+        ~StreamGuard() {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } st2_guard{st2, sorted_ev, gathered_ev};
+    TSG_CUDA(cudaEventRecord(sorted_ev, st));
+    TSG_CUDA(cudaStreamWaitEvent(st2, sorted_ev, 0));
+    // one 256-entry piece per block (short blocks, so K3's kernels on the higher-priority shard
+    // stream get SMs as gather blocks retire)
+    const unsigned gather_grid = static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 0x7FFFFFFFull));
+    k_gather_words<<<gather_grid, 256, 0, st2>>>(words_orig.as<uint8_t>(), ix.pos, ix.words, ix.run_lo,
+                                                 ix.run_hi, ix.quad_lo, ix.quad_hi, N, ix.ws,
+                                                 !ix.fw ? nullptr : rec64 ? words_orig.as<uint8_t>() + 16
+                                                                          : fine_orig.as<uint8_t>(),
+                                                 ix.fine, ix.fws, wst, fst);
     TSG_LAUNCHED();
+    TSG_CUDA(cudaEventRecord(gathered_ev, st2));
     TSG_CUDA(cudaEventRecord(ev[2], st));
 
     // K3 leaves. Root subtrees = runs of equal root key (top w key bits).
@@ -481,6 +505,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     k_page_key<<<grid_for(ix.P, 256, sms), 256, 0, st>>>(keys, ix.page_off, ix.P, ix.page_key);
     TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpy2DAsync(ix.page_dir, 8, ix.page_key, 256 * 8, 8, ndir, cudaMemcpyDeviceToDevice, st));
+    TSG_CUDA(cudaStreamWaitEvent(st, gathered_ev, 0));  // words and run boxes are in index order
     k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.run_lo, ix.page_off, ix.P, ix.ws,
                                                               ix.page_lo, ix.page_hi);
     TSG_LAUNCHED();
