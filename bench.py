@@ -130,6 +130,26 @@ NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tm
                "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
 
 
+def ncu_binding(kernel):
+    """The binding on-chip resource of a query kernel from the committed ncu capture: the L1/LSU
+    data pipe's wavefronts (shared-memory table lookups + global loads) as a fraction of peak, time-
+    weighted over the kernel's launches of one batch."""
+    if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
+        return None
+    with open(NCU_SUMMARY) as f:
+        reps = json.load(f)["reports"]
+    recs = [r for name in NCU_REPORTS[kernel] for r in reps.get(name, [])]
+    if not recs or any("lsu_pipe_pct" not in r for r in recs):
+        return None
+    t = sum(r["time_us"] for r in recs)
+    lsu = sum(r["lsu_pipe_pct"] * r["time_us"] for r in recs) / t / 100
+    shared = sum(r["lsu_shared_pct"] * r["time_us"] for r in recs) / t / 100
+    dram = sum(r["dram_pct_peak"] * r["time_us"] for r in recs) / t / 100
+    return {"resource": "L1/LSU data pipe wavefronts (shared-memory table lookups + global loads)",
+            "frac": round(lsu, 3), "shared_part": round(shared, 3), "dram_frac_of_ncu_peak": round(dram, 3),
+            "source": os.path.relpath(NCU_SUMMARY, ROOT)}
+
+
 def ncu_traffic(kernel, nq):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per batch (all its launches of one
     batch: both waves for lbscan / refine), from the committed `ncu --set full` capture of the c2
@@ -628,7 +648,8 @@ def run_ours(args):
                          "per_kernel_us_per_query": {g: round(v * 1e3 / nqt, 2) for g, v in group_ms.items()},
                          "per_slot_us_per_query": [round(v * 1e3 / nqt, 2) for v in prof_ms],
                          "profiled_pass_s": round(prof_s, 4),
-                         "lbscan_smem": smem_roof},
+                         "lbscan_smem": smem_roof,
+                         "binding": ncu_binding(dom) if args.config == "c2" and world == 1 and nq == 100 else None},
             "flat_scan_roofline": None if flat is None else {
                 "formula": "SURVEY 8(d): N*w + C_min*4n bytes per query",
                 "bytes_per_query": round(flat["bytes_per_query"]), "mean_cmin": round(flat["mean_cmin"], 1),

@@ -30,6 +30,8 @@ METRICS = [
     ("stall_barrier", "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", 1.0),
     ("stall_wait", "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", 1.0),
     ("smem_bank_conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", 1.0),
+    ("lsu_pipe_pct", "l1tex__data_pipe_lsu_wavefronts.sum.pct_of_peak_sustained_elapsed", 1.0),
+    ("lsu_shared_pct", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", 1.0),
     ("inst_executed", "smsp__inst_executed.sum", 1.0),
 ]
 
