@@ -430,9 +430,9 @@ __device__ __forceinline__ unsigned long long publish(QueryWork* wk, double s, u
     return atomicMin(&wk->bsf_bits, sb) > sb ? 1 : 0;
 }
 
-// A (min, max) box pair of a w <= 16 word (32 contiguous bytes, 32-byte aligned) in one 256-bit
-// load: one request per lane instead of two, half the L1 wavefronts of the box loads (the box
-// filters are bound by the L1/LSU data pipe).
+// A (min, max) box pair of a w <= 16 word, or a 32-byte fine row (32 contiguous bytes, 32-byte
+// aligned), in one 256-bit load: one request per lane instead of two, half the L1 wavefronts of
+// those loads (the box filters are bound by the L1/LSU data pipe).
 __device__ __forceinline__ void ld_box_pair(const uint8_t* p, uint4& lo, uint4& hi) {
     asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
@@ -1802,17 +1802,37 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
 #pragma unroll
                 for (int k = 0; k < kPer; ++k) acc[k] = 0.f;
 #pragma unroll
-                for (int h = 0; h < FW / 16; ++h) {
-                    uint4 v[kPer];
+                if constexpr (FW == 32) {
+                    // a 32-byte fine row (index order) in one 256-bit load: one L1 wavefront per row
+                    uint4 va[kPer], vb[kPer];
 #pragma unroll
-                    for (int k = 0; k < kPer; ++k)
-                        v[k] = kp[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws + 16 * h)  // index order
-                                     : make_uint4(0, 0, 0, 0);
+                    for (int k = 0; k < kPer; ++k) {
+                        va[k] = vb[k] = make_uint4(0, 0, 0, 0);
+                        if (kp[k]) ld_box_pair(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws, va[k], vb[k]);
+                    }
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
 #pragma unroll
                         for (int k = 0; k < kPer; ++k)
-                            acc[k] = __fadd_rd(acc[k], fine_lut_at(s_flut, (16 * h + i) * 256 + byte_of(v[k], i)));
+                            acc[k] = __fadd_rd(acc[k], fine_lut_at(s_flut, i * 256 + byte_of(va[k], i)));
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+#pragma unroll
+                        for (int k = 0; k < kPer; ++k)
+                            acc[k] = __fadd_rd(acc[k], fine_lut_at(s_flut, (16 + i) * 256 + byte_of(vb[k], i)));
+                } else {
+                    for (int h = 0; h < FW / 16; ++h) {
+                        uint4 v[kPer];
+#pragma unroll
+                        for (int k = 0; k < kPer; ++k)
+                            v[k] = kp[k] ? ld_stream_u4(ix.fine + static_cast<uint64_t>(rcp[k]) * ix.fws + 16 * h)  // index order
+                                         : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+#pragma unroll
+                            for (int k = 0; k < kPer; ++k)
+                                acc[k] = __fadd_rd(acc[k], fine_lut_at(s_flut, (16 * h + i) * 256 + byte_of(v[k], i)));
+                    }
                 }
                 const float bnd2 = bound_from_bits(ld_volatile_u64(&wk->bsf_bits));
 #pragma unroll
