@@ -193,8 +193,19 @@ __global__ void k_split(const Range* __restrict__ open, int level, const uint64_
     }
 }
 
+// Pages of a leaf [a, b): cut at run boundaries inside the leaf (the first page
+// ends at the kPage-th entry counted from a's run, later pages start on run
+// boundaries), so only the leaf's own two ends split a run box between pages
+// (a run shared by two pages is bounded, and its quads scanned, once per page).
+__device__ __forceinline__ uint32_t first_page_end(uint32_t a, uint32_t b) {
+    return min(b, a / kRun * kRun + kPage);
+}
+
 __global__ void k_page_count(const uint32_t* __restrict__ leaf_off, uint64_t L, uint32_t* __restrict__ count) {
-    GRID_STRIDE(l, L) count[l] = (leaf_off[l + 1] - leaf_off[l] + kPage - 1) / kPage;
+    GRID_STRIDE(l, L) {
+        const uint32_t a = leaf_off[l], b = leaf_off[l + 1], e = first_page_end(a, b);
+        count[l] = 1 + (b - e + kPage - 1) / kPage;
+    }
 }
 
 __global__ void k_page_write(const uint32_t* __restrict__ leaf_off, uint64_t L, const uint32_t* __restrict__ base,
@@ -202,7 +213,7 @@ __global__ void k_page_write(const uint32_t* __restrict__ leaf_off, uint64_t L, 
     GRID_STRIDE(l, L) {
         const uint32_t a = leaf_off[l], b = leaf_off[l + 1];
         uint32_t k = base[l];
-        for (uint32_t s = a; s < b; s += kPage, ++k) {
+        for (uint32_t s = a; s < b; s = s == a ? first_page_end(a, b) : s + kPage, ++k) {
             page_off[k] = s;
             page_leaf[k] = static_cast<uint32_t>(l);
         }
