@@ -72,36 +72,46 @@ __device__ __forceinline__ uint32_t root_key(const uint8_t* word, int w) {
     return r;
 }
 
+// Structure of the entries (positions in range and counted, symbol bits, order).
 __global__ void k_audit_entries(const uint8_t* __restrict__ words, const uint32_t* __restrict__ pos, uint64_t N,
-                                int w, int ws, int bits, int key_bits, const uint8_t* __restrict__ rederived,
-                                const uint8_t* __restrict__ fine, const uint8_t* __restrict__ fine_rederived, int fw,
-                                int fws, unsigned* __restrict__ seen, AuditCounters* c) {
+                                int w, int ws, int bits, int key_bits, unsigned* __restrict__ seen, AuditCounters* c) {
     const unsigned low_mask = bits >= 8 ? 0u : (1u << (8 - bits)) - 1u;
     AUDIT_STRIDE(i, N) {
         const uint32_t p = pos[i];
         const uint8_t* wi = words + i * ws;
-        if (p >= N) {
-            report(c, kPosRange, i);
-        } else {
-            atomicAdd(&seen[p], 1u);
-            const uint8_t* wr = rederived + static_cast<uint64_t>(p) * ws;
-            bool same = true;
-            for (int g = 0; g < w; ++g) same = same && wi[g] == wr[g];
-            if (!same) report(c, kWordMismatch, p);
-            if (fine) {
-                bool fsame = true;
-                const uint8_t* fi = fine + i * fws;
-                const uint8_t* fr = fine_rederived + static_cast<uint64_t>(p) * fws;
-                for (int g = 0; g < fw; ++g) fsame = fsame && fi[g] == fr[g];
-                if (!fsame) report(c, kFineMismatch, p);
-            }
-        }
+        if (p >= N) report(c, kPosRange, i);
+        else atomicAdd(&seen[p], 1u);
         bool clean = true;
         for (int g = 0; g < w; ++g) clean = clean && (wi[g] & low_mask) == 0;
         if (!clean) report(c, kSymbolBits, i);
         if (i + 1 < N) {
             const uint64_t ka = sort_key(wi, w, key_bits), kb = sort_key(wi + ws, w, key_bits);
             if (ka > kb || (ka == kb && pos[i + 1] <= p)) report(c, kOrder, i);
+        }
+    }
+}
+
+// Stored words / fine rows of the entries whose series lies in [p0, p1) against
+// the re-derivation of those series (one chunk of positions at a time, so the
+// audit's scratch stays bounded on a 100M-series index).
+__global__ void k_audit_words(const uint8_t* __restrict__ words, const uint32_t* __restrict__ pos, uint64_t N, int w,
+                              int ws, uint64_t p0, uint64_t p1, const uint8_t* __restrict__ rederived,
+                              const uint8_t* __restrict__ fine, const uint8_t* __restrict__ fine_rederived, int fw,
+                              int fws, AuditCounters* c) {
+    AUDIT_STRIDE(i, N) {
+        const uint64_t p = pos[i];
+        if (p < p0 || p >= p1) continue;
+        const uint8_t* wi = words + i * ws;
+        const uint8_t* wr = rederived + (p - p0) * ws;
+        bool same = true;
+        for (int g = 0; g < w; ++g) same = same && wi[g] == wr[g];
+        if (!same) report(c, kWordMismatch, p);
+        if (fine) {
+            bool fsame = true;
+            const uint8_t* fi = fine + i * fws;
+            const uint8_t* fr = fine_rederived + (p - p0) * fws;
+            for (int g = 0; g < fw; ++g) fsame = fsame && fi[g] == fr[g];
+            if (!fsame) report(c, kFineMismatch, p);
         }
     }
 }
@@ -264,21 +274,28 @@ void audit_index(DevIndex& s, tsg_validation_report* out) {
     fr.p.push_back(c);
     TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&seen), N * sizeof(unsigned), st));
     fr.p.push_back(seen);
-    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rw), N * s.ws, st));
+    // re-derivation chunk: at most 8M series (128 MB of words, 256 MB of fine rows)
+    const uint64_t chunk = std::min<uint64_t>(N, 8ull << 20);
+    TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rw), chunk * s.ws, st));
     fr.p.push_back(rw);
     if (s.fw) {
-        TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rf), N * s.fws, st));
+        TSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rf), chunk * s.fws, st));
         fr.p.push_back(rf);
     }
     AuditCounters init{};
     for (auto& f : init.first) f = ~0ull;
     TSG_CUDA(cudaMemcpyAsync(c, &init, sizeof(init), cudaMemcpyHostToDevice, st));
     TSG_CUDA(cudaMemsetAsync(seen, 0, N * sizeof(unsigned), st));
-    // the re-derivation: K1 over the rows in dataset order
-    summarise(s.rows, N, s.n, s.w, s.bits, s.thr, rw, nullptr, nullptr, st, rf);
     const int sms = s.sms;
-    k_audit_entries<<<audit_grid(N, sms), 256, 0, st>>>(s.words, s.pos, N, s.w, s.ws, s.bits, s.key_bits, rw, s.fw ? s.fine : nullptr,
-                                                        rf, s.fw, s.fws, seen, c);
+    // the re-derivation: K1 over the rows in dataset order, chunk by chunk
+    for (uint64_t p0 = 0; p0 < N; p0 += chunk) {
+        const uint64_t cnt = std::min(chunk, N - p0);
+        summarise(s.rows + p0 * s.n, cnt, s.n, s.w, s.bits, s.thr, rw, nullptr, nullptr, st, rf);
+        k_audit_words<<<audit_grid(N, sms), 256, 0, st>>>(s.words, s.pos, N, s.w, s.ws, p0, p0 + cnt, rw,
+                                                          s.fw ? s.fine : nullptr, rf, s.fw, s.fws, c);
+        TSG_LAUNCHED();
+    }
+    k_audit_entries<<<audit_grid(N, sms), 256, 0, st>>>(s.words, s.pos, N, s.w, s.ws, s.bits, s.key_bits, seen, c);
     TSG_LAUNCHED();
     k_audit_seen<<<audit_grid(N, sms), 256, 0, st>>>(seen, N, c);
     TSG_LAUNCHED();

@@ -188,7 +188,7 @@ struct LocalGroup {
     std::vector<unsigned long long*> snap;
     std::vector<uint32_t> snap_cap;
     std::vector<cudaEvent_t> packed, imported;
-    std::vector<bool> started;
+    std::vector<unsigned char> started;  // per shard, written by its own thread (not vector<bool>: no shared words)
 
     void arrive_and_wait() {
         std::unique_lock<std::mutex> lk(mu);
@@ -267,7 +267,7 @@ public:
         k_import_bsf<<<grid_for(nq), 128, 0, st>>>(work, nq, p);
         TSG_LAUNCHED();
         TSG_CUDA(cudaEventRecord(g.imported[rank], st));
-        g.started[rank] = true;
+        g.started[rank] = 1;
         g.arrive_and_wait();
     }
     void merge_results(const DevResult*, uint32_t, DevResult*, cudaStream_t) override {
@@ -327,7 +327,7 @@ std::shared_ptr<LocalGroup> make_local_group(int shards, int device) {
     g->snap_cap.assign(shards, 0);
     g->packed.assign(shards, nullptr);
     g->imported.assign(shards, nullptr);
-    g->started.assign(shards, false);
+    g->started.assign(shards, 0);
     for (int k = 0; k < shards; ++k) {
         TSG_CUDA(cudaEventCreateWithFlags(&g->packed[k], cudaEventDisableTiming));
         TSG_CUDA(cudaEventCreateWithFlags(&g->imported[k], cudaEventDisableTiming));

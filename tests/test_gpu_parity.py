@@ -577,6 +577,10 @@ def test_headline_config_answers_equal_reference_golden():
         text = "".join("%d %d %.17g\n" % (k, int(r["position"]), float(r["distance"])) for k, r in enumerate(res))
         assert hashlib.sha256(text.encode()).hexdigest() == meta["answers_sha256"]
         assert text == golden
+    # and the 100M-series index passes the full audit (chunked re-derivation of every word)
+    r = tg.validate_index(index)
+    assert r.ok(), r.violations
+    assert r.total_entries == N
     index.free()
     del rows
     torch.cuda.empty_cache()
