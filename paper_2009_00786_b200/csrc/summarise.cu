@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -53,6 +54,9 @@ struct SumArgs {
     uint8_t* fine;        // may be null: fine summary rows (fws bytes each)
     int fw, fws;
     int wst, fst;         // output strides of words / fine rows (bytes): ws / fws, or a shared record stride
+    int pad_after_fine;   // record layout: zero bytes written after each fine row (the record's tail), so
+                          // the record's last 32-byte sector is written whole (a partial sector costs a
+                          // DRAM read-modify-write: profiles/micro/dram_granularity.cu)
     uint64_t key_mask;    // sort keys keep these bits (the sorted key width)
 };
 
@@ -230,6 +234,8 @@ __global__ void __launch_bounds__(kSumThreads, 2)
                     const unsigned u6 = __shfl_down_sync(0xFFFFFFFFu, u, 6);
                     if (ok && (g & 7) == 0)
                         *reinterpret_cast<uint4*>(a.fine + idx * a.fst + 2 * g) = make_uint4(u, u2, u4, u6);
+                    if (ok && g == 8 && a.pad_after_fine == 16)
+                        *reinterpret_cast<uint4*>(a.fine + idx * a.fst + 32) = make_uint4(0, 0, 0, 0);
                 }
             }
             __syncwarp();
@@ -340,6 +346,9 @@ void summarise(const float* rows, uint64_t count, int n, int w, int bits, const 
     a.fine = a.fw ? fine : nullptr;
     a.wst = record_stride > 0 ? record_stride : a.ws;
     a.fst = record_stride > 0 ? record_stride : a.fws;
+    // 64-byte records of a 16-byte word + 32-byte fine row: 16 bytes of tail
+    static const bool no_pad = std::getenv("TSG_NO_RECORD_PAD") != nullptr;  // A/B
+    a.pad_after_fine = !no_pad && record_stride == 64 && a.ws == 16 && a.fws == 32 && a.fine ? 16 : 0;
     a.key_mask = key_bits >= 64 ? ~0ull : key_bits <= 0 ? 0ull : ~0ull << (64 - key_bits);
 
     int dev = 0, sms = 0;
