@@ -183,7 +183,10 @@ __global__ void k_audit_pages(const uint8_t* __restrict__ words, const uint32_t*
                               const uint8_t* __restrict__ group_hi, AuditCounters* c) {
     AUDIT_STRIDE(p, P) {
         const uint32_t a = page_off[p], b = page_off[p + 1], l = page_leaf[p];
-        bool tile = l < L && a < b && b - a <= kPage && (p > 0 || a == 0) && (p + 1 < P || b == N);
+        // pages tile the index, at most kPage entries each, within kPage / kRun aligned runs (the bound
+        // kernel's run items per page)
+        bool tile = l < L && a < b && b - a <= kPage && (b - 1) / kRun - a / kRun < kPage / kRun && (p > 0 || a == 0) &&
+                    (p + 1 < P || b == N);
         if (tile) {
             const uint32_t la = leaf_off[l], lb = leaf_off[l + 1];
             tile = la <= a && b <= lb && (a == la || (p > 0 && page_leaf[p - 1] == l)) &&

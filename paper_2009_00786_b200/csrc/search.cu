@@ -824,7 +824,10 @@ __global__ void __launch_bounds__(kThreads)
 // the BSF is listed, clipped to its page: run wave 0 (bound <= split x BSF,
 // front of the slot's run list) or wave 1 (back). Survivors are staged per
 // warp and written with one 64-bit atomic per flush (both waves' counts).
-constexpr int kRunsPerPage = kPage / kRun + 1;  // an unaligned page touches at most 9 runs
+// Pages are cut on run boundaries inside a leaf and the first page of a leaf ends at the kPage-th
+// entry from the start of its first run (build.cu first_page_end): every page lies within kPage /
+// kRun aligned runs (an arbitrary 128-entry window would touch 9).
+constexpr int kRunsPerPage = kPage / kRun;
 constexpr int kRunStage = 128;
 #ifndef TSG_BOUND_PL
 #define TSG_BOUND_PL 2
