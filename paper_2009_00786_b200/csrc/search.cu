@@ -524,39 +524,6 @@ __device__ __forceinline__ uint32_t claim_ahead(QueryWork* work, int q, int k) {
     return threadIdx.x == 0 ? atomicAdd(&work[q].next[k], 1u) : ~0u;
 }
 
-// Block-wide slot reservation: each thread brings two counts (< 2^16 per
-// block); returns its first slot in each of two global lists, with one
-// atomicAdd per list per block. All threads of the block must call it.
-__device__ __forceinline__ uint2 block_reserve(unsigned c0, unsigned c1, unsigned* ctr0, unsigned* ctr1) {
-    __shared__ uint32_t s_cnt[kWarps];
-    __shared__ uint32_t s_base[2];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t mine = c0 | (c1 << 16);
-    uint32_t incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_cnt[warp] = incl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t tot = 0;
-        for (int i = 0; i < kWarps; ++i) {
-            const uint32_t c = s_cnt[i];
-            s_cnt[i] = tot;
-            tot += c;
-        }
-        s_base[0] = (tot & 0xFFFFu) ? atomicAdd(ctr0, tot & 0xFFFFu) : 0u;
-        s_base[1] = (tot >> 16) && ctr1 ? atomicAdd(ctr1, tot >> 16) : 0u;
-    }
-    __syncthreads();
-    const uint32_t before = s_cnt[warp] + (incl - mine);
-    const uint2 r = make_uint2(s_base[0] + (before & 0xFFFFu), s_base[1] + (before >> 16));
-    __syncthreads();  // s_cnt / s_base are reused by the next call
-    return r;
-}
-
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
     return v;
@@ -802,8 +769,12 @@ __global__ void __launch_bounds__(kThreads)
                 keep = box_bound<H, W16>(s_lut, q4, gl, gh, ix.w) <= bound;
                 pruned += keep ? 0 : 1;
             }
-            const uint32_t at = block_reserve(keep ? 1u : 0u, 0, &wk->ngroups, nullptr).x;
-            if (keep) gsurv[at] = static_cast<uint32_t>(g);
+            // warp-aggregated reservation (one atomic per warp, no block barrier)
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+            uint32_t at = 0;
+            if ((threadIdx.x & 31) == 0 && m) at = atomicAdd(&wk->ngroups, static_cast<unsigned>(__popc(m)));
+            at = __shfl_sync(0xFFFFFFFFu, at, 0);
+            if (keep) gsurv[at + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = static_cast<uint32_t>(g);
         }
     }
     pruned = warp_sum(pruned);
