@@ -593,7 +593,7 @@ def run_ours(args):
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
     lookups = (boxes + lb_entries) * ws
     lbscan_s = group_ms["lbscan"] * 1e-3
-    smem_peak = props.multi_processor_count * sm_clock_mhz * 1e6 * 32
+    smem_peak = props.multi_processor_count * sm_clock_mhz * 1e6 * 32 * world  # all ranks' SMs
     smem_roof = {"kernel": "lbscan", "bound": "smem", "unit": "table lookups/s",
                  "achieved": lookups / lbscan_s if lbscan_s > 0 else 0.0, "peak": smem_peak,
                  "frac": round(lookups / lbscan_s / smem_peak, 4) if lbscan_s > 0 else 0.0,
@@ -638,8 +638,10 @@ def run_ours(args):
                     "d2h_bytes_per_step": nq * 72},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
-                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4),
+                         "peak": hbm * world, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / (hbm * world), 4),
+                         "peak_note": "per-GPU measured peak x ranks (achieved is the whole job's bytes / max-rank time)"
+                                      if world > 1 else "one GPU",
                          "traffic": traffic,
                          "algorithmic_bytes_per_batch": round(dom_bytes * nq),
                          "batch_queries": nq,
