@@ -164,7 +164,10 @@ tsg_status tsg_index_build(tsg_ctx* ctx, const float* host_rows, uint64_t count,
 
 /* Build from rows already resident in device memory on the context's first
  * device. The index borrows them: they must stay valid until tsg_index_free.
- * Single-device contexts only. */
+ * Single-device contexts only. Ordering: the library reads device inputs on its
+ * own non-blocking stream, so every write to them (on any stream) must have
+ * completed before the call — synchronise the producing stream first (the
+ * Python mirror synchronises torch's current stream of the tensor's device). */
 tsg_status tsg_index_build_device(tsg_ctx* ctx, const float* dev_rows, uint64_t count,
                                   uint64_t length, const tsg_config* cfg,
                                   uint64_t position_offset, tsg_index** out,
@@ -212,7 +215,8 @@ tsg_status tsg_search(tsg_index* index, const float* host_queries, uint32_t nq,
                       tsg_result* out);
 
 /* Same for queries already in device memory (first device of the index).
- * out is a HOST array. */
+ * out is a HOST array. The same ordering rule as tsg_index_build_device: the
+ * queries must be complete (producing stream synchronised) when called. */
 tsg_status tsg_search_device(tsg_index* index, const float* dev_queries, uint32_t nq,
                              tsg_result* out);
 
