@@ -66,13 +66,13 @@ enum Stat { kLbNode = 0, kLbEntry, kRealDist, kBsfUpd, kPruned, kQueueIns };
 // Resident blocks per SM the persistent kernels are compiled for (register
 // caps; -D overrides for tuning runs).
 #ifndef TSG_MINB_LBSCAN
-#define TSG_MINB_LBSCAN 5
+#define TSG_MINB_LBSCAN 4  // 5 until the block-wide query selection: with the switch stalls gone the kernel is issue-bound and 64 registers beat 40 warps (12.55 -> 12.11 us/query)
 #endif
 #ifndef TSG_MINB_REFINE
 #define TSG_MINB_REFINE 4
 #endif
 #ifndef TSG_MINB_BOUND
-#define TSG_MINB_BOUND 5  // 4 until round 2; 5 since the run box pairs (bound 8.31 -> 8.17 us/query, ab_tune2.sh)
+#define TSG_MINB_BOUND 4  // 5 while bound was latency-bound (round 2a); 4 since the block-wide query selection (7.17 -> 6.89 us/query)
 #endif
 // w = 16 box bounds clamp with the native u16x2 min/max (0: byte-SIMD __vmaxu4 / __vminu4)
 #ifndef TSG_BOX_U16
@@ -322,109 +322,12 @@ __device__ __forceinline__ float box_bound(const float* s_lut, const uint4* q4, 
     return word_bound<W16>(s_lut, c, w);
 }
 
-// --------------------------------------------- 16-bit fixed-point table
-// lbscan's copy of the [w][256] table (TSG_LUT16): entries scaled so that the
-// query's pruning bound maps to ~65000 and stored as u16 (saturating), two per
-// shared-memory bank word. A lookup is one LDS.U16 (random symbols collide on
-// half as many distinct bank words as with floats), a bound is an integer sum
-// (IADD3: two lookups per add) compared with an integer threshold.
-// Soundness: floor(t x S) <= t x S and saturation only lowers an entry, so
-// isum <= S x (float-table sum); isum > thr with thr >= bound x S (both
-// roundings up) therefore implies the float-table sum > bound. The candidate's
-// bound isum x inv (inv <= 1 / S, rounded down) is <= the float-table sum.
-// Tightness: < 1 unit per segment, w / 65000 of the bound.
-// query selection of the persistent kernels by the whole block (0: thread 0 scans serially)
-#ifndef TSG_BLOCK_SELECT
-#define TSG_BLOCK_SELECT 1
-#endif
+// ------------------------------------------------ scheduling switches
 // the refinement kernels' blocks start at queries in proportion to the queries' chunk counts (bound and
 // lbscan measured slower with it: 7.18 -> 7.43 and 12.53 -> 13.14 us/query on c2)
 #ifndef TSG_WEIGHTED_START
 #define TSG_WEIGHTED_START 1
 #endif
-#ifndef TSG_LUT16
-#define TSG_LUT16 0
-#endif
-
-struct Fix16 {
-    float scale, inv;
-    uint32_t thr;
-};
-
-__device__ __forceinline__ Fix16 fix16_of(float bound) {
-    Fix16 f;
-    if (bound < 3.0e38f) {
-        f.scale = fminf(__fdiv_rd(65000.f, fmaxf(bound, 1e-30f)), 1e30f);
-        f.inv = __fdiv_rd(1.f, f.scale);
-        f.thr = __float2uint_ru(__fmul_ru(bound, f.scale));
-    } else {  // no best-so-far yet: nothing is pruned
-        f.scale = 0.f;
-        f.inv = 0.f;
-        f.thr = 0xFFFFFFFFu;
-    }
-    return f;
-}
-
-__device__ __forceinline__ uint32_t fix16_entry(float t, float scale) {
-    return min(__float2uint_rd(__fmul_rd(t, scale)), 65535u);  // NaN -> 0, +inf -> saturated
-}
-
-__device__ __forceinline__ float fix16_bound(uint32_t isum, const Fix16& f) {
-    return __fmul_rd(__uint2float_rn(isum), f.inv);  // isum < 2^24: exact conversion
-}
-
-// load_prepared for the fixed-point copy.
-__device__ __forceinline__ void load_prepared16(const float* __restrict__ lut_g, const QueryWork* wk, int w,
-                                                uint16_t* s_lut, unsigned char* qsym, float scale) {
-    const float4* src = reinterpret_cast<const float4*>(lut_g);
-    uint2* dst = reinterpret_cast<uint2*>(s_lut);
-    for (int i = threadIdx.x; i < w * 64; i += blockDim.x) {
-        const float4 v = src[i];
-        dst[i] = make_uint2(fix16_entry(v.x, scale) | (fix16_entry(v.y, scale) << 16),
-                            fix16_entry(v.z, scale) | (fix16_entry(v.w, scale) << 16));
-    }
-    for (int i = threadIdx.x; i < kMaxW; i += blockDim.x) qsym[i] = i < w ? wk->qsym[i] : 0;
-    __syncthreads();
-}
-
-template <bool W16>
-__device__ __forceinline__ uint32_t word_bound16(const uint16_t* s_lut, const uint4* v, int w) {
-    uint32_t lb = 0;
-    if (W16) {
-#pragma unroll
-        for (int s = 0; s < 16; ++s) lb += s_lut[s * 256 + byte_of(v[0], s)];
-    } else {
-        for (int s = 0; s < w; ++s) lb += s_lut[s * 256 + byte_of(v[s >> 4], s & 15)];
-    }
-    return lb;
-}
-
-__device__ __forceinline__ uint32_t box_quad16_fix(const uint16_t* s_lut, int s0, uint32_t q, uint32_t lo, uint32_t hi) {
-    const uint32_t ce = vmin_u16x2(vmax_u16x2(q & 0x00FF00FFu, lo & 0x00FF00FFu), hi & 0x00FF00FFu);
-    const uint32_t co = vmin_u16x2(vmax_u16x2(__byte_perm(q, 0, 0x4341), __byte_perm(lo, 0, 0x4341)),
-                                   __byte_perm(hi, 0, 0x4341));
-    const char* b = reinterpret_cast<const char*>(s_lut);
-    // the upper lane shifted right by 15 is its byte offset (2 x symbol)
-    return static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(b + (s0 + 0) * 512 + ((ce << 1) & 0x1FEu))) +
-           static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(b + (s0 + 1) * 512 + ((co << 1) & 0x1FEu))) +
-           static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(b + (s0 + 2) * 512 + (ce >> 15))) +
-           static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(b + (s0 + 3) * 512 + (co >> 15)));
-}
-
-template <int H, bool W16>
-__device__ __forceinline__ uint32_t box_bound16(const uint16_t* s_lut, const uint4* q4, const uint4* lo, const uint4* hi,
-                                                int w) {
-    if constexpr (W16 && TSG_BOX_U16) {
-        return box_quad16_fix(s_lut, 0, q4[0].x, lo[0].x, hi[0].x) + box_quad16_fix(s_lut, 4, q4[0].y, lo[0].y, hi[0].y) +
-               box_quad16_fix(s_lut, 8, q4[0].z, lo[0].z, hi[0].z) + box_quad16_fix(s_lut, 12, q4[0].w, lo[0].w, hi[0].w);
-    }
-    uint4 c[H];
-#pragma unroll
-    for (int h = 0; h < H; ++h)
-        c[h] = make_uint4(__vminu4(__vmaxu4(q4[h].x, lo[h].x), hi[h].x), __vminu4(__vmaxu4(q4[h].y, lo[h].y), hi[h].y),
-                          __vminu4(__vmaxu4(q4[h].z, lo[h].z), hi[h].z), __vminu4(__vmaxu4(q4[h].w, lo[h].w), hi[h].w));
-    return word_bound16<W16>(s_lut, c, w);
-}
 
 // ---------------------------------------------------- row refinement
 struct F8 {
@@ -610,21 +513,9 @@ __device__ __forceinline__ int claim(QueryWork* work, int nq, int k, int& cur, u
     return r;
 }
 
-// Thread 0: the first query from `cur` on whose chunk counter `k` has work
-// left (-1 if none); takes no chunk (the block's warps claim their own).
-template <typename NChunks>
-__device__ __forceinline__ int select_query(QueryWork* work, int nq, int k, int cur, NChunks nchunks) {
-    int q = cur;
-    for (int tries = 0; tries < nq; ++tries) {
-        QueryWork* wk = work + q;
-        if (ld_volatile_u32(&wk->next[k]) < nchunks(wk)) return q;
-        q = q + 1 == nq ? 0 : q + 1;
-    }
-    return -1;
-}
-
-// The same choice made by the whole block at once: every thread tests one query (nq <= the
-// batch slots), the first with work in circular order from `cur` wins. A serial scan by thread 0
+// The block's next query: the first from `cur` on (circular) whose chunk counter `k` has work
+// left, -1 if none; it takes no chunk (the block's warps claim their own). The whole block
+// chooses at once: every thread tests one query (nq <= the batch slots). A serial scan by thread 0
 // costs up to nq dependent L2 round trips per query switch - tens of microseconds at the end of
 // every launch, when each block finds every query exhausted. Begins with a barrier (the previous
 // query's shared state is free afterwards) and returns the same query in every thread.
@@ -1029,7 +920,6 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     __shared__ uint2 s_pg[kWarps][kWChunk];      // the warp chunk's surviving pages
     __shared__ uint2 s_r[kWarps][kRunStage];     // staged surviving runs
     __shared__ float s_l[kWarps][kRunStage];
-    __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
@@ -1045,14 +935,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         // Query loop (block level; the only barriers): pick a query with
         // chunks left and load its table; the warps then claim chunks of it
         // on their own until it is exhausted.
-#if TSG_BLOCK_SELECT
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
-#else
-        __syncthreads();  // every warp is done with the previous query
-        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
-        __syncthreads();
-        const int q = s_sel;
-#endif
         if (q < 0) break;
         cur = q;
         QueryWork* wk = S.work + q;
@@ -1280,10 +1163,6 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     constexpr int kRing = 64;  // per-warp ring queues (entry ranges), power of two
     constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
-#if TSG_LUT16
-    uint16_t* s_lut16 = reinterpret_cast<uint16_t*>(s_lut);
-    Fix16 fx{0.f, 0.f, 0u};
-#endif
     __shared__ __align__(16) unsigned char qsym[kMaxW];
     __shared__ uint32_t s_pos[kWarps][kStageCap];
     __shared__ float s_lb[kWarps][kStageCap];
@@ -1362,16 +1241,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         qh += take;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-#if TSG_LUT16
-            const uint32_t ib = word_bound16<W16>(s_lut16, wv[k], ix.w);
-            const float lb = fix16_bound(ib, fx);
-            scanned += ok[k] ? 1 : 0;
-            stage(ok[k] && ib <= fx.thr, e[k], lb);
-#else
             const float lb = word_bound<W16>(s_lut, wv[k], ix.w);
             scanned += ok[k] ? 1 : 0;
             stage(ok[k] && lb <= bound, e[k], lb);
-#endif
         }
     };
     // Quads of up to 8 queued runs: lane 4k + u bounds quad u of run k.
@@ -1399,11 +1271,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             }
         }
         rh += take;
-#if TSG_LUT16
-        const bool pass = ok && box_bound16<H, W16>(s_lut16, q4, bl, bh, ix.w) <= fx.thr;
-#else
         const bool pass = ok && box_bound<H, W16>(s_lut, q4, bl, bh, ix.w) <= bound;
-#endif
         pruned += ok && !pass ? 1 : 0;
         boxes += ok ? 1 : 0;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
@@ -1420,26 +1288,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     // left, load its table; then every warp claims chunks of it on its own
     // (lane 0, the next claim issued while the current chunk runs) until it
     // is exhausted, drains its queues and flushes its stage.
-    __shared__ int s_sel;
     for (;;) {
-#if TSG_BLOCK_SELECT
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
-#else
-        __syncthreads();  // every warp is done with the previous query
-        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
-        __syncthreads();
-        const int q = s_sel;
-#endif
         if (q < 0) break;
         cur = q;
         wk = S.work + q;
         bound = bound_from_bits(wk->bsf_bits);
-#if TSG_LUT16
-        fx = fix16_of(bound);
-        load_prepared16(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut16, qsym, fx.scale);
-#else
         load_prepared(S.lut + static_cast<uint64_t>(q) * S.lut_len, wk, ix.w, s_lut, qsym);
-#endif
 #pragma unroll
         for (int h = 0; h < H; ++h) q4[h] = *reinterpret_cast<const uint4*>(qsym + 16 * h);
         // Page wave 0 splits its candidates into refinement waves A and B by
@@ -1540,7 +1395,6 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
     const int fw = FW > 0 ? FW : ix.fw;
     float* s_flut = reinterpret_cast<float*>(s_dyn);                                         // [fw][256]
     double* s_qd = reinterpret_cast<double*>(s_dyn + static_cast<size_t>(fw) * 256 * 4);    // [n]
-    __shared__ int s_sel;
     __shared__ uint16_t s_c[kWarps][32 * K];  // kept records: offset in the chunk
     __shared__ uint32_t s_p[kWarps][32 * K];  // and their dataset rows (pos of the entry)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1569,14 +1423,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
     cur = weighted_start(S.work, nq, cur, nchunks);
 #endif
     for (;;) {
-#if TSG_BLOCK_SELECT
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
-#else
-        __syncthreads();  // every warp is done with the previous query
-        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
-        __syncthreads();
-        const int q = s_sel;
-#endif
         if (q < 0) break;
         cur = q;
         QueryWork* wk = S.work + q;
@@ -1816,7 +1663,6 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
     FineLutT* s_flut = reinterpret_cast<FineLutT*>(s_qd + 8 * 8 * kTq);                        // [FW][256]
     __shared__ __align__(8) uint64_t s_bar[kGroups][3];
     __shared__ uint32_t s_c[kWarps][kChunk], s_p[kWarps][kChunk];
-    __shared__ int s_sel;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = threadIdx.x / kRowLanes, j8 = lane & (kRowLanes - 1);
     const int wg = lane / kRowLanes;  // group within the warp
     const int gbase = lane & ~(kRowLanes - 1);
@@ -1917,14 +1763,7 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
     cur = weighted_start(S.work, nq, cur, nchunks);
 #endif
     for (;;) {
-#if TSG_BLOCK_SELECT
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
-#else
-        __syncthreads();  // every warp is done with the previous query
-        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
-        __syncthreads();
-        const int q = s_sel;
-#endif
         if (q < 0) break;
         cur = q;
         QueryWork* wk = S.work + q;
@@ -2471,7 +2310,6 @@ template <int M>
 __global__ void __launch_bounds__(kThreads)
     k_refine_dtw(IndexView ix, SlotView S, const float* __restrict__ queries, int nq, int wave) {
     extern __shared__ float s_qe[];
-    __shared__ int s_sel;
     const int n = ix.n;
     const int lane = threadIdx.x & 31;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
@@ -2497,14 +2335,7 @@ __global__ void __launch_bounds__(kThreads)
     cur = weighted_start(S.work, nq, cur, nchunks);
 #endif
     for (;;) {
-#if TSG_BLOCK_SELECT
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
-#else
-        __syncthreads();  // every warp is done with the previous query
-        if (threadIdx.x == 0) s_sel = select_query(S.work, nq, k_next, cur, nchunks);
-        __syncthreads();
-        const int q = s_sel;
-#endif
         if (q < 0) break;
         cur = q;
         QueryWork* wk = S.work + q;
@@ -2895,8 +2726,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
         1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
                               static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
     const unsigned bound_grid = static_cast<unsigned>(sms * blocks_per_sm(bound, lut_bytes));
-    const size_t scan_lut_bytes = TSG_LUT16 ? lut_bytes / 2 : lut_bytes;  // lbscan's fixed-point copy
-    const unsigned scan_grid = static_cast<unsigned>(sms * blocks_per_sm(lbscan, scan_lut_bytes));
+    const unsigned scan_grid = static_cast<unsigned>(sms * blocks_per_sm(lbscan, lut_bytes));
     const unsigned refine_grid = tma ? static_cast<unsigned>(sms * blocks_per_sm(refine_tma, tma_bytes))
                                      : static_cast<unsigned>(sms * blocks_per_sm(refine, qd_bytes));
     const unsigned fin_x = std::max(1u, std::min(256u, static_cast<unsigned>(sms * 32 / nq)));
@@ -2972,7 +2802,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
                         TSG_LAUNCHED();
                     });
                 mark(4, [&] {
-                    lbscan<<<scan_grid, kThreads, scan_lut_bytes, st>>>(iv, sv, inq, wave);
+                    lbscan<<<scan_grid, kThreads, lut_bytes, st>>>(iv, sv, inq, wave);
                     TSG_LAUNCHED();
                 });
                 mark(wave == 0 ? 3 : 5, [&] {
