@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
-    unsigned long long pruned = 0, nodes = 0;
+    uint32_t pruned = 0, nodes = 0;  // per lane and query
     int cnt = 0;
     auto nchunks = [pass](const QueryWork* wk) -> uint32_t {
         if (wk->overflow) return 0;
@@ -1082,11 +1082,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         // leave the query: the stage and the counters
         if (cnt) flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
         cnt = 0;
-        pruned = warp_sum(pruned);
-        nodes = warp_sum(nodes);
+        const unsigned long long pr = warp_sum(static_cast<unsigned long long>(pruned));
+        const unsigned long long nd = warp_sum(static_cast<unsigned long long>(nodes));
         if (lane == 0) {
-            if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
-            if (nodes) atomicAdd(&wk->stats[kLbNode], nodes);
+            if (pr) atomicAdd(&wk->stats[kPruned], pr);
+            if (nd) atomicAdd(&wk->stats[kLbNode], nd);
         }
         pruned = nodes = 0;
     }
@@ -1095,6 +1095,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 // ------------------------------------------------------------ lbscan
 
 constexpr int kStageCap = 256;
+#ifndef TSG_SCAN_QK
+#define TSG_SCAN_QK 2
+#endif
 
 // Writes a warp's staged candidates: refinement wave A (bound <= cut) grows
 // upward after the seed range, wave B downward from the top of the slot's
@@ -1161,6 +1164,7 @@ template <int WS, bool W16>
 __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     k_lbscan(IndexView ix, SlotView S, int nq, int wave) {
     constexpr int kRing = 64;  // per-warp ring queues (entry ranges), power of two
+    constexpr int kQK = TSG_SCAN_QK;  // words per lane per drain (at most 8 kQK - 1 + 32 quads queue: kQK <= 4)
     constexpr int H = WS / 16;
     extern __shared__ float s_lut[];
     __shared__ __align__(16) unsigned char qsym[kMaxW];
@@ -1180,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     const float* surv_lb = nullptr;
     int cnt = 0;
     uint32_t rh = 0, rt = 0, qh = 0, qt = 0;  // ring heads / tails (warp-uniform)
-    unsigned long long scanned = 0, pruned = 0, boxes = 0;
+    uint32_t scanned = 0, pruned = 0, boxes = 0;  // per lane and query (32-bit: one add per count in the hot loops)
     const int k_next = wave == 0 ? kNextScan0 : kNextScan1;
     auto nchunks = [wave](const QueryWork* w) -> uint32_t {
         if (w->overflow) return 0;
@@ -1191,13 +1195,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
         if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
         cnt = 0;
-        scanned = warp_sum(scanned);
-        pruned = warp_sum(pruned);
-        boxes = warp_sum(boxes);
+        const unsigned long long sc = warp_sum(static_cast<unsigned long long>(scanned));
+        const unsigned long long pr = warp_sum(static_cast<unsigned long long>(pruned));
+        const unsigned long long bx = warp_sum(static_cast<unsigned long long>(boxes));
         if (lane == 0) {
-            if (scanned) atomicAdd(&wk->stats[kLbEntry], scanned);
-            if (pruned) atomicAdd(&wk->stats[kPruned], pruned);
-            if (boxes) atomicAdd(&wk->boxes, boxes);
+            if (sc) atomicAdd(&wk->stats[kLbEntry], sc);
+            if (pr) atomicAdd(&wk->stats[kPruned], pr);
+            if (bx) atomicAdd(&wk->boxes, bx);
         }
         scanned = pruned = boxes = 0;
     };
@@ -1217,14 +1221,14 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             cnt = 0;
         }
     };
-    // Words of up to 16 queued quads: lane 4k + u takes entry u of quads k and k + 8.
+    // Words of up to 8 kQK queued quads: lane 4j + u takes entry u of quads j, j + 8, ...
     auto drain_quads = [&]() {
-        const uint32_t take = min(qt - qh, 16u);
-        uint4 wv[2][H];
-        uint32_t e[2];
-        bool ok[2];
+        const uint32_t take = min(qt - qh, 8u * kQK);
+        uint4 wv[kQK][H];
+        uint32_t e[kQK];
+        bool ok[kQK];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kQK; ++k) {
             const uint32_t qi = 8 * k + (lane >> 2);
             ok[k] = false;
             e[k] = 0;
@@ -1240,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         }
         qh += take;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < kQK; ++k) {
             const float lb = word_bound<W16>(s_lut, wv[k], ix.w);
             scanned += ok[k] ? 1 : 0;
             stage(ok[k] && lb <= bound, e[k], lb);
@@ -1281,7 +1285,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         }
         qt += __popc(m);
         __syncwarp();
-        while (qt - qh >= 16) drain_quads();
+        while (qt - qh >= 8u * kQK) drain_quads();
     };
 
     // Query loop (block level; the only barriers): pick a query with chunks
