@@ -125,15 +125,20 @@ def peaks():
     return 6650.0, "fallback"
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "round2c_ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "round2d_ncu_summary.json")
 NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tma.ncu-rep"],
                "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
 
 
+RANDOM_BW = os.path.join(ROOT, "profiles", "micro", "random_bw_b200.json")
+
+
 def ncu_binding(kernel):
-    """The binding on-chip resource of a query kernel from the committed ncu capture: the L1/LSU
-    data pipe's wavefronts (shared-memory table lookups + global loads) as a fraction of peak, time-
-    weighted over the kernel's launches of one batch."""
+    """What binds a query kernel, from the committed ncu capture, time-weighted over the kernel's
+    launches of one batch: the issue slots (the kernels are instruction-issue-bound since the
+    query-switch stalls were removed), the L1/LSU data pipe and shared-memory part of it, and the
+    DRAM side against the RANDOM-LINE rate of this B200 (profiles/micro/random_bw.cu): the reads
+    are scattered 128-byte lines, which HBM3e serves at ~4.7 TB/s, not at the sequential peak."""
     if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
         return None
     with open(NCU_SUMMARY) as f:
@@ -142,18 +147,27 @@ def ncu_binding(kernel):
     if not recs or any("lsu_pipe_pct" not in r for r in recs):
         return None
     t = sum(r["time_us"] for r in recs)
+    issue = sum(r["issue_active_pct"] * r["time_us"] for r in recs) / t / 100
     lsu = sum(r["lsu_pipe_pct"] * r["time_us"] for r in recs) / t / 100
     shared = sum(r["lsu_shared_pct"] * r["time_us"] for r in recs) / t / 100
     dram = sum(r["dram_pct_peak"] * r["time_us"] for r in recs) / t / 100
-    return {"resource": "L1/LSU data pipe wavefronts (shared-memory table lookups + global loads)",
-            "frac": round(lsu, 3), "shared_part": round(shared, 3), "dram_frac_of_ncu_peak": round(dram, 3),
-            "source": os.path.relpath(NCU_SUMMARY, ROOT)}
+    out = {"resource": "instruction issue slots (smsp__issue_active), time-weighted over the batch's launches",
+           "frac": round(issue, 3), "lsu_data_pipe_frac": round(lsu, 3), "lsu_shared_part": round(shared, 3),
+           "dram_frac_of_ncu_peak": round(dram, 3), "source": os.path.relpath(NCU_SUMMARY, ROOT)}
+    if os.path.exists(RANDOM_BW):
+        with open(RANDOM_BW) as f:
+            peak = json.load(f)["random_line_peak_gbs"]
+        gbs = sum(r.get("dram_read_MB", 0.0) + r.get("dram_write_MB", 0.0) for r in recs) * 1e-3 / (t * 1e-6)
+        out["dram_random_line"] = {"achieved_gbs": round(gbs, 1), "peak_gbs": peak, "frac": round(gbs / peak, 3),
+                                   "peak_def": "random 128-byte line reads over a 4-32 GB span, CUDA events",
+                                   "source": os.path.relpath(RANDOM_BW, ROOT)}
+    return out
 
 
 def ncu_traffic(kernel, nq):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per batch (all its launches of one
     batch: both waves for lbscan / refine), from the committed `ncu --set full` capture of the c2
-    bench command (profiles/ncu_round2c.sh); None when the capture does not match this run."""
+    bench command (profiles/ncu_round2d.sh); None when the capture does not match this run."""
     if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
         return None
     with open(NCU_SUMMARY) as f:
