@@ -2493,10 +2493,21 @@ __global__ void __launch_bounds__(kThreads)
     if (!overflow && nties <= kTieCap) {
         // every row that can be the answer is in the seed range or the tie list: block 0 decides
         if (blockIdx.x != 0) return;
-        const unsigned ns = wk->nseed;
-        for (unsigned i = threadIdx.x; i < ns + nties; i += blockDim.x) {
-            const double sv = i < ns ? cand_sq[i] : wk->tie_sq[i - ns];
-            if (sv <= lim && sqrt(sv) == dist) mine = min(mine, i < ns ? ix.pos[cand_pos[i]] : wk->tie_row[i - ns]);
+        // four records per thread per step, loads first (a dependent-load chain per step otherwise)
+        const unsigned ns = wk->nseed, total = ns + nties;
+        for (unsigned i0 = threadIdx.x; i0 < total; i0 += 4 * blockDim.x) {
+            double sv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned i = i0 + u * blockDim.x;
+                sv[u] = i >= total ? INFINITY : i < ns ? cand_sq[i] : wk->tie_sq[i - ns];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned i = i0 + u * blockDim.x;
+                if (sv[u] <= lim && sqrt(sv[u]) == dist)
+                    mine = min(mine, i < ns ? ix.pos[cand_pos[i]] : wk->tie_row[i - ns]);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mine = min(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, o));
