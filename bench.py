@@ -183,16 +183,62 @@ def ncu_traffic(kernel, nq):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle-reason sampling during the timed region (B200_PROFILING.md clocks
+    line). NVML is initialised BEFORE the region and polled from a thread every 5 ms: starting
+    an `nvidia-smi -lms` process inside a 50 ms region perturbed it (its driver initialisation cost
+    the device-query pass up to 3%); nvidia-smi remains the fallback when pynvml is missing."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.nvml = None
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.max_mhz = 0.0
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            # CUDA_VISIBLE_DEVICES remaps indices: resolve the torch device through its PCI bus id
+            try:
+                import torch
+
+                bus = torch.cuda.get_device_properties(device).pci_bus_id
+                dom = torch.cuda.get_device_properties(device).pci_domain_id
+                dev_id = torch.cuda.get_device_properties(device).pci_device_id
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(f"{dom:08X}:{bus:02X}:{dev_id:02X}.0".encode())
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.nvml = pynvml
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                try:
+                    rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle))
+                except Exception:
+                    rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle))
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        if self.nvml:
+            import threading
+
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -203,6 +249,10 @@ class Clocks:
 
     def __exit__(self, *a):
         self.lines = []
+        if self.nvml:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -211,7 +261,17 @@ class Clocks:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nvml:
+            nv = self.nvml
+            bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+            for mhz, rs in self.samples:
+                sm.append(mhz)
+                reasons.update(n for n, b in bits.items() if rs & b)
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz or None,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 5 ms polling"}
         for l in getattr(self, "lines", []):
             parts = [p.strip() for p in l.split(",")]
             if len(parts) < 7:
@@ -221,11 +281,11 @@ class Clocks:
                 mx = max(mx, float(parts[2]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[3:7]):
+            for n, v in zip(self.NAMES, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 def dist_setup():

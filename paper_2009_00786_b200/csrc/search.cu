@@ -536,14 +536,48 @@ __device__ __forceinline__ int select_query_block(QueryWork* work, int nq, int k
     return cur + t >= nq ? cur + t - nq : cur + t;
 }
 
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+
+// Blocks a launch needs: with little work in the batch (one easy query: a few chunks) a full
+// persistent grid only costs - every block loads the query's table and polls the same counters -
+// so a launch with fewer chunks than kMinChunks per block retires its surplus blocks at once
+// (c5 sigma 0.01 / 0.1: batch 1 10.1K -> 10.9K / 6.6K -> 7.3K q/s, batch 8 55.6K -> 62.3K / 36K;
+// 8 chunks per block was slower from batch 8 up). Returns the number of active blocks (0 in a
+// surplus block, which returns at once) and sets the uniform start query over the active blocks.
+// Ends with a barrier.
+#ifndef TSG_MIN_CHUNKS
+#define TSG_MIN_CHUNKS 1
+#endif
+constexpr unsigned kMinChunks = TSG_MIN_CHUNKS;  // chunks per active block
+template <typename NChunks>
+__device__ __forceinline__ unsigned active_blocks(const QueryWork* work, int nq, NChunks nchunks, int& cur) {
+    __shared__ unsigned long long s_total;
+    if (threadIdx.x == 0) s_total = 0;
+    __syncthreads();
+    unsigned long long mine = 0;
+    for (int t = threadIdx.x; t < nq; t += blockDim.x) mine += nchunks(work + t);
+    mine = warp_sum(mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_total, mine);
+    __syncthreads();
+    const unsigned long long want = (s_total + kMinChunks - 1) / kMinChunks;
+    const unsigned active = static_cast<unsigned>(min(static_cast<unsigned long long>(gridDim.x), max(want, 1ull)));
+    if (blockIdx.x >= active) return 0;
+    cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / active);
+    return active;
+}
+
 // A block's first query, weighted by the queries' chunk counts: block b starts at the query
-// where the running chunk total crosses (b + 1/2) / gridDim.x of all chunks, so every query gets
+// where the running chunk total crosses (b + 1/2) / active blocks of all chunks, so every query gets
 // blocks in proportion to its work and most blocks stay with one query for the whole launch
 // (a uniform start leaves the blocks of easy queries switching through the batch). Up to
 // kWeightedMax queries (else `fallback`). Ends with a barrier.
 constexpr int kWeightedMax = 256;
 template <typename NChunks>
-__device__ __forceinline__ int weighted_start(const QueryWork* work, int nq, int fallback, NChunks nchunks) {
+__device__ __forceinline__ int weighted_start(const QueryWork* work, int nq, int fallback, unsigned active,
+                                              NChunks nchunks) {
     __shared__ uint32_t s_w[kWeightedMax];
     __shared__ int s_start;
     if (nq < 2 || nq > kWeightedMax || nq > static_cast<int>(blockDim.x)) return fallback;
@@ -560,7 +594,7 @@ __device__ __forceinline__ int weighted_start(const QueryWork* work, int nq, int
         }
         const unsigned long long total = __shfl_sync(0xFFFFFFFFu, incl, 31);
         // the first query whose inclusive prefix exceeds the block's target
-        const unsigned long long target = total * (2ull * blockIdx.x + 1) / (2ull * gridDim.x);
+        const unsigned long long target = total * (2ull * blockIdx.x + 1) / (2ull * active);
         const bool here = total > 0 && incl > target && incl - mine <= target;
         if (lane == 0) s_start = fallback;
         __syncwarp();
@@ -584,11 +618,6 @@ __device__ __forceinline__ int weighted_start(const QueryWork* work, int nq, int
 // Thread 0 reserves the block's next chunk of query q (read by the next claim).
 __device__ __forceinline__ uint32_t claim_ahead(QueryWork* work, int q, int k) {
     return threadIdx.x == 0 ? atomicAdd(&work[q].next[k], 1u) : ~0u;
-}
-
-__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    return v;
 }
 
 // ----------------------------------------------------------- prepare
@@ -931,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
         const uint32_t items = pass == 0 ? wk->ngroups * static_cast<uint32_t>(kGroup) : wk->ndefer;
         return (items + kWChunk - 1) / kWChunk;
     };
+    if (!active_blocks(S.work, nq, nchunks, cur)) return;
     for (;;) {
         // Query loop (block level; the only barriers): pick a query with
         // chunks left and load its table; the warps then claim chunks of it
@@ -1292,6 +1322,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     // left, load its table; then every warp claims chunks of it on its own
     // (lane 0, the next claim issued while the current chunk runs) until it
     // is exhausted, drains its queues and flushes its stage.
+    if (!active_blocks(S.work, nq, nchunks, cur)) return;
     for (;;) {
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
         if (q < 0) break;
@@ -1423,8 +1454,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_FINE)
         return static_cast<uint32_t>((e - b + 32 * K - 1) / (32 * K));
     };
     unsigned long long calcs = 0, refined = 0, updates = 0;
+    const unsigned active = active_blocks(S.work, nq, nchunks, cur);
+    if (!active) return;
 #if TSG_WEIGHTED_START
-    cur = weighted_start(S.work, nq, cur, nchunks);
+    cur = weighted_start(S.work, nq, cur, active, nchunks);
 #endif
     for (;;) {
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
@@ -1763,8 +1796,10 @@ __global__ void __launch_bounds__(kThreads, FW > 0 ? TSG_MINB_TMA_FINE : TSG_MIN
         __syncwarp(gmask);  // the buffer is free again
         return sum;
     };
+    const unsigned active = active_blocks(S.work, nq, nchunks, cur);
+    if (!active) return;
 #if TSG_WEIGHTED_START
-    cur = weighted_start(S.work, nq, cur, nchunks);
+    cur = weighted_start(S.work, nq, cur, active, nchunks);
 #endif
     for (;;) {
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
@@ -2335,8 +2370,10 @@ __global__ void __launch_bounds__(kThreads)
         return static_cast<uint32_t>((e - b + 31) / 32);
     };
     unsigned long long refined = 0, updates = 0;
+    const unsigned active = active_blocks(S.work, nq, nchunks, cur);
+    if (!active) return;
 #if TSG_WEIGHTED_START
-    cur = weighted_start(S.work, nq, cur, nchunks);
+    cur = weighted_start(S.work, nq, cur, active, nchunks);
 #endif
     for (;;) {
         const int q = select_query_block(S.work, nq, k_next, cur, nchunks);
@@ -2740,8 +2777,14 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
                               static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
-    const unsigned bound_grid = static_cast<unsigned>(sms * blocks_per_sm(bound, lut_bytes));
-    const unsigned scan_grid = static_cast<unsigned>(sms * blocks_per_sm(lbscan, lut_bytes));
+    // TSG_GRID_CAP (A/B runs): blocks per SM of the persistent kernels
+    static const int grid_cap = [] {
+        const char* e = std::getenv("TSG_GRID_CAP");
+        return e ? std::max(1, std::atoi(e)) : 1 << 20;
+    }();
+    auto capped = [&](int b) { return static_cast<unsigned>(sms * std::min(b, grid_cap)); };
+    const unsigned bound_grid = capped(blocks_per_sm(bound, lut_bytes));
+    const unsigned scan_grid = capped(blocks_per_sm(lbscan, lut_bytes));
     const unsigned refine_grid = tma ? static_cast<unsigned>(sms * blocks_per_sm(refine_tma, tma_bytes))
                                      : static_cast<unsigned>(sms * blocks_per_sm(refine, qd_bytes));
     const unsigned fin_x = std::max(1u, std::min(256u, static_cast<unsigned>(sms * 32 / nq)));
@@ -2761,7 +2804,7 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     unsigned tma_fine_grid = 0;
     if (tma_fine) {
         set_max_smem(reinterpret_cast<const void*>(refine_tma_fine), 180 * 1024);
-        tma_fine_grid = static_cast<unsigned>(sms * blocks_per_sm(refine_tma_fine, tma_fine_bytes));
+        tma_fine_grid = capped(blocks_per_sm(refine_tma_fine, tma_fine_bytes));
     }
     unsigned fine_grid = 0;
     if (fine) {
