@@ -842,30 +842,45 @@ __global__ void __launch_bounds__(kThreads)
             else pruned += 1;
         }
         __syncthreads();
-        // groups of the surviving tops: one per thread
+        // groups of the surviving tops: kGP per thread per step, loads first, and one warp-
+        // aggregated reservation per step (one item per step was a dependent chain of a box load
+        // and an atomic's round trip: groups + bound 6.60 -> 6.31 us per c2 query)
         const unsigned items = s_ntop * kGroup;
-        for (unsigned i0 = 0; i0 < items; i0 += kThreads) {
-            const unsigned i = i0 + threadIdx.x;
-            uint64_t g = ix.NG;
-            if (i < items) g = static_cast<uint64_t>(s_top[i / kGroup]) * kGroup + i % kGroup;
-            bool keep = false;
-            if (g < ix.NG) {
-                uint4 gl[H], gh[H];
+        const unsigned lane = threadIdx.x & 31, below = (1u << lane) - 1u;
+        for (unsigned i0 = 0; i0 < items; i0 += kThreads * kGP) {
+            uint64_t g[kGP];
+            uint4 gl[kGP][H], gh[kGP][H];
+#pragma unroll
+            for (int k = 0; k < kGP; ++k) {
+                const unsigned i = i0 + k * kThreads + threadIdx.x;
+                g[k] = i < items ? static_cast<uint64_t>(s_top[i / kGroup]) * kGroup + i % kGroup : ix.NG;
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    gl[h] = ld_stream_u4(ix.group_lo + g * WS + 16 * h);
-                    gh[h] = ld_stream_u4(ix.group_hi + g * WS + 16 * h);
+                    gl[k][h] = g[k] < ix.NG ? ld_stream_u4(ix.group_lo + g[k] * WS + 16 * h) : make_uint4(0, 0, 0, 0);
+                    gh[k][h] = g[k] < ix.NG ? ld_stream_u4(ix.group_hi + g[k] * WS + 16 * h) : make_uint4(0, 0, 0, 0);
                 }
-                nodes += 1;
-                keep = box_bound<H, W16>(s_lut, q4, gl, gh, ix.w) <= bound;
-                pruned += keep ? 0 : 1;
             }
-            // warp-aggregated reservation (one atomic per warp, no block barrier)
-            const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+            unsigned m[kGP], total = 0;
+            bool keep[kGP];
+#pragma unroll
+            for (int k = 0; k < kGP; ++k) {
+                keep[k] = false;
+                if (g[k] < ix.NG) {
+                    nodes += 1;
+                    keep[k] = box_bound<H, W16>(s_lut, q4, gl[k], gh[k], ix.w) <= bound;
+                    pruned += keep[k] ? 0 : 1;
+                }
+                m[k] = __ballot_sync(0xFFFFFFFFu, keep[k]);
+                total += __popc(m[k]);
+            }
             uint32_t at = 0;
-            if ((threadIdx.x & 31) == 0 && m) at = atomicAdd(&wk->ngroups, static_cast<unsigned>(__popc(m)));
+            if (lane == 0 && total) at = atomicAdd(&wk->ngroups, total);
             at = __shfl_sync(0xFFFFFFFFu, at, 0);
-            if (keep) gsurv[at + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] = static_cast<uint32_t>(g);
+#pragma unroll
+            for (int k = 0; k < kGP; ++k) {
+                if (keep[k]) gsurv[at + __popc(m[k] & below)] = static_cast<uint32_t>(g[k]);
+                at += __popc(m[k]);
+            }
         }
     }
     pruned = warp_sum(pruned);
@@ -1023,17 +1038,23 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     pruned += !seeded && lb > bound ? 1 : 0;
                 }
                 // pages beyond split x bound wait for pass 1 (one atomic per warp and chunk)
+                unsigned dm[kBoundPL], dtotal = 0;
 #pragma unroll
                 for (int k = 0; k < kBoundPL; ++k) {
-                    const unsigned m = __ballot_sync(0xFFFFFFFFu, defer[k]);
-                    uint32_t base = 0;
-                    if (lane == 0 && m) base = atomicAdd(&wk->ndefer, static_cast<unsigned>(__popc(m)));
-                    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                    dm[k] = __ballot_sync(0xFFFFFFFFu, defer[k]);
+                    dtotal += __popc(dm[k]);
+                }
+                uint32_t base = 0;
+                if (lane == 0 && dtotal) base = atomicAdd(&wk->ndefer, dtotal);
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+#pragma unroll
+                for (int k = 0; k < kBoundPL; ++k) {
                     if (defer[k]) {
-                        const uint32_t at = base + __popc(m & below);
+                        const uint32_t at = base + __popc(dm[k] & below);
                         dpage[at] = make_uint2(ea[k], eb[k]);
                         dpage_lb[at] = plb[k];
                     }
+                    base += __popc(dm[k]);
                 }
             } else {
                 // the deferred pages, re-tested against the tightened BSF
@@ -2774,9 +2795,15 @@ void search_batch(DevIndex& ix, const DevIndex::Slots& slots, const float* d_que
     }();
     const unsigned seed_fine_x = seed_env ? static_cast<unsigned>(seed_env)
                                           : std::max(8u, static_cast<unsigned>(ix.sms) / nq);
+    // Two waves of group blocks over the batch (c2: groups + bound 6.31 -> 6.19 us/query against one
+    // wave; three are no better); TSG_GROUP_WAVES overrides (A/B runs).
+    static const int group_waves = [] {
+        const char* e = std::getenv("TSG_GROUP_WAVES");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
     const unsigned group_x = static_cast<unsigned>(std::max<uint64_t>(
         1, std::min<uint64_t>((ix.NT + kThreads * kGP - 1) / (kThreads * kGP),
-                              static_cast<uint64_t>(sms) * blocks_per_sm(groups, lut_bytes) / nq)));
+                              static_cast<uint64_t>(group_waves) * sms * blocks_per_sm(groups, lut_bytes) / nq)));
     // TSG_GRID_CAP (A/B runs): blocks per SM of the persistent kernels
     static const int grid_cap = [] {
         const char* e = std::getenv("TSG_GRID_CAP");
