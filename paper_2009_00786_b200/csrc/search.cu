@@ -446,6 +446,33 @@ __device__ __forceinline__ void ld_box_pair(const uint8_t* p, uint4& lo, uint4& 
                  : "l"(p));
 }
 
+#ifndef TSG_SMEM_ADDR
+#define TSG_SMEM_ADDR 1
+#endif
+// Shared-memory accesses through a 32-bit shared address kept in a register. The address of a
+// per-warp shared array costs ~10 instructions each time the compiler re-derives it (thread id,
+// cluster CTA rank, window base, shifts, masks), which it does at every use in the persistent
+// kernels' hot loops; an address passed through an empty asm statement is opaque and stays put.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));
+    return a;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u2(uint32_t a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
 // L2 prefetch of boxes / words a few steps before they are read (the box
 // filters are bound by load latency; TSG_PREFETCH=0 for A/B builds).
 #ifndef TSG_PREFETCH
@@ -965,6 +992,9 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     __shared__ uint2 s_r[kWarps][kRunStage];     // staged surviving runs
     __shared__ float s_l[kWarps][kRunStage];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TSG_SMEM_ADDR
+    const uint32_t a_pg = smem_addr(&s_pg[warp][0]), a_r = smem_addr(&s_r[warp][0]), a_l = smem_addr(&s_l[warp][0]);
+#endif
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
@@ -1075,7 +1105,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 #pragma unroll
             for (int k = 0; k < kBoundPL; ++k) {
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, keep[k]);
+#if TSG_SMEM_ADDR
+                if (keep[k]) sts_u2(a_pg + 8u * (np + __popc(m & below)), make_uint2(ea[k], eb[k]));
+#else
                 if (keep[k]) s_pg[warp][np + __popc(m & below)] = make_uint2(ea[k], eb[k]);
+#endif
                 np += __popc(m);
             }
             __syncwarp();
@@ -1091,7 +1125,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     e0[u] = e1[u] = 0;
                     uint64_t r = 0;
                     if (j < nri) {
+#if TSG_SMEM_ADDR
+                        const uint2 pg = lds_u2(a_pg + 8u * (j / kRunsPerPage));
+#else
                         const uint2 pg = s_pg[warp][j / kRunsPerPage];
+#endif
                         r = pg.x / kRun + j % kRunsPerPage;
                         e0[u] = max(pg.x, static_cast<uint32_t>(r * kRun));
                         e1[u] = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
@@ -1117,8 +1155,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     const unsigned m = __ballot_sync(0xFFFFFFFFu, pass_);
                     if (pass_) {
                         const int slot = cnt + __popc(m & below);
+#if TSG_SMEM_ADDR
+                        sts_u2(a_r + 8u * slot, make_uint2(e0[u], e1[u]));
+                        sts_f32(a_l + 4u * slot, lb);
+#else
                         s_r[warp][slot] = make_uint2(e0[u], e1[u]);
                         s_l[warp][slot] = lb;
+#endif
                     }
                     cnt += __popc(m);
                     __syncwarp();
@@ -1224,6 +1267,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     __shared__ uint2 s_rq[kWarps][kRing];  // surviving runs
     __shared__ uint2 s_qq[kWarps][kRing];  // surviving quads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if TSG_SMEM_ADDR
+    const uint32_t a_rq = smem_addr(&s_rq[warp][0]), a_qq = smem_addr(&s_qq[warp][0]);
+    const uint32_t a_pos = smem_addr(&s_pos[warp][0]), a_lb = smem_addr(&s_lb[warp][0]);
+#endif
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
@@ -1262,8 +1309,13 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         if (!m) return;
         if (pass) {
             const int slot = cnt + __popc(m & below);
+#if TSG_SMEM_ADDR
+            sts_u32(a_pos + 4u * slot, e);  // the flush maps entries to dataset rows
+            sts_f32(a_lb + 4u * slot, lb);
+#else
             s_pos[warp][slot] = e;  // the flush maps entries to dataset rows
             s_lb[warp][slot] = lb;
+#endif
         }
         cnt += __popc(m);
         __syncwarp();
@@ -1284,7 +1336,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             ok[k] = false;
             e[k] = 0;
             if (qi < take) {
+#if TSG_SMEM_ADDR
+                const uint2 rr = lds_u2(a_qq + 8u * ((qh + qi) & (kRing - 1)));
+#else
                 const uint2 rr = s_qq[warp][(qh + qi) & (kRing - 1)];
+#endif
                 e[k] = rr.x + (lane & 3);
                 ok[k] = e[k] < rr.y;
             }
@@ -1308,7 +1364,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         bool ok = false;
         uint32_t e0 = 0, e1 = 0, qd = 0;
         if (k < take) {
+#if TSG_SMEM_ADDR
+            const uint2 rr = lds_u2(a_rq + 8u * ((rh + k) & (kRing - 1)));
+#else
             const uint2 rr = s_rq[warp][(rh + k) & (kRing - 1)];
+#endif
             qd = (rr.x / kRun) * (kRun / kQuad) + u;  // the run's aligned quads
             e0 = max(rr.x, qd * kQuad);
             e1 = min(rr.y, qd * kQuad + kQuad);
@@ -1331,7 +1391,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         boxes += ok ? 1 : 0;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
         if (pass) {
+#if TSG_SMEM_ADDR
+            sts_u2(a_qq + 8u * ((qt + __popc(m & below)) & (kRing - 1)), make_uint2(e0, e1));
+#else
             s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
+#endif
             if (TSG_PREFETCH) prefetch_l2_bytes(ix.words + static_cast<uint64_t>(e0) * WS, (e1 - e0) * WS);  // read when 16 quads queue
         }
         qt += __popc(m);
@@ -1381,7 +1445,11 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             }
             const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
             if (pass) {
+#if TSG_SMEM_ADDR
+                sts_u2(a_rq + 8u * ((rt + __popc(m & below)) & (kRing - 1)), run);
+#else
                 s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
+#endif
                 if (TSG_PREFETCH) {  // the run's quad boxes are read a few drains later
                     const uint64_t qd0 = static_cast<uint64_t>(run.x / kRun) * (kRun / kQuad);
                     prefetch_l2_bytes(ix.quad_lo + qd0 * 2 * WS, (kRun / kQuad) * 2 * WS);  // the run's 128-byte line
