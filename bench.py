@@ -125,7 +125,7 @@ def peaks():
     return 6650.0, "fallback"
 
 
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "round2d_ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "round2e_ncu_summary.json")
 NCU_REPORTS = {"lbscan": ["prof_k_lbscan.ncu-rep"], "refine": ["prof_k_refine_tma.ncu-rep"],
                "bound": ["prof_k_groups.ncu-rep", "prof_k_bound.ncu-rep"], "summarise": ["prof_k_summarise.ncu-rep"]}
 
@@ -167,7 +167,7 @@ def ncu_binding(kernel):
 def ncu_traffic(kernel, nq):
     """dram__bytes_read.sum + dram__bytes_write.sum of `kernel` per batch (all its launches of one
     batch: both waves for lbscan / refine), from the committed `ncu --set full` capture of the c2
-    bench command (profiles/ncu_round2d.sh); None when the capture does not match this run."""
+    bench command (profiles/ncu_round2e.sh); None when the capture does not match this run."""
     if not os.path.exists(NCU_SUMMARY) or kernel not in NCU_REPORTS:
         return None
     with open(NCU_SUMMARY) as f:
