@@ -338,6 +338,21 @@ def test_many_batches_one_call(oracle):
     check_against_scan(oracle, rows, queries.astype(np.float32), cfg)
 
 
+@pytest.mark.parametrize("slots", [1, 3, 320])
+def test_batch_widths_stay_exact(oracle, monkeypatch, slots):
+    """Query slots from 1 to more than a block has threads (TSG_BATCH): the persistent kernels'
+    block-wide query selection strides over the batch, the weighted refinement start falls back
+    to the uniform one above 256 queries, and launches with less work than blocks retire their
+    surplus blocks (easy member queries next to hard ones)."""
+    monkeypatch.setenv("TSG_BATCH", str(slots))
+    rows = oracle.generate(6000, 64, 531)
+    rng = np.random.default_rng(7)
+    queries = np.concatenate([oracle.generate(200, 64, 532), rows[rng.integers(0, 6000, 130)],
+                              rows[rng.integers(0, 6000, 20)] + 0.5 * rng.standard_normal((20, 64)).astype(np.float32)])
+    cfg = tg.IndexConfig(n=64, w=16, leaf_capacity=40)
+    check_against_scan(oracle, rows, queries.astype(np.float32), cfg)
+
+
 def test_approximate_batch_matches_single(oracle):
     rows = oracle.generate(3000, 128, 519)
     index = tg.build_index(rows, tg.IndexConfig(n=128, w=16, leaf_capacity=30))
