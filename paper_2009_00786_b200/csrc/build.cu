@@ -225,16 +225,32 @@ __global__ void k_page_key(const uint64_t* __restrict__ keys, const uint32_t* __
     GRID_STRIDE(p, P) page_key[p] = keys[page_off[p]];
 }
 
-// One warp per page: bytewise min / max over the page's entries, from the run
-// box pairs of the aligned runs inside the page and the words of its ragged
-// ends (a page is <= kPage entries, cut from a leaf that need not start on a
-// run boundary): ~0.6 GB read for c2 instead of every word (1.6 GB).
+// Eight lanes per page (four pages per warp): bytewise min / max over the page's entries, from the
+// run box pairs of the aligned runs inside the page and the words of its ragged ends (a page is
+// <= kPage entries, cut from a leaf that need not start on a run boundary): ~0.6 GB read for c2
+// instead of every word (1.6 GB). Pages are cut on run boundaries, so most have eight items, one
+// per lane. The bytes are reduced as even / odd 16-bit lanes with the native u16x2 min / max
+// (__vminu4 / __vmaxu4 are emulated in ~7 instructions each; one warp per page with five shuffle
+// rounds of them made this kernel instruction-bound: 0.58 ms on c2).
+__device__ __forceinline__ uint32_t min16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t max16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+
 __global__ void k_page_box(const uint8_t* __restrict__ words, const uint8_t* __restrict__ run_pairs,
                            const uint32_t* __restrict__ page_off, uint64_t P, int ws, uint8_t* __restrict__ lo_out,
                            uint8_t* __restrict__ hi_out) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-    for (uint64_t p = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; p < P; p += warps) {
+    constexpr int kLanes = 8;
+    const int j8 = threadIdx.x & (kLanes - 1);
+    const unsigned gmask = 0xFFu << (threadIdx.x & 31 & ~(kLanes - 1));
+    const uint64_t groups = static_cast<uint64_t>(gridDim.x) * (blockDim.x / kLanes);
+    for (uint64_t p = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / kLanes; p < P; p += groups) {
         const uint32_t a = page_off[p], b = page_off[p + 1];
         const uint32_t ra = (a + kRun - 1) / kRun, rb = b / kRun;  // full runs [ra, rb)
         const uint32_t head_end = ra < rb ? ra * kRun : b;           // words [a, head_end) and [tail, b)
@@ -242,8 +258,14 @@ __global__ void k_page_box(const uint8_t* __restrict__ words, const uint8_t* __r
         const uint32_t nhead = head_end - a, nruns = ra < rb ? rb - ra : 0, ntail = b - tail;
         const uint32_t items = nhead + nruns + ntail;
         for (int h = 0; h < ws / 16; ++h) {
-            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
-            for (uint32_t it = lane; it < items; it += 32) {
+            // even / odd bytes of the four words of a 16-byte piece, as u16x2 lanes
+            uint32_t mne[4], mno[4], mxe[4], mxo[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                mne[k] = mno[k] = 0x00FF00FFu;
+                mxe[k] = mxo[k] = 0u;
+            }
+            for (uint32_t it = j8; it < items; it += kLanes) {
                 uint4 xl, xh;
                 if (it < nhead || it >= nhead + nruns) {
                     const uint32_t e = it < nhead ? a + it : tail + (it - nhead - nruns);
@@ -253,23 +275,35 @@ __global__ void k_page_box(const uint8_t* __restrict__ words, const uint8_t* __r
                     xl = *reinterpret_cast<const uint4*>(run_pairs + r * 2 * ws + 16 * h);
                     xh = *reinterpret_cast<const uint4*>(run_pairs + r * 2 * ws + ws + 16 * h);
                 }
-                mn = make_uint4(__vminu4(mn.x, xl.x), __vminu4(mn.y, xl.y), __vminu4(mn.z, xl.z), __vminu4(mn.w, xl.w));
-                mx = make_uint4(__vmaxu4(mx.x, xh.x), __vmaxu4(mx.y, xh.y), __vmaxu4(mx.z, xh.z), __vmaxu4(mx.w, xh.w));
+                const uint32_t l[4] = {xl.x, xl.y, xl.z, xl.w}, u[4] = {xh.x, xh.y, xh.z, xh.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mne[k] = min16x2(mne[k], l[k] & 0x00FF00FFu);
+                    mno[k] = min16x2(mno[k], __byte_perm(l[k], 0, 0x4341));
+                    mxe[k] = max16x2(mxe[k], u[k] & 0x00FF00FFu);
+                    mxo[k] = max16x2(mxo[k], __byte_perm(u[k], 0, 0x4341));
+                }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                mn.x = __vminu4(mn.x, __shfl_xor_sync(0xFFFFFFFFu, mn.x, o));
-                mn.y = __vminu4(mn.y, __shfl_xor_sync(0xFFFFFFFFu, mn.y, o));
-                mn.z = __vminu4(mn.z, __shfl_xor_sync(0xFFFFFFFFu, mn.z, o));
-                mn.w = __vminu4(mn.w, __shfl_xor_sync(0xFFFFFFFFu, mn.w, o));
-                mx.x = __vmaxu4(mx.x, __shfl_xor_sync(0xFFFFFFFFu, mx.x, o));
-                mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xFFFFFFFFu, mx.y, o));
-                mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xFFFFFFFFu, mx.z, o));
-                mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xFFFFFFFFu, mx.w, o));
+            for (int o = kLanes / 2; o > 0; o >>= 1) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mne[k] = min16x2(mne[k], __shfl_xor_sync(gmask, mne[k], o));
+                    mno[k] = min16x2(mno[k], __shfl_xor_sync(gmask, mno[k], o));
+                    mxe[k] = max16x2(mxe[k], __shfl_xor_sync(gmask, mxe[k], o));
+                    mxo[k] = max16x2(mxo[k], __shfl_xor_sync(gmask, mxo[k], o));
+                }
             }
-            if (lane == 0) {
-                *reinterpret_cast<uint4*>(lo_out + p * ws + 16 * h) = mn;
-                *reinterpret_cast<uint4*>(hi_out + p * ws + 16 * h) = mx;
+            if (j8 == 0) {
+                // bytes back in place: even lanes at bytes 0 / 2, odd lanes at bytes 1 / 3
+                uint32_t mn[4], mx[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    mn[k] = __byte_perm(mne[k], mno[k], 0x6240);
+                    mx[k] = __byte_perm(mxe[k], mxo[k], 0x6240);
+                }
+                *reinterpret_cast<uint4*>(lo_out + p * ws + 16 * h) = make_uint4(mn[0], mn[1], mn[2], mn[3]);
+                *reinterpret_cast<uint4*>(hi_out + p * ws + 16 * h) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
             }
         }
     }
@@ -517,7 +551,7 @@ void build_layout(DevIndex& ix, double* ms_sum, double* ms_org, double* ms_leaf,
     TSG_LAUNCHED();
     TSG_CUDA(cudaMemcpy2DAsync(ix.page_dir, 8, ix.page_key, 256 * 8, 8, ndir, cudaMemcpyDeviceToDevice, st));
     TSG_CUDA(cudaStreamWaitEvent(st, gathered_ev, 0));  // words and run boxes are in index order
-    k_page_box<<<grid_for(ix.P * 32, 256, sms), 256, 0, st>>>(ix.words, ix.run_lo, ix.page_off, ix.P, ix.ws,
+    k_page_box<<<grid_for(ix.P * 8, 256, sms), 256, 0, st>>>(ix.words, ix.run_lo, ix.page_off, ix.P, ix.ws,
                                                               ix.page_lo, ix.page_hi);
     TSG_LAUNCHED();
     k_group_box<<<grid_for(ix.NG * (ix.ws / 16), 256, sms), 256, 0, st>>>(ix.page_lo, ix.page_hi, ix.P, ix.NG, ix.ws,
