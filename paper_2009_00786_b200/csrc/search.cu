@@ -446,9 +446,6 @@ __device__ __forceinline__ void ld_box_pair(const uint8_t* p, uint4& lo, uint4& 
                  : "l"(p));
 }
 
-#ifndef TSG_SMEM_ADDR
-#define TSG_SMEM_ADDR 1
-#endif
 // Shared-memory accesses through a 32-bit shared address kept in a register. The address of a
 // per-warp shared array costs ~10 instructions each time the compiler re-derives it (thread id,
 // cluster CTA rank, window base, shifts, masks), which it does at every use in the persistent
@@ -461,6 +458,16 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __device__ __forceinline__ uint2 lds_u2(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ void sts_u2(uint32_t a, uint2 v) {
@@ -938,13 +945,11 @@ constexpr int kRunStage = 128;
 #endif
 constexpr int kBoundPL = TSG_BOUND_PL;  // pages per lane per bound chunk
 
-__device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, const float* s_l, int cnt, int lane,
-                                           float cut, uint64_t rcap, uint2* __restrict__ surv,
+__device__ __forceinline__ void flush_runs(QueryWork* wk, uint32_t a_r, uint32_t a_l, int cnt, int lo_cnt, int lane,
+                                           float cut, uint32_t rcap, uint2* __restrict__ surv,
                                            float* __restrict__ surv_lb) {
-    // one 64-bit atomic reserves both waves' slots for the whole stage
-    int lo_cnt = 0;
-    for (int i = lane; i < cnt; i += 32) lo_cnt += s_l[i] <= cut ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
+    // one 64-bit atomic reserves both waves' slots for the whole stage (lo_cnt: the staged runs
+    // with bound <= cut, counted while staging)
     unsigned long long old = 0;
     if (lane == 0) {
         old = atomicAdd(&wk->runs, static_cast<unsigned long long>(lo_cnt) |
@@ -953,24 +958,25 @@ __device__ __forceinline__ void flush_runs(QueryWork* wk, const uint2* s_r, cons
             atomicExch(&wk->overflow, 1u);  // cannot happen with rcap = R + P; never write out of range
     }
     old = __shfl_sync(0xFFFFFFFFu, old, 0);
-    uint64_t at_lo = old & 0xFFFFFFFFull, at_hi = old >> 32;
+    uint32_t at_lo = static_cast<uint32_t>(old), at_hi = static_cast<uint32_t>(old >> 32);
     const unsigned below = (1u << lane) - 1u;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < cnt;
-        const float lb = valid ? s_l[i] : 0.f;
+        const float lb = valid ? lds_f32(a_l + 4u * i) : 0.f;
+        const uint2 r = valid ? lds_u2(a_r + 8u * i) : make_uint2(0, 0);
         const bool low = valid && lb <= cut;
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
         if (low) {
-            const uint64_t at = at_lo + __popc(ml & below);
+            const uint32_t at = at_lo + __popc(ml & below);
             if (at < rcap) {
-                surv[at] = s_r[i];
+                surv[at] = r;
                 surv_lb[at] = lb;
             }
         } else if (valid) {
-            const uint64_t off = at_hi + __popc(mh & below);
+            const uint32_t off = at_hi + __popc(mh & below);
             if (off < rcap) {
-                surv[rcap - 1 - off] = s_r[i];
+                surv[rcap - 1 - off] = r;
                 surv_lb[rcap - 1 - off] = lb;
             }
         }
@@ -992,14 +998,12 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
     __shared__ uint2 s_r[kWarps][kRunStage];     // staged surviving runs
     __shared__ float s_l[kWarps][kRunStage];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#if TSG_SMEM_ADDR
     const uint32_t a_pg = smem_addr(&s_pg[warp][0]), a_r = smem_addr(&s_r[warp][0]), a_l = smem_addr(&s_l[warp][0]);
-#endif
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
     uint32_t pruned = 0, nodes = 0;  // per lane and query
-    int cnt = 0;
+    int cnt = 0, cnt_lo = 0;         // staged runs, and those of them for wave 0 (bound <= cut)
     auto nchunks = [pass](const QueryWork* wk) -> uint32_t {
         if (wk->overflow) return 0;
         const uint32_t items = pass == 0 ? wk->ngroups * static_cast<uint32_t>(kGroup) : wk->ndefer;
@@ -1105,11 +1109,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 #pragma unroll
             for (int k = 0; k < kBoundPL; ++k) {
                 const unsigned m = __ballot_sync(0xFFFFFFFFu, keep[k]);
-#if TSG_SMEM_ADDR
                 if (keep[k]) sts_u2(a_pg + 8u * (np + __popc(m & below)), make_uint2(ea[k], eb[k]));
-#else
-                if (keep[k]) s_pg[warp][np + __popc(m & below)] = make_uint2(ea[k], eb[k]);
-#endif
                 np += __popc(m);
             }
             __syncwarp();
@@ -1125,11 +1125,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     e0[u] = e1[u] = 0;
                     uint64_t r = 0;
                     if (j < nri) {
-#if TSG_SMEM_ADDR
                         const uint2 pg = lds_u2(a_pg + 8u * (j / kRunsPerPage));
-#else
-                        const uint2 pg = s_pg[warp][j / kRunsPerPage];
-#endif
                         r = pg.x / kRun + j % kRunsPerPage;
                         e0[u] = max(pg.x, static_cast<uint32_t>(r * kRun));
                         e1[u] = min(pg.y, static_cast<uint32_t>(r * kRun + kRun));
@@ -1155,27 +1151,23 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
                     const unsigned m = __ballot_sync(0xFFFFFFFFu, pass_);
                     if (pass_) {
                         const int slot = cnt + __popc(m & below);
-#if TSG_SMEM_ADDR
                         sts_u2(a_r + 8u * slot, make_uint2(e0[u], e1[u]));
                         sts_f32(a_l + 4u * slot, lb);
-#else
-                        s_r[warp][slot] = make_uint2(e0[u], e1[u]);
-                        s_l[warp][slot] = lb;
-#endif
                     }
                     cnt += __popc(m);
+                    if (pass == 0) cnt_lo += __popc(__ballot_sync(0xFFFFFFFFu, pass_ && lb <= cut));
                     __syncwarp();
                     if (cnt > kRunStage - 32) {
-                        flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
-                        cnt = 0;
+                        flush_runs(wk, a_r, a_l, cnt, cnt_lo, lane, cut, static_cast<uint32_t>(S.rcap), surv, surv_lb);
+                        cnt = cnt_lo = 0;
                     }
                 }
             }
             chunk = __shfl_sync(0xFFFFFFFFu, pre, 0);
         }
         // leave the query: the stage and the counters
-        if (cnt) flush_runs(wk, s_r[warp], s_l[warp], cnt, lane, cut, S.rcap, surv, surv_lb);
-        cnt = 0;
+        if (cnt) flush_runs(wk, a_r, a_l, cnt, cnt_lo, lane, cut, static_cast<uint32_t>(S.rcap), surv, surv_lb);
+        cnt = cnt_lo = 0;
         const unsigned long long pr = warp_sum(static_cast<unsigned long long>(pruned));
         const unsigned long long nd = warp_sum(static_cast<unsigned long long>(nodes));
         if (lane == 0) {
@@ -1199,14 +1191,12 @@ constexpr int kStageCap = 256;
 // slot that would overflow is detected exactly (the query is then flagged
 // and rerun with a full-size slot; nothing is written out of range).
 // cut = +inf sends everything to A, cut < 0 everything to B.
-__device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos, const float* s_lb, int cnt, int lane,
+__device__ __forceinline__ void flush_stage(QueryWork* wk, uint32_t a_pos, uint32_t a_lb, int cnt, int lo_cnt, int lane,
                                             float cut, uint64_t cap, uint32_t* __restrict__ cand_pos,
                                             float* __restrict__ cand_lb) {
     // one 64-bit atomic reserves both waves' records for the whole stage (per 32
-    // records it contended on c4, where every warp queues millions per query)
-    int lo_cnt = 0;
-    for (int i = lane; i < cnt; i += 32) lo_cnt += s_lb[i] <= cut ? 1 : 0;
-    for (int o = 16; o > 0; o >>= 1) lo_cnt += __shfl_xor_sync(0xFFFFFFFFu, lo_cnt, o);
+    // records it contended on c4, where every warp queues millions per query);
+    // lo_cnt: the staged records with bound <= cut, counted while staging
     unsigned long long old = 0;
     if (lane == 0) {
         old = atomicAdd(&wk->cand, static_cast<unsigned long long>(lo_cnt) |
@@ -1215,14 +1205,14 @@ __device__ __forceinline__ void flush_stage(QueryWork* wk, const uint32_t* s_pos
     }
     old = __shfl_sync(0xFFFFFFFFu, old, 0);
     uint64_t bl = old & 0xFFFFFFFFull, bh = old >> 32;
+    const unsigned below = (1u << lane) - 1u;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
         const int i = i0 + lane;
         const bool valid = i < cnt;
-        const float lb = valid ? s_lb[i] : 0.f;
+        const float lb = valid ? lds_f32(a_lb + 4u * i) : 0.f;
         const bool low = valid && lb <= cut;
-        const uint32_t row = valid ? s_pos[i] : 0u;  // index entries (mapped to rows only when refined)
+        const uint32_t row = valid ? lds_u32(a_pos + 4u * i) : 0u;  // index entries (mapped to rows only when refined)
         const unsigned ml = __ballot_sync(0xFFFFFFFFu, low), mh = __ballot_sync(0xFFFFFFFFu, valid && !low);
-        const unsigned below = (1u << lane) - 1u;
         if (low) {
             const uint64_t at = bl + __popc(ml & below);
             if (at < cap) {
@@ -1267,10 +1257,8 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     __shared__ uint2 s_rq[kWarps][kRing];  // surviving runs
     __shared__ uint2 s_qq[kWarps][kRing];  // surviving quads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#if TSG_SMEM_ADDR
     const uint32_t a_rq = smem_addr(&s_rq[warp][0]), a_qq = smem_addr(&s_qq[warp][0]);
     const uint32_t a_pos = smem_addr(&s_pos[warp][0]), a_lb = smem_addr(&s_lb[warp][0]);
-#endif
     const unsigned below = (1u << lane) - 1u;
     int cur = static_cast<int>(static_cast<uint64_t>(blockIdx.x) * nq / gridDim.x);
     uint4 q4[H];
@@ -1280,7 +1268,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
     float* cand_lb = nullptr;
     const uint2* surv = nullptr;
     const float* surv_lb = nullptr;
-    int cnt = 0;
+    int cnt = 0, cnt_lo = 0;                  // staged candidates, and those of them for wave A (bound <= cut)
     uint32_t rh = 0, rt = 0, qh = 0, qt = 0;  // ring heads / tails (warp-uniform)
     uint32_t scanned = 0, pruned = 0, boxes = 0;  // per lane and query (32-bit: one add per count in the hot loops)
     const int k_next = wave == 0 ? kNextScan0 : kNextScan1;
@@ -1291,8 +1279,8 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         return (ns + 31) / 32;
     };
     auto leave_query = [&]() {  // flush this warp's stage and counters to the loaded query
-        if (cnt) flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
-        cnt = 0;
+        if (cnt) flush_stage(wk, a_pos, a_lb, cnt, cnt_lo, lane, cut, S.cap, cand_pos, cand_lb);
+        cnt = cnt_lo = 0;
         const unsigned long long sc = warp_sum(static_cast<unsigned long long>(scanned));
         const unsigned long long pr = warp_sum(static_cast<unsigned long long>(pruned));
         const unsigned long long bx = warp_sum(static_cast<unsigned long long>(boxes));
@@ -1309,19 +1297,15 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         if (!m) return;
         if (pass) {
             const int slot = cnt + __popc(m & below);
-#if TSG_SMEM_ADDR
             sts_u32(a_pos + 4u * slot, e);  // the flush maps entries to dataset rows
             sts_f32(a_lb + 4u * slot, lb);
-#else
-            s_pos[warp][slot] = e;  // the flush maps entries to dataset rows
-            s_lb[warp][slot] = lb;
-#endif
         }
         cnt += __popc(m);
+        if (wave == 0) cnt_lo += __popc(__ballot_sync(0xFFFFFFFFu, pass && lb <= cut));
         __syncwarp();
         if (cnt > kStageCap - 32) {
-            flush_stage(wk, s_pos[warp], s_lb[warp], cnt, lane, cut, S.cap, cand_pos, cand_lb);
-            cnt = 0;
+            flush_stage(wk, a_pos, a_lb, cnt, cnt_lo, lane, cut, S.cap, cand_pos, cand_lb);
+            cnt = cnt_lo = 0;
         }
     };
     // Words of up to 8 kQK queued quads: lane 4j + u takes entry u of quads j, j + 8, ...
@@ -1336,11 +1320,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             ok[k] = false;
             e[k] = 0;
             if (qi < take) {
-#if TSG_SMEM_ADDR
                 const uint2 rr = lds_u2(a_qq + 8u * ((qh + qi) & (kRing - 1)));
-#else
-                const uint2 rr = s_qq[warp][(qh + qi) & (kRing - 1)];
-#endif
                 e[k] = rr.x + (lane & 3);
                 ok[k] = e[k] < rr.y;
             }
@@ -1364,11 +1344,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         bool ok = false;
         uint32_t e0 = 0, e1 = 0, qd = 0;
         if (k < take) {
-#if TSG_SMEM_ADDR
             const uint2 rr = lds_u2(a_rq + 8u * ((rh + k) & (kRing - 1)));
-#else
-            const uint2 rr = s_rq[warp][(rh + k) & (kRing - 1)];
-#endif
             qd = (rr.x / kRun) * (kRun / kQuad) + u;  // the run's aligned quads
             e0 = max(rr.x, qd * kQuad);
             e1 = min(rr.y, qd * kQuad + kQuad);
@@ -1391,11 +1367,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
         boxes += ok ? 1 : 0;
         const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
         if (pass) {
-#if TSG_SMEM_ADDR
             sts_u2(a_qq + 8u * ((qt + __popc(m & below)) & (kRing - 1)), make_uint2(e0, e1));
-#else
-            s_qq[warp][(qt + __popc(m & below)) & (kRing - 1)] = make_uint2(e0, e1);
-#endif
             if (TSG_PREFETCH) prefetch_l2_bytes(ix.words + static_cast<uint64_t>(e0) * WS, (e1 - e0) * WS);  // read when 16 quads queue
         }
         qt += __popc(m);
@@ -1445,11 +1417,7 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_LBSCAN)
             }
             const unsigned m = __ballot_sync(0xFFFFFFFFu, pass);
             if (pass) {
-#if TSG_SMEM_ADDR
                 sts_u2(a_rq + 8u * ((rt + __popc(m & below)) & (kRing - 1)), run);
-#else
-                s_rq[warp][(rt + __popc(m & below)) & (kRing - 1)] = run;
-#endif
                 if (TSG_PREFETCH) {  // the run's quad boxes are read a few drains later
                     const uint64_t qd0 = static_cast<uint64_t>(run.x / kRun) * (kRun / kQuad);
                     prefetch_l2_bytes(ix.quad_lo + qd0 * 2 * WS, (kRun / kQuad) * 2 * WS);  // the run's 128-byte line
