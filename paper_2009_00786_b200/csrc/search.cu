@@ -796,12 +796,29 @@ __global__ void __launch_bounds__(kThreads)
     const float* flut = fine ? S.fine_lut + static_cast<uint64_t>(q) * S.fine_lut_len : nullptr;
     const int j8 = lane & (kRowLanes - 1);
     const unsigned gmask = 0xFFu << (lane & ~(kRowLanes - 1));
-    for (uint64_t e = a + group; e < b; e += ngroups) {  // groups run independently
-        const uint32_t p = ix.pos[e];
+    // The next row's position and (32-wide fine summary) its four fine bytes of this lane are
+    // loaded one row ahead: the per-row chain position -> fine bytes -> table -> row was serial.
+    const bool fine32 = fine && ix.fw == 32;
+    uint64_t e = a + group;
+    uint32_t p = e < b ? ix.pos[e] : 0u;
+    uint32_t fb = fine32 && e < b ? *reinterpret_cast<const uint32_t*>(ix.fine + e * ix.fws + 4 * j8) : 0u;
+    for (; e < b; e += ngroups) {  // groups run independently
+        const uint64_t en = e + ngroups;
+        const uint32_t p_cur = p, fb_cur = fb;
+        if (en < b) {
+            p = ix.pos[en];
+            if (fine32) fb = *reinterpret_cast<const uint32_t*>(ix.fine + en * ix.fws + 4 * j8);
+        }
         if (fine && e >= a + ngroups) {
             const uint8_t* f = ix.fine + e * ix.fws;  // fine rows are in index order
             float acc = 0.f;
-            for (int sg = j8; sg < ix.fw; sg += kRowLanes) acc = __fadd_rd(acc, __ldg(flut + sg * 256 + f[sg]));
+            if (fine32) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    acc = __fadd_rd(acc, __ldg(flut + (4 * j8 + i) * 256 + ((fb_cur >> (8 * i)) & 255u)));
+            } else {
+                for (int sg = j8; sg < ix.fw; sg += kRowLanes) acc = __fadd_rd(acc, __ldg(flut + sg * 256 + f[sg]));
+            }
 #pragma unroll
             for (int o = kRowLanes / 2; o > 0; o >>= 1) acc = __fadd_rd(acc, __shfl_xor_sync(gmask, acc, o));
             if (acc > bound_from_bits(ld_volatile_u64(&wk->bsf_bits))) {
@@ -812,7 +829,7 @@ __global__ void __launch_bounds__(kThreads)
                 continue;
             }
         }
-        const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p) * ix.n, s_qd, ix.n, &wk->bsf_bits);
+        const double s = group_row_sq<VEC>(ix.rows + static_cast<uint64_t>(p_cur) * ix.n, s_qd, ix.n, &wk->bsf_bits);
         if (j8 == 0) {
             cand_pos[e - a] = static_cast<uint32_t>(e);  // candidate records hold index entries
             updates += publish(wk, s, e - a, cand_sq, ~0u);
