@@ -956,7 +956,10 @@ __global__ void __launch_bounds__(kThreads)
 // entry from the start of its first run (build.cu first_page_end): every page lies within kPage /
 // kRun aligned runs (an arbitrary 128-entry window would touch 9).
 constexpr int kRunsPerPage = kPage / kRun;
-constexpr int kRunStage = 128;
+#ifndef TSG_RUN_STAGE
+#define TSG_RUN_STAGE 256  // 128 until round 2e: half the flushes (each an atomic round trip), bound 5.77 -> 5.66 us/query; 64: 6.06
+#endif
+constexpr int kRunStage = TSG_RUN_STAGE;  // staged surviving runs per warp
 #ifndef TSG_BOUND_PL
 #define TSG_BOUND_PL 2
 #endif
@@ -1197,7 +1200,10 @@ __global__ void __launch_bounds__(kThreads, TSG_MINB_BOUND)
 
 // ------------------------------------------------------------ lbscan
 
-constexpr int kStageCap = 256;
+#ifndef TSG_STAGE_CAP
+#define TSG_STAGE_CAP 256  // 512 costs lbscan a block per SM (11.85 -> 13.4 us/query)
+#endif
+constexpr int kStageCap = TSG_STAGE_CAP;  // staged candidates per warp
 #ifndef TSG_SCAN_QK
 #define TSG_SCAN_QK 2
 #endif
